@@ -1,0 +1,406 @@
+"""Benchmark: NeRF-XL distributed training step (fwd+bwd+Adam) on B200.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--config c3] [--impl ours|reference]
+
+N>1 is launched by the driver with torch.distributed.run (one rank per GPU, NCCL).
+A step = sample rays (K1) -> hash grid + MLP fwd (K2, K3) -> segment composite (K4)
+-> all-gather of packets -> global composite + loss + its backward (K5) -> K4 bwd ->
+MLP/hash bwd -> Adam, over one batch of synthetic rays (BASELINE.json configs; see
+paper_2404_16221_b200/workloads.py).  Rank 0 prints ONE JSON line.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import math
+import os
+import statistics
+import subprocess
+import sys
+import tempfile
+import time
+from pathlib import Path
+
+import numpy as np
+
+ROOT = Path(__file__).resolve().parent
+sys.path.insert(0, str(ROOT))
+
+METRIC = "train rays/sec (fwd+bwd)"
+UNIT = "rays/s"
+
+# Algorithmic cost per unit of work: bytes (hbm) or flops (tensor)
+# per sample for the per-sample kernels.
+KERNEL_COST = {
+    # t0,t1 (16) + ray id (4) + 16 levels x 8 corners x float2 (1024) + enc fp16 (64)
+    "vr_hash_fwd": ("hbm", 1108.0),
+    # t0,t1,ray id (20) + denc f32 (128) + 16 x 8 float2 atomics (1024)
+    "vr_hash_bwd": ("hbm", 1172.0),
+    # 2 * (32*64 + 64*16 + 32*64 + 64*64 + 64*3)
+    "vr_mlp_fwd": ("tensor", 18816.0),
+    # recomputed forward + activation grads + weight grads
+    "vr_mlp_bwd": ("tensor", 3 * 18816.0),
+    # t0,t1 (16) + sig_rgb (16); packets amortised
+    "vr_segment_fwd": ("hbm", 32.0),
+    # t0,t1 (16) + sig_rgb (16) + dsig_rgb (16)
+    "vr_segment_bwd": ("hbm", 48.0),
+}
+
+
+def load_peaks():
+    p = ROOT / "MEASURED_PEAKS.json"
+    if p.exists():
+        d = json.loads(p.read_text())
+        return {"hbm": float(d["hbm_gbs"]), "tensor": float(d["bf16_tflops_sustained"]),
+                "tensor_burst": float(d["bf16_tflops"]), "source": "measured",
+                "sm_max_mhz": d.get("sm_max_mhz")}
+    return {"hbm": 6650.0, "tensor": 1400.0, "tensor_burst": 1590.0, "source": "fallback",
+            "sm_max_mhz": 1965.0}
+
+
+class EventTimer:
+    """CUDA events around every C-ABI call (current stream); per-entry-point totals."""
+
+    def __init__(self):
+        import torch
+
+        self.torch = torch
+        self.pending = []
+        self.open = {}
+
+    def before(self, name):
+        e = self.torch.cuda.Event(enable_timing=True)
+        e.record()
+        self.open[name] = e
+
+    def after(self, name):
+        e = self.torch.cuda.Event(enable_timing=True)
+        e.record()
+        self.pending.append((name, self.open.pop(name), e))
+
+    def totals(self):
+        out = {}
+        for name, a, b in self.pending:
+            ms = a.elapsed_time(b)
+            t, n = out.get(name, (0.0, 0))
+            out[name] = (t + ms, n + 1)
+        return out
+
+
+class ClockSampler:
+    """nvidia-smi clocks/throttle reasons sampled during the timed region."""
+
+    Q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,"
+         "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+         "clocks_event_reasons.sw_power_cap,utilization.gpu")
+
+    def __init__(self, index: int):
+        self.index = index
+        self.proc = None
+        self.file = None
+
+    def start(self):
+        try:
+            self.file = tempfile.NamedTemporaryFile("w+", suffix=".csv", delete=False)
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", f"--id={self.index}", f"--query-gpu={self.Q}",
+                 "--format=csv,noheader,nounits", "-lms", "100"],
+                stdout=self.file, stderr=subprocess.DEVNULL)
+        except (OSError, FileNotFoundError):
+            self.proc = None
+
+    def stop(self):
+        if self.proc is None:
+            return None
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=5)
+        except subprocess.TimeoutExpired:
+            self.proc.kill()
+        self.file.flush()
+        rows = []
+        for line in Path(self.file.name).read_text().splitlines():
+            parts = [p.strip() for p in line.split(",")]
+            if len(parts) >= 7:
+                rows.append(parts)
+        os.unlink(self.file.name)
+        if not rows:
+            return None
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for r in rows for i in range(4) if r[2 + i].lower() == "active"})
+        loaded = [r for r in rows if r[6].isdigit() and int(r[6]) > 50] or rows
+        sm = [float(r[0]) for r in loaded if r[0].replace(".", "").isdigit()]
+        mx = [float(r[1]) for r in rows if r[1].replace(".", "").isdigit()]
+        return {"sm_mhz": statistics.median(sm) if sm else None,
+                "sm_max_mhz": max(mx) if mx else None, "reasons": reasons,
+                "samples": len(rows), "samples_under_load": len(loaded)}
+
+
+def dist_env():
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return rank, world, local
+
+
+def build_pool(w, rank, world, dev, group, seed_base=1):
+    import paper_2404_16221_b200 as vr
+
+    tree = w.tree
+    lo, cnt = vr.owned_regions(len(tree.leaves), rank, world)
+    cfg = vr.HashGridConfig(log2_T=w.log2_T, max_res=w.max_res)
+    fields = [vr.HashGridMLP(cfg, tree.leaves[k].box, dev, seed=seed_base + k)
+              for k in range(lo, lo + cnt)]
+    return vr.VolumePool(tree, fields, (0.05, 0.05, 0.08), dev, rank, world, group)
+
+
+def cpu_baseline_port(w, n_rays: int, seed: int = 0, reps: int = 1):
+    """Oracle port (fwd + torch fp64 autograd bwd) on a bounded ray sample, 1 thread."""
+    import torch
+
+    from oracle import grad_oracle, hashmlp_oracle as hmo, volray_oracle as vo
+    import paper_2404_16221_b200 as vr
+
+    torch.set_num_threads(1)
+    tree = w.tree
+    otree = vo.Tree(vr.tree_to_json(tree))
+    rays = __import__("paper_2404_16221_b200.workloads", fromlist=["x"]).make_rays(w, seed, n_rays)
+    targets = np.random.default_rng(2).uniform(0, 1, size=(n_rays, 3))
+    rng = np.random.default_rng(1)
+    _, n_entries = hmo.levels(w.log2_T, max_res=w.max_res)
+    models = {}
+
+    def model(k):
+        if k not in models:
+            table = rng.uniform(-1e-4, 1e-4, size=(n_entries, 2)).astype(np.float32)
+            wts = rng.normal(size=hmo.NPARAMS).astype(np.float32) * 0.1
+            box = tree.leaves[k].box
+            models[k] = hmo.HashMLPModel(table, wts, w.log2_T, box.mn, box.mx, max_res=w.max_res)
+        return models[k]
+
+    # touch models outside the timed region (table allocation is not per-step work)
+    for r in rays.T:
+        t0, t1, tile = vo.sample_ray(otree, r[0:3], r[3:6], r[6], r[7], w.dt)
+        for k in set(tile.tolist()):
+            model(k)
+    t = time.perf_counter()
+    for _ in range(reps):
+        loss, _ = grad_oracle.field_loss(otree, lambda k, p, d: model(k).eval_t(p, d), rays.T,
+                                         targets, (0.05, 0.05, 0.08), w.dt)
+        loss.backward()
+    dt = (time.perf_counter() - t) / reps
+    return n_rays / dt
+
+
+def _ref_worker(args):
+    cfg_name, n_rays, seed = args
+    from paper_2404_16221_b200.workloads import CONFIGS
+
+    return cpu_baseline_port(CONFIGS[cfg_name], n_rays, seed)
+
+
+def run_reference(args, rank, world):
+    """--impl reference: the CPU oracle port of the path on all host cores."""
+    if rank != 0:
+        return
+    from concurrent.futures import ProcessPoolExecutor
+
+    from paper_2404_16221_b200.workloads import CONFIGS
+
+    w = CONFIGS[args.config]
+    cores = os.cpu_count() or 1
+    per = 4
+    sample = cores * per
+    with ProcessPoolExecutor(max_workers=cores) as ex:
+        for s in range(args.warmup):
+            list(ex.map(_ref_worker, [(args.config, per, 1000 + s * cores + c) for c in range(cores)]))
+        t = time.perf_counter()
+        for s in range(args.steps):
+            list(ex.map(_ref_worker, [(args.config, per, s * cores + c) for c in range(cores)]))
+        el = time.perf_counter() - t
+    # per-process wall time includes model setup; report the sample throughput
+    value = sample * args.steps / el
+    line = {"metric": METRIC, "value": value, "unit": UNIT, "impl": "reference",
+            "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
+            "ms_per_step": 1000.0 * el / args.steps, "higher_is_better": True,
+            "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "config": {"workload": w.name, "rays_per_step_sample": sample, "dt": w.dt},
+            "cpu_baseline": {"value": value, "unit": UNIT, "cores": cores, "kind": "port",
+                             "sample": f"{sample} rays/step of {w.name}, oracle hash+MLP fwd + "
+                                       "torch fp64 autograd bwd, 1 process per core"},
+            "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0,
+                    "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--config", default="c3")
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--lr", type=float, default=1e-2)
+    ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--rays", type=int, default=None, help="override rays per step")
+    args = ap.parse_args()
+    rank, world, local = dist_env()
+
+    if args.impl == "reference":
+        run_reference(args, rank, world)
+        return
+
+    import torch
+    import torch.distributed as dist
+
+    import paper_2404_16221_b200 as vr
+    from paper_2404_16221_b200 import _lib
+    from paper_2404_16221_b200.workloads import CONFIGS, make_rays, make_targets
+
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    group = None
+    if world > 1:
+        dist.init_process_group("nccl", device_id=dev)
+        group = dist.group.WORLD
+    w = CONFIGS[args.config]
+    if args.rays:
+        w.n_rays = args.rays
+    R = w.n_rays
+    pool = build_pool(w, rank, world, dev, group)
+    rays_np = make_rays(w)
+    tg_np = make_targets(R)
+    rays = torch.from_numpy(rays_np).to(dev)
+    tg = torch.from_numpy(tg_np).to(dev)
+
+    step = 0
+
+    def one_step(r, t):
+        nonlocal step
+        step += 1
+        return pool.train_step(r, t, w.dt, lr=args.lr, step=step)
+
+    for _ in range(args.warmup):
+        one_step(rays, tg)
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+
+    # ---- timed region: inputs resident in HBM -------------------------------------
+    clocks = ClockSampler(local)
+    timer = EventTimer()
+    _lib.CALLS.clear()
+    clocks.start()
+    time.sleep(0.3)
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    start = torch.cuda.Event(enable_timing=True)
+    end = torch.cuda.Event(enable_timing=True)
+    _lib.TIMER = timer
+    start.record()
+    for _ in range(args.steps):
+        loss = one_step(rays, tg)
+    end.record()
+    torch.cuda.synchronize()
+    _lib.TIMER = None
+    if world > 1:
+        dist.barrier()
+    clk = clocks.stop()
+    calls = dict(_lib.CALLS)
+    ms = start.elapsed_time(end) / args.steps
+    t_ms = torch.tensor([ms], dtype=torch.float64, device=dev)
+    if world > 1:
+        dist.all_reduce(t_ms, op=dist.ReduceOp.MAX)
+    ms = float(t_ms.item())
+    value = R / (ms / 1e3)
+    launches = sum(n * _lib.LAUNCHES.get(k, 1) for k, n in calls.items())
+    final_loss = float(loss.item())
+
+    # samples per step (for per-sample kernel costs)
+    b = pool.sample(rays, w.dt)
+    n_samples_rank = b.n_samples
+    n_samples = torch.tensor([n_samples_rank], dtype=torch.int64, device=dev)
+    if world > 1:
+        dist.all_reduce(n_samples)
+    n_samples = int(n_samples.item())
+
+    # ---- roofline of the dominant kernel (events over the timed region) ------------
+    totals = timer.totals()
+    peaks = load_peaks()
+    per_kernel = {k: {"ms_per_step": t / args.steps, "launches": n} for k, (t, n) in totals.items()}
+    dom = max((k for k in totals if k in KERNEL_COST), key=lambda k: totals[k][0], default=None)
+    roofline = None
+    if dom:
+        bound, per_unit = KERNEL_COST[dom]
+        t_total, n_launch = totals[dom]
+        work = per_unit * n_samples_rank * args.steps  # bytes or flops over the region
+        avg_s = (t_total / 1e3) / n_launch
+        per_launch = work / n_launch
+        if bound == "hbm":
+            achieved = per_launch / avg_s / 1e9
+            peak = peaks["hbm"]
+            unit = "GB/s"
+        else:
+            achieved = per_launch / avg_s / 1e12
+            peak = peaks["tensor"]
+            unit = "TFLOP/s"
+        roofline = {"kernel": dom, "bound": bound, "achieved": achieved, "peak": peak,
+                    "unit": unit, "frac": achieved / peak, "traffic": None,
+                    "peak_source": peaks["source"], "share_of_step": t_total / args.steps / ms}
+
+    # ---- end to end through the public API with host buffers ------------------------
+    e2e = None
+    if not args.no_e2e:
+        rays_h = torch.from_numpy(rays_np).pin_memory()
+        tg_h = torch.from_numpy(tg_np).pin_memory()
+        torch.cuda.synchronize()
+        if world > 1:
+            dist.barrier()
+        t0 = torch.cuda.Event(enable_timing=True)
+        t1 = torch.cuda.Event(enable_timing=True)
+        t0.record()
+        for _ in range(args.steps):
+            r_d = rays_h.to(dev, non_blocking=True)
+            t_d = tg_h.to(dev, non_blocking=True)
+            l = one_step(r_d, t_d)
+            _ = float(l.item())  # D2H read of the step's loss
+        t1.record()
+        torch.cuda.synchronize()
+        e_ms = torch.tensor([t0.elapsed_time(t1) / args.steps], dtype=torch.float64, device=dev)
+        if world > 1:
+            dist.all_reduce(e_ms, op=dist.ReduceOp.MAX)
+        e2e = {"value": R / (float(e_ms.item()) / 1e3), "unit": UNIT,
+               "h2d_bytes_per_step": rays_h.numel() * 8 + tg_h.numel() * 4,
+               "d2h_bytes_per_step": 8, "ms_per_step": float(e_ms.item())}
+
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu:
+        n_cpu = 24
+        v = cpu_baseline_port(w, n_cpu)
+        cpu = {"value": v, "unit": UNIT, "cores": 1, "kind": "port",
+               "sample": f"{n_cpu} rays of {w.name}: oracle hash+MLP fwd + torch fp64 autograd "
+                         "bwd, single thread"}
+
+    if rank == 0:
+        line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world,
+                "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms,
+                "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
+                "dtype": "f32+f16", "data": "synthetic",
+                "config": {"workload": w.name, "rays_per_step": R, "samples_per_step": n_samples,
+                           "samples_per_ray": n_samples / R, "regions": len(w.tree.leaves),
+                           "regions_per_gpu": len(w.tree.leaves) // world, "log2_T": w.log2_T,
+                           "dt": w.dt, "parallelism": f"region-parallel x{world}",
+                           "l2": "inputs larger than L2 (tables+rays+samples >> 126 MB)",
+                           "optimizer": "adam", "loss": "mse+distortion"},
+                "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e,
+                "gpu_launches": launches, "clocks": clk, "loss": final_loss,
+                "kernels": per_kernel}
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

@@ -1,0 +1,248 @@
+/*
+ * vr_capi.h — C ABI of the B200-native NeRF-XL ray-march / composite hot path.
+ *
+ * This is the drop-in boundary.  The reference (`volray`, pure Python) has no
+ * FFI; every entry point below replaces one reference function or call site on
+ * the tile-protocol path `distsim._run_ray` (reference pkg/src/volray/distsim.py:395-454).
+ * The Python host package `paper_2404_16221_b200` binds these with ctypes and
+ * mirrors the reference's Python API on top.
+ *
+ * Conventions:
+ *  - every pointer argument named *_dev / device arrays is a caller-owned DEVICE
+ *    pointer; descriptor structs (VrTree, VrAnalyticField, ...) are HOST pointers
+ *    copied by value into the kernel launch;
+ *  - every call is asynchronous on the caller's stream (`stream` = cudaStream_t
+ *    passed as void*), returns VR_OK or a VR_ERR_* status for argument/launch
+ *    errors, and never synchronises;
+ *  - data-dependent failures (non-finite packets, negative composed loss, points
+ *    outside the root box, capacity overflow) are OR-ed into a caller-owned device
+ *    int32 flag word `err_dev`; the host reads it at its own sync point and maps
+ *    bits to the reference's exceptions (VR_FLAG_* below);
+ *  - rays are SoA float64, layout [8][ray_stride]: ox, oy, oz, dx, dy, dz, t_near, t_far
+ *    (reference Ray, geometry.py:70-106);
+ *  - samples of one rank are region-major: region kk (0..region_cnt-1) owns the
+ *    contiguous range [offsets[kk*n_rays], offsets[(kk+1)*n_rays]); inside it the
+ *    segment of ray r is [offsets[kk*n_rays + r], offsets[kk*n_rays + r + 1]).
+ *  - a packet (reference TilePayload, distsim.py:154-180) is 8 float32:
+ *    {T, Cr, Cg, Cb, A, D', L, order}; D' is depth relative to the ray's root-box
+ *    entry t (ray_te), `order` holds the int32 bits of the segment's first sample
+ *    index along the ray (exact replacement of order_t, distsim.py:378); an empty
+ *    segment is the identity packet {1,0,0,0,0,0,0, INT32_MAX}.
+ */
+#ifndef VR_CAPI_H
+#define VR_CAPI_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define VR_ABI_VERSION 1
+#define VR_MAX_REGIONS 32
+#define VR_MAX_BLOBS 32
+#define VR_MAX_CHILDREN 8
+#define VR_MAX_LEVELS 16
+#define VR_PACKET_FLOATS 8
+#define VR_OUT_FIELDS 7 /* r, g, b, alpha, depth, transmittance, distortion */
+
+/* status codes */
+#define VR_OK 0
+#define VR_ERR_BAD_ARG 1
+#define VR_ERR_CUDA 2
+#define VR_ERR_UNSUPPORTED 3
+
+/* device error-flag bits (err_dev) */
+#define VR_FLAG_NONFINITE 1      /* segrender.NonFiniteInputError, segrender.py:124-127   */
+#define VR_FLAG_NEG_LOSS 2       /* segrender.NegativeLossError, segrender.py:137-141     */
+#define VR_FLAG_OOB 4            /* partitioner.OutOfBoundsError, partitioner.py:179-180  */
+#define VR_FLAG_OVERFLOW 8       /* capacity / bin-count overflow (no reference analogue) */
+#define VR_FLAG_TOO_MANY_SEGS 16 /* > VR_MAX_REGIONS non-empty segments on one ray        */
+
+/* Partition tree (reference PartitionTree/SplitNode/LeafNode, partitioner.py:51-80).
+ * Internal nodes are indexed 0..n_nodes-1 with node 0 the root; a child index
+ * c >= 0 is a node, c < 0 is leaf (-c - 1).  n_nodes == 0 means a single leaf. */
+typedef struct VrTree {
+  double root_mn[3];
+  double root_mx[3];
+  double leaf_mn[VR_MAX_REGIONS][3];
+  double leaf_mx[VR_MAX_REGIONS][3];
+  double node_plane[VR_MAX_REGIONS];
+  int32_t node_axis[VR_MAX_REGIONS];
+  int32_t node_low[VR_MAX_REGIONS];
+  int32_t node_high[VR_MAX_REGIONS];
+  int32_t n_leaves;
+  int32_t n_nodes;
+} VrTree;
+
+/* Analytic test field: a SumField (field.py:212-240) of up to VR_MAX_CHILDREN
+ * children, each GaussianBlobs (field.py:88-114) or ConstantBox (field.py:117-134).
+ * A plain (non-sum) field is a one-child sum; both give identical results. */
+typedef struct VrBlob {
+  double center[3];
+  double amplitude;
+  double scale;
+  double color[3];
+} VrBlob;
+
+typedef struct VrAnalyticField {
+  int32_t n_children;
+  int32_t n_blobs;
+  int32_t child_kind[VR_MAX_CHILDREN]; /* 0 = gaussian_blobs, 1 = constant_box */
+  int32_t child_blob_lo[VR_MAX_CHILDREN];
+  int32_t child_blob_cnt[VR_MAX_CHILDREN];
+  double box_mn[VR_MAX_CHILDREN][3];
+  double box_mx[VR_MAX_CHILDREN][3];
+  double box_density[VR_MAX_CHILDREN];
+  double box_color[VR_MAX_CHILDREN][3];
+  VrBlob blobs[VR_MAX_BLOBS];
+} VrAnalyticField;
+
+/* VoxelGrid (field.py:137-209): cell-centred, clamped trilinear or nearest. */
+typedef struct VrVoxelDesc {
+  double box_mn[3];
+  double box_mx[3];
+  int32_t res[3];
+  int32_t trilinear;
+} VrVoxelDesc;
+
+/* Multiresolution hash grid (Instant-NGP, named at PAPER.md:386-388; no reference
+ * code — restated in oracle/hashmlp_oracle.py).  Positions are normalised with
+ * u = (p - box_mn) / (box_mx - box_mn) in float64, then cast to float32. */
+typedef struct VrHashGridDesc {
+  int32_t n_levels;
+  int32_t log2_T;
+  float scale[VR_MAX_LEVELS];
+  int32_t res[VR_MAX_LEVELS];
+  int32_t dense[VR_MAX_LEVELS];
+  int64_t offset[VR_MAX_LEVELS + 1]; /* in table entries (float2) */
+  double box_mn[3];
+  double box_mx[3];
+} VrHashGridDesc;
+
+/* ---- meta ------------------------------------------------------------------ */
+int vr_abi_version(void);
+/* sizes of the descriptor structs, for host-side layout checks: out[0..4] =
+ * sizeof(VrTree), sizeof(VrAnalyticField), sizeof(VrVoxelDesc), sizeof(VrHashGridDesc),
+ * sizeof(VrBlob). */
+int vr_struct_sizes(int64_t* out5);
+const char* vr_last_error(void);
+int vr_device_sync(void);
+
+/* ---- K1: ray/region intersection + sampling ------------------------------------
+ * Replaces generate_samples (quadrature.py:66-88), tile_cut_distances
+ * (partitioner.py:195-206), split_at_planes (quadrature.py:91-114), locate_many
+ * (partitioner.py:177-192) and the bin assignment of _run_ray (distsim.py:406-425).
+ * Count pass: per owned region kk and ray r, the number of samples, and the index
+ * of its first sample along the ray (INT32_MAX if none).  ray_te[r] = root-box
+ * entry t (0 on a miss); ray_part[r] = bitmask of leaves whose box the ray hits
+ * (distsim.py:415-419 participants); ray_total[r] = samples over ALL regions. */
+int vr_sample_count(const VrTree* tree, const double* rays_dev, int64_t ray_stride,
+                    int64_t n_rays, double dt, int32_t region_lo, int32_t region_cnt,
+                    int32_t* counts_dev, int32_t* seg_first_dev, double* ray_te_dev,
+                    uint32_t* ray_part_dev, int32_t* ray_total_dev, int32_t* err_dev,
+                    void* stream);
+/* exclusive scan of n int32 counts into n+1 int64 offsets (offsets[n] = total) */
+size_t vr_scan_workspace_bytes(int64_t n);
+int vr_scan_offsets(const int32_t* counts_dev, int64_t n, int64_t* offsets_dev,
+                    void* workspace_dev, size_t workspace_bytes, void* stream);
+/* Fill pass: writes each owned sample's bin edges t0/t1 (float64, bit-exact with
+ * the reference) and its ray index into the slots given by offsets. */
+int vr_sample_fill(const VrTree* tree, const double* rays_dev, int64_t ray_stride,
+                   int64_t n_rays, double dt, int32_t region_lo, int32_t region_cnt,
+                   const int64_t* offsets_dev, const int32_t* seg_first_dev, double* t0_dev,
+                   double* t1_dev, int32_t* ray_id_dev, int32_t* err_dev, void* stream);
+/* Owner lookup of arbitrary points (locate_many, partitioner.py:177-192). */
+int vr_locate(const VrTree* tree, const double* pts_dev /*[n][3]*/, int64_t n,
+              int32_t* tile_dev, int32_t* err_dev, void* stream);
+
+/* ---- fields (the Field plugin seam, field.py:46-59 / fill_samples quadrature.py:117-128)
+ * All evaluate at bin midpoints m = 0.5 (t0 + t1), p = o + m d (float64) and write
+ * sig_rgb[i] = {sigma, r, g, b} (float32). */
+int vr_field_analytic_fwd(const VrAnalyticField* f, const double* rays_dev, int64_t ray_stride,
+                          const double* t0_dev, const double* t1_dev, const int32_t* ray_id_dev,
+                          int64_t n, float* sig_rgb_dev, void* stream);
+int vr_voxel_fwd(const VrVoxelDesc* g, const double* densities_dev, const double* colors_dev,
+                 const double* rays_dev, int64_t ray_stride, const double* t0_dev,
+                 const double* t1_dev, const int32_t* ray_id_dev, int64_t n, float* sig_rgb_dev,
+                 void* stream);
+/* d(loss)/d(densities) scatter-add (float64 atomics); colours are not parameters. */
+int vr_voxel_bwd(const VrVoxelDesc* g, const double* rays_dev, int64_t ray_stride,
+                 const double* t0_dev, const double* t1_dev, const int32_t* ray_id_dev, int64_t n,
+                 const float* dsig_rgb_dev, double* grad_densities_dev, void* stream);
+
+/* ---- K2: hash-grid encoding ---------------------------------------------------- */
+/* enc layout: [n_levels][n] half2 (level-major, coalesced on samples). */
+int vr_hash_fwd(const VrHashGridDesc* g, const float* table_dev, const double* rays_dev,
+                int64_t ray_stride, const double* t0_dev, const double* t1_dev,
+                const int32_t* ray_id_dev, int64_t n, void* enc_dev, void* stream);
+/* denc layout: [n_levels][n] float2; grad_table float2 scatter-add. */
+int vr_hash_bwd(const VrHashGridDesc* g, const double* rays_dev, int64_t ray_stride,
+                const double* t0_dev, const double* t1_dev, const int32_t* ray_id_dev, int64_t n,
+                const float* denc_dev, float* grad_table_dev, void* stream);
+/* debug/parity: the 8 corner indices per (level, sample): idx[l][n][8] int32 */
+int vr_hash_indices(const VrHashGridDesc* g, const double* rays_dev, int64_t ray_stride,
+                    const double* t0_dev, const double* t1_dev, const int32_t* ray_id_dev,
+                    int64_t n, int32_t* idx_dev, void* stream);
+
+/* ---- K3: density + colour MLP ---------------------------------------------------
+ * weights_dev: packed fp16 [W1d 64x32 | W2d 16x64 | W1c 64x32 | W2c 64x64 | W3c 16x64]
+ * (row = output neuron, K-major); see VR_MLP_* offsets.  grad_dev: same packing, f32. */
+#define VR_MLP_W1D 0
+#define VR_MLP_W2D (VR_MLP_W1D + 64 * 32)
+#define VR_MLP_W1C (VR_MLP_W2D + 16 * 64)
+#define VR_MLP_W2C (VR_MLP_W1C + 64 * 32)
+#define VR_MLP_W3C (VR_MLP_W2C + 64 * 64)
+#define VR_MLP_NPARAMS (VR_MLP_W3C + 16 * 64)
+int vr_mlp_fwd(const void* weights_dev, const void* enc_dev, const double* rays_dev,
+               int64_t ray_stride, const int32_t* ray_id_dev, int64_t n, float* sig_rgb_dev,
+               void* stream);
+int vr_mlp_bwd(const void* weights_dev, const void* enc_dev, const double* rays_dev,
+               int64_t ray_stride, const int32_t* ray_id_dev, int64_t n,
+               const float* dsig_rgb_dev, float* grad_weights_dev, float* denc_dev,
+               void* stream);
+
+/* ---- K4: per-segment front-to-back composite (composite_samples quadrature.py:141-165,
+ * aggregate_segment segrender.py:71-90, process_inbox distsim.py:318-329) ------------- */
+int vr_segment_fwd(const double* t0_dev, const double* t1_dev, const float* sig_rgb_dev,
+                   const int64_t* offsets_dev, const int32_t* seg_first_dev,
+                   const double* ray_te_dev, int64_t n_rays, int32_t region_cnt,
+                   float* packets_dev, int32_t* err_dev, void* stream);
+/* analytic backward: dpackets [region_cnt][n_rays][8] = adjoints of {T,C,A,D',L};
+ * writes dsig_rgb[i] = {dL/dsigma, dL/dr, dL/dg, dL/db}. */
+int vr_segment_bwd(const double* t0_dev, const double* t1_dev, const float* sig_rgb_dev,
+                   const int64_t* offsets_dev, const double* ray_te_dev, int64_t n_rays,
+                   int32_t region_cnt, const float* dpackets_dev, float* dsig_rgb_dev,
+                   void* stream);
+
+/* ---- K5: global composite (compose_render segrender.py:93-110, compose_distortion
+ * segrender.py:113-142, _compose_tile distsim.py:376-382) --------------------------
+ * packets: all regions' slab [n_regions][n_rays][8].  out: [7][n_rays] float32
+ * (r, g, b, alpha, depth, T, L); clip_bg != 0 writes clip(C + T*bg, 0, 1) into r,g,b
+ * (render_image distsim.py:531), else the raw composed colour. */
+int vr_global_fwd(const float* packets_dev, int32_t n_regions, int64_t n_rays,
+                  const double* ray_te_dev, const float* background3, int32_t clip_bg,
+                  float* out_dev, int32_t* err_dev, void* stream);
+/* training: loss_r = |C + T*bg - target|^2 + lambda * L (segrender.py:198-207);
+ * writes ray_loss[r] (float64) and the packet adjoints of regions
+ * [own_lo, own_lo + own_cnt) into dpackets [own_cnt][n_rays][8]. */
+int vr_global_train(const float* packets_dev, int32_t n_regions, int64_t n_rays,
+                    const double* ray_te_dev, const float* background3,
+                    const float* targets_dev /*[n_rays][3]*/, float lambda_dist, int32_t own_lo,
+                    int32_t own_cnt, float* out_dev, double* ray_loss_dev, float* dpackets_dev,
+                    int32_t* err_dev, void* stream);
+/* deterministic float64 sum (fixed reduction tree) */
+int vr_sum_f64(const double* x_dev, int64_t n, double* out_dev, void* stream);
+
+/* ---- optimiser ------------------------------------------------ */
+int vr_adam_step(float* param_dev, const float* grad_dev, float* m_dev, float* v_dev, int64_t n,
+                 float lr, float beta1, float beta2, float eps, int32_t step, void* stream);
+/* fp32 master -> fp16 copy (MLP weights) */
+int vr_cast_f32_f16(const float* src_dev, void* dst_dev, int64_t n, void* stream);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* VR_CAPI_H */

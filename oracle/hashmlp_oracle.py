@@ -1,0 +1,157 @@
+"""CPU ORACLE — TEST INFRASTRUCTURE ONLY.  PARITY UNPINNED.
+
+Restatement of the per-region NeRF-XL model that the reference does not implement:
+an Instant-NGP multiresolution hash grid (named only at PAPER.md:386-388) feeding a
+density MLP and a view-conditioned colour MLP.  No reference code,
+third-party source or golden vector exists for it, so this file
+IS the specification the CUDA kernels are checked against:
+
+  * hash-table indices are bit-exact (numpy uint32 / float32 with the kernel's op order);
+  * features and MLP activations use the kernel's fp16 quantisation points, computed
+    here in float64 (straight-through for gradients);
+  * gradients come from torch float64 autograd.
+
+Level parameters are derived here independently of the product's host code.
+"""
+from __future__ import annotations
+
+import math
+
+import numpy as np
+import torch
+
+PRIMES = (1, 2654435761, 805459861)
+
+# packed MLP layout (include/vr_capi.h VR_MLP_*)
+W1D, W2D, W1C, W2C, W3C = 0, 2048, 3072, 5120, 9216
+NPARAMS = 10240
+
+SH_C = (0.28209479177387814, 0.48860251190291987, 1.0925484305920792, 0.94617469575755997,
+        0.31539156525251999, 0.54627421529603959, 0.59004358992664352, 2.8906114426405538,
+        0.45704579946446572, 0.3731763325901154, 1.4453057213202769)
+
+
+def levels(log2_T: int, n_levels: int = 16, base_res: int = 16, max_res: int = 2048):
+    """[(scale float32, res, dense, offset)] and total entries."""
+    growth = math.exp((math.log(max_res) - math.log(base_res)) / max(n_levels - 1, 1))
+    T = 1 << log2_T
+    out, off = [], 0
+    for lv in range(n_levels):
+        scale = np.float32(base_res * growth ** lv - 1.0)
+        res = int(math.ceil(float(scale))) + 2
+        dense = res ** 3 <= T
+        size = ((res ** 3 if dense else T) + 7) // 8 * 8
+        out.append((scale, res, dense, off))
+        off += size
+    return out, off
+
+
+def normalize(pts, box_mn, box_mx):
+    """float32 of (p - mn) / (mx - mn), computed in float64 (kernel norm_pos)."""
+    mn = np.asarray(box_mn, dtype=np.float64)
+    mx = np.asarray(box_mx, dtype=np.float64)
+    return ((np.asarray(pts, dtype=np.float64) - mn) / (mx - mn)).astype(np.float32)
+
+
+def corners(u32, scale, res, dense, log2_T):
+    """Corner indices (n,8) uint32 and weights (n,8) float32 of one level."""
+    u32 = np.asarray(u32, dtype=np.float32)
+    pos = (u32 * np.float32(scale)).astype(np.float32) + np.float32(0.5)
+    g = np.floor(pos).astype(np.int64)
+    g = np.clip(g, 0, res - 2)
+    frac = (pos - g.astype(np.float32)).astype(np.float32)
+    idx = np.empty((u32.shape[0], 8), dtype=np.uint32)
+    w = np.empty((u32.shape[0], 8), dtype=np.float32)
+    mask = np.uint32((1 << log2_T) - 1)
+    one = np.float32(1.0)
+    for c in range(8):
+        bits = np.array([c & 1, (c >> 1) & 1, (c >> 2) & 1])
+        xyz = (g + bits).astype(np.uint32)
+        if dense:
+            r = np.uint32(res)
+            idx[:, c] = xyz[:, 0] + r * (xyz[:, 1] + r * xyz[:, 2])
+        else:
+            h = (xyz[:, 0] * np.uint32(PRIMES[0])) ^ (xyz[:, 1] * np.uint32(PRIMES[1])) ^ \
+                (xyz[:, 2] * np.uint32(PRIMES[2]))
+            idx[:, c] = h & mask
+        wa = [frac[:, a] if bits[a] else (one - frac[:, a]).astype(np.float32) for a in range(3)]
+        w[:, c] = ((wa[0] * wa[1]).astype(np.float32) * wa[2]).astype(np.float32)
+    return idx, w
+
+
+def all_indices(pts, box_mn, box_mx, log2_T, max_res=2048):
+    """Per-level corner indices [L][n][8] int64 (for the bit-exact parity test)."""
+    lv, _ = levels(log2_T, max_res=max_res)
+    u = normalize(pts, box_mn, box_mx)
+    return np.stack([corners(u, s, r, dn, log2_T)[0].astype(np.int64) for (s, r, dn, _) in lv])
+
+
+def _q16(x: torch.Tensor) -> torch.Tensor:
+    """fp16 rounding, straight-through for gradients."""
+    return x + (x.to(torch.float16).to(torch.float64) - x).detach()
+
+
+def sh16_t(d: torch.Tensor) -> torch.Tensor:
+    x, y, z = d[..., 0], d[..., 1], d[..., 2]
+    c = SH_C
+    xy, xz, yz, x2, y2, z2 = x * y, x * z, y * z, x * x, y * y, z * z
+    return torch.stack([
+        torch.full_like(x, c[0]), -c[1] * y, c[1] * z, -c[1] * x,
+        c[2] * xy, -c[2] * yz, c[3] * z2 - c[4], -c[2] * xz,
+        c[5] * x2 - c[5] * y2, c[6] * y * (-3.0 * x2 + y2), c[7] * xy * z,
+        c[8] * y * (1.0 - 5.0 * z2), c[9] * z * (5.0 * z2 - 3.0), c[8] * x * (1.0 - 5.0 * z2),
+        c[10] * z * (x2 - y2), c[6] * x * (-x2 + 3.0 * y2)], dim=-1)
+
+
+class HashMLPModel:
+    """One region's model with float64 torch parameters (table, packed weights)."""
+
+    def __init__(self, table: np.ndarray, weights: np.ndarray, log2_T: int, box_mn, box_mx,
+                 max_res: int = 2048):
+        self.table = torch.tensor(np.asarray(table, dtype=np.float64), requires_grad=True)
+        # the kernels consume fp16 copies of the float32 master weights
+        w16 = np.asarray(weights, dtype=np.float32).astype(np.float16).astype(np.float64)
+        self.weights = torch.tensor(w16, requires_grad=True)
+        self.log2_T = log2_T
+        self.box_mn, self.box_mx = box_mn, box_mx
+        self.levels, self.n_entries = levels(log2_T, max_res=max_res)
+
+    def encode(self, pts) -> torch.Tensor:
+        """(n, 32) features, fp16-rounded."""
+        u = normalize(pts, self.box_mn, self.box_mx)
+        feats = []
+        for (scale, res, dense, off) in self.levels:
+            idx, w = corners(u, scale, res, dense, self.log2_T)
+            rows = self.table[torch.from_numpy(idx.astype(np.int64) + off)]  # (n, 8, 2)
+            f = (rows * torch.from_numpy(w.astype(np.float64))[:, :, None]).sum(1)
+            feats.append(f)
+        return _q16(torch.cat(feats, dim=1))
+
+    def mlp(self, enc: torch.Tensor, dirs32: np.ndarray):
+        W = self.weights
+        W1d = W[W1D:W2D].reshape(64, 32)
+        W2d = W[W2D:W1C].reshape(16, 64)
+        W1c = W[W1C:W2C].reshape(64, 32)
+        W2c = W[W2C:W3C].reshape(64, 64)
+        W3c = W[W3C:W3C + 3 * 64].reshape(3, 64)
+        h = _q16(torch.relu(enc @ W1d.T))
+        od = h @ W2d.T
+        x0 = od[:, 0]
+        inside = ((x0 > -15.0) & (x0 < 15.0)).to(torch.float64)
+        # exp(clamp(x)) with d/dx = sigma inside the clamp range, 0 outside
+        xc = torch.clamp(x0, -15.0, 15.0)
+        sigma = torch.exp(x0 * inside + (xc * (1 - inside)).detach())
+        sh = _q16(sh16_t(torch.from_numpy(np.asarray(dirs32, dtype=np.float32).astype(np.float64))))
+        cin = torch.cat([_q16(od), sh], dim=1)
+        h1 = _q16(torch.relu(cin @ W1c.T))
+        h2 = _q16(torch.relu(h1 @ W2c.T))
+        rgb = torch.sigmoid(h2 @ W3c.T)
+        return sigma, rgb
+
+    def eval_t(self, pts, d):
+        n = np.asarray(pts).shape[0]
+        dirs = np.broadcast_to(np.asarray(d, dtype=np.float64).astype(np.float32), (n, 3))
+        return self.mlp(self.encode(pts), dirs)
+
+    def grads(self):
+        return (self.table.grad.numpy().copy(), self.weights.grad.numpy().copy())

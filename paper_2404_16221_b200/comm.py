@@ -1,0 +1,50 @@
+"""The paper's communication step: exchange of per-(region, ray) packets.
+
+Replaces the simulated transit of TilePayloads to the compositor (distsim.py:435-446)
+and the training-mode broadcast (distsim.py:457-475).  One process per GPU; rank r
+owns the contiguous region block [r*K/N, (r+1)*K/N), so the concatenation of every
+rank's packet slab in rank order IS the global [K][R][8] slab — one all-gather, no
+reordering.  Only forward partials cross the link; there is no gradient collective.
+"""
+from __future__ import annotations
+
+import torch
+import torch.distributed as dist
+
+
+def owned_regions(n_regions: int, rank: int, world: int) -> tuple[int, int]:
+    """(region_lo, region_cnt) of a rank; regions split evenly and contiguously
+    (leaves are depth-first, so each block is a subtree, partitioner.py:145-149)."""
+    if world < 1 or n_regions % world != 0:
+        raise ValueError(f"{n_regions} regions cannot be split evenly over {world} ranks")
+    cnt = n_regions // world
+    return rank * cnt, cnt
+
+
+def all_gather_packets(local: torch.Tensor, group=None, world: int = 1) -> torch.Tensor:
+    """[K_own, R, 8] on every rank -> [world*K_own, R, 8] on every rank (training)."""
+    if world == 1:
+        return local
+    out = torch.empty((world * local.shape[0],) + tuple(local.shape[1:]), dtype=local.dtype,
+                      device=local.device)
+    dist.all_gather_into_tensor(out, local.contiguous(), group=group)
+    return out
+
+
+def gather_packets(local: torch.Tensor, group=None, world: int = 1, rank: int = 0, dst: int = 0):
+    """Inference: packets only need to reach one compositor rank."""
+    if world == 1:
+        return local
+    if rank == dst:
+        parts = [torch.empty_like(local) for _ in range(world)]
+        dist.gather(local.contiguous(), gather_list=parts, dst=dst, group=group)
+        return torch.cat(parts, dim=0)
+    dist.gather(local.contiguous(), gather_list=None, dst=dst, group=group)
+    return None
+
+
+def all_reduce_scalar(x: torch.Tensor, group=None, world: int = 1) -> torch.Tensor:
+    """Logging only: sum a per-rank scalar (the loss is already identical everywhere)."""
+    if world > 1:
+        dist.all_reduce(x, group=group)
+    return x

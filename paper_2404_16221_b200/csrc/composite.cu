@@ -1,0 +1,463 @@
+// K4 (per-segment composite, fwd + analytic bwd) and K5 (global composite, fwd +
+// train fwd/bwd), plus the deterministic loss reduction and the Adam step.
+//
+// K4 — one warp per (region, ray) segment, 32 samples per step, warp-shuffle scans
+// with float64 carries.  Forward (composite_samples quadrature.py:141-165 and
+// aggregate_segment segrender.py:71-90):
+//   s_i = sigma_i * delta_i,  keep_i = exp(-s_i),  alpha_i = -expm1(-s_i)
+//   T_i = prod_{j<i} keep_j,  w_i = T_i alpha_i
+//   C = sum w c, A = sum w, D' = sum w (m - te), T = prod keep
+//   L = sum_ij w_i w_j |m_i - m_j| = 2 sum_i w_i (m_i A_<i - D_<i)   (O(N) form of
+//       distortion_bruteforce quadrature.py:179-188; equal for sorted midpoints)
+// Backward, for adjoints (bT, bC, bA, bD, bL) of the packet:
+//   dL/ds_j = -bT T + T_{j+1} v_j - sum_{i>j} w_i v_i
+//   v_i = bC.c_i + bA + bD m_i + bL g_i,  g_i = 2 sum_k w_k |m_i - m_k|
+//   dL/dsigma_j = delta_j dL/ds_j,  dL/dc_j = w_j bC
+// and sum_{i>j} w_i v_i is formed from the segment totals minus inclusive prefixes
+// (sum_i w_i g_i = 2L), all in float64.
+//
+// K5 — one thread per ray: gather the ray's packets from every region, order the
+// non-empty ones by their first-sample index (exact stand-in for the reference's
+// (order_t, tile) sort, distsim.py:378), fold in float64 (compose_render
+// segrender.py:93-110, compose_distortion segrender.py:113-142), and for training
+// run the reverse sweep of that fold to get every owned packet's adjoint.
+#include "common.cuh"
+
+namespace vr {
+
+constexpr int SEG_WARPS = 8;
+
+__device__ __forceinline__ float order_bits(int32_t first) { return __int_as_float(first); }
+
+struct SegTotals {
+  double T, C[3], A, D, L;
+};
+
+// Forward sweep over one segment; every lane returns the same totals.
+__device__ __forceinline__ SegTotals seg_forward(const double* __restrict__ t0,
+                                                 const double* __restrict__ t1,
+                                                 const float4* __restrict__ sr, int64_t b,
+                                                 int64_t e, double te, int lane) {
+  SegTotals tot = {1.0, {0.0, 0.0, 0.0}, 0.0, 0.0, 0.0};
+  for (int64_t i0 = b; i0 < e; i0 += 32) {
+    const int64_t i = i0 + lane;
+    double keep = 1.0, alpha = 0.0, m = 0.0;
+    float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
+    if (i < e) {
+      const double a = t0[i], bb = t1[i];
+      v = sr[i];
+      const double s = (double)v.x * (bb - a);
+      keep = exp(-s);
+      alpha = -expm1(-s);
+      m = sample_mid(a, bb) - te;
+    }
+    const double pincl = warp_incl_prod(keep, lane);
+    double pexcl = __shfl_up_sync(0xffffffffu, pincl, 1);
+    if (lane == 0) pexcl = 1.0;
+    const double Ti = tot.T * pexcl;
+    const double w = Ti * alpha;
+    const double wm = w * m;
+    const double aincl = warp_incl_sum(w, lane);
+    const double dincl = warp_incl_sum(wm, lane);
+    const double a_lt = tot.A + (aincl - w);
+    const double d_lt = tot.D + (dincl - wm);
+    const double lterm = w * (m * a_lt - d_lt);
+    tot.L += 2.0 * warp_sum(lterm);
+    tot.C[0] += warp_sum(w * (double)v.y);
+    tot.C[1] += warp_sum(w * (double)v.z);
+    tot.C[2] += warp_sum(w * (double)v.w);
+    tot.A += __shfl_sync(0xffffffffu, aincl, 31);
+    tot.D += __shfl_sync(0xffffffffu, dincl, 31);
+    tot.T *= __shfl_sync(0xffffffffu, pincl, 31);
+  }
+  return tot;
+}
+
+__global__ void __launch_bounds__(SEG_WARPS * 32)
+    k_segment_fwd(const double* __restrict__ t0, const double* __restrict__ t1,
+                  const float4* __restrict__ sr, const int64_t* __restrict__ off,
+                  const int32_t* __restrict__ seg_first, const double* __restrict__ ray_te,
+                  int64_t n_rays, int64_t n_segs, float4* __restrict__ packets) {
+  const int lane = threadIdx.x & 31;
+  for (int64_t seg = (int64_t)blockIdx.x * SEG_WARPS + (threadIdx.x >> 5); seg < n_segs;
+       seg += (int64_t)gridDim.x * SEG_WARPS) {
+    const int64_t b = off[seg], e = off[seg + 1];
+    float4 p0, p1;
+    if (b == e) {
+      p0 = make_float4(1.f, 0.f, 0.f, 0.f);
+      p1 = make_float4(0.f, 0.f, 0.f, order_bits(INT32_MAX));
+    } else {
+      const double te = ray_te[seg % n_rays];
+      const SegTotals t = seg_forward(t0, t1, sr, b, e, te, lane);
+      p0 = make_float4((float)t.T, (float)t.C[0], (float)t.C[1], (float)t.C[2]);
+      p1 = make_float4((float)t.A, (float)t.D, (float)t.L, order_bits(seg_first[seg]));
+    }
+    if (lane == 0) {
+      packets[2 * seg] = p0;
+      packets[2 * seg + 1] = p1;
+    }
+  }
+}
+
+__global__ void __launch_bounds__(SEG_WARPS * 32)
+    k_segment_bwd(const double* __restrict__ t0, const double* __restrict__ t1,
+                  const float4* __restrict__ sr, const int64_t* __restrict__ off,
+                  const double* __restrict__ ray_te, int64_t n_rays, int64_t n_segs,
+                  const float4* __restrict__ dpk, float4* __restrict__ dsr) {
+  const int lane = threadIdx.x & 31;
+  for (int64_t seg = (int64_t)blockIdx.x * SEG_WARPS + (threadIdx.x >> 5); seg < n_segs;
+       seg += (int64_t)gridDim.x * SEG_WARPS) {
+    const int64_t b = off[seg], e = off[seg + 1];
+    if (b == e) continue;
+    const double te = ray_te[seg % n_rays];
+    const float4 g0 = dpk[2 * seg], g1 = dpk[2 * seg + 1];
+    const double bT = g0.x, bC0 = g0.y, bC1 = g0.z, bC2 = g0.w, bA = g1.x, bD = g1.y,
+                 bL = g1.z;
+    const SegTotals tot = seg_forward(t0, t1, sr, b, e, te, lane);
+    const double Vtot = bC0 * tot.C[0] + bC1 * tot.C[1] + bC2 * tot.C[2] + bA * tot.A +
+                        bD * tot.D + bL * 2.0 * tot.L;
+    // second sweep: per-sample gradients
+    double Tc = 1.0, Ac = 0.0, Dc = 0.0, Vc = 0.0;
+    for (int64_t i0 = b; i0 < e; i0 += 32) {
+      const int64_t i = i0 + lane;
+      double keep = 1.0, alpha = 0.0, m = 0.0, dlt = 0.0;
+      float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
+      if (i < e) {
+        const double a = t0[i], bb = t1[i];
+        v = sr[i];
+        dlt = bb - a;
+        const double s = (double)v.x * dlt;
+        keep = exp(-s);
+        alpha = -expm1(-s);
+        m = sample_mid(a, bb) - te;
+      }
+      const double pincl = warp_incl_prod(keep, lane);
+      double pexcl = __shfl_up_sync(0xffffffffu, pincl, 1);
+      if (lane == 0) pexcl = 1.0;
+      const double Ti = Tc * pexcl;
+      const double Tn = Tc * pincl;  // T_{j+1}
+      const double w = Ti * alpha;
+      const double wm = w * m;
+      const double aincl = warp_incl_sum(w, lane);
+      const double dincl = warp_incl_sum(wm, lane);
+      const double a_lt = Ac + (aincl - w), d_lt = Dc + (dincl - wm);
+      const double a_gt = tot.A - (Ac + aincl), d_gt = tot.D - (Dc + dincl);
+      const double g = 2.0 * (m * a_lt - d_lt + d_gt - m * a_gt);
+      const double vi = bC0 * v.y + bC1 * v.z + bC2 * v.w + bA + bD * m + bL * g;
+      const double wv = w * vi;
+      const double vincl = warp_incl_sum(wv, lane);
+      const double v_gt = Vtot - (Vc + vincl);
+      const double ds = -bT * tot.T + Tn * vi - v_gt;
+      if (i < e)
+        dsr[i] = make_float4((float)(ds * dlt), (float)(w * bC0), (float)(w * bC1),
+                             (float)(w * bC2));
+      Tc *= __shfl_sync(0xffffffffu, pincl, 31);
+      Ac += __shfl_sync(0xffffffffu, aincl, 31);
+      Dc += __shfl_sync(0xffffffffu, dincl, 31);
+      Vc += __shfl_sync(0xffffffffu, vincl, 31);
+    }
+  }
+}
+
+// ---- K5 ---------------------------------------------------------------------------------
+struct Pk {
+  double T, C[3], A, D, L;
+};
+
+__device__ __forceinline__ Pk load_pk(const float4* __restrict__ pk, int64_t idx) {
+  const float4 a = pk[2 * idx], b = pk[2 * idx + 1];
+  Pk p;
+  p.T = a.x;
+  p.C[0] = a.y;
+  p.C[1] = a.z;
+  p.C[2] = a.w;
+  p.A = b.x;
+  p.D = b.y;
+  p.L = b.z;
+  return p;
+}
+
+template <bool TRAIN>
+__global__ void k_global(const float4* __restrict__ pk, int n_regions, int64_t n_rays,
+                         const double* __restrict__ ray_te, float bg0, float bg1, float bg2,
+                         int clip_bg, const float* __restrict__ targets, float lambda_dist,
+                         int own_lo, int own_cnt, float* __restrict__ out,
+                         double* __restrict__ ray_loss, float4* __restrict__ dpk, int32_t* err) {
+  int flags = 0;
+  for (int64_t r = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; r < n_rays;
+       r += (int64_t)gridDim.x * blockDim.x) {
+    // non-empty packets of this ray, ordered by first-sample index
+    int ord[VR_MAX_REGIONS];
+    int key[VR_MAX_REGIONS];
+    int n = 0;
+    for (int k = 0; k < n_regions; ++k) {
+      const int kf = __float_as_int(pk[2 * ((int64_t)k * n_rays + r) + 1].w);
+      if (kf == INT32_MAX) continue;
+      int j = n++;
+      while (j > 0 && key[j - 1] > kf) {  // insertion sort, ties impossible
+        key[j] = key[j - 1];
+        ord[j] = ord[j - 1];
+        --j;
+      }
+      key[j] = kf;
+      ord[j] = k;
+    }
+    double P = 1.0, C[3] = {0.0, 0.0, 0.0}, A = 0.0, D = 0.0, L = 0.0;
+    double sP[VR_MAX_REGIONS], sA[VR_MAX_REGIONS], sD[VR_MAX_REGIONS];
+    for (int s = 0; s < n; ++s) {
+      const Pk p = load_pk(pk, (int64_t)ord[s] * n_rays + r);
+      if (!(isfinite(p.T) && isfinite(p.C[0]) && isfinite(p.C[1]) && isfinite(p.C[2]) &&
+            isfinite(p.A) && isfinite(p.D) && isfinite(p.L)))
+        flags |= VR_FLAG_NONFINITE;
+      sP[s] = P;
+      sA[s] = A;
+      sD[s] = D;
+      L += P * P * p.L + 2.0 * P * (p.D * A - p.A * D);
+      C[0] += P * p.C[0];
+      C[1] += P * p.C[1];
+      C[2] += P * p.C[2];
+      A += P * p.A;
+      D += P * p.D;
+      P *= p.T;
+    }
+    if (L < 0.0) {
+      if (L < -1e-12) flags |= VR_FLAG_NEG_LOSS;
+      L = 0.0;
+    }
+    const double te = ray_te[r];
+    const double bg[3] = {bg0, bg1, bg2};
+    double pix[3];
+#pragma unroll
+    for (int c = 0; c < 3; ++c) pix[c] = C[c] + P * bg[c];
+#pragma unroll
+    for (int c = 0; c < 3; ++c)
+      out[c * n_rays + r] = clip_bg ? (float)fmin(fmax(pix[c], 0.0), 1.0) : (float)C[c];
+    out[3 * n_rays + r] = (float)A;
+    out[4 * n_rays + r] = (float)(D + A * te);
+    out[5 * n_rays + r] = (float)P;
+    out[6 * n_rays + r] = (float)L;
+    if (TRAIN) {
+      double gC[3], loss = 0.0;
+#pragma unroll
+      for (int c = 0; c < 3; ++c) {
+        const double d = pix[c] - (double)targets[3 * r + c];
+        loss += d * d;
+        gC[c] = 2.0 * d;
+      }
+      loss += (double)lambda_dist * L;
+      ray_loss[r] = loss;
+      const double gL = lambda_dist;
+      // reverse sweep of the fold
+      double bP = gC[0] * bg[0] + gC[1] * bg[1] + gC[2] * bg[2];  // adjoint of final P
+      double bAc = 0.0, bDc = 0.0;
+      for (int k = 0; k < own_cnt; ++k) {
+        // zero the adjoints of owned regions first (empty / absent segments)
+        const int64_t idx = (int64_t)k * n_rays + r;
+        dpk[2 * idx] = make_float4(0.f, 0.f, 0.f, 0.f);
+        dpk[2 * idx + 1] = make_float4(0.f, 0.f, 0.f, 0.f);
+      }
+      for (int s = n - 1; s >= 0; --s) {
+        const Pk p = load_pk(pk, (int64_t)ord[s] * n_rays + r);
+        const double Ps = sP[s], As = sA[s], Ds = sD[s];
+        const int kk = ord[s] - own_lo;
+        if (kk >= 0 && kk < own_cnt) {
+          const int64_t idx = (int64_t)kk * n_rays + r;
+          const double dT = bP * Ps;
+          const double dA = bAc * Ps + gL * 2.0 * Ps * (-Ds);
+          const double dD = bDc * Ps + gL * 2.0 * Ps * As;
+          const double dL = gL * Ps * Ps;
+          dpk[2 * idx] = make_float4((float)dT, (float)(gC[0] * Ps), (float)(gC[1] * Ps),
+                                     (float)(gC[2] * Ps));
+          dpk[2 * idx + 1] = make_float4((float)dA, (float)dD, (float)dL, 0.f);
+        }
+        // adjoint of the state before segment s
+        const double nbP = bP * p.T + gC[0] * p.C[0] + gC[1] * p.C[1] + gC[2] * p.C[2] +
+                           bAc * p.A + bDc * p.D +
+                           gL * (2.0 * Ps * p.L + 2.0 * (p.D * As - p.A * Ds));
+        const double nbA = bAc + gL * 2.0 * Ps * p.D;
+        const double nbD = bDc - gL * 2.0 * Ps * p.A;
+        bP = nbP;
+        bAc = nbA;
+        bDc = nbD;
+      }
+    }
+  }
+  if (flags) atomicOr(err, flags);
+}
+
+// ---- deterministic float64 sum ---------------------------------------------------------
+constexpr int SUM_BLOCKS = 296;
+constexpr int SUM_THREADS = 256;
+
+__global__ void k_sum_partial(const double* __restrict__ x, int64_t n, double* partial) {
+  __shared__ double sh[SUM_THREADS];
+  double acc = 0.0;
+  for (int64_t i = blockIdx.x * (int64_t)SUM_THREADS + threadIdx.x; i < n;
+       i += (int64_t)SUM_BLOCKS * SUM_THREADS)
+    acc += x[i];
+  sh[threadIdx.x] = acc;
+  __syncthreads();
+  for (int o = SUM_THREADS / 2; o > 0; o >>= 1) {
+    if (threadIdx.x < o) sh[threadIdx.x] += sh[threadIdx.x + o];
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) partial[blockIdx.x] = sh[0];
+}
+
+__global__ void k_sum_final(const double* partial, double* out) {
+  if (threadIdx.x == 0 && blockIdx.x == 0) {
+    double acc = 0.0;
+    for (int i = 0; i < SUM_BLOCKS; ++i) acc += partial[i];
+    out[0] = acc;
+  }
+}
+
+// ---- Adam ------------------------------------------------------------------------------
+__global__ void k_adam(float4* __restrict__ p, const float4* __restrict__ g, float4* __restrict__ m,
+                       float4* __restrict__ v, int64_t n4, float lr, float b1, float b2, float eps,
+                       float bc1, float bc2) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n4;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    float4 pp = p[i], gg = g[i], mm = m[i], vv = v[i];
+    float* pa = &pp.x;
+    float* ga = &gg.x;
+    float* ma = &mm.x;
+    float* va = &vv.x;
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      ma[k] = b1 * ma[k] + (1.f - b1) * ga[k];
+      va[k] = b2 * va[k] + (1.f - b2) * ga[k] * ga[k];
+      pa[k] -= lr * (ma[k] / bc1) / (sqrtf(va[k] / bc2) + eps);
+    }
+    p[i] = pp;
+    m[i] = mm;
+    v[i] = vv;
+  }
+}
+
+__global__ void k_adam_tail(float* p, const float* g, float* m, float* v, int64_t lo, int64_t n,
+                            float lr, float b1, float b2, float eps, float bc1, float bc2) {
+  for (int64_t i = lo + threadIdx.x; i < n; i += blockDim.x) {
+    m[i] = b1 * m[i] + (1.f - b1) * g[i];
+    v[i] = b2 * v[i] + (1.f - b2) * g[i] * g[i];
+    p[i] -= lr * (m[i] / bc1) / (sqrtf(v[i] / bc2) + eps);
+  }
+}
+
+__global__ void k_cast_f16(const float* __restrict__ src, __half* __restrict__ dst, int64_t n) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x)
+    dst[i] = __float2half_rn(src[i]);
+}
+
+}  // namespace vr
+
+using namespace vr;
+
+extern "C" int vr_segment_fwd(const double* t0, const double* t1, const float* sr,
+                              const int64_t* off, const int32_t* seg_first, const double* ray_te,
+                              int64_t n_rays, int32_t region_cnt, float* packets, int32_t* err,
+                              void* stream) {
+  (void)err;
+  if (n_rays < 0 || region_cnt < 1 || region_cnt > VR_MAX_REGIONS) {
+    set_error("vr_segment_fwd: bad argument");
+    return VR_ERR_BAD_ARG;
+  }
+  const int64_t n_segs = n_rays * region_cnt;
+  if (n_segs == 0) return VR_OK;
+  k_segment_fwd<<<grid_for(ceil_div(n_segs, SEG_WARPS), 1, 8), SEG_WARPS * 32, 0,
+                  (cudaStream_t)stream>>>(t0, t1, reinterpret_cast<const float4*>(sr), off,
+                                          seg_first, ray_te, n_rays, n_segs,
+                                          reinterpret_cast<float4*>(packets));
+  return check_launch("vr_segment_fwd");
+}
+
+extern "C" int vr_segment_bwd(const double* t0, const double* t1, const float* sr,
+                              const int64_t* off, const double* ray_te, int64_t n_rays,
+                              int32_t region_cnt, const float* dpk, float* dsr, void* stream) {
+  if (n_rays < 0 || region_cnt < 1 || region_cnt > VR_MAX_REGIONS) {
+    set_error("vr_segment_bwd: bad argument");
+    return VR_ERR_BAD_ARG;
+  }
+  const int64_t n_segs = n_rays * region_cnt;
+  if (n_segs == 0) return VR_OK;
+  k_segment_bwd<<<grid_for(ceil_div(n_segs, SEG_WARPS), 1, 8), SEG_WARPS * 32, 0,
+                  (cudaStream_t)stream>>>(t0, t1, reinterpret_cast<const float4*>(sr), off,
+                                          ray_te, n_rays, n_segs,
+                                          reinterpret_cast<const float4*>(dpk),
+                                          reinterpret_cast<float4*>(dsr));
+  return check_launch("vr_segment_bwd");
+}
+
+extern "C" int vr_global_fwd(const float* pk, int32_t n_regions, int64_t n_rays,
+                             const double* ray_te, const float* bg, int32_t clip_bg, float* out,
+                             int32_t* err, void* stream) {
+  if (n_regions < 1 || n_regions > VR_MAX_REGIONS || n_rays < 0 || !bg || !err) {
+    set_error("vr_global_fwd: bad argument");
+    return VR_ERR_BAD_ARG;
+  }
+  if (n_rays == 0) return VR_OK;
+  k_global<false><<<grid_for(n_rays, 128), 128, 0, (cudaStream_t)stream>>>(
+      reinterpret_cast<const float4*>(pk), n_regions, n_rays, ray_te, bg[0], bg[1], bg[2],
+      clip_bg, nullptr, 0.f, 0, 0, out, nullptr, nullptr, err);
+  return check_launch("vr_global_fwd");
+}
+
+extern "C" int vr_global_train(const float* pk, int32_t n_regions, int64_t n_rays,
+                               const double* ray_te, const float* bg, const float* targets,
+                               float lambda_dist, int32_t own_lo, int32_t own_cnt, float* out,
+                               double* ray_loss, float* dpk, int32_t* err, void* stream) {
+  if (n_regions < 1 || n_regions > VR_MAX_REGIONS || n_rays < 0 || !bg || !err || own_lo < 0 ||
+      own_cnt < 1 || own_lo + own_cnt > n_regions) {
+    set_error("vr_global_train: bad argument");
+    return VR_ERR_BAD_ARG;
+  }
+  if (n_rays == 0) return VR_OK;
+  k_global<true><<<grid_for(n_rays, 128), 128, 0, (cudaStream_t)stream>>>(
+      reinterpret_cast<const float4*>(pk), n_regions, n_rays, ray_te, bg[0], bg[1], bg[2], 0,
+      targets, lambda_dist, own_lo, own_cnt, out, ray_loss, reinterpret_cast<float4*>(dpk), err);
+  return check_launch("vr_global_train");
+}
+
+extern "C" int vr_sum_f64(const double* x, int64_t n, double* out, void* stream) {
+  if (n < 0 || !out) {
+    set_error("vr_sum_f64: bad argument");
+    return VR_ERR_BAD_ARG;
+  }
+  static double* partial = nullptr;
+  if (!partial && cudaMalloc(&partial, SUM_BLOCKS * sizeof(double)) != cudaSuccess) {
+    set_error("vr_sum_f64: cudaMalloc failed");
+    return VR_ERR_CUDA;
+  }
+  k_sum_partial<<<SUM_BLOCKS, SUM_THREADS, 0, (cudaStream_t)stream>>>(x, n, partial);
+  k_sum_final<<<1, 32, 0, (cudaStream_t)stream>>>(partial, out);
+  return check_launch("vr_sum_f64");
+}
+
+extern "C" int vr_adam_step(float* p, const float* g, float* m, float* v, int64_t n, float lr,
+                            float b1, float b2, float eps, int32_t step, void* stream) {
+  if (n < 0 || step < 1) {
+    set_error("vr_adam_step: bad argument");
+    return VR_ERR_BAD_ARG;
+  }
+  if (n == 0) return VR_OK;
+  const float bc1 = 1.f - powf(b1, (float)step), bc2 = 1.f - powf(b2, (float)step);
+  const bool aligned = ((uintptr_t)p | (uintptr_t)g | (uintptr_t)m | (uintptr_t)v) % 16 == 0;
+  const int64_t n4 = aligned ? n / 4 : 0;
+  cudaStream_t s = (cudaStream_t)stream;
+  if (n4)
+    k_adam<<<grid_for(n4, 256), 256, 0, s>>>((float4*)p, (const float4*)g, (float4*)m,
+                                             (float4*)v, n4, lr, b1, b2, eps, bc1, bc2);
+  if (4 * n4 < n) k_adam_tail<<<1, 256, 0, s>>>(p, g, m, v, 4 * n4, n, lr, b1, b2, eps, bc1, bc2);
+  return check_launch("vr_adam_step");
+}
+
+extern "C" int vr_cast_f32_f16(const float* src, void* dst, int64_t n, void* stream) {
+  if (n < 0) {
+    set_error("vr_cast_f32_f16: bad argument");
+    return VR_ERR_BAD_ARG;
+  }
+  if (n == 0) return VR_OK;
+  k_cast_f16<<<grid_for(n, 256), 256, 0, (cudaStream_t)stream>>>(src, (__half*)dst, n);
+  return check_launch("vr_cast_f32_f16");
+}

@@ -1,0 +1,320 @@
+// K1 — warp-per-ray ray/region intersection and per-segment sample generation.
+//
+// One warp owns one ray.  Lanes intersect the leaf boxes in parallel (lane per box),
+// compact and sort the cut distances in shared memory, then walk the global dt
+// grid 32 bins at a time (lane per bin), split each bin at the cuts, locate every
+// sub-bin's midpoint and write it into its region's segment.  All geometry is
+// float64 with explicit round-to-nearest intrinsics so the bin edges, midpoints
+// and tile ids are bit-identical to the reference:
+//   generate_samples    quadrature.py:66-88
+//   split_at_planes     quadrature.py:91-114
+//   tile_cut_distances  partitioner.py:195-206
+//   locate_many         partitioner.py:177-192
+//   participants        distsim.py:415-419
+// Regions are contiguous along a ray (each leaf is an intersection of half-spaces
+// whose predicates are monotone in t), so a sample's slot inside its segment is
+// (index along the ray) - (index of the segment's first sample).
+#include <cub/device/device_scan.cuh>
+#include <cub/iterator/transform_input_iterator.cuh>
+
+#include "common.cuh"
+
+namespace vr {
+
+constexpr int K1_WARPS = 4;
+
+struct K1Smem {
+  VrTree tree;
+  double cand[K1_WARPS][2 * VR_MAX_REGIONS];
+  double cut[K1_WARPS][2 * VR_MAX_REGIONS];
+  int candf[K1_WARPS][2 * VR_MAX_REGIONS];
+  int cnt[K1_WARPS][VR_MAX_REGIONS];
+  int first[K1_WARPS][VR_MAX_REGIONS];
+  int64_t off[K1_WARPS][VR_MAX_REGIONS];
+  int64_t end[K1_WARPS][VR_MAX_REGIONS];
+};
+
+template <bool FILL>
+__global__ void __launch_bounds__(K1_WARPS * 32)
+    k_sample(const VrTree tree_param, const double* __restrict__ rays, int64_t stride,
+             int64_t n_rays, double dt, int region_lo, int region_cnt, int32_t* counts,
+             int32_t* seg_first, double* ray_te, uint32_t* ray_part, int32_t* ray_total,
+             const int64_t* __restrict__ offsets, double* t0o, double* t1o, int32_t* rido,
+             int32_t* err) {
+  __shared__ K1Smem sm;
+  {
+    const uint64_t* src = reinterpret_cast<const uint64_t*>(&tree_param);
+    uint64_t* dst = reinterpret_cast<uint64_t*>(&sm.tree);
+    for (int i = threadIdx.x; i < (int)(sizeof(VrTree) / 8); i += blockDim.x) dst[i] = src[i];
+  }
+  __syncthreads();
+  const VrTree& tree = sm.tree;
+  const int lane = threadIdx.x & 31;
+  const int warp = threadIdx.x >> 5;
+  const int n_leaves = tree.n_leaves;
+  double* cand = sm.cand[warp];
+  double* cut = sm.cut[warp];
+  int flags = 0;
+
+  for (int64_t r = (int64_t)blockIdx.x * K1_WARPS + warp; r < n_rays;
+       r += (int64_t)gridDim.x * K1_WARPS) {
+    const RayD ray = load_ray(rays, stride, r);
+    double te, tx;
+    const bool hit = ray_box(ray, tree.root_mn, tree.root_mx, te, tx);
+
+    // --- leaf boxes: participation mask and candidate cut distances --------------
+    uint32_t part = 0;
+    int ncand = 0;
+    for (int j0 = 0; j0 < n_leaves; j0 += 32) {
+      const int j = j0 + lane;
+      double a = 0.0, b = 0.0;
+      bool h = false;
+      if (j < n_leaves) h = ray_box(ray, tree.leaf_mn[j], tree.leaf_mx[j], a, b);
+      part |= __ballot_sync(0xffffffffu, h) << j0;
+      const bool ca = hit && h && te < a && a < tx;
+      const bool cb = hit && h && te < b && b < tx;
+      const unsigned ma = __ballot_sync(0xffffffffu, ca);
+      const unsigned mb = __ballot_sync(0xffffffffu, cb);
+      const unsigned below = (1u << lane) - 1u;
+      if (ca) cand[ncand + __popc(ma & below)] = a;
+      if (cb) cand[ncand + __popc(ma) + __popc(mb & below)] = b;
+      ncand += __popc(ma) + __popc(mb);
+    }
+    __syncwarp();
+
+    // --- sort + dedup the cuts (Python set semantics, sorted) ---------------------
+    int* candf = sm.candf[warp];
+    for (int i = lane; i < ncand; i += 32) {
+      const double v = cand[i];
+      int f = 1;
+      for (int k = 0; k < i; ++k)
+        if (cand[k] == v) f = 0;
+      candf[i] = f;
+    }
+    __syncwarp();
+    int ncut = 0;
+    for (int i = 0; i < ncand; ++i) ncut += candf[i];
+    for (int i = lane; i < ncand; i += 32) {
+      if (candf[i]) {
+        const double v = cand[i];
+        int rank = 0;
+        for (int k = 0; k < ncand; ++k) rank += (candf[k] && cand[k] < v) ? 1 : 0;
+        cut[rank] = v;
+      }
+    }
+    // per-ray region counters
+    if (lane < region_cnt) {
+      sm.cnt[warp][lane] = 0;
+      sm.first[warp][lane] = INT32_MAX;
+      if (FILL) {
+        const int64_t idx = (int64_t)lane * n_rays + r;
+        sm.first[warp][lane] = seg_first[idx];
+        sm.off[warp][lane] = offsets[idx];
+        sm.end[warp][lane] = offsets[idx + 1];
+      }
+    }
+    __syncwarp();
+
+    int total = 0;
+    const double span = hit ? dsub(tx, te) : 0.0;
+    if (hit && span > VR_SLIVER) {
+      // --- global grid (quadrature.py:79-88) ---------------------------------------
+      const double q = ddiv(span, dt);
+      if (!(q < 1.0e9)) {
+        flags |= VR_FLAG_OVERFLOW;
+      } else {
+        const int64_t n = (int64_t)floor(q);
+        const double e_n = dadd(te, dmul((double)n, dt));
+        const int64_t nb = (dsub(tx, e_n) > VR_SLIVER) ? n + 1 : n;  // append tx / replace
+        int carry = 0;
+        for (int64_t c0 = 0; c0 < nb; c0 += 32) {
+          const int64_t k = c0 + lane;
+          double t0 = 0.0, t1 = 0.0;
+          int i0 = 0, i1 = 0;
+          int ne = 0;
+          if (k < nb) {
+            t0 = (k == nb) ? tx : dadd(te, dmul((double)k, dt));
+            t1 = (k + 1 == nb) ? tx : dadd(te, dmul((double)(k + 1), dt));
+            if (dsub(t1, t0) > VR_SLIVER) {
+              // inner cuts strictly inside (t0, t1)  (quadrature.py:106)
+              while (i0 < ncut && !(cut[i0] > t0)) ++i0;
+              i1 = i0;
+              while (i1 < ncut && cut[i1] < t1) ++i1;
+              double a = t0;
+              for (int s = i0; s <= i1; ++s) {
+                const double b = (s < i1) ? cut[s] : t1;
+                if (dsub(b, a) > VR_SLIVER) ++ne;
+                a = b;
+              }
+            }
+          }
+          const int incl = warp_incl_sum_i(ne, lane);
+          int gidx = carry + incl - ne;
+          carry += __shfl_sync(0xffffffffu, incl, 31);
+          if (ne > 0) {
+            double a = t0;
+            for (int s = i0; s <= i1; ++s) {
+              const double b = (s < i1) ? cut[s] : t1;
+              if (dsub(b, a) > VR_SLIVER) {
+                const double m = sample_mid(a, b);
+                double p[3];
+                point_at(ray, m, p);
+                bool oob;
+                const int g = locate_point(tree, p, oob);
+                if (oob) flags |= VR_FLAG_OOB;
+                const int kk = g - region_lo;
+                if (kk >= 0 && kk < region_cnt) {
+                  if (!FILL) {
+                    atomicAdd(&sm.cnt[warp][kk], 1);
+                    atomicMin(&sm.first[warp][kk], gidx);
+                  } else {
+                    const int64_t pos = sm.off[warp][kk] + (int64_t)(gidx - sm.first[warp][kk]);
+                    if (pos >= sm.off[warp][kk] && pos < sm.end[warp][kk]) {
+                      t0o[pos] = a;
+                      t1o[pos] = b;
+                      rido[pos] = (int32_t)r;
+                    } else {
+                      flags |= VR_FLAG_OVERFLOW;
+                    }
+                  }
+                }
+                ++gidx;
+              }
+              a = b;
+            }
+          }
+        }
+        total = carry;
+      }
+    }
+    __syncwarp();
+    if (!FILL) {
+      if (lane < region_cnt) {
+        const int64_t idx = (int64_t)lane * n_rays + r;
+        const int c = sm.cnt[warp][lane];
+        counts[idx] = c;
+        seg_first[idx] = c ? sm.first[warp][lane] : INT32_MAX;
+      }
+      if (lane == 0) {
+        ray_te[r] = hit ? te : 0.0;
+        if (ray_part) ray_part[r] = part;
+        if (ray_total) ray_total[r] = total;
+      }
+    }
+    __syncwarp();
+  }
+  flags = (int)__reduce_or_sync(0xffffffffu, (unsigned)flags);
+  if (flags && lane == 0) atomicOr(err, flags);
+}
+
+__global__ void k_locate(const VrTree tree, const double* __restrict__ pts, int64_t n,
+                         int32_t* tile, int32_t* err) {
+  int flags = 0;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    double p[3] = {pts[3 * i], pts[3 * i + 1], pts[3 * i + 2]};
+    bool oob;
+    const int g = locate_point(tree, p, oob);
+    tile[i] = oob ? -1 : g;
+    if (oob) flags |= VR_FLAG_OOB;
+  }
+  if (flags) atomicOr(err, flags);
+}
+
+struct ToI64 {
+  __host__ __device__ int64_t operator()(int32_t v) const { return (int64_t)v; }
+};
+
+__global__ void k_scan_tail(const int32_t* counts, int64_t n, int64_t* offsets) {
+  if (n == 0) {
+    offsets[0] = 0;
+  } else {
+    offsets[n] = offsets[n - 1] + (int64_t)counts[n - 1];
+  }
+}
+
+static bool valid_tree(const VrTree* t) {
+  return t && t->n_leaves >= 1 && t->n_leaves <= VR_MAX_REGIONS && t->n_nodes >= 0 &&
+         t->n_nodes < VR_MAX_REGIONS && (t->n_nodes == 0 ? t->n_leaves == 1 : true);
+}
+
+}  // namespace vr
+
+using namespace vr;
+
+extern "C" int vr_sample_count(const VrTree* tree, const double* rays, int64_t stride,
+                               int64_t n_rays, double dt, int32_t region_lo, int32_t region_cnt,
+                               int32_t* counts, int32_t* seg_first, double* ray_te,
+                               uint32_t* ray_part, int32_t* ray_total, int32_t* err,
+                               void* stream) {
+  if (!valid_tree(tree) || !(dt > 0.0) || region_lo < 0 || region_cnt < 1 ||
+      region_lo + region_cnt > tree->n_leaves || n_rays < 0 || !err) {
+    set_error("vr_sample_count: bad argument");
+    return VR_ERR_BAD_ARG;
+  }
+  if (n_rays == 0) return VR_OK;
+  const int grid = grid_for(ceil_div(n_rays, K1_WARPS), 1, 16);
+  k_sample<false><<<grid, K1_WARPS * 32, 0, (cudaStream_t)stream>>>(
+      *tree, rays, stride, n_rays, dt, region_lo, region_cnt, counts, seg_first, ray_te,
+      ray_part, ray_total, nullptr, nullptr, nullptr, nullptr, err);
+  return check_launch("vr_sample_count");
+}
+
+extern "C" int vr_sample_fill(const VrTree* tree, const double* rays, int64_t stride,
+                              int64_t n_rays, double dt, int32_t region_lo, int32_t region_cnt,
+                              const int64_t* offsets, const int32_t* seg_first, double* t0,
+                              double* t1, int32_t* ray_id, int32_t* err, void* stream) {
+  if (!valid_tree(tree) || !(dt > 0.0) || region_lo < 0 || region_cnt < 1 ||
+      region_lo + region_cnt > tree->n_leaves || n_rays < 0 || !err) {
+    set_error("vr_sample_fill: bad argument");
+    return VR_ERR_BAD_ARG;
+  }
+  if (n_rays == 0) return VR_OK;
+  const int grid = grid_for(ceil_div(n_rays, K1_WARPS), 1, 16);
+  k_sample<true><<<grid, K1_WARPS * 32, 0, (cudaStream_t)stream>>>(
+      *tree, rays, stride, n_rays, dt, region_lo, region_cnt, nullptr,
+      const_cast<int32_t*>(seg_first), nullptr, nullptr, nullptr, offsets, t0, t1, ray_id, err);
+  return check_launch("vr_sample_fill");
+}
+
+extern "C" int vr_locate(const VrTree* tree, const double* pts, int64_t n, int32_t* tile,
+                         int32_t* err, void* stream) {
+  if (!valid_tree(tree) || n < 0 || !err) {
+    set_error("vr_locate: bad argument");
+    return VR_ERR_BAD_ARG;
+  }
+  if (n == 0) return VR_OK;
+  k_locate<<<grid_for(n, 256), 256, 0, (cudaStream_t)stream>>>(*tree, pts, n, tile, err);
+  return check_launch("vr_locate");
+}
+
+extern "C" size_t vr_scan_workspace_bytes(int64_t n) {
+  size_t bytes = 0;
+  cub::TransformInputIterator<int64_t, ToI64, const int32_t*> it(nullptr, ToI64());
+  cub::DeviceScan::ExclusiveSum(nullptr, bytes, it, (int64_t*)nullptr, n > 0 ? n : 1);
+  return bytes + 256;
+}
+
+extern "C" int vr_scan_offsets(const int32_t* counts, int64_t n, int64_t* offsets, void* ws,
+                               size_t ws_bytes, void* stream) {
+  if (n < 0 || !offsets) {
+    set_error("vr_scan_offsets: bad argument");
+    return VR_ERR_BAD_ARG;
+  }
+  cudaStream_t s = (cudaStream_t)stream;
+  if (n > 0) {
+    size_t need = 0;
+    cub::TransformInputIterator<int64_t, ToI64, const int32_t*> it(counts, ToI64());
+    cub::DeviceScan::ExclusiveSum(nullptr, need, it, offsets, n, s);
+    if (need > ws_bytes) {
+      set_error("vr_scan_offsets: workspace too small");
+      return VR_ERR_BAD_ARG;
+    }
+    if (cub::DeviceScan::ExclusiveSum(ws, need, it, offsets, n, s) != cudaSuccess) {
+      set_error("vr_scan_offsets: cub scan failed");
+      return VR_ERR_CUDA;
+    }
+  }
+  k_scan_tail<<<1, 1, 0, s>>>(counts, n, offsets);
+  return check_launch("vr_scan_offsets");
+}

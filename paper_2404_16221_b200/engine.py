@@ -1,0 +1,354 @@
+"""Per-rank engine: the B200 replacement of the reference's tile protocol.
+
+Reference call stack replaced (distsim._run_ray, distsim.py:395-454):
+
+    _prepare_samples + bin assignment   -> K1  vr_sample_count / vr_scan_offsets / vr_sample_fill
+    Worker.process_inbox: fill_samples  -> region field kernels (analytic / voxel / hash+MLP)
+    Worker.process_inbox: composite     -> K4  vr_segment_fwd        (one packet per segment)
+    transit + stats.record              -> comm.all_gather_packets / gather_packets (NCCL)
+    _compose_tile / _broadcast_compose  -> K5  vr_global_fwd / vr_global_train
+    (no reference)                      -> K5 bwd, K4 bwd, field bwd, Adam
+
+One ``VolumePool`` per process (one process per GPU).  Rank r owns a contiguous
+block of regions; every rank sees the whole (replicated) ray batch and produces
+samples only for its own regions.
+"""
+from __future__ import annotations
+
+import ctypes
+import time
+from dataclasses import dataclass
+
+import numpy as np
+import torch
+
+from . import _lib, comm
+from .errors import ProtocolMismatchError
+from .fields import RegionField, Scene, region_field_for
+from .geometry import Aabb, Camera, Ray, camera_rays, rays_to_soa, vec3
+from .partition import PartitionTree
+from .stats import COMPOSITOR, SCALARS_PER_TILE_PACKET, CommStats
+
+PROTOCOLS = ("mono", "sample_broadcast", "tile_aggregate")
+_ALIASES = {"sample": "sample_broadcast", "tile": "tile_aggregate"}
+
+
+def canonical_protocol(name: str) -> str:
+    name = _ALIASES.get(name, name)
+    if name not in PROTOCOLS:
+        raise ValueError(f"unknown protocol {name!r}; choose from {PROTOCOLS + tuple(_ALIASES)}")
+    return name
+
+
+@dataclass
+class SampleBatch:
+    """K1 output for one rank: region-major sample SoA plus per-segment metadata."""
+
+    n_rays: int
+    region_lo: int
+    region_cnt: int
+    counts: torch.Tensor  # int32 [cnt*R]
+    seg_first: torch.Tensor  # int32 [cnt*R]
+    offsets: torch.Tensor  # int64 [cnt*R + 1]
+    ray_te: torch.Tensor  # float64 [R]
+    ray_part: torch.Tensor  # int32 [R] (uint32 leaf-hit bitmask)
+    ray_total: torch.Tensor  # int32 [R]
+    t0: torch.Tensor  # float64 [N]
+    t1: torch.Tensor  # float64 [N]
+    ray_id: torch.Tensor  # int32 [N]
+    region_bounds: list  # host: sample offset of each owned region, len cnt+1
+
+    @property
+    def n_samples(self) -> int:
+        return self.region_bounds[-1]
+
+    def region_slice(self, kk: int):
+        lo, hi = self.region_bounds[kk], self.region_bounds[kk + 1]
+        return lo, hi
+
+
+@dataclass
+class RayAggregate:
+    """Composed per-ray result (quadrature.py:49-59)."""
+
+    color: np.ndarray
+    alpha: float
+    depth: float
+    transmittance: float
+    distortion: float
+
+
+class VolumePool:
+    """GPU-resident analogue of WorkerPool (distsim.py:347-364) for one rank."""
+
+    def __init__(self, tree: PartitionTree, fields, background=(0.0, 0.0, 0.0), device=None,
+                 rank: int = 0, world: int = 1, group=None):
+        self.tree = tree
+        self.tree_c = tree.to_c()
+        self.n_regions = len(tree.leaves)
+        self.rank, self.world, self.group = rank, world, group
+        self.region_lo, self.region_cnt = comm.owned_regions(self.n_regions, rank, world)
+        if len(fields) != self.region_cnt:
+            raise ValueError(f"need {self.region_cnt} region fields, got {len(fields)}")
+        self.fields = list(fields)
+        self.background = np.asarray(background, dtype=np.float64)
+        self.device = torch.device(device) if device is not None else torch.device("cuda")
+        self.err = torch.zeros(1, dtype=torch.int32, device=self.device)
+        self._ws = None
+        self._bg = (ctypes.c_float * 3)()
+        _lib.load()
+
+    @property
+    def num_workers(self) -> int:
+        return self.n_regions
+
+    # ---- helpers ----------------------------------------------------------------------
+    def _stream(self):
+        return _lib.stream_ptr()
+
+    def check(self, where: str = "") -> None:
+        """Read and clear the device error word; raise the reference exception."""
+        flags = int(self.err.item())
+        if flags:
+            self.err.zero_()
+            _lib.raise_flags(flags, where)
+
+    def rays_to_device(self, rays) -> torch.Tensor:
+        if isinstance(rays, torch.Tensor):
+            t = rays
+        else:
+            t = torch.from_numpy(np.ascontiguousarray(rays, dtype=np.float64))
+        if t.dtype != torch.float64 or t.dim() != 2 or t.shape[0] != 8:
+            raise ValueError("rays must be float64 SoA [8][R]")
+        return t.to(self.device, non_blocking=True).contiguous()
+
+    def _workspace(self, n: int) -> torch.Tensor:
+        need = int(_lib.load().vr_scan_workspace_bytes(n))
+        if self._ws is None or self._ws.numel() < need:
+            self._ws = torch.empty(need, dtype=torch.uint8, device=self.device)
+        return self._ws
+
+    # ---- K1 ----------------------------------------------------------------------------
+    def sample(self, rays: torch.Tensor, dt: float) -> SampleBatch:
+        if not dt > 0.0:
+            raise ValueError("dt must be > 0")
+        R = rays.shape[1]
+        cnt = self.region_cnt
+        dev = self.device
+        s = self._stream()
+        counts = torch.empty(cnt * R, dtype=torch.int32, device=dev)
+        seg_first = torch.empty(cnt * R, dtype=torch.int32, device=dev)
+        ray_te = torch.empty(R, dtype=torch.float64, device=dev)
+        ray_part = torch.empty(R, dtype=torch.int32, device=dev)
+        ray_total = torch.empty(R, dtype=torch.int32, device=dev)
+        tc = _lib.addr(self.tree_c)
+        _lib.call("vr_sample_count", tc, _lib.ptr(rays), rays.shape[1], R, float(dt),
+                  self.region_lo, cnt, _lib.ptr(counts), _lib.ptr(seg_first), _lib.ptr(ray_te),
+                  _lib.ptr(ray_part), _lib.ptr(ray_total), _lib.ptr(self.err), s)
+        offsets = torch.empty(cnt * R + 1, dtype=torch.int64, device=dev)
+        ws = self._workspace(cnt * R)
+        _lib.call("vr_scan_offsets", _lib.ptr(counts), cnt * R, _lib.ptr(offsets), _lib.ptr(ws),
+                  ws.numel(), s)
+        # the single host sync of a step: sample totals per region (allocation sizes)
+        bounds = offsets[torch.arange(cnt + 1, device=dev) * R].cpu().tolist()
+        self.check("in sampling")
+        N = int(bounds[-1])
+        t0 = torch.empty(max(N, 1), dtype=torch.float64, device=dev)
+        t1 = torch.empty(max(N, 1), dtype=torch.float64, device=dev)
+        ray_id = torch.empty(max(N, 1), dtype=torch.int32, device=dev)
+        if N:
+            _lib.call("vr_sample_fill", tc, _lib.ptr(rays), rays.shape[1], R, float(dt),
+                      self.region_lo, cnt, _lib.ptr(offsets), _lib.ptr(seg_first), _lib.ptr(t0),
+                      _lib.ptr(t1), _lib.ptr(ray_id), _lib.ptr(self.err), s)
+        return SampleBatch(R, self.region_lo, cnt, counts, seg_first, offsets, ray_te, ray_part,
+                           ray_total, t0, t1, ray_id, [int(b) for b in bounds])
+
+    # ---- fields -------------------------------------------------------------------------
+    def evaluate(self, rays: torch.Tensor, b: SampleBatch) -> torch.Tensor:
+        sig_rgb = torch.empty((max(b.n_samples, 1), 4), dtype=torch.float32, device=self.device)
+        s = self._stream()
+        for kk, f in enumerate(self.fields):
+            lo, hi = b.region_slice(kk)
+            if hi > lo:
+                f.forward(rays, b.t0[lo:], b.t1[lo:], b.ray_id[lo:], hi - lo, sig_rgb[lo:], s)
+        return sig_rgb
+
+    def field_backward(self, rays, b: SampleBatch, dsig_rgb: torch.Tensor) -> None:
+        s = self._stream()
+        for kk, f in enumerate(self.fields):
+            lo, hi = b.region_slice(kk)
+            if hi > lo and f.trainable:
+                f.backward(rays, b.t0[lo:], b.t1[lo:], b.ray_id[lo:], hi - lo, dsig_rgb[lo:], s)
+
+    # ---- K4 ----------------------------------------------------------------------------
+    def local_packets(self, b: SampleBatch, sig_rgb: torch.Tensor) -> torch.Tensor:
+        pk = torch.empty((b.region_cnt, b.n_rays, 8), dtype=torch.float32, device=self.device)
+        _lib.call("vr_segment_fwd", _lib.ptr(b.t0), _lib.ptr(b.t1), _lib.ptr(sig_rgb),
+                  _lib.ptr(b.offsets), _lib.ptr(b.seg_first), _lib.ptr(b.ray_te), b.n_rays,
+                  b.region_cnt, _lib.ptr(pk), _lib.ptr(self.err), self._stream())
+        return pk
+
+    # ---- K5 ----------------------------------------------------------------------------
+    def _set_bg(self, background):
+        bg = self.background if background is None else vec3(background)
+        for c in range(3):
+            self._bg[c] = float(bg[c])
+        return self._bg
+
+    def compose(self, packets: torch.Tensor, b: SampleBatch, background=None,
+                clip: bool = True) -> torch.Tensor:
+        out = torch.empty((7, b.n_rays), dtype=torch.float32, device=self.device)
+        _lib.call("vr_global_fwd", _lib.ptr(packets), packets.shape[0], b.n_rays,
+                  _lib.ptr(b.ray_te), _lib.addr(self._set_bg(background)), 1 if clip else 0, _lib.ptr(out),
+                  _lib.ptr(self.err), self._stream())
+        return out
+
+    # ---- entry points ------------------------------------------------------------------
+    def render_rays(self, rays, dt: float, background=None, clip: bool = True):
+        """Batched render.  Returns (out [7][R] on rank 0 / None elsewhere, batch);
+        out rows: r, g, b (C + T*bg clipped, or raw C if clip=False), alpha, depth, T, L."""
+        rays = self.rays_to_device(rays)
+        b = self.sample(rays, dt)
+        sig_rgb = self.evaluate(rays, b)
+        local = self.local_packets(b, sig_rgb)
+        allp = comm.gather_packets(local, self.group, self.world, self.rank)
+        if allp is None:
+            return None, b
+        return self.compose(allp, b, background, clip), b
+
+    def loss_and_grad(self, rays, targets, dt: float, lambda_dist: float = 1.0,
+                      background=None):
+        """Forward + backward of the NeRF-XL loss (segrender.py:198-207 definition:
+        sum over rays of |C + T*bg - target|^2 + lambda * distortion).  Gradients
+        accumulate into the owned region fields; returns (loss [1] float64 device
+        tensor, out [7][R], batch)."""
+        rays = self.rays_to_device(rays)
+        tg = torch.as_tensor(targets, dtype=torch.float32).to(self.device, non_blocking=True)
+        tg = tg.reshape(-1, 3).contiguous()
+        if tg.shape[0] != rays.shape[1]:
+            raise ValueError("targets must be (R, 3)")
+        s = self._stream()
+        b = self.sample(rays, dt)
+        sig_rgb = self.evaluate(rays, b)
+        local = self.local_packets(b, sig_rgb)
+        allp = comm.all_gather_packets(local, self.group, self.world)
+        R = b.n_rays
+        out = torch.empty((7, R), dtype=torch.float32, device=self.device)
+        ray_loss = torch.empty(R, dtype=torch.float64, device=self.device)
+        dpk = torch.empty((b.region_cnt, R, 8), dtype=torch.float32, device=self.device)
+        _lib.call("vr_global_train", _lib.ptr(allp), allp.shape[0], R, _lib.ptr(b.ray_te),
+                  _lib.addr(self._set_bg(background)), _lib.ptr(tg), float(lambda_dist), self.region_lo,
+                  self.region_cnt, _lib.ptr(out), _lib.ptr(ray_loss), _lib.ptr(dpk),
+                  _lib.ptr(self.err), s)
+        loss = torch.empty(1, dtype=torch.float64, device=self.device)
+        _lib.call("vr_sum_f64", _lib.ptr(ray_loss), R, _lib.ptr(loss), s)
+        dsig = torch.zeros((max(b.n_samples, 1), 4), dtype=torch.float32, device=self.device)
+        _lib.call("vr_segment_bwd", _lib.ptr(b.t0), _lib.ptr(b.t1), _lib.ptr(sig_rgb),
+                  _lib.ptr(b.offsets), _lib.ptr(b.ray_te), R, b.region_cnt, _lib.ptr(dpk),
+                  _lib.ptr(dsig), s)
+        self.field_backward(rays, b, dsig)
+        return loss, out, b
+
+    def zero_grad(self):
+        for f in self.fields:
+            f.zero_grad()
+
+    def train_step(self, rays, targets, dt: float, lr: float = 1e-2, step: int = 1,
+                   lambda_dist: float = 1.0, background=None):
+        """One training iteration: zero grads, fwd+bwd, Adam.  Returns the device loss."""
+        self.zero_grad()
+        loss, _, _ = self.loss_and_grad(rays, targets, dt, lambda_dist, background)
+        for f in self.fields:
+            if f.trainable:
+                f.step(lr, step)
+        return loss
+
+    # ---- accounting ----------------------------------------------------------------------
+    def comm_stats(self, b: SampleBatch, broadcast_all: bool = False) -> CommStats:
+        """Reference-style scalar counts (distsim.py:415-446) from the K1 outputs."""
+        st = CommStats()
+        st.rays = b.n_rays
+        part = b.ray_part.to(torch.int64) & 0xFFFFFFFF
+        per_leaf = [int(((part >> k) & 1).sum().item()) for k in range(self.n_regions)]
+        st.participations = int(sum(per_leaf))
+        st.samples_assigned = int(b.ray_total.to(torch.int64).sum().item())
+        for k, n in enumerate(per_leaf):
+            if n:
+                st.record(k, COMPOSITOR, SCALARS_PER_TILE_PACKET * n, n)
+        if broadcast_all:
+            nparts = torch.zeros_like(part)
+            for k in range(self.n_regions):
+                nparts += (part >> k) & 1
+            for k in range(self.n_regions):
+                mine = (part >> k) & 1
+                # leaf k receives every other participant's packet on rays it joins
+                recv = int((mine * (nparts - 1)).sum().item())
+                if recv:
+                    st._party(k).scalars_received += SCALARS_PER_TILE_PACKET * recv
+                    st._party(k).messages_received += recv
+                sent = int((mine * (nparts - 1)).sum().item())
+                st._party(k).scalars_sent += SCALARS_PER_TILE_PACKET * sent
+                st._party(k).messages_sent += sent
+        st.link_bytes = (self.world - 1) * self.region_cnt * b.n_rays * 32 if self.world > 1 else 0
+        return st
+
+
+def spawn(tree: PartitionTree, scene: Scene, device=None, rank: int = 0, world: int = 1,
+          group=None) -> VolumePool:
+    """One region field per owned leaf (spawn, distsim.py:358-364)."""
+    lo, cnt = comm.owned_regions(len(tree.leaves), rank, world)
+    dev = torch.device(device) if device is not None else torch.device("cuda")
+    fields = [region_field_for(scene.field, tree.leaves[k], tree, dev) for k in range(lo, lo + cnt)]
+    return VolumePool(tree, fields, scene.background, dev, rank, world, group)
+
+
+def _aggregate_from_out(out: np.ndarray, i: int) -> RayAggregate:
+    return RayAggregate(out[0:3, i].astype(np.float64), float(out[3, i]), float(out[4, i]),
+                        float(out[5, i]), float(out[6, i]))
+
+
+def render_ray(pool: VolumePool, ray: Ray, protocol: str, dt: float, rng=None,
+               broadcast_all: bool = False):
+    """One ray (distsim.py:478-490); returns (RayAggregate, CommStats).  ``rng`` is
+    accepted for API parity: the GPU composite is order-independent by construction."""
+    if pool.num_workers == 0:
+        raise ProtocolMismatchError("worker pool is empty")
+    protocol = canonical_protocol(protocol)
+    if protocol != "tile_aggregate":
+        raise NotImplementedError(f"protocol {protocol!r} is not on the B200 path (SURVEY §8(f))")
+    out, b = pool.render_rays(rays_to_soa([ray]), dt, clip=False)
+    st = pool.comm_stats(b, broadcast_all)
+    if out is None:
+        return None, st
+    return _aggregate_from_out(out.cpu().numpy(), 0), st
+
+
+def render_image(pool: VolumePool, camera: Camera, protocol: str, dt: float, background=None,
+                 threads: int = 1, shuffle_seed=None, broadcast_all: bool = False):
+    """One primary ray per pixel (distsim.py:495-542); returns ((h,w,3) float64 image
+    with pixel = clip(C + T*bg, 0, 1), CommStats).  ``threads``/``shuffle_seed`` are
+    accepted for API parity (the GPU path is scheduling-independent)."""
+    if pool.num_workers == 0:
+        raise ProtocolMismatchError("worker pool is empty")
+    protocol = canonical_protocol(protocol)
+    if protocol != "tile_aggregate":
+        raise NotImplementedError(f"protocol {protocol!r} is not on the B200 path (SURVEY §8(f))")
+    t0 = time.perf_counter()
+    rays = camera_rays(camera, pool.tree.root_box)
+    out, b = pool.render_rays(rays, dt, background=background, clip=True)
+    st = pool.comm_stats(b, broadcast_all)
+    if out is None:
+        return None, st
+    img = out[0:3].T.contiguous().cpu().numpy().astype(np.float64)
+    pool.check("in render_image")
+    st.add_time("render", time.perf_counter() - t0)
+    return img.reshape(camera.height, camera.width, 3), st
+
+
+def write_ppm(path, image: np.ndarray) -> None:
+    """Binary PPM, quantisation floor(c*255 + 0.5) (distsim.py:545-551)."""
+    h, w = image.shape[:2]
+    data = np.floor(np.clip(image, 0.0, 1.0) * 255.0 + 0.5).astype(np.uint8)
+    with open(path, "wb") as f:
+        f.write(f"P6\n{w} {h}\n255\n".encode("ascii"))
+        f.write(data.tobytes())

@@ -1,0 +1,328 @@
+"""GPU parity: the CUDA path (through the C ABI) against the reference's golden
+vectors and the oracle.
+
+Tolerances (north_star): sample edges / owner ids / hash indices bit-exact;
+colour, opacity, depth <= 1e-4 abs; loss <= 1e-5 rel; gradients <= 1e-3 rel.
+"""
+import json
+
+import numpy as np
+import pytest
+import torch
+
+import paper_2404_16221_b200 as vr
+from conftest import GOLDEN, load_npz, render_fixtures, sampler_fixtures
+from oracle import grad_oracle, hashmlp_oracle as hmo, volray_oracle as vo
+
+pytestmark = pytest.mark.gpu
+
+DEV = "cuda:0"
+
+
+class _NoField(vr.RegionField):
+    def forward(self, *a):
+        raise AssertionError("not used")
+
+
+def _pool(tree, fields=None, rank=0, world=1, bg=(0.0, 0.0, 0.0)):
+    lo, cnt = vr.owned_regions(len(tree.leaves), rank, world)
+    if fields is None:
+        fields = [_NoField() for _ in range(cnt)]
+    return vr.VolumePool(tree, fields, bg, DEV, rank, world)
+
+
+def _soa(rows):
+    return np.ascontiguousarray(np.asarray(rows, dtype=np.float64).T)
+
+
+def _flatten_batch(b):
+    """(ray, t0, t1, region) of every owned sample, sorted by (ray, t0)."""
+    R = b.n_rays
+    off = b.offsets.cpu().numpy()
+    n = int(off[-1])
+    seg = np.repeat(np.arange(b.region_cnt * R), np.diff(off))
+    region = seg // R + b.region_lo
+    rid = b.ray_id[:n].cpu().numpy().astype(np.int64)
+    assert np.array_equal(rid, seg % R)
+    t0 = b.t0[:n].cpu().numpy()
+    t1 = b.t1[:n].cpu().numpy()
+    order = np.lexsort((t0, rid))
+    return rid[order], t0[order], t1[order], region[order]
+
+
+@pytest.mark.parametrize("name", sampler_fixtures())
+@pytest.mark.parametrize("world", [1, 2])
+def test_sampler_bit_exact(name, world):
+    g = load_npz(name)
+    tree = vr.tree_from_json(g["tree"])
+    K = len(tree.leaves)
+    if K % world:
+        pytest.skip("regions not divisible")
+    rays = _soa(g["rays"])
+    ref_ray = np.repeat(np.arange(len(g["counts"])), g["counts"])
+    for rank in range(world):
+        pool = _pool(tree, rank=rank, world=world)
+        b = pool.sample(pool.rays_to_device(rays), float(g["dt"]))
+        torch.cuda.synchronize()
+        pool.check()
+        rid, t0, t1, region = _flatten_batch(b)
+        sel = (g["tile"] >= pool.region_lo) & (g["tile"] < pool.region_lo + pool.region_cnt)
+        assert np.array_equal(rid, ref_ray[sel])
+        assert np.array_equal(t0, g["t0"][sel]), "bin edges t0 differ"
+        assert np.array_equal(t1, g["t1"][sel]), "bin edges t1 differ"
+        assert np.array_equal(region, g["tile"][sel]), "owner tiles differ"
+        assert np.array_equal(b.ray_total.cpu().numpy(), g["counts"])
+        assert np.array_equal(b.ray_te.cpu().numpy(), g["te"])
+        part = b.ray_part.cpu().numpy().astype(np.int64) & 0xFFFFFFFF
+        assert np.array_equal(part, g["part"])
+        # segment order key = index of the region's first sample along the ray
+        sf = b.seg_first.cpu().numpy().reshape(pool.region_cnt, -1)
+        starts = np.concatenate([[0], np.cumsum(g["counts"])])
+        for r in range(0, len(g["counts"]), 7):
+            tiles = g["tile"][starts[r]:starts[r + 1]]
+            for kk in range(pool.region_cnt):
+                hit = np.nonzero(tiles == pool.region_lo + kk)[0]
+                want = hit[0] if hit.size else np.iinfo(np.int32).max
+                assert sf[kk, r] == want
+
+
+def test_sampler_empty_and_bad_args(cuda_device):
+    g = load_npz("sampler_random_d2.npz")
+    tree = vr.tree_from_json(g["tree"])
+    pool = _pool(tree)
+    b = pool.sample(pool.rays_to_device(np.zeros((8, 0))), 0.1)
+    assert b.n_samples == 0
+    with pytest.raises(ValueError):
+        pool.sample(pool.rays_to_device(_soa(g["rays"][:4])), 0.0)
+
+
+def _scene_pool(g, world=1, rank=0):
+    tree = vr.tree_from_json(g["tree"])
+    scene = vr.scene_from_json(g["scene"])
+    return vr.spawn(tree, scene, DEV, rank, world), tree, scene
+
+
+@pytest.mark.parametrize("name", render_fixtures())
+def test_render_matches_reference(name):
+    g = load_npz(name)
+    pool, tree, scene = _scene_pool(g)
+    out, b = pool.render_rays(_soa(g["rays"]), float(g["dt"]), clip=False)
+    torch.cuda.synchronize()
+    pool.check()
+    got = out.cpu().numpy().T.astype(np.float64)  # (R, 7): C, A, depth, T, L
+    ref = g["out"]
+    np.testing.assert_allclose(got[:, 0:3], ref[:, 0:3], atol=1e-4, rtol=0)
+    np.testing.assert_allclose(got[:, 3], ref[:, 3], atol=1e-4, rtol=0)
+    np.testing.assert_allclose(got[:, 4], ref[:, 4], atol=1e-4, rtol=0)
+    np.testing.assert_allclose(got[:, 5], ref[:, 5], atol=1e-4, rtol=0)
+    np.testing.assert_allclose(got[:, 6], ref[:, 6], atol=1e-4, rtol=1e-4)
+
+
+def test_render_image_matches_reference():
+    g = load_npz("image_three_blobs.npz")
+    pool, tree, scene = _scene_pool(g)
+    cam = vr.Camera.from_json(g["camera"])
+    img, st = vr.render_image(pool, cam, "tile", float(g["dt"]))
+    np.testing.assert_allclose(img, g["image"], atol=1e-4, rtol=0)
+    ref_bytes = np.floor(np.clip(g["image"], 0, 1) * 255 + 0.5).astype(np.uint8)
+    got_bytes = np.floor(np.clip(img, 0, 1) * 255 + 0.5).astype(np.uint8)
+    assert np.mean(ref_bytes == got_bytes) > 0.999
+    assert st.scalars_sent_total == g["stats"]["scalars_sent_total"]
+    assert [w["scalars_sent"] for w in vr.stats_json(st, "tile_aggregate", 4)["per_worker"]] == \
+        [w["scalars_sent"] for w in g["stats"]["per_worker"]]
+
+
+def test_multi_rank_composite_is_bitwise_identical():
+    """Config 2: packets produced by 2 simulated ranks and gathered give exactly the
+    single-rank composite (the training-mode agreement check, distsim.py:457-475)."""
+    g = load_npz("render_three_blobs_k4.npz")
+    rays = _soa(g["rays"])
+    dt = float(g["dt"])
+    pool1, tree, scene = _scene_pool(g)
+    out1, _ = pool1.render_rays(rays, dt)
+    parts = []
+    for rank in range(2):
+        p, _, _ = _scene_pool(g, world=2, rank=rank)
+        rd = p.rays_to_device(rays)
+        b = p.sample(rd, dt)
+        parts.append(p.local_packets(b, p.evaluate(rd, b)))
+        if rank == 0:
+            b0 = b
+    allp = torch.cat(parts, 0)
+    p0, _, _ = _scene_pool(g, world=2, rank=0)
+    out2 = p0.compose(allp, b0)
+    assert torch.equal(out1, out2)
+
+
+def _grad_setup():
+    doc = json.loads((GOLDEN / "grad_voxel_room.json").read_text())
+    tree = vr.tree_from_json(doc["tree"])
+    scene = vr.scene_from_json(doc["scene"])
+    rays = _soa(doc["rays"])
+    targets = np.full((rays.shape[1], 3), doc["target"])
+    return doc, tree, scene, rays, targets
+
+
+def test_voxel_gradients_match_reference_fd():
+    doc, tree, scene, rays, targets = _grad_setup()
+    pool = vr.spawn(tree, scene, DEV)
+    pool.zero_grad()
+    loss, out, b = pool.loss_and_grad(rays, targets, doc["dt"])
+    torch.cuda.synchronize()
+    pool.check()
+    assert loss.item() == pytest.approx(doc["loss"], rel=1e-5)
+    for e in doc["entries"]:
+        g = pool.fields[e["tile"]].grad[tuple(e["index"])].item()
+        fd = e["global"]
+        assert abs(g - fd) <= 1e-3 * abs(fd) + 1e-6, (e, g)
+
+
+@pytest.mark.parametrize("world", [2, 4])
+def test_voxel_gradients_locality(world):
+    """Each rank's gradient equals the corresponding slice of the single-rank gradient
+    (no gradient all-reduce needed: segrender.py:209-221 LOCAL == GLOBAL)."""
+    doc, tree, scene, rays, targets = _grad_setup()
+    full = vr.spawn(tree, scene, DEV)
+    full.zero_grad()
+    full.loss_and_grad(rays, targets, doc["dt"])
+    rd = full.rays_to_device(rays)
+    pools = [vr.spawn(tree, scene, DEV, r, world) for r in range(world)]
+    batches, sigs, locs = [], [], []
+    for p in pools:
+        p.zero_grad()
+        b = p.sample(rd, doc["dt"])
+        s = p.evaluate(rd, b)
+        batches.append(b)
+        sigs.append(s)
+        locs.append(p.local_packets(b, s))
+    allp = torch.cat(locs, 0)
+    tg = torch.as_tensor(targets, dtype=torch.float32, device=DEV).contiguous()
+    import ctypes
+    from paper_2404_16221_b200 import _lib
+    losses = []
+    for p, b, s in zip(pools, batches, sigs):
+        R = b.n_rays
+        out = torch.empty((7, R), dtype=torch.float32, device=DEV)
+        rl = torch.empty(R, dtype=torch.float64, device=DEV)
+        dpk = torch.empty((b.region_cnt, R, 8), dtype=torch.float32, device=DEV)
+        _lib.call("vr_global_train", _lib.ptr(allp), allp.shape[0], R, _lib.ptr(b.ray_te),
+                  _lib.addr(p._set_bg(None)), _lib.ptr(tg), 1.0, p.region_lo, p.region_cnt,
+                  _lib.ptr(out), _lib.ptr(rl), _lib.ptr(dpk), _lib.ptr(p.err), _lib.stream_ptr())
+        losses.append(rl.sum().item())
+        dsig = torch.zeros((max(b.n_samples, 1), 4), dtype=torch.float32, device=DEV)
+        _lib.call("vr_segment_bwd", _lib.ptr(b.t0), _lib.ptr(b.t1), _lib.ptr(s), _lib.ptr(b.offsets),
+                  _lib.ptr(b.ray_te), R, b.region_cnt, _lib.ptr(dpk), _lib.ptr(dsig),
+                  _lib.stream_ptr())
+        p.field_backward(rd, b, dsig)
+    assert len(set(losses)) == 1  # bitwise identical loss on every rank
+    for p in pools:
+        for kk, f in enumerate(p.fields):
+            ref = full.fields[p.region_lo + kk].grad
+            assert torch.allclose(f.grad, ref, rtol=1e-6, atol=1e-12)
+
+
+def test_nonfinite_packet_raises():
+    g = load_npz("render_three_blobs_k4.npz")
+    pool, _, _ = _scene_pool(g)
+    rays = pool.rays_to_device(_soa(g["rays"][:16]))
+    b = pool.sample(rays, float(g["dt"]))
+    pk = pool.local_packets(b, pool.evaluate(rays, b))
+    nonempty = (pk[:, :, 7].view(torch.int32) != np.iinfo(np.int32).max).nonzero()
+    k, r = nonempty[0].tolist()
+    pk[k, r, 0] = float("nan")
+    pool.compose(pk, b)
+    with pytest.raises(vr.NonFiniteInputError):
+        pool.check()
+
+
+# ---- hash grid + MLP (parity unpinned: checked against oracle/hashmlp_oracle.py) ------
+
+def _hash_setup(log2_T=14, K=2, n_rays=48, seed=0, restriction=False):
+    rng = np.random.default_rng(seed)
+    root = vr.Aabb([-1, -1, -1], [1, 1, 1])
+    tree = vr.grid_tree(root, "x" * int(np.log2(K))) if K > 1 else vr.grid_tree(root, "")
+    cfg = vr.HashGridConfig(log2_T=log2_T, max_res=256)
+    fields, models = [], []
+    table0 = weights0 = None
+    for k in range(K):
+        box = root if restriction else tree.leaves[k].box
+        _, n_entries = hmo.levels(log2_T, max_res=256)
+        if table0 is None or not restriction:
+            table0 = rng.uniform(-1.0, 1.0, size=(n_entries, 2)).astype(np.float32)
+            w = np.zeros(hmo.NPARAMS, dtype=np.float32)
+            for off, rows, cols in ((0, 64, 32), (2048, 16, 64), (3072, 64, 32), (5120, 64, 64),
+                                    (9216, 3, 64)):
+                w[off:off + rows * cols] = rng.normal(size=rows * cols) / np.sqrt(cols)
+            weights0 = w
+        f = vr.HashGridMLP(cfg, box, DEV, table=torch.from_numpy(table0.copy()),
+                           weights=torch.from_numpy(weights0.copy()))
+        fields.append(f)
+        models.append(hmo.HashMLPModel(table0, weights0, log2_T, box.mn, box.mx, max_res=256))
+    pool = vr.VolumePool(tree, fields, (0.2, 0.3, 0.4), DEV)
+    rays = np.stack([vo_ray for vo_ray in (_rand_ray(rng) for _ in range(n_rays))], axis=1)
+    targets = rng.uniform(0, 1, size=(n_rays, 3))
+    return pool, tree, models, rays, targets
+
+
+def _rand_ray(rng):
+    while True:
+        o = rng.uniform(-2.4, 2.4, size=3)
+        t = rng.uniform(-0.8, 0.8, size=3)
+        d = t - o
+        n = np.linalg.norm(d)
+        if n > 1e-6:
+            d = d / n
+            return np.array([*o, *d, 0.0, 20.0])
+
+
+def test_hash_indices_bit_exact():
+    pool, tree, models, rays, _ = _hash_setup(log2_T=12, K=2)
+    rd = pool.rays_to_device(rays)
+    b = pool.sample(rd, 0.03)
+    from paper_2404_16221_b200 import _lib
+    for kk, f in enumerate(pool.fields):
+        lo, hi = b.region_slice(kk)
+        n = hi - lo
+        idx = torch.empty((16, n, 8), dtype=torch.int32, device=DEV)
+        _lib.call("vr_hash_indices", _lib.addr(f.desc), _lib.ptr(rd), rd.shape[1],
+                  _lib.ptr(b.t0[lo:]), _lib.ptr(b.t1[lo:]), _lib.ptr(b.ray_id[lo:]), n,
+                  _lib.ptr(idx), _lib.stream_ptr())
+        t0 = b.t0[lo:hi].cpu().numpy()
+        t1 = b.t1[lo:hi].cpu().numpy()
+        r = b.ray_id[lo:hi].cpu().numpy()
+        m = 0.5 * (t0 + t1)
+        pts = rays[0:3, r].T + m[:, None] * rays[3:6, r].T
+        want = hmo.all_indices(pts, f.box.mn, f.box.mx, 12, max_res=256)
+        assert np.array_equal(idx.cpu().numpy().astype(np.int64), want)
+
+
+@pytest.mark.parametrize("restriction", [False, True])
+def test_hashmlp_loss_and_grads_match_oracle(restriction):
+    pool, tree, models, rays, targets = _hash_setup(log2_T=14, K=2, restriction=restriction)
+    dt = 0.04
+    pool.zero_grad()
+    loss, out, b = pool.loss_and_grad(rays, targets, dt)
+    torch.cuda.synchronize()
+    pool.check()
+    otree = vo.Tree(vr.tree_to_json(tree))
+    oloss, oout = grad_oracle.field_loss(otree, lambda k, pts, d: models[k].eval_t(pts, d),
+                                         rays.T, targets, (0.2, 0.3, 0.4), dt)
+    oloss.backward()
+    got = out.cpu().numpy().T
+    np.testing.assert_allclose(got[:, 0:4], oout[:, 0:4], atol=1e-4, rtol=0)
+    np.testing.assert_allclose(got[:, 5], oout[:, 5], atol=1e-4, rtol=0)
+    assert loss.item() == pytest.approx(oloss.item(), rel=1e-5)
+    for kk, f in enumerate(pool.fields):
+        gt, gw = models[kk].grads()
+        mine_t = f.grad_table.cpu().numpy().astype(np.float64)
+        mine_w = f.grad_weights.cpu().numpy().astype(np.float64)
+        rel_t = np.linalg.norm(mine_t - gt) / max(np.linalg.norm(gt), 1e-30)
+        rel_w = np.linalg.norm(mine_w - gw) / max(np.linalg.norm(gw), 1e-30)
+        assert rel_t <= 1e-3, rel_t
+        assert rel_w <= 1e-3, rel_w
+
+
+def test_train_step_decreases_loss():
+    pool, tree, models, rays, targets = _hash_setup(log2_T=14, K=2, n_rays=256)
+    losses = [pool.train_step(rays, targets, 0.04, lr=1e-2, step=s).item() for s in range(1, 21)]
+    assert losses[-1] < losses[0]
