@@ -202,6 +202,17 @@ int vr_mlp_bwd(const void* weights_dev, const void* enc_dev, const double* rays_
                int64_t ray_stride, const int32_t* ray_id_dev, int64_t n,
                const float* dsig_rgb_dev, float* grad_weights_dev, float* denc_dev,
                void* stream);
+/* Same MLP on the 5th-gen tensor cores (tcgen05.mma kind::f16, TMEM accumulators,
+ * persistent 128-sample tiles).  The production path; vr_mlp_fwd / vr_mlp_bwd are the
+ * CUDA-core reference kernels it is tested against.  The backward raises
+ * VR_FLAG_OVERFLOW in err_dev if a gradient is not representable in fp16. */
+int vr_mlp_fwd_tc(const void* weights_dev, const void* enc_dev, const double* rays_dev,
+                  int64_t ray_stride, const int32_t* ray_id_dev, int64_t n, float* sig_rgb_dev,
+                  void* stream);
+int vr_mlp_bwd_tc(const void* weights_dev, const void* enc_dev, const double* rays_dev,
+                  int64_t ray_stride, const int32_t* ray_id_dev, int64_t n,
+                  const float* dsig_rgb_dev, float* grad_weights_dev, float* denc_dev,
+                  int32_t* err_dev, void* stream);
 
 /* ---- K4: per-segment front-to-back composite (composite_samples quadrature.py:141-165,
  * aggregate_segment segrender.py:71-90, process_inbox distsim.py:318-329) ------------- */

@@ -120,10 +120,18 @@ class HashMLPModel:
         """(n, 32) features, fp16-rounded."""
         u = normalize(pts, self.box_mn, self.box_mx)
         feats = []
+        tab32 = self.table.detach().numpy().astype(np.float32)
         for (scale, res, dense, off) in self.levels:
             idx, w = corners(u, scale, res, dense, self.log2_T)
-            rows = self.table[torch.from_numpy(idx.astype(np.int64) + off)]  # (n, 8, 2)
+            gidx = idx.astype(np.int64) + off
+            rows = self.table[torch.from_numpy(gidx)]  # (n, 8, 2)
             f = (rows * torch.from_numpy(w.astype(np.float64))[:, :, None]).sum(1)
+            # forward value: the kernel's float32 sum in corner order (bit-exact);
+            # gradient: the exact linear map
+            f32 = np.zeros((u.shape[0], 2), dtype=np.float32)
+            for c in range(8):
+                f32 = (f32 + (w[:, c:c + 1] * tab32[gidx[:, c]]).astype(np.float32)).astype(np.float32)
+            f = f + (torch.from_numpy(f32.astype(np.float64)) - f).detach()
             feats.append(f)
         return _q16(torch.cat(feats, dim=1))
 

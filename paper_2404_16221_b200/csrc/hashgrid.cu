@@ -7,7 +7,8 @@
 //   g   = clamp(floor(pos), 0, res_l - 2),  f = pos - g
 //   corner c = (cx, cy, cz):  idx = dense_l ? x + res*(y + res*z)
 //                                           : (x ^ y*2654435761 ^ z*805459861) & (T-1)
-//   w_c = (wx * wy) * wz,  feat_l = sum_c w_c * table[offset_l + idx_c]   (F = 2)
+//   w_c = (wx * wy) * wz,  feat_l = sum_c w_c * table[offset_l + idx_c]   (F = 2,
+//   float32, corner order c = 0..7, no FMA)
 // Encodings are written level-major enc[l][n] as half2 so both the gather kernel
 // and the MLP read them coalesced.  The backward scatters w_c * dfeat with vector
 // float2 atomics (red.global.add.v2.f32 on sm_90+).
@@ -89,11 +90,13 @@ __global__ void __launch_bounds__(HASH_THREADS)
       float2 v[8];
 #pragma unroll
       for (int k = 0; k < 8; ++k) v[k] = __ldg(tl + c.idx[k]);
+      // explicit round-to-nearest mul/add (no FMA): features are bit-identical to the
+      // float32 restatement in oracle/hashmlp_oracle.py
       float a0 = 0.f, a1 = 0.f;
 #pragma unroll
       for (int k = 0; k < 8; ++k) {
-        a0 += c.w[k] * v[k].x;
-        a1 += c.w[k] * v[k].y;
+        a0 = __fadd_rn(a0, __fmul_rn(c.w[k], v[k].x));
+        a1 = __fadd_rn(a1, __fmul_rn(c.w[k], v[k].y));
       }
       enc[(int64_t)l * n + i] = __floats2half2_rn(a0, a1);
     }

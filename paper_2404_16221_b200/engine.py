@@ -94,6 +94,9 @@ class VolumePool:
         self.background = np.asarray(background, dtype=np.float64)
         self.device = torch.device(device) if device is not None else torch.device("cuda")
         self.err = torch.zeros(1, dtype=torch.int32, device=self.device)
+        for f in self.fields:
+            if hasattr(f, "err"):
+                f.err = self.err  # kernels of the fields report into the pool's flag word
         self._ws = None
         self._bg = (ctypes.c_float * 3)()
         _lib.load()

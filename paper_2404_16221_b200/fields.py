@@ -276,7 +276,11 @@ class HashGridMLP(RegionField):
     trainable = True
 
     def __init__(self, cfg: HashGridConfig, box: Aabb, device, seed=0, table_init=1e-4,
-                 table=None, weights=None):
+                 table=None, weights=None, mlp_impl: str = "tc"):
+        if mlp_impl not in ("tc", "cuda"):
+            raise ValueError("mlp_impl must be 'tc' (tcgen05 tensor cores) or 'cuda' (reference)")
+        self.mlp_impl = mlp_impl
+        self.err = torch.zeros(1, dtype=torch.int32, device=device)  # replaced by the pool's
         self.cfg = cfg
         self.box = box
         self.desc = hash_desc(cfg, box)
@@ -315,17 +319,23 @@ class HashGridMLP(RegionField):
         _lib.call("vr_hash_fwd", _lib.addr(self.desc), _lib.ptr(self.table), _lib.ptr(rays),
                   rays.shape[1], _lib.ptr(t0), _lib.ptr(t1), _lib.ptr(ray_id), n,
                   _lib.ptr(enc), stream)
-        _lib.call("vr_mlp_fwd", _lib.ptr(self.weights16), _lib.ptr(enc), _lib.ptr(rays),
-                  rays.shape[1], _lib.ptr(ray_id), n, _lib.ptr(sig_rgb), stream)
+        _lib.call("vr_mlp_fwd_tc" if self.mlp_impl == "tc" else "vr_mlp_fwd",
+                  _lib.ptr(self.weights16), _lib.ptr(enc), _lib.ptr(rays), rays.shape[1],
+                  _lib.ptr(ray_id), n, _lib.ptr(sig_rgb), stream)
 
     def backward(self, rays, t0, t1, ray_id, n, dsig_rgb, stream):
         if n == 0:
             return
         enc = self._enc  # written by the forward of the same step
         denc = torch.empty(16 * n * 2, dtype=torch.float32, device=rays.device)
-        _lib.call("vr_mlp_bwd", _lib.ptr(self.weights16), _lib.ptr(enc), _lib.ptr(rays),
-                  rays.shape[1], _lib.ptr(ray_id), n, _lib.ptr(dsig_rgb),
-                  _lib.ptr(self.grad_weights), _lib.ptr(denc), stream)
+        if self.mlp_impl == "tc":
+            _lib.call("vr_mlp_bwd_tc", _lib.ptr(self.weights16), _lib.ptr(enc), _lib.ptr(rays),
+                      rays.shape[1], _lib.ptr(ray_id), n, _lib.ptr(dsig_rgb),
+                      _lib.ptr(self.grad_weights), _lib.ptr(denc), _lib.ptr(self.err), stream)
+        else:
+            _lib.call("vr_mlp_bwd", _lib.ptr(self.weights16), _lib.ptr(enc), _lib.ptr(rays),
+                      rays.shape[1], _lib.ptr(ray_id), n, _lib.ptr(dsig_rgb),
+                      _lib.ptr(self.grad_weights), _lib.ptr(denc), stream)
         _lib.call("vr_hash_bwd", _lib.addr(self.desc), _lib.ptr(rays), rays.shape[1],
                   _lib.ptr(t0), _lib.ptr(t1), _lib.ptr(ray_id), n, _lib.ptr(denc),
                   _lib.ptr(self.grad_table), stream)

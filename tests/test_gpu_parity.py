@@ -248,7 +248,7 @@ def _hash_setup(log2_T=14, K=2, n_rays=48, seed=0, restriction=False):
         box = root if restriction else tree.leaves[k].box
         _, n_entries = hmo.levels(log2_T, max_res=256)
         if table0 is None or not restriction:
-            table0 = rng.uniform(-1.0, 1.0, size=(n_entries, 2)).astype(np.float32)
+            table0 = rng.uniform(-0.3, 0.3, size=(n_entries, 2)).astype(np.float32)
             w = np.zeros(hmo.NPARAMS, dtype=np.float32)
             for off, rows, cols in ((0, 64, 32), (2048, 16, 64), (3072, 64, 32), (5120, 64, 64),
                                     (9216, 3, 64)):
@@ -318,6 +318,7 @@ def test_hashmlp_loss_and_grads_match_oracle(restriction):
         mine_w = f.grad_weights.cpu().numpy().astype(np.float64)
         rel_t = np.linalg.norm(mine_t - gt) / max(np.linalg.norm(gt), 1e-30)
         rel_w = np.linalg.norm(mine_w - gw) / max(np.linalg.norm(gw), 1e-30)
+        print(f"region {kk}: grad rel err table {rel_t:.2e} weights {rel_w:.2e}")
         assert rel_t <= 1e-3, rel_t
         assert rel_w <= 1e-3, rel_w
 
@@ -326,3 +327,55 @@ def test_train_step_decreases_loss():
     pool, tree, models, rays, targets = _hash_setup(log2_T=14, K=2, n_rays=256)
     losses = [pool.train_step(rays, targets, 0.04, lr=1e-2, step=s).item() for s in range(1, 21)]
     assert losses[-1] < losses[0]
+
+
+@pytest.mark.parametrize("n", [1, 127, 128, 1000, 40000])
+def test_mlp_tensor_core_matches_cuda_core(n):
+    """tcgen05 MLP (production) vs the CUDA-core reference kernel: same fp16
+    quantisation points, fp32 accumulation -> agreement to accumulation order."""
+    from paper_2404_16221_b200 import _lib
+    g = torch.Generator(device="cpu").manual_seed(n)
+    w32 = vr.fields.init_mlp_weights(g).to(DEV)
+    w16 = w32.half()
+    enc = (torch.randn((16, n, 2), generator=g) * 0.5).half().to(DEV).contiguous()
+    R = max(n // 7, 1)
+    d = torch.randn((R, 3), generator=g, dtype=torch.float64)
+    d = d / d.norm(dim=1, keepdim=True)
+    rays = torch.zeros((8, R), dtype=torch.float64)
+    rays[3:6] = d.T
+    rays = rays.to(DEV)
+    rid = torch.randint(0, R, (n,), generator=g, dtype=torch.int32).to(DEV)
+    s = _lib.stream_ptr()
+    outs = []
+    for name in ("vr_mlp_fwd", "vr_mlp_fwd_tc"):
+        o = torch.empty((n, 4), dtype=torch.float32, device=DEV)
+        _lib.call(name, _lib.ptr(w16), _lib.ptr(enc), _lib.ptr(rays), R, _lib.ptr(rid), n,
+                  _lib.ptr(o), s)
+        outs.append(o)
+    torch.cuda.synchronize()
+    a, b = outs
+    assert torch.isfinite(b).all()
+    rel = ((a - b).abs() / (a.abs() + 1e-3)).max().item()
+    assert rel < 2e-3, rel
+    assert (a - b).abs()[:, 1:].max().item() < 1e-4
+    dsr = (torch.randn((n, 4), generator=g) * 0.1).to(DEV)
+    grads = []
+    err = torch.zeros(1, dtype=torch.int32, device=DEV)
+    for name in ("vr_mlp_bwd", "vr_mlp_bwd_tc"):
+        gw = torch.zeros(_lib.VR_MLP_NPARAMS, dtype=torch.float32, device=DEV)
+        de = torch.empty((16, n, 2), dtype=torch.float32, device=DEV)
+        args = [_lib.ptr(w16), _lib.ptr(enc), _lib.ptr(rays), R, _lib.ptr(rid), n, _lib.ptr(dsr),
+                _lib.ptr(gw), _lib.ptr(de)]
+        if name.endswith("_tc"):
+            args.append(_lib.ptr(err))
+        _lib.call(name, *args, s)
+        grads.append((gw, de))
+    torch.cuda.synchronize()
+    assert err.item() == 0
+    (gw_a, de_a), (gw_b, de_b) = grads
+    # random (unstructured) inputs: fp16 activation rounding flips between fp32
+    # accumulation orders dominate the difference (scripts/debug_mlp.py measures both
+    # kernels against a float64 reference: same order of error)
+    assert ((gw_a - gw_b).norm() / gw_a.norm()).item() < 5e-3
+    assert ((de_a - de_b).norm() / de_a.norm()).item() < 5e-3
+    assert gw_b[_lib.VR_MLP_W3C + 3 * 64:].abs().max().item() == 0.0
