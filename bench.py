@@ -289,7 +289,6 @@ def main():
 
     # ---- timed region: inputs resident in HBM -------------------------------------
     clocks = ClockSampler(local)
-    timer = EventTimer()
     _lib.CALLS.clear()
     clocks.start()
     time.sleep(0.3)
@@ -298,17 +297,31 @@ def main():
         dist.barrier()
     start = torch.cuda.Event(enable_timing=True)
     end = torch.cuda.Event(enable_timing=True)
-    _lib.TIMER = timer
     start.record()
     for _ in range(args.steps):
         loss = one_step(rays, tg)
     end.record()
     torch.cuda.synchronize()
-    _lib.TIMER = None
     if world > 1:
         dist.barrier()
     clk = clocks.stop()
     calls = dict(_lib.CALLS)
+
+    # ---- second timed region, same steps, CUDA events around every C-ABI launch:
+    # per-kernel durations for the roofline (kept out of the headline number because
+    # the per-launch event records add host work after the step's sync point)
+    timer = EventTimer()
+    torch.cuda.synchronize()
+    _lib.TIMER = timer
+    p0 = torch.cuda.Event(enable_timing=True)
+    p1 = torch.cuda.Event(enable_timing=True)
+    p0.record()
+    for _ in range(args.steps):
+        one_step(rays, tg)
+    p1.record()
+    torch.cuda.synchronize()
+    _lib.TIMER = None
+    ms_instrumented = p0.elapsed_time(p1) / args.steps
     ms = start.elapsed_time(end) / args.steps
     t_ms = torch.tensor([ms], dtype=torch.float64, device=dev)
     if world > 1:
@@ -346,9 +359,17 @@ def main():
             achieved = per_launch / avg_s / 1e12
             peak = peaks["tensor"]
             unit = "TFLOP/s"
+        traffic = None
+        tp = ROOT / "profiles" / "traffic.json"
+        if tp.exists():  # DRAM bytes/sample from the committed ncu --set full capture
+            per_sample = json.loads(tp.read_text()).get(dom)
+            if per_sample:
+                traffic = per_sample * n_samples_rank * args.steps / n_launch
         roofline = {"kernel": dom, "bound": bound, "achieved": achieved, "peak": peak,
-                    "unit": unit, "frac": achieved / peak, "traffic": None,
-                    "peak_source": peaks["source"], "share_of_step": t_total / args.steps / ms}
+                    "unit": unit, "frac": achieved / peak, "traffic": traffic,
+                    "algorithmic_per_launch": per_launch, "peak_source": peaks["source"],
+                    "share_of_step": t_total / args.steps / ms_instrumented,
+                    "ms_per_step_instrumented": ms_instrumented}
 
     # ---- end to end through the public API with host buffers ------------------------
     e2e = None
