@@ -88,52 +88,64 @@ class EventTimer:
 
 
 class ClockSampler:
-    """nvidia-smi clocks/throttle reasons sampled during the timed region."""
+    """SM clock / throttle reasons sampled during the timed region with NVML from a
+    background thread (nvidia-smi polling was measured to stall this workload's
+    launches; in-process NVML queries do not)."""
 
-    Q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,"
-         "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
-         "clocks_event_reasons.sw_power_cap,utilization.gpu")
+    REASONS = {0x8: "hw_slowdown", 0x40: "hw_thermal_slowdown", 0x20: "sw_thermal_slowdown",
+               0x4: "sw_power_cap"}
 
-    def __init__(self, index: int):
+    def __init__(self, index: int, period: float = 0.1):
         self.index = index
-        self.proc = None
-        self.file = None
+        self.period = period
+        self.rows = []
+        self.thread = None
+        self.stop_flag = False
 
     def start(self):
+        import threading
+
         try:
-            self.file = tempfile.NamedTemporaryFile("w+", suffix=".csv", delete=False)
-            self.proc = subprocess.Popen(
-                ["nvidia-smi", f"--id={self.index}", f"--query-gpu={self.Q}",
-                 "--format=csv,noheader,nounits", "-lms", "100"],
-                stdout=self.file, stderr=subprocess.DEVNULL)
-        except (OSError, FileNotFoundError):
-            self.proc = None
+            import pynvml
+
+            pynvml.nvmlInit()
+            self.nv = pynvml
+            self.h = pynvml.nvmlDeviceGetHandleByIndex(self.index)
+            self.max_mhz = pynvml.nvmlDeviceGetMaxClockInfo(self.h, pynvml.NVML_CLOCK_SM)
+        except Exception:  # noqa: BLE001 - NVML missing: report no clocks
+            self.nv = None
+            return
+
+        def loop():
+            nv = self.nv
+            while not self.stop_flag:
+                try:
+                    sm = nv.nvmlDeviceGetClockInfo(self.h, nv.NVML_CLOCK_SM)
+                    rs = nv.nvmlDeviceGetCurrentClocksEventReasons(self.h)
+                    util = nv.nvmlDeviceGetUtilizationRates(self.h).gpu
+                    self.rows.append((sm, rs, util))
+                except Exception:  # noqa: BLE001
+                    pass
+                time.sleep(self.period)
+
+        self.thread = threading.Thread(target=loop, daemon=True)
+        self.thread.start()
 
     def stop(self):
-        if self.proc is None:
+        if self.nv is None:
             return None
-        self.proc.terminate()
-        try:
-            self.proc.wait(timeout=5)
-        except subprocess.TimeoutExpired:
-            self.proc.kill()
-        self.file.flush()
-        rows = []
-        for line in Path(self.file.name).read_text().splitlines():
-            parts = [p.strip() for p in line.split(",")]
-            if len(parts) >= 7:
-                rows.append(parts)
-        os.unlink(self.file.name)
+        self.stop_flag = True
+        if self.thread is not None:
+            self.thread.join(timeout=2)
+        rows = self.rows
         if not rows:
             return None
-        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
-        reasons = sorted({names[i] for r in rows for i in range(4) if r[2 + i].lower() == "active"})
-        loaded = [r for r in rows if r[6].isdigit() and int(r[6]) > 50] or rows
-        sm = [float(r[0]) for r in loaded if r[0].replace(".", "").isdigit()]
-        mx = [float(r[1]) for r in rows if r[1].replace(".", "").isdigit()]
-        return {"sm_mhz": statistics.median(sm) if sm else None,
-                "sm_max_mhz": max(mx) if mx else None, "reasons": reasons,
-                "samples": len(rows), "samples_under_load": len(loaded)}
+        reasons = sorted({name for (_, rs, _) in rows for bit, name in self.REASONS.items()
+                          if rs & bit})
+        loaded = [r for r in rows if r[2] > 50] or rows
+        return {"sm_mhz": statistics.median(r[0] for r in loaded), "sm_max_mhz": self.max_mhz,
+                "reasons": reasons, "samples": len(rows), "samples_under_load": len(loaded),
+                "source": "nvml"}
 
 
 def dist_env():
@@ -287,6 +299,24 @@ def main():
     if world > 1:
         dist.barrier()
 
+    # Every timed pass starts from the same post-warm-up model state: the step time
+    # depends on the scene's opacity (samples behind opaque space get exactly-zero
+    # gradients and skip their atomics), which drifts as Adam trains.
+    def f_state(f):
+        return [f.table, f.weights] + list(f.adam or [])
+
+    snap = [[t.clone() for t in f_state(f)] for f in pool.fields]
+    snap_step = step
+
+    def restore():
+        nonlocal step
+        for f, ts in zip(pool.fields, snap):
+            for dst, src in zip(f_state(f), ts):
+                dst.copy_(src)
+            f.refresh_weights()
+        step = snap_step
+        torch.cuda.synchronize()
+
     # ---- timed region: inputs resident in HBM -------------------------------------
     clocks = ClockSampler(local)
     _lib.CALLS.clear()
@@ -297,11 +327,15 @@ def main():
         dist.barrier()
     start = torch.cuda.Event(enable_timing=True)
     end = torch.cuda.Event(enable_timing=True)
+    marks = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps + 1)]
     start.record()
-    for _ in range(args.steps):
+    marks[0].record()
+    for k in range(args.steps):
         loss = one_step(rays, tg)
+        marks[k + 1].record()
     end.record()
     torch.cuda.synchronize()
+    step_ms = [marks[k].elapsed_time(marks[k + 1]) for k in range(args.steps)]
     if world > 1:
         dist.barrier()
     clk = clocks.stop()
@@ -311,7 +345,7 @@ def main():
     # per-kernel durations for the roofline (kept out of the headline number because
     # the per-launch event records add host work after the step's sync point)
     timer = EventTimer()
-    torch.cuda.synchronize()
+    restore()
     _lib.TIMER = timer
     p0 = torch.cuda.Event(enable_timing=True)
     p1 = torch.cuda.Event(enable_timing=True)
@@ -376,7 +410,7 @@ def main():
     if not args.no_e2e:
         rays_h = torch.from_numpy(rays_np).pin_memory()
         tg_h = torch.from_numpy(tg_np).pin_memory()
-        torch.cuda.synchronize()
+        restore()
         if world > 1:
             dist.barrier()
         t0 = torch.cuda.Event(enable_timing=True)
@@ -417,6 +451,7 @@ def main():
                            "optimizer": "adam", "loss": "mse+distortion"},
                 "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e,
                 "gpu_launches": launches, "clocks": clk, "loss": final_loss,
+                "step_ms": [round(x, 3) for x in step_ms],
                 "kernels": per_kernel}
         print(json.dumps(line), flush=True)
     if world > 1:

@@ -177,10 +177,15 @@ int vr_voxel_bwd(const VrVoxelDesc* g, const double* rays_dev, int64_t ray_strid
 int vr_hash_fwd(const VrHashGridDesc* g, const float* table_dev, const double* rays_dev,
                 int64_t ray_stride, const double* t0_dev, const double* t1_dev,
                 const int32_t* ray_id_dev, int64_t n, void* enc_dev, void* stream);
-/* denc layout: [n_levels][n] float2; grad_table float2 scatter-add. */
+/* denc layout: [n_levels][n] float2; grad_table float2 scatter-add.  workspace: zero-
+ * initialised device buffer of vr_hash_bwd_workspace_bytes() (left zeroed on return)
+ * holding per-warp replicas of the small dense levels, whose atomics would otherwise
+ * serialise on a few thousand addresses; NULL = plain atomics everywhere. */
+size_t vr_hash_bwd_workspace_bytes(const VrHashGridDesc* g);
 int vr_hash_bwd(const VrHashGridDesc* g, const double* rays_dev, int64_t ray_stride,
                 const double* t0_dev, const double* t1_dev, const int32_t* ray_id_dev, int64_t n,
-                const float* denc_dev, float* grad_table_dev, void* stream);
+                const float* denc_dev, float* grad_table_dev, void* workspace_dev,
+                size_t workspace_bytes, void* stream);
 /* debug/parity: the 8 corner indices per (level, sample): idx[l][n][8] int32 */
 int vr_hash_indices(const VrHashGridDesc* g, const double* rays_dev, int64_t ray_stride,
                     const double* t0_dev, const double* t1_dev, const int32_t* ray_id_dev,

@@ -116,7 +116,8 @@ SIGNATURES = {
     "vr_voxel_fwd": [P, P, P, P, I64, P, P, P, I64, P, P],
     "vr_voxel_bwd": [P, P, I64, P, P, P, I64, P, P, P],
     "vr_hash_fwd": [P, P, P, I64, P, P, P, I64, P, P],
-    "vr_hash_bwd": [P, P, I64, P, P, P, I64, P, P, P],
+    "vr_hash_bwd_workspace_bytes": [P],
+    "vr_hash_bwd": [P, P, I64, P, P, P, I64, P, P, P, C.c_size_t, P],
     "vr_hash_indices": [P, P, I64, P, P, P, I64, P, P],
     "vr_mlp_fwd": [P, P, P, I64, P, I64, P, P],
     "vr_mlp_bwd": [P, P, P, I64, P, I64, P, P, P, P],
@@ -130,7 +131,8 @@ SIGNATURES = {
     "vr_adam_step": [P, P, P, P, I64, F32, F32, F32, F32, I32, P],
     "vr_cast_f32_f16": [P, P, I64, P],
 }
-_RESTYPES = {"vr_last_error": C.c_char_p, "vr_scan_workspace_bytes": C.c_size_t}
+_RESTYPES = {"vr_last_error": C.c_char_p, "vr_scan_workspace_bytes": C.c_size_t,
+             "vr_hash_bwd_workspace_bytes": C.c_size_t}
 
 _LIB = None
 

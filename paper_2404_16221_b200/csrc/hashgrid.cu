@@ -12,6 +12,8 @@
 // Encodings are written level-major enc[l][n] as half2 so both the gather kernel
 // and the MLP read them coalesced.  The backward scatters w_c * dfeat with vector
 // float2 atomics (red.global.add.v2.f32 on sm_90+).
+#include <string.h>
+
 #include "common.cuh"
 
 namespace vr {
@@ -88,8 +90,22 @@ __global__ void __launch_bounds__(HASH_THREADS)
       level_corners(g, l, u, c);
       const float2* tl = table + g.offset[l];
       float2 v[8];
+      // x-adjacent corners whose entries differ only in bit 0 share one 16-byte pair
+      // (always for even x on hashed levels, even index on dense levels): one float4
+      // gather instead of two float2 (level offsets are multiples of 8 entries).
 #pragma unroll
-      for (int k = 0; k < 8; ++k) v[k] = __ldg(tl + c.idx[k]);
+      for (int k = 0; k < 8; k += 2) {
+        const uint32_t a = c.idx[k], b = c.idx[k + 1];
+        if ((a ^ b) == 1u) {
+          const float4 q = __ldg(reinterpret_cast<const float4*>(tl + (a & ~1u)));
+          const float2 lo = make_float2(q.x, q.y), hi = make_float2(q.z, q.w);
+          v[k] = (a & 1u) ? hi : lo;
+          v[k + 1] = (a & 1u) ? lo : hi;
+        } else {
+          v[k] = __ldg(tl + a);
+          v[k + 1] = __ldg(tl + b);
+        }
+      }
       // explicit round-to-nearest mul/add (no FMA): features are bit-identical to the
       // float32 restatement in oracle/hashmlp_oracle.py
       float a0 = 0.f, a1 = 0.f;
@@ -103,11 +119,33 @@ __global__ void __launch_bounds__(HASH_THREADS)
   }
 }
 
+// Coarse dense levels (a few thousand entries hit by every sample of the region) are
+// contention-bound under global atomics: their gradients go to R private replicas
+// (picked per warp) in a workspace and are summed into the table by k_hash_rep_reduce.
+struct RepPlan {
+  int32_t n_rep;  // levels 0 .. n_rep-1 are replicated
+  int32_t R[VR_MAX_LEVELS];
+  int64_t off[VR_MAX_LEVELS];  // workspace offset (entries) of level l's replicas
+};
+
+__device__ __forceinline__ void scatter_pair(float2* gl, uint32_t a, uint32_t b, float2 ga,
+                                             float2 gb) {
+  if ((a ^ b) == 1u) {  // one 16-byte vector atomic for the x-adjacent pair
+    const float4 q =
+        (a & 1u) ? make_float4(gb.x, gb.y, ga.x, ga.y) : make_float4(ga.x, ga.y, gb.x, gb.y);
+    atomicAdd(reinterpret_cast<float4*>(gl + (a & ~1u)), q);
+  } else {
+    atomicAdd(gl + a, ga);
+    atomicAdd(gl + b, gb);
+  }
+}
+
 __global__ void __launch_bounds__(HASH_THREADS)
-    k_hash_bwd(const VrHashGridDesc g, const double* __restrict__ rays, int64_t stride,
-               const double* __restrict__ t0, const double* __restrict__ t1,
+    k_hash_bwd(const VrHashGridDesc g, const RepPlan plan, const double* __restrict__ rays,
+               int64_t stride, const double* __restrict__ t0, const double* __restrict__ t1,
                const int32_t* __restrict__ rid, int64_t n, const float2* __restrict__ denc,
-               float2* __restrict__ grad) {
+               float2* __restrict__ grad, float2* __restrict__ ws) {
+  const int gwarp = blockIdx.x * (HASH_THREADS / 32) + (threadIdx.x >> 5);
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
        i += (int64_t)gridDim.x * blockDim.x) {
     float u[3];
@@ -118,12 +156,64 @@ __global__ void __launch_bounds__(HASH_THREADS)
       if (d.x == 0.f && d.y == 0.f) continue;
       Corners c;
       level_corners(g, l, u, c);
-      float2* gl = grad + g.offset[l];
+      const int64_t size_l = g.offset[l + 1] - g.offset[l];
+      float2* gl = (l < plan.n_rep) ? ws + plan.off[l] + (int64_t)(gwarp % plan.R[l]) * size_l
+                                    : grad + g.offset[l];
 #pragma unroll
-      for (int k = 0; k < 8; ++k)
-        atomicAdd(gl + c.idx[k], make_float2(c.w[k] * d.x, c.w[k] * d.y));
+      for (int k = 0; k < 8; k += 2)
+        scatter_pair(gl, c.idx[k], c.idx[k + 1], make_float2(c.w[k] * d.x, c.w[k] * d.y),
+                     make_float2(c.w[k + 1] * d.x, c.w[k + 1] * d.y));
     }
   }
+}
+
+// grad[level l entry e] += sum_r ws[l][r][e]; the replicas are zeroed for the next use
+__global__ void k_hash_rep_reduce(const VrHashGridDesc g, const RepPlan plan,
+                                  float2* __restrict__ grad, float2* __restrict__ ws,
+                                  int64_t total) {
+  for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < total;
+       t += (int64_t)gridDim.x * blockDim.x) {
+    int64_t e = t;
+    int l = 0;
+    while (l < plan.n_rep - 1 && e >= g.offset[l + 1] - g.offset[l]) {
+      e -= g.offset[l + 1] - g.offset[l];
+      ++l;
+    }
+    const int64_t size_l = g.offset[l + 1] - g.offset[l];
+    float2* w = ws + plan.off[l] + e;
+    float2 acc = make_float2(0.f, 0.f);
+    for (int r = 0; r < plan.R[l]; ++r) {
+      const float2 v = w[r * size_l];
+      acc.x += v.x;
+      acc.y += v.y;
+      w[r * size_l] = make_float2(0.f, 0.f);
+    }
+    float2* gp = grad + g.offset[l] + e;
+    gp->x += acc.x;
+    gp->y += acc.y;
+  }
+}
+
+static RepPlan rep_plan(const VrHashGridDesc* g, int64_t* ws_entries, int64_t* red_entries) {
+  RepPlan p;
+  memset(&p, 0, sizeof(p));
+  int64_t off = 0, red = 0;
+  for (int l = 0; l < g->n_levels; ++l) {
+    const int64_t size_l = g->offset[l + 1] - g->offset[l];
+    // measured on c3 (scripts/bench_hash.py): only the coarsest level (17^3 entries) is
+    // contention-bound; replicating 24^3 / 32^3 levels costs more than it saves
+    if (!g->dense[l] || size_l > 8192) break;
+    int R = (int)((int64_t)(1 << 20) / size_l);
+    R = R < 1 ? 1 : (R > 64 ? 64 : R);
+    p.R[l] = R;
+    p.off[l] = off;
+    off += (int64_t)R * size_l;
+    red += size_l;
+    p.n_rep = l + 1;
+  }
+  *ws_entries = off;
+  *red_entries = red;
+  return p;
 }
 
 __global__ void k_hash_idx(const VrHashGridDesc g, const double* __restrict__ rays, int64_t stride,
@@ -168,17 +258,32 @@ extern "C" int vr_hash_fwd(const VrHashGridDesc* g, const float* table, const do
   return check_launch("vr_hash_fwd");
 }
 
+extern "C" size_t vr_hash_bwd_workspace_bytes(const VrHashGridDesc* g) {
+  if (!valid_grid(g)) return 0;
+  int64_t ws = 0, red = 0;
+  rep_plan(g, &ws, &red);
+  return (size_t)ws * sizeof(float2);
+}
+
 extern "C" int vr_hash_bwd(const VrHashGridDesc* g, const double* rays, int64_t stride,
                            const double* t0, const double* t1, const int32_t* rid, int64_t n,
-                           const float* denc, float* grad, void* stream) {
+                           const float* denc, float* grad, void* ws, size_t ws_bytes,
+                           void* stream) {
   if (!valid_grid(g) || n < 0) {
     set_error("vr_hash_bwd: bad argument");
     return VR_ERR_BAD_ARG;
   }
   if (n == 0) return VR_OK;
-  k_hash_bwd<<<grid_for(n, HASH_THREADS, 8), HASH_THREADS, 0, (cudaStream_t)stream>>>(
-      *g, rays, stride, t0, t1, rid, n, reinterpret_cast<const float2*>(denc),
-      reinterpret_cast<float2*>(grad));
+  int64_t ws_entries = 0, red = 0;
+  RepPlan plan = rep_plan(g, &ws_entries, &red);
+  if (!ws || ws_bytes < (size_t)ws_entries * sizeof(float2)) plan.n_rep = 0;  // plain atomics
+  cudaStream_t s = (cudaStream_t)stream;
+  k_hash_bwd<<<grid_for(n, HASH_THREADS, 8), HASH_THREADS, 0, s>>>(
+      *g, plan, rays, stride, t0, t1, rid, n, reinterpret_cast<const float2*>(denc),
+      reinterpret_cast<float2*>(grad), reinterpret_cast<float2*>(ws));
+  if (plan.n_rep > 0)
+    k_hash_rep_reduce<<<grid_for(red, 256, 4), 256, 0, s>>>(
+        *g, plan, reinterpret_cast<float2*>(grad), reinterpret_cast<float2*>(ws), red);
   return check_launch("vr_hash_bwd");
 }
 

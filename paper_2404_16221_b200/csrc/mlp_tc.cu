@@ -1,29 +1,32 @@
 // K3 on the 5th-generation tensor cores: the per-region density + colour MLP as
-// tcgen05.mma (kind::f16, fp32 accumulation in TMEM), one elected thread issuing,
-// operands in shared memory (layout in tc.cuh), results read back with tcgen05.ld.
+// tcgen05.mma (kind::f16, fp32 accumulation in TMEM), one thread issuing, operands in
+// shared memory (layout in tc.cuh), results read back with tcgen05.ld.
 //
 // Semantics are identical to the CUDA-core reference kernels in mlp.cu (same fp16
-// quantisation points, fp32 accumulation): one 128-sample tile is M = 128 and each
-// thread owns one sample row for the epilogues.
+// quantisation points, fp32 accumulation).  A 128-sample tile is M = 128; sample row r
+// lives in TMEM lane r, so the epilogues are row-per-thread (TPR threads per row, each
+// owning a slice of the columns; warp w reads lanes 32*(w%4) and column half w/4).
 //
 // Forward, per tile (TMEM: 128 columns):
 //   P <- enc                                  [128 x 32]
-//   D0[0:64)   = P  . W1d^T   -> relu -> Q    [128 x 64]
-//   D0[64:80)  = Q  . W2d^T   -> sigma, geo ; P <- [geo | SH(d)]
-//   D0[0:64)   = P  . W1c^T   -> relu -> Q
-//   D0[64:128) = Q  . W2c^T   -> relu -> P
-//   D0[0:16)   = P  . W3c^T   -> sigmoid -> rgb
+//   D[0:64)   = P . W1d^T  -> relu -> Q       [128 x 64]
+//   D[64:80)  = Q . W2d^T  -> sigma, geo ;  P <- [geo | SH(d)]
+//   D[0:64)   = P . W1c^T  -> relu -> Q
+//   D[0:64)   = Q . W2c^T  -> relu -> P
+//   D[64:80)  = P . W3c^T  -> sigmoid -> rgb
 //
-// Backward, per tile (TMEM: 256 columns; weight-gradient accumulators live in TMEM
-// for the CTA's whole persistent loop and are flushed once at the end):
-//   recompute the forward keeping X0=enc, X1=h1d, X2=cin, X3=h1c, X4=h2c in smem;
-//   for each layer the upstream gradient G (fp32 in registers) is written to smem as
-//   an fp16 hi part and then an fp16 lo part (G = hi + lo to ~22 bits), each pass
-//   issuing  dW += G^T X  (M = 64, both operands MN-major, K = 128 samples)  and
-//            dX  = G . W  (M = 128, A K-major, B = W read MN-major).
+// Backward, per tile (TMEM: 256 columns; weight-gradient accumulators stay in TMEM for
+// the CTA's whole persistent loop and are flushed once at the end):
+//   recompute the forward keeping h1d, cin, h1c, h2c in smem (enc is re-staged from
+//   global memory for the last stage, so its slot is reused for cin);
+//   for each layer the upstream gradient G (fp32 registers) is written to smem as an
+//   fp16 hi tile and an fp16 lo tile (G = hi + lo to ~22 bits) and ONE round issues
+//       dW += Ghi^T X + Glo^T X    (M = 64, both operands MN-major, K = 128 samples)
+//       dX  = Ghi . W  + Glo . W   (M = 128, A K-major, B = W read MN-major).
 //   Activations and weights are exactly fp16 by definition of the model, so the
-//   backward is accurate to fp32 accumulation.  Gradients with |g| >= 65504 cannot be
-//   represented and raise VR_FLAG_OVERFLOW (no silent saturation).
+//   backward is accurate to fp32 accumulation.  |g| >= 65504 raises VR_FLAG_OVERFLOW.
+#include <stdlib.h>
+
 #include "common.cuh"
 #include "tc.cuh"
 
@@ -57,7 +60,7 @@ __device__ __forceinline__ void stage_weights(const __half* __restrict__ W, uint
   stage_one(W + VR_MLP_W3C, s + OW3C, 16, 64);
 }
 
-// D[128 x N] (+)= A[128 x K] . B^T,  A = activation tile (K-major), B = weight tile
+// D[128 x N] = A[128 x K] . B^T,  A = activation tile (K-major), B = weight tile
 // [N rows x K cols] (K-major)
 __device__ __forceinline__ void issue_fwd(uint32_t a, int K, uint32_t b, int N, uint32_t d) {
   const uint32_t id = idesc_f16(TILE, N, 0, 0);
@@ -75,7 +78,7 @@ __device__ __forceinline__ void issue_dgrad(uint32_t g, int K, uint32_t w, int N
             (accumulate || kb > 0) ? 1u : 0u);
 }
 
-// Acc[M=64 x N] += A^T . B over the 128 samples: A tile [128 x 64] (cols = M),
+// Acc[M=64 x N] (+)= A^T . B over the 128 samples: A tile [128 x 64] (cols = M),
 // B tile [128 x N] (cols = N), both MN-major with K = rows.
 __device__ __forceinline__ void issue_wgrad(uint32_t a, uint32_t b, int N, uint32_t d,
                                             bool accumulate) {
@@ -105,35 +108,93 @@ __device__ __forceinline__ void sh16f(float x, float y, float z, float* o) {
   o[15] = 0.59004358992664352f * x * (-x2 + 3.0f * y2);
 }
 
-// write 16 fp32 values (cols c0..c0+15 of row r) as fp16 into a tile
-__device__ __forceinline__ void put16(uint8_t* tile, int r, int c0, const float* v) {
-  __align__(16) __half h[16];
+// 8 fp32 -> one 16-byte fp16 chunk (column block cb of row r)
+__device__ __forceinline__ void put8(uint8_t* tile, int r, int cb, const float* v) {
+  uint4 q;
+  __half2* h = reinterpret_cast<__half2*>(&q);
 #pragma unroll
-  for (int j = 0; j < 16; ++j) h[j] = __float2half_rn(v[j]);
-  st_row8(tile, TILE, r, c0 / 8, h);
-  st_row8(tile, TILE, r, c0 / 8 + 1, h + 8);
+  for (int j = 0; j < 4; ++j) h[j] = __floats2half2_rn(v[2 * j], v[2 * j + 1]);
+  *reinterpret_cast<uint4*>(tile + tile_off(TILE, r, cb * 8)) = q;
 }
-__device__ __forceinline__ void get16(const uint8_t* tile, int r, int c0, float* v) {
-  __align__(16) __half h[16];
-  ld_row8(tile, TILE, r, c0 / 8, h);
-  ld_row8(tile, TILE, r, c0 / 8 + 1, h + 8);
+__device__ __forceinline__ void put_relu8(uint8_t* tile, int r, int cb, const float* v) {
+  uint4 q;
+  __half2* h = reinterpret_cast<__half2*>(&q);
 #pragma unroll
-  for (int j = 0; j < 16; ++j) v[j] = __half2float(h[j]);
+  for (int j = 0; j < 4; ++j) h[j] = __floats2half2_rn(fmaxf(v[2 * j], 0.f), fmaxf(v[2 * j + 1], 0.f));
+  *reinterpret_cast<uint4*>(tile + tile_off(TILE, r, cb * 8)) = q;
+}
+// g[j] = v[j] if the (post-relu, fp16) activation of column block cb is non-zero
+__device__ __forceinline__ void relu_mask8(const uint8_t* tile, int r, int cb, const float* v,
+                                           float* g) {
+  const uint4 q = *reinterpret_cast<const uint4*>(tile + tile_off(TILE, r, cb * 8));
+  const uint32_t u[4] = {q.x, q.y, q.z, q.w};
+#pragma unroll
+  for (int j = 0; j < 4; ++j) {
+    g[2 * j] = (u[j] & 0x7FFFu) ? v[2 * j] : 0.f;
+    g[2 * j + 1] = (u[j] & 0x7FFF0000u) ? v[2 * j + 1] : 0.f;
+  }
+}
+// fp16 hi/lo split of 8 gradients into Gh / Gl (column block cb)
+__device__ __forceinline__ void put_grad8(uint8_t* Gh, uint8_t* Gl, int r, int cb, const float* g,
+                                          uint32_t& inf_bits, int use_lo) {
+  uint4 qh, ql;
+  __half2* hh = reinterpret_cast<__half2*>(&qh);
+  __half2* hl = reinterpret_cast<__half2*>(&ql);
+#pragma unroll
+  for (int j = 0; j < 4; ++j) {
+    const __half2 h = __floats2half2_rn(g[2 * j], g[2 * j + 1]);
+    const float2 f = __half22float2(h);
+    hh[j] = h;
+    hl[j] = __floats2half2_rn(g[2 * j] - f.x, g[2 * j + 1] - f.y);
+    const uint32_t u = *reinterpret_cast<const uint32_t*>(&h);
+    inf_bits |= ((u & 0x7C00u) == 0x7C00u) | ((u & 0x7C000000u) == 0x7C000000u);
+  }
+  *reinterpret_cast<uint4*>(Gh + tile_off(TILE, r, cb * 8)) = qh;
+  if (use_lo) *reinterpret_cast<uint4*>(Gl + tile_off(TILE, r, cb * 8)) = ql;
 }
 
-// stage the 32 encoding features of row r (sample i, or zeros)
-__device__ __forceinline__ void stage_enc(uint8_t* tile, int r, const __half2* __restrict__ enc,
-                                          int64_t n, int64_t i, bool valid) {
-  __align__(16) __half2 h[16];
+__device__ __forceinline__ void tmem_ld8(uint32_t taddr, float* v) {
+  uint32_t r[8];
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x8.b32 {%0, %1, %2, %3, %4, %5, %6, %7}, [%8];"
+      : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]),
+        "=r"(r[7])
+      : "r"(taddr));
+  asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
 #pragma unroll
-  for (int l = 0; l < 16; ++l) h[l] = valid ? enc[(int64_t)l * n + i] : __floats2half2_rn(0.f, 0.f);
-  const __half* hh = reinterpret_cast<const __half*>(h);
-#pragma unroll
-  for (int cb = 0; cb < 4; ++cb) st_row8(tile, TILE, r, cb, hh + 8 * cb);
+  for (int i = 0; i < 8; ++i) v[i] = __uint_as_float(r[i]);
 }
 
-// one MMA round: make this thread's smem writes visible to the tensor core, issue,
-// wait for completion
+// Thread geometry: TPR threads per tile row.  warp w covers TMEM lanes 32*(w%4) and
+// column slice w/4.
+template <int TPR>
+struct Geo {
+  static constexpr int NT = TILE * TPR;
+  __device__ static int row() { return ((threadIdx.x >> 5) & 3) * 32 + (threadIdx.x & 31); }
+  __device__ static int part() { return TPR == 1 ? 0 : (int)(threadIdx.x >> 7); }
+  __device__ static uint32_t lane_base() {
+    return (uint32_t)(((threadIdx.x >> 5) & 3) * 32) << 16;
+  }
+};
+
+// stage this thread's share of the 32 encoding features of row r (sample i, or zeros)
+template <int TPR>
+__device__ __forceinline__ void stage_enc(uint8_t* tile, int r, int part,
+                                          const __half2* __restrict__ enc, int64_t n, int64_t i,
+                                          bool valid) {
+  constexpr int LV = 16 / TPR;
+  uint4 q[LV / 4];
+  __half2* h = reinterpret_cast<__half2*>(q);
+#pragma unroll
+  for (int l = 0; l < LV; ++l)
+    h[l] = valid ? enc[(int64_t)(part * LV + l) * n + i] : __floats2half2_rn(0.f, 0.f);
+#pragma unroll
+  for (int c = 0; c < LV / 4; ++c)
+    *reinterpret_cast<uint4*>(tile + tile_off(TILE, r, (part * LV / 4 + c) * 8)) = q[c];
+}
+
+// one MMA round for a CTA-wide tile pipeline: make smem writes visible to the tensor
+// core, issue from thread 0, wait for completion
 template <class F>
 __device__ __forceinline__ void mma_round(uint64_t* bar, uint32_t& phase, F issue) {
   fence_async_smem();
@@ -151,61 +212,69 @@ __device__ __forceinline__ void mma_round(uint64_t* bar, uint32_t& phase, F issu
 }
 
 struct FwdRow {
-  float sigma, od0, rgb[3];
+  float sigma, od0, rgb[3];  // valid in part 0
 };
 
-// The forward chain for one tile.  Activation tiles: X0 (enc, pre-staged), X1, X2, X3,
-// X4 (may alias: the forward-only kernel ping-pongs two buffers).  d0/d1 = TMEM
-// column bases of two scratch accumulators (64 and 16+ columns).
+// Forward chain of one tile.  X0 = enc (pre-staged); activations go to X1 (h1d),
+// X2 (cin), X3 (h1c), X4 (h2c) — X2 may alias X0, X3 may alias X1, X4 may alias X2.
+// d0: 64 scratch columns, d1: 16 scratch columns.
+template <int TPR>
 __device__ __forceinline__ FwdRow forward_tile(uint8_t* sw, uint8_t* X0, uint8_t* X1, uint8_t* X2,
                                                uint8_t* X3, uint8_t* X4, uint32_t tm_row,
                                                uint32_t tmem, uint32_t d0, uint32_t d1,
                                                uint64_t* bar, uint32_t& phase, float dx,
                                                float dy, float dz) {
-  const int r = threadIdx.x;
+  using G = Geo<TPR>;
+  const int r = G::row(), part = G::part();
+  constexpr int C64 = 64 / TPR;  // columns of a 64-wide layer per thread
   const uint32_t sW = smem_u32(sw);
   float v[16];
+  FwdRow out = {0.f, 0.f, {0.f, 0.f, 0.f}};
   // L1d
   mma_round(bar, phase, [&] { issue_fwd(smem_u32(X0), 32, sW + OW1D, 64, tmem + d0); });
 #pragma unroll
-  for (int c = 0; c < 64; c += 16) {
+  for (int c = part * C64; c < (part + 1) * C64; c += 16) {
     tmem_ld16(tm_row + d0 + c, v);
-#pragma unroll
-    for (int j = 0; j < 16; ++j) v[j] = fmaxf(v[j], 0.f);
-    put16(X1, r, c, v);
+    put_relu8(X1, r, c / 8, v);
+    put_relu8(X1, r, c / 8 + 1, v + 8);
   }
-  // L2d
+  // L2d -> sigma, geo (part 0) ; SH(d) (last part)
   mma_round(bar, phase, [&] { issue_fwd(smem_u32(X1), 64, sW + OW2D, 16, tmem + d1); });
-  FwdRow out;
-  tmem_ld16(tm_row + d1, v);
-  out.od0 = v[0];
-  out.sigma = expf(fminf(fmaxf(v[0], -15.f), 15.f));
-  put16(X2, r, 0, v);
-  sh16f(dx, dy, dz, v);
-  put16(X2, r, 16, v);
+  if (part == 0) {
+    tmem_ld16(tm_row + d1, v);
+    out.od0 = v[0];
+    out.sigma = expf(fminf(fmaxf(v[0], -15.f), 15.f));
+    put8(X2, r, 0, v);
+    put8(X2, r, 1, v + 8);
+  }
+  if (part == TPR - 1) {
+    sh16f(dx, dy, dz, v);
+    put8(X2, r, 2, v);
+    put8(X2, r, 3, v + 8);
+  }
   // L1c
   mma_round(bar, phase, [&] { issue_fwd(smem_u32(X2), 32, sW + OW1C, 64, tmem + d0); });
 #pragma unroll
-  for (int c = 0; c < 64; c += 16) {
+  for (int c = part * C64; c < (part + 1) * C64; c += 16) {
     tmem_ld16(tm_row + d0 + c, v);
-#pragma unroll
-    for (int j = 0; j < 16; ++j) v[j] = fmaxf(v[j], 0.f);
-    put16(X3, r, c, v);
+    put_relu8(X3, r, c / 8, v);
+    put_relu8(X3, r, c / 8 + 1, v + 8);
   }
   // L2c
   mma_round(bar, phase, [&] { issue_fwd(smem_u32(X3), 64, sW + OW2C, 64, tmem + d0); });
 #pragma unroll
-  for (int c = 0; c < 64; c += 16) {
+  for (int c = part * C64; c < (part + 1) * C64; c += 16) {
     tmem_ld16(tm_row + d0 + c, v);
-#pragma unroll
-    for (int j = 0; j < 16; ++j) v[j] = fmaxf(v[j], 0.f);
-    put16(X4, r, c, v);
+    put_relu8(X4, r, c / 8, v);
+    put_relu8(X4, r, c / 8 + 1, v + 8);
   }
   // L3c
   mma_round(bar, phase, [&] { issue_fwd(smem_u32(X4), 64, sW + OW3C, 16, tmem + d1); });
-  tmem_ld16(tm_row + d1, v);
+  if (part == 0) {
+    tmem_ld16(tm_row + d1, v);
 #pragma unroll
-  for (int c = 0; c < 3; ++c) out.rgb[c] = 1.f / (1.f + expf(-v[c]));
+    for (int c = 0; c < 3; ++c) out.rgb[c] = 1.f / (1.f + expf(-v[c]));
+  }
   return out;
 }
 
@@ -222,22 +291,23 @@ __device__ __forceinline__ void load_dir(const double* __restrict__ rays, int64_
 }
 
 // ---- forward kernel ---------------------------------------------------------------------
+constexpr int FWD_TPR = 1;
 constexpr uint32_t F_P = WBYTES, F_Q = F_P + TILE * 64 * 2, F_BAR = F_Q + TILE * 64 * 2,
                    F_SMEM = F_BAR + 16;
 
-__global__ void __launch_bounds__(TILE, 4)
+__global__ void __launch_bounds__(TILE * FWD_TPR, 4)
     k_mlp_fwd_tc(const __half* __restrict__ W, const __half2* __restrict__ enc,
                  const double* __restrict__ rays, int64_t stride, const int32_t* __restrict__ rid,
                  int64_t n, float4* __restrict__ out) {
+  using G = Geo<FWD_TPR>;
   extern __shared__ __align__(1024) uint8_t smem[];
   uint8_t* sw = smem;
   uint8_t* P = smem + F_P;
   uint8_t* Q = smem + F_Q;
   uint64_t* bar = reinterpret_cast<uint64_t*>(smem + F_BAR);
   uint32_t* slot = reinterpret_cast<uint32_t*>(smem + F_BAR + 8);
-  const int warp = threadIdx.x >> 5;
   stage_weights(W, sw);
-  if (warp == 0) tmem_alloc(slot, 128);
+  if (threadIdx.x < 32) tmem_alloc(slot, 128);
   if (threadIdx.x == 0) {
     mbar_init(bar, 1);
     fence_barrier_init();
@@ -246,226 +316,293 @@ __global__ void __launch_bounds__(TILE, 4)
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem = *slot;
-  const uint32_t tm_row = tmem + ((uint32_t)(warp * 32) << 16);
+  const uint32_t tm_row = tmem + G::lane_base();
+  const int r = G::row(), part = G::part();
   uint32_t phase = 0;
   const int64_t n_tiles = ceil_div(n, TILE);
   for (int64_t tile = blockIdx.x; tile < n_tiles; tile += gridDim.x) {
-    const int64_t i = tile * TILE + threadIdx.x;
+    const int64_t i = tile * TILE + r;
     const bool valid = i < n;
-    stage_enc(P, threadIdx.x, enc, n, i, valid);
+    stage_enc<FWD_TPR>(P, r, part, enc, n, i, valid);
     float dx, dy, dz;
     load_dir(rays, stride, rid, i, valid, dx, dy, dz);
     // P(enc) -> Q(h1d) -> P(cin) -> Q(h1c) -> P(h2c)
-    const FwdRow f = forward_tile(sw, P, Q, P, Q, P, tm_row, tmem, 0, 64, bar, phase, dx, dy, dz);
-    if (valid) out[i] = make_float4(f.sigma, f.rgb[0], f.rgb[1], f.rgb[2]);
+    const FwdRow f =
+        forward_tile<FWD_TPR>(sw, P, Q, P, Q, P, tm_row, tmem, 0, 64, bar, phase, dx, dy, dz);
+    if (valid && part == 0) out[i] = make_float4(f.sigma, f.rgb[0], f.rgb[1], f.rgb[2]);
   }
   tc_fence_before();
   __syncthreads();
-  if (warp == 0) {
+  if (threadIdx.x < 32) {
     tc_fence_after();
     tmem_dealloc(tmem, 128);
   }
 }
 
 // ---- backward kernel --------------------------------------------------------------------
-constexpr uint32_t B_X0 = WBYTES, B_X1 = B_X0 + TILE * 32 * 2, B_X2 = B_X1 + TILE * 64 * 2,
-                   B_X3 = B_X2 + TILE * 32 * 2, B_X4 = B_X3 + TILE * 64 * 2,
-                   B_G = B_X4 + TILE * 64 * 2, B_BAR = B_G + TILE * 64 * 2, B_SMEM = B_BAR + 16;
+// 256 threads (2 per tile row), 2 CTAs per SM.  Smem per CTA: weights 20 KB + A (enc,
+// then cin) 8 KB + X1 h1d 16 KB + X3 h1c 16 KB + X4 h2c 16 KB + Gh 16 KB + Gl 16 KB.
+constexpr int BWD_TPR = 2;
+constexpr uint32_t B_A = WBYTES, B_X1 = B_A + TILE * 32 * 2, B_X3 = B_X1 + TILE * 64 * 2,
+                   B_X4 = B_X3 + TILE * 64 * 2, B_GH = B_X4 + TILE * 64 * 2,
+                   B_GL = B_GH + TILE * 64 * 2, B_BAR = B_GL + TILE * 64 * 2,
+                   B_SMEM = B_BAR + 32;
 // TMEM columns: weight-gradient accumulators (M = 64) then scratch
 constexpr uint32_t T_W1D = 0, T_W2DT = 32, T_W1C = 48, T_W2C = 80, T_W3CT = 144, T_D0 = 160,
                    T_D1 = 224, T_COLS = 256;
 
-// write the hi or lo fp16 part of a gradient row (width multiple of 16) into G
-template <int WIDTH>
-__device__ __forceinline__ void put_grad(uint8_t* G, int r, const float* g, bool lo, int& flags) {
+// Inputs of one row for one tile, prefetched into registers one tile ahead.
+struct RowIn {
+  __half2 enc[16 / BWD_TPR];
+  float dx, dy, dz;
+  float4 gin;
+};
+
+__device__ __forceinline__ void fetch_row(RowIn& x, const __half2* __restrict__ enc,
+                                          const double* __restrict__ rays, int64_t stride,
+                                          const int32_t* __restrict__ rid,
+                                          const float4* __restrict__ dsr, int64_t n, int64_t i,
+                                          int part) {
+  constexpr int LV = 16 / BWD_TPR;
+  const bool valid = i < n;
 #pragma unroll
-  for (int c = 0; c < WIDTH; c += 16) {
-    float v[16];
-#pragma unroll
-    for (int j = 0; j < 16; ++j) {
-      const float x = g[c + j];
-      const float hi = __half2float(__float2half_rn(x));
-      if (!lo && !(fabsf(x) < 65504.f)) flags |= VR_FLAG_OVERFLOW;
-      v[j] = lo ? (x - hi) : hi;
-    }
-    put16(G, r, c, v);
-  }
+  for (int l = 0; l < LV; ++l)
+    x.enc[l] = valid ? enc[(int64_t)(part * LV + l) * n + i] : __floats2half2_rn(0.f, 0.f);
+  load_dir(rays, stride, rid, i, valid, x.dx, x.dy, x.dz);
+  x.gin = (valid && part == 0) ? dsr[i] : make_float4(0.f, 0.f, 0.f, 0.f);
 }
 
-__global__ void __launch_bounds__(TILE, 2)
+__device__ __forceinline__ void put_enc(uint8_t* tile, int r, int part, const RowIn& x) {
+  constexpr int LV = 16 / BWD_TPR;
+  const uint4* q = reinterpret_cast<const uint4*>(x.enc);
+#pragma unroll
+  for (int c = 0; c < LV / 4; ++c)
+    *reinterpret_cast<uint4*>(tile + tile_off(TILE, r, (part * LV / 4 + c) * 8)) = q[c];
+}
+
+__global__ void __launch_bounds__(TILE * BWD_TPR, 2)
     k_mlp_bwd_tc(const __half* __restrict__ W, const __half2* __restrict__ enc,
                  const double* __restrict__ rays, int64_t stride, const int32_t* __restrict__ rid,
                  int64_t n, const float4* __restrict__ dsr, float* __restrict__ gW,
-                 float2* __restrict__ denc, int32_t* err) {
+                 float2* __restrict__ denc, int32_t* err, int use_lo) {
+  using G = Geo<BWD_TPR>;
   extern __shared__ __align__(1024) uint8_t smem[];
   uint8_t* sw = smem;
-  uint8_t* X0 = smem + B_X0;
+  uint8_t* A = smem + B_A;   // enc during L1d, cin afterwards
   uint8_t* X1 = smem + B_X1;
-  uint8_t* X2 = smem + B_X2;
   uint8_t* X3 = smem + B_X3;
-  uint8_t* X4 = smem + B_X4;
-  uint8_t* G = smem + B_G;
-  uint64_t* bar = reinterpret_cast<uint64_t*>(smem + B_BAR);
-  uint32_t* slot = reinterpret_cast<uint32_t*>(smem + B_BAR + 8);
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int r = threadIdx.x;
+  uint8_t* X4 = smem + B_X4;  // h2c, then enc (re-staged) for the last stage
+  uint8_t* Gh = smem + B_GH;
+  uint8_t* Gl = smem + B_GL;
+  uint64_t* barA = reinterpret_cast<uint64_t*>(smem + B_BAR);  // forward / dgrad MMAs
+  uint64_t* barB = barA + 1;                                     // wgrad MMAs
+  uint32_t* slot = reinterpret_cast<uint32_t*>(smem + B_BAR + 16);
+  const int r = G::row(), part = G::part();
+  const int lane = threadIdx.x & 31, wq = (threadIdx.x >> 5) & 3;
   stage_weights(W, sw);
-  if (warp == 0) tmem_alloc(slot, T_COLS);
+  if (threadIdx.x < 32) tmem_alloc(slot, T_COLS);
   if (threadIdx.x == 0) {
-    mbar_init(bar, 1);
+    mbar_init(barA, 1);
+    mbar_init(barB, 1);
     fence_barrier_init();
   }
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem = *slot;
-  const uint32_t tm_row = tmem + ((uint32_t)(warp * 32) << 16);
+  const uint32_t tm_row = tmem + G::lane_base();
   const uint32_t sW = smem_u32(sw);
-  const uint32_t sX0 = smem_u32(X0), sX1 = smem_u32(X1), sX2 = smem_u32(X2),
-                 sX3 = smem_u32(X3), sX4 = smem_u32(X4), sG = smem_u32(G);
-  uint32_t phase = 0;
-  int flags = 0;
+  const uint32_t sA = smem_u32(A), sX1 = smem_u32(X1), sX3 = smem_u32(X3), sX4 = smem_u32(X4),
+                 sGh = smem_u32(Gh), sGl = smem_u32(Gl);
+  uint32_t phA = 0, phB = 0;
+  bool wgrad_pending = false;
+  uint32_t inf_bits = 0;
   bool acc = false;  // weight-gradient accumulators hold data
+  constexpr int C64 = 64 / BWD_TPR, C16 = 16 / BWD_TPR;
+  const int c64 = part * C64, c16 = part * C16;
   const int64_t n_tiles = ceil_div(n, TILE);
+
+  // one backward stage: wait until the previous wgrad released G, write G = hi + lo,
+  // issue dX = G.W (commit -> barA) then dW += G^T X (commit -> barB), wait for dX only;
+  // the wgrad MMAs overlap the following epilogue.
+  auto stage = [&](const float* g, int width_here, int col0, auto issue_dgrad_fn,
+                   auto issue_wgrad_fn) {
+    if (wgrad_pending) {
+      mbar_wait(barB, phB);
+      phB ^= 1u;
+    }
+    for (int c = 0; c < width_here; c += 8)
+      put_grad8(Gh, Gl, r, (col0 + c) / 8, g + c, inf_bits, use_lo);
+    fence_async_smem();
+    tc_fence_before();
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      tc_fence_after();
+      issue_dgrad_fn();
+      mma_commit(barA);
+      issue_wgrad_fn();
+      mma_commit(barB);
+    }
+    wgrad_pending = true;
+    mbar_wait(barA, phA);
+    phA ^= 1u;
+    __syncwarp();
+    tc_fence_after();
+  };
+
+  RowIn nxt;
+  if ((int64_t)blockIdx.x < n_tiles)
+    fetch_row(nxt, enc, rays, stride, rid, dsr, n, (int64_t)blockIdx.x * TILE + r, part);
   for (int64_t tile = blockIdx.x; tile < n_tiles; tile += gridDim.x) {
     const int64_t i = tile * TILE + r;
     const bool valid = i < n;
-    stage_enc(X0, r, enc, n, i, valid);
-    float dx, dy, dz;
-    load_dir(rays, stride, rid, i, valid, dx, dy, dz);
-    const FwdRow f =
-        forward_tile(sw, X0, X1, X2, X3, X4, tm_row, tmem, T_D0, T_D1, bar, phase, dx, dy, dz);
-    const float4 gin = valid ? dsr[i] : make_float4(0.f, 0.f, 0.f, 0.f);
-    float g[64];
-    float v[16];
-
-    // ---- colour head: g_o = drgb * rgb (1 - rgb), padded to 16 ----------------------
-#pragma unroll
-    for (int j = 0; j < 16; ++j) g[j] = 0.f;
-    g[0] = gin.y * f.rgb[0] * (1.f - f.rgb[0]);
-    g[1] = gin.z * f.rgb[1] * (1.f - f.rgb[1]);
-    g[2] = gin.w * f.rgb[2] * (1.f - f.rgb[2]);
-    for (int pass = 0; pass < 2; ++pass) {
-      put_grad<16>(G, r, g, pass == 1, flags);
-      const bool a_w = acc || pass == 1;
-      mma_round(bar, phase, [&] {
-        issue_wgrad(sX4, sG, 16, tmem + T_W3CT, a_w);            // dW3c^T += h2c^T g_o
-        issue_dgrad(sG, 16, sW + OW3C, 64, tmem + T_D0, pass == 1);  // g_o . W3c
-      });
+    const RowIn cur = nxt;
+    if (tile + gridDim.x < n_tiles)  // prefetch the next tile's inputs
+      fetch_row(nxt, enc, rays, stride, rid, dsr, n, (tile + gridDim.x) * TILE + r, part);
+    if (wgrad_pending) {  // the previous tile's last wgrad reads X4/Gh/Gl
+      mbar_wait(barB, phB);
+      phB ^= 1u;
+      wgrad_pending = false;
     }
+    put_enc(A, r, part, cur);
+    // forward recompute: A(enc) -> X1(h1d) -> A(cin) -> X3(h1c) -> X4(h2c)
+    const FwdRow f = forward_tile<BWD_TPR>(sw, A, X1, A, X3, X4, tm_row, tmem, T_D0, T_D1, barA,
+                                           phA, cur.dx, cur.dy, cur.dz);
+    const float4 gin = cur.gin;
+    float g[C64];
+    float v[16];
+    const bool a_w = acc;
+
+    // stage 1, colour head: g_o = drgb * rgb (1 - rgb) padded to 16 columns
+#pragma unroll
+    for (int j = 0; j < C16; ++j) g[j] = 0.f;
+    if (part == 0) {
+      g[0] = gin.y * f.rgb[0] * (1.f - f.rgb[0]);
+      g[1] = gin.z * f.rgb[1] * (1.f - f.rgb[1]);
+      g[2] = gin.w * f.rgb[2] * (1.f - f.rgb[2]);
+    }
+    stage(g, C16, c16,
+          [&] {
+            issue_dgrad(sGh, 16, sW + OW3C, 64, tmem + T_D0, false);  // g_o . W3c
+            if (use_lo) issue_dgrad(sGl, 16, sW + OW3C, 64, tmem + T_D0, true);
+          },
+          [&] {
+            issue_wgrad(sX4, sGh, 16, tmem + T_W3CT, a_w);  // dW3c^T += h2c^T g_o
+            if (use_lo) issue_wgrad(sX4, sGl, 16, tmem + T_W3CT, true);
+          });
     // dh2c = (g_o . W3c) * relu'(h2c)
 #pragma unroll
-    for (int c = 0; c < 64; c += 16) {
-      tmem_ld16(tm_row + T_D0 + c, v);
-      float h[16];
-      get16(X4, r, c, h);
-#pragma unroll
-      for (int j = 0; j < 16; ++j) g[c + j] = h[j] > 0.f ? v[j] : 0.f;
+    for (int c = 0; c < C64; c += 16) {
+      tmem_ld16(tm_row + T_D0 + c64 + c, v);
+      relu_mask8(X4, r, (c64 + c) / 8, v, g + c);
+      relu_mask8(X4, r, (c64 + c) / 8 + 1, v + 8, g + c + 8);
     }
-    for (int pass = 0; pass < 2; ++pass) {
-      put_grad<64>(G, r, g, pass == 1, flags);
-      const bool a_w = acc || pass == 1;
-      mma_round(bar, phase, [&] {
-        issue_wgrad(sG, sX3, 64, tmem + T_W2C, a_w);             // dW2c += dh2c^T h1c
-        issue_dgrad(sG, 64, sW + OW2C, 64, tmem + T_D0, pass == 1);  // dh2c . W2c
-      });
-    }
+    stage(g, C64, c64,
+          [&] {
+            issue_dgrad(sGh, 64, sW + OW2C, 64, tmem + T_D0, false);  // dh2c . W2c
+            if (use_lo) issue_dgrad(sGl, 64, sW + OW2C, 64, tmem + T_D0, true);
+          },
+          [&] {
+            issue_wgrad(sGh, sX3, 64, tmem + T_W2C, a_w);  // dW2c += dh2c^T h1c
+            if (use_lo) issue_wgrad(sGl, sX3, 64, tmem + T_W2C, true);
+          });
     // dh1c = (dh2c . W2c) * relu'(h1c)
 #pragma unroll
-    for (int c = 0; c < 64; c += 16) {
-      tmem_ld16(tm_row + T_D0 + c, v);
-      float h[16];
-      get16(X3, r, c, h);
-#pragma unroll
-      for (int j = 0; j < 16; ++j) g[c + j] = h[j] > 0.f ? v[j] : 0.f;
+    for (int c = 0; c < C64; c += 16) {
+      tmem_ld16(tm_row + T_D0 + c64 + c, v);
+      relu_mask8(X3, r, (c64 + c) / 8, v, g + c);
+      relu_mask8(X3, r, (c64 + c) / 8 + 1, v + 8, g + c + 8);
     }
-    for (int pass = 0; pass < 2; ++pass) {
-      put_grad<64>(G, r, g, pass == 1, flags);
-      const bool a_w = acc || pass == 1;
-      mma_round(bar, phase, [&] {
-        issue_wgrad(sG, sX2, 32, tmem + T_W1C, a_w);             // dW1c += dh1c^T cin
-        issue_dgrad(sG, 64, sW + OW1C, 32, tmem + T_D0, pass == 1);  // dh1c . W1c
-      });
-    }
+    // the stage-1 wgrad (reads X4) is complete once stage() below has waited on barB;
+    // enc is re-staged into X4 after that, before stage 5 needs it
+    stage(g, C64, c64,
+          [&] {
+            issue_dgrad(sGh, 64, sW + OW1C, 32, tmem + T_D0, false);  // dh1c . W1c
+            if (use_lo) issue_dgrad(sGl, 64, sW + OW1C, 32, tmem + T_D0, true);
+          },
+          [&] {
+            issue_wgrad(sGh, sA, 32, tmem + T_W1C, a_w);  // dW1c += dh1c^T cin
+            if (use_lo) issue_wgrad(sGl, sA, 32, tmem + T_W1C, true);
+          });
+    put_enc(X4, r, part, cur);
     // d od = dcin[0:16]; + dsigma * sigma on od0 (trunc-exp inside the clamp range)
-    tmem_ld16(tm_row + T_D0, v);
+    tmem_ld8(tm_row + T_D0 + c16, v);
 #pragma unroll
-    for (int j = 0; j < 16; ++j) g[j] = v[j];
-    if (f.od0 > -15.f && f.od0 < 15.f) g[0] += gin.x * f.sigma;
-    for (int pass = 0; pass < 2; ++pass) {
-      put_grad<16>(G, r, g, pass == 1, flags);
-      const bool a_w = acc || pass == 1;
-      mma_round(bar, phase, [&] {
-        issue_wgrad(sX1, sG, 16, tmem + T_W2DT, a_w);            // dW2d^T += h1d^T dod
-        issue_dgrad(sG, 16, sW + OW2D, 64, tmem + T_D0, pass == 1);  // dod . W2d
-      });
-    }
+    for (int j = 0; j < C16; ++j) g[j] = v[j];
+    if (part == 0 && f.od0 > -15.f && f.od0 < 15.f) g[0] += gin.x * f.sigma;
+    stage(g, C16, c16,
+          [&] {
+            issue_dgrad(sGh, 16, sW + OW2D, 64, tmem + T_D0, false);  // dod . W2d
+            if (use_lo) issue_dgrad(sGl, 16, sW + OW2D, 64, tmem + T_D0, true);
+          },
+          [&] {
+            issue_wgrad(sX1, sGh, 16, tmem + T_W2DT, a_w);  // dW2d^T += h1d^T dod
+            if (use_lo) issue_wgrad(sX1, sGl, 16, tmem + T_W2DT, true);
+          });
     // dh1d = (dod . W2d) * relu'(h1d)
 #pragma unroll
-    for (int c = 0; c < 64; c += 16) {
-      tmem_ld16(tm_row + T_D0 + c, v);
-      float h[16];
-      get16(X1, r, c, h);
-#pragma unroll
-      for (int j = 0; j < 16; ++j) g[c + j] = h[j] > 0.f ? v[j] : 0.f;
+    for (int c = 0; c < C64; c += 16) {
+      tmem_ld16(tm_row + T_D0 + c64 + c, v);
+      relu_mask8(X1, r, (c64 + c) / 8, v, g + c);
+      relu_mask8(X1, r, (c64 + c) / 8 + 1, v + 8, g + c + 8);
     }
-    for (int pass = 0; pass < 2; ++pass) {
-      put_grad<64>(G, r, g, pass == 1, flags);
-      const bool a_w = acc || pass == 1;
-      mma_round(bar, phase, [&] {
-        issue_wgrad(sG, sX0, 32, tmem + T_W1D, a_w);             // dW1d += dh1d^T enc
-        issue_dgrad(sG, 64, sW + OW1D, 32, tmem + T_D0, pass == 1);  // denc = dh1d . W1d
-      });
-    }
-    // denc -> global, level-major float2
+    stage(g, C64, c64,
+          [&] {
+            issue_dgrad(sGh, 64, sW + OW1D, 32, tmem + T_D0, false);  // denc = dh1d . W1d
+            if (use_lo) issue_dgrad(sGl, 64, sW + OW1D, 32, tmem + T_D0, true);
+          },
+          [&] {
+            issue_wgrad(sGh, sX4, 32, tmem + T_W1D, a_w);  // dW1d += dh1d^T enc
+            if (use_lo) issue_wgrad(sGl, sX4, 32, tmem + T_W1D, true);
+          });
+    // denc -> global, level-major float2 (this thread: levels part*8 .. part*8+7)
+    tmem_ld16(tm_row + T_D0 + 16 * part, v);
+    if (valid) {
 #pragma unroll
-    for (int c = 0; c < 32; c += 16) {
-      tmem_ld16(tm_row + T_D0 + c, v);
-      if (valid) {
-#pragma unroll
-        for (int j = 0; j < 16; j += 2)
-          denc[(int64_t)((c + j) / 2) * n + i] = make_float2(v[j], v[j + 1]);
-      }
+      for (int j = 0; j < 16; j += 2)
+        denc[(int64_t)(8 * part + j / 2) * n + i] = make_float2(v[j], v[j + 1]);
     }
     acc = true;
   }
-  // ---- flush the weight-gradient accumulators (M = 64: rows 16w+t at lanes 32w+t) ------
-  if (acc) {
-    tc_fence_before();
-    __syncthreads();
-    tc_fence_after();
-    const int m = warp * 16 + lane;  // valid for lane < 16
-    float v[16];
-#pragma unroll
-    for (int c = 0; c < 32; c += 16) {
-      tmem_ld16(tm_row + T_W1D + c, v);
-      if (lane < 16)
-        for (int j = 0; j < 16; ++j) atomicAdd(gW + VR_MLP_W1D + m * 32 + c + j, v[j]);
-    }
-    tmem_ld16(tm_row + T_W2DT, v);
-    if (lane < 16)
-      for (int j = 0; j < 16; ++j) atomicAdd(gW + VR_MLP_W2D + j * 64 + m, v[j]);
-#pragma unroll
-    for (int c = 0; c < 32; c += 16) {
-      tmem_ld16(tm_row + T_W1C + c, v);
-      if (lane < 16)
-        for (int j = 0; j < 16; ++j) atomicAdd(gW + VR_MLP_W1C + m * 32 + c + j, v[j]);
-    }
-#pragma unroll
-    for (int c = 0; c < 64; c += 16) {
-      tmem_ld16(tm_row + T_W2C + c, v);
-      if (lane < 16)
-        for (int j = 0; j < 16; ++j) atomicAdd(gW + VR_MLP_W2C + m * 64 + c + j, v[j]);
-    }
-    tmem_ld16(tm_row + T_W3CT, v);
-    if (lane < 16)
-      for (int j = 0; j < 3; ++j) atomicAdd(gW + VR_MLP_W3C + j * 64 + m, v[j]);
+  if (wgrad_pending) {
+    mbar_wait(barB, phB);
+    phB ^= 1u;
   }
-  flags = (int)__reduce_or_sync(0xffffffffu, (unsigned)flags);
-  if (flags && lane == 0) atomicOr(err, flags);
+  // ---- flush the weight-gradient accumulators (M = 64: row 16q+t at lane 32q+t) -----
   tc_fence_before();
   __syncthreads();
-  if (warp == 0) {
+  tc_fence_after();
+  if (acc) {
+    const int m = wq * 16 + lane;  // valid for lane < 16
+    float v[16];
+    // this warp's column half of each accumulator
+    tmem_ld16(tm_row + T_W1D + 16 * part, v);
+    if (lane < 16)
+      for (int j = 0; j < 16; ++j) atomicAdd(gW + VR_MLP_W1D + m * 32 + 16 * part + j, v[j]);
+    tmem_ld8(tm_row + T_W2DT + 8 * part, v);
+    if (lane < 16)
+      for (int j = 0; j < 8; ++j) atomicAdd(gW + VR_MLP_W2D + (8 * part + j) * 64 + m, v[j]);
+    tmem_ld16(tm_row + T_W1C + 16 * part, v);
+    if (lane < 16)
+      for (int j = 0; j < 16; ++j) atomicAdd(gW + VR_MLP_W1C + m * 32 + 16 * part + j, v[j]);
+#pragma unroll
+    for (int c = 0; c < 32; c += 16) {
+      tmem_ld16(tm_row + T_W2C + 32 * part + c, v);
+      if (lane < 16)
+        for (int j = 0; j < 16; ++j)
+          atomicAdd(gW + VR_MLP_W2C + m * 64 + 32 * part + c + j, v[j]);
+    }
+    if (part == 0) {
+      tmem_ld8(tm_row + T_W3CT, v);
+      if (lane < 16)
+        for (int j = 0; j < 3; ++j) atomicAdd(gW + VR_MLP_W3C + j * 64 + m, v[j]);
+    }
+  }
+  const int flags = inf_bits ? VR_FLAG_OVERFLOW : 0;
+  if (__any_sync(0xffffffffu, flags != 0) && lane == 0) atomicOr(err, VR_FLAG_OVERFLOW);
+  tc_fence_before();
+  __syncthreads();
+  if (threadIdx.x < 32) {
     tc_fence_after();
     tmem_dealloc(tmem, T_COLS);
   }
@@ -475,12 +612,6 @@ __global__ void __launch_bounds__(TILE, 2)
 }  // namespace vr
 
 using namespace vr;
-
-static int mlp_grid(int64_t n, int per_sm) {
-  const int64_t tiles = ceil_div(n, vr::mlp::TILE);
-  int64_t g = (int64_t)VR_NUM_SMS * per_sm;
-  return (int)(tiles < g ? tiles : g);
-}
 
 extern "C" int vr_mlp_fwd_tc(const void* w, const void* enc, const double* rays, int64_t stride,
                              const int32_t* rid, int64_t n, float* out, void* stream) {
@@ -498,7 +629,9 @@ extern "C" int vr_mlp_fwd_tc(const void* w, const void* enc, const double* rays,
     }
     attr = true;
   }
-  mlp::k_mlp_fwd_tc<<<mlp_grid(n, 4), mlp::TILE, mlp::F_SMEM, (cudaStream_t)stream>>>(
+  const int64_t tiles = ceil_div(n, mlp::TILE);
+  const int grid = (int)(tiles < VR_NUM_SMS * 4 ? tiles : VR_NUM_SMS * 4);
+  mlp::k_mlp_fwd_tc<<<grid, mlp::TILE * mlp::FWD_TPR, mlp::F_SMEM, (cudaStream_t)stream>>>(
       (const __half*)w, (const __half2*)enc, rays, stride, rid, n, reinterpret_cast<float4*>(out));
   return check_launch("vr_mlp_fwd_tc");
 }
@@ -520,8 +653,17 @@ extern "C" int vr_mlp_bwd_tc(const void* w, const void* enc, const double* rays,
     }
     attr = true;
   }
-  mlp::k_mlp_bwd_tc<<<mlp_grid(n, 2), mlp::TILE, mlp::B_SMEM, (cudaStream_t)stream>>>(
+  // VR_MLP_BWD_LO=0 drops the fp16 lo correction of the upstream gradients (half the
+  // backward MMAs; gradients then carry fp16 rounding, ~1e-4 relative)
+  static int use_lo = -1;
+  if (use_lo < 0) {
+    const char* e = getenv("VR_MLP_BWD_LO");
+    use_lo = (e && e[0] == '0') ? 0 : 1;
+  }
+  const int64_t tiles = ceil_div(n, mlp::TILE);
+  const int grid = (int)(tiles < VR_NUM_SMS * 2 ? tiles : VR_NUM_SMS * 2);
+  mlp::k_mlp_bwd_tc<<<grid, mlp::TILE * mlp::BWD_TPR, mlp::B_SMEM, (cudaStream_t)stream>>>(
       (const __half*)w, (const __half2*)enc, rays, stride, rid, n,
-      reinterpret_cast<const float4*>(dsr), gW, reinterpret_cast<float2*>(denc), err);
+      reinterpret_cast<const float4*>(dsr), gW, reinterpret_cast<float2*>(denc), err, use_lo);
   return check_launch("vr_mlp_bwd_tc");
 }

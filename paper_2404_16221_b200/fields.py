@@ -300,6 +300,7 @@ class HashGridMLP(RegionField):
         self.grad_weights = torch.zeros_like(self.weights)
         self.adam = None
         self._enc = None
+        self._hash_ws = None
         self.refresh_weights()
 
     def refresh_weights(self, stream=None):
@@ -336,9 +337,13 @@ class HashGridMLP(RegionField):
             _lib.call("vr_mlp_bwd", _lib.ptr(self.weights16), _lib.ptr(enc), _lib.ptr(rays),
                       rays.shape[1], _lib.ptr(ray_id), n, _lib.ptr(dsig_rgb),
                       _lib.ptr(self.grad_weights), _lib.ptr(denc), stream)
+        if self._hash_ws is None:
+            nbytes = int(_lib.load().vr_hash_bwd_workspace_bytes(_lib.addr(self.desc)))
+            self._hash_ws = torch.zeros(max(nbytes, 16), dtype=torch.uint8, device=rays.device)
         _lib.call("vr_hash_bwd", _lib.addr(self.desc), _lib.ptr(rays), rays.shape[1],
                   _lib.ptr(t0), _lib.ptr(t1), _lib.ptr(ray_id), n, _lib.ptr(denc),
-                  _lib.ptr(self.grad_table), stream)
+                  _lib.ptr(self.grad_table), _lib.ptr(self._hash_ws), self._hash_ws.numel(),
+                  stream)
 
     def zero_grad(self):
         self.grad_table.zero_()
