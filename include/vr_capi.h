@@ -219,6 +219,22 @@ int vr_mlp_bwd_tc(const void* weights_dev, const void* enc_dev, const double* ra
                   const float* dsig_rgb_dev, float* grad_weights_dev, float* denc_dev,
                   int32_t* err_dev, void* stream);
 
+/* ---- K2 + K3 fused (production training path) ------------------------------------
+ * Forward: the tensor-core MLP kernel computes each row's hash encoding itself (no
+ * encoding round trip through HBM before the MLP) and, if enc_out != NULL, writes it
+ * (level-major half2) for the backward.  Backward: the MLP backward scatters the
+ * hash-grid gradients straight from its last epilogue (no d(enc) round trip);
+ * workspace as for vr_hash_bwd. */
+int vr_field_fwd_tc(const VrHashGridDesc* g, const float* table_dev, const void* weights_dev,
+                    const double* rays_dev, int64_t ray_stride, const double* t0_dev,
+                    const double* t1_dev, const int32_t* ray_id_dev, int64_t n, void* enc_out_dev,
+                    float* sig_rgb_dev, void* stream);
+int vr_field_bwd_tc(const VrHashGridDesc* g, const void* weights_dev, const void* enc_dev,
+                    const double* rays_dev, int64_t ray_stride, const double* t0_dev,
+                    const double* t1_dev, const int32_t* ray_id_dev, int64_t n,
+                    const float* dsig_rgb_dev, float* grad_weights_dev, float* grad_table_dev,
+                    void* workspace_dev, size_t workspace_bytes, int32_t* err_dev, void* stream);
+
 /* ---- K4: per-segment front-to-back composite (composite_samples quadrature.py:141-165,
  * aggregate_segment segrender.py:71-90, process_inbox distsim.py:318-329) ------------- */
 int vr_segment_fwd(const double* t0_dev, const double* t1_dev, const float* sig_rgb_dev,

@@ -163,3 +163,40 @@ class HashMLPModel:
 
     def grads(self):
         return (self.table.grad.numpy().copy(), self.weights.grad.numpy().copy())
+
+
+class CompactHashMLPModel(HashMLPModel):
+    """The same model storing only the table entries a known point set touches.
+
+    Used to time the CPU port on the big configs (T = 2^19..2^22 per region) without
+    dense float64 tables and dense autograd gradients dominating the measurement;
+    arithmetic is identical to HashMLPModel on those points."""
+
+    def __init__(self, entry_init, weights, log2_T: int, box_mn, box_mx, pts, max_res: int = 2048):
+        self.log2_T = log2_T
+        self.box_mn, self.box_mx = box_mn, box_mx
+        self.levels, self.n_entries = levels(log2_T, max_res=max_res)
+        u = normalize(pts, box_mn, box_mx)
+        touched = [corners(u, s, r, dn, log2_T)[0].astype(np.int64).ravel() + off
+                   for (s, r, dn, off) in self.levels]
+        self.uniq = np.unique(np.concatenate(touched))
+        table = np.asarray(entry_init(self.uniq), dtype=np.float64)
+        self.table = torch.tensor(table, requires_grad=True)
+        w16 = np.asarray(weights, dtype=np.float32).astype(np.float16).astype(np.float64)
+        self.weights = torch.tensor(w16, requires_grad=True)
+
+    def encode(self, pts) -> torch.Tensor:
+        u = normalize(pts, self.box_mn, self.box_mx)
+        feats = []
+        tab32 = self.table.detach().numpy().astype(np.float32)
+        for (scale, res, dense, off) in self.levels:
+            idx, w = corners(u, scale, res, dense, self.log2_T)
+            loc = np.searchsorted(self.uniq, idx.astype(np.int64) + off)
+            rows = self.table[torch.from_numpy(loc)]
+            f = (rows * torch.from_numpy(w.astype(np.float64))[:, :, None]).sum(1)
+            f32 = np.zeros((u.shape[0], 2), dtype=np.float32)
+            for c in range(8):
+                f32 = (f32 + (w[:, c:c + 1] * tab32[loc[:, c]]).astype(np.float32)).astype(np.float32)
+            f = f + (torch.from_numpy(f32.astype(np.float64)) - f).detach()
+            feats.append(f)
+        return _q16(torch.cat(feats, dim=1))

@@ -1,0 +1,145 @@
+// Device building blocks of the multiresolution hash-grid encoding (K2), shared by the
+// standalone kernels (hashgrid.cu) and the fused field kernels (mlp_tc.cu).  The
+// arithmetic spec is in hashgrid.cu's header and restated in oracle/hashmlp_oracle.py.
+#pragma once
+
+#include "common.cuh"
+
+namespace vr {
+
+// u = float32((p - box_mn) / (box_mx - box_mn)) for p = o + m d (float64, no FMA)
+__device__ __forceinline__ void norm_pos_od(const VrHashGridDesc& g, const double o[3],
+                                            const double d[3], double m, float u[3]) {
+#pragma unroll
+  for (int a = 0; a < 3; ++a) {
+    const double p = dadd(o[a], dmul(m, d[a]));
+    u[a] = (float)ddiv(dsub(p, g.box_mn[a]), dsub(g.box_mx[a], g.box_mn[a]));
+  }
+}
+
+__device__ __forceinline__ void norm_pos(const VrHashGridDesc& g, const double* __restrict__ rays,
+                                         int64_t stride, const double* __restrict__ t0,
+                                         const double* __restrict__ t1,
+                                         const int32_t* __restrict__ rid, int64_t i, float u[3]) {
+  const int64_t r = rid[i];
+  const double m = sample_mid(t0[i], t1[i]);
+  double o[3], d[3];
+#pragma unroll
+  for (int a = 0; a < 3; ++a) {
+    o[a] = __ldg(rays + a * stride + r);
+    d[a] = __ldg(rays + (3 + a) * stride + r);
+  }
+  norm_pos_od(g, o, d, m, u);
+}
+
+struct Corners {
+  uint32_t idx[8];
+  float w[8];
+};
+
+__device__ __forceinline__ void level_corners(const VrHashGridDesc& g, int l, const float u[3],
+                                              Corners& c) {
+  const float scale = g.scale[l];
+  const int res = g.res[l];
+  int gi[3];
+  float fr[3];
+#pragma unroll
+  for (int a = 0; a < 3; ++a) {
+    const float pos = __fadd_rn(__fmul_rn(u[a], scale), 0.5f);
+    int gg = (int)floorf(pos);
+    gg = min(max(gg, 0), res - 2);
+    gi[a] = gg;
+    fr[a] = __fsub_rn(pos, (float)gg);
+  }
+  const uint32_t mask = (1u << g.log2_T) - 1u;
+  const bool dense = g.dense[l] != 0;
+#pragma unroll
+  for (int c8 = 0; c8 < 8; ++c8) {
+    const int cx = c8 & 1, cy = (c8 >> 1) & 1, cz = (c8 >> 2) & 1;
+    const uint32_t x = (uint32_t)(gi[0] + cx), y = (uint32_t)(gi[1] + cy),
+                   z = (uint32_t)(gi[2] + cz);
+    c.idx[c8] = dense ? x + (uint32_t)res * (y + (uint32_t)res * z)
+                      : (x ^ (y * 2654435761u) ^ (z * 805459861u)) & mask;
+    const float wx = cx ? fr[0] : __fsub_rn(1.f, fr[0]);
+    const float wy = cy ? fr[1] : __fsub_rn(1.f, fr[1]);
+    const float wz = cz ? fr[2] : __fsub_rn(1.f, fr[2]);
+    c.w[c8] = __fmul_rn(__fmul_rn(wx, wy), wz);
+  }
+}
+
+// Feature of one level.  x-adjacent corners whose entries differ only in bit 0 share
+// one 16-byte pair (always for even x on hashed levels, even index on dense levels):
+// one float4 gather instead of two float2 (level offsets are multiples of 8 entries).
+// Explicit round-to-nearest mul/add (no FMA): bit-identical to the float32 oracle.
+__device__ __forceinline__ float2 gather_level(const float2* __restrict__ tl, const Corners& c) {
+  float2 v[8];
+#pragma unroll
+  for (int k = 0; k < 8; k += 2) {
+    const uint32_t a = c.idx[k], b = c.idx[k + 1];
+    if ((a ^ b) == 1u) {
+      const float4 q = __ldg(reinterpret_cast<const float4*>(tl + (a & ~1u)));
+      const float2 lo = make_float2(q.x, q.y), hi = make_float2(q.z, q.w);
+      v[k] = (a & 1u) ? hi : lo;
+      v[k + 1] = (a & 1u) ? lo : hi;
+    } else {
+      v[k] = __ldg(tl + a);
+      v[k + 1] = __ldg(tl + b);
+    }
+  }
+  float a0 = 0.f, a1 = 0.f;
+#pragma unroll
+  for (int k = 0; k < 8; ++k) {
+    a0 = __fadd_rn(a0, __fmul_rn(c.w[k], v[k].x));
+    a1 = __fadd_rn(a1, __fmul_rn(c.w[k], v[k].y));
+  }
+  return make_float2(a0, a1);
+}
+
+__device__ __forceinline__ void scatter_pair(float2* gl, uint32_t a, uint32_t b, float2 ga,
+                                             float2 gb) {
+  if ((a ^ b) == 1u) {  // one 16-byte vector atomic for the x-adjacent pair
+    const float4 q =
+        (a & 1u) ? make_float4(gb.x, gb.y, ga.x, ga.y) : make_float4(ga.x, ga.y, gb.x, gb.y);
+    atomicAdd(reinterpret_cast<float4*>(gl + (a & ~1u)), q);
+  } else {
+    atomicAdd(gl + a, ga);
+    atomicAdd(gl + b, gb);
+  }
+}
+
+// Coarse dense levels (a few thousand entries hit by every sample of the region) are
+// contention-bound under global atomics: their gradients go to R private replicas
+// (picked per warp) in a workspace, summed into the table by k_hash_rep_reduce.
+struct RepPlan {
+  int32_t n_rep;  // levels 0 .. n_rep-1 are replicated
+  int32_t R[VR_MAX_LEVELS];
+  int64_t off[VR_MAX_LEVELS];  // workspace offset (entries) of level l's replicas
+};
+
+// scatter d(feature) of level l for one sample
+__device__ __forceinline__ void scatter_level(const VrHashGridDesc& g, const RepPlan& plan,
+                                              int l, const float u[3], float2 d, int gwarp,
+                                              float2* __restrict__ grad, float2* __restrict__ ws) {
+  if (d.x == 0.f && d.y == 0.f) return;
+  Corners c;
+  level_corners(g, l, u, c);
+  const int64_t size_l = g.offset[l + 1] - g.offset[l];
+  float2* gl = (l < plan.n_rep) ? ws + plan.off[l] + (int64_t)(gwarp % plan.R[l]) * size_l
+                                : grad + g.offset[l];
+#pragma unroll
+  for (int k = 0; k < 8; k += 2)
+    scatter_pair(gl, c.idx[k], c.idx[k + 1], make_float2(c.w[k] * d.x, c.w[k] * d.y),
+                 make_float2(c.w[k + 1] * d.x, c.w[k + 1] * d.y));
+}
+
+// host: replica plan + workspace / reduction sizes (entries)
+RepPlan hash_rep_plan(const VrHashGridDesc* g, int64_t* ws_entries, int64_t* red_entries);
+// host: sum the replicas into grad and zero them (enqueued on stream)
+int hash_rep_reduce(const VrHashGridDesc* g, const RepPlan& plan, int64_t red_entries,
+                    float* grad, void* ws, void* stream);
+
+}  // namespace vr
+
+namespace vr {
+bool valid_grid(const VrHashGridDesc* g);
+}  // namespace vr

@@ -26,8 +26,10 @@
 //   Activations and weights are exactly fp16 by definition of the model, so the
 //   backward is accurate to fp32 accumulation.  |g| >= 65504 raises VR_FLAG_OVERFLOW.
 #include <stdlib.h>
+#include <string.h>
 
 #include "common.cuh"
+#include "hashgrid.cuh"
 #include "tc.cuh"
 
 namespace vr {
@@ -195,8 +197,15 @@ __device__ __forceinline__ void stage_enc(uint8_t* tile, int r, int part,
 
 // one MMA round for a CTA-wide tile pipeline: make smem writes visible to the tensor
 // core, issue from thread 0, wait for completion
-template <class F>
-__device__ __forceinline__ void mma_round(uint64_t* bar, uint32_t& phase, F issue) {
+// `overlap` runs on every thread after the MMAs are issued and before waiting for them
+// (independent SIMT work hidden under the tensor-core latency).
+struct NoOverlap {
+  __device__ __forceinline__ void operator()(int) const {}
+};
+
+template <class F, class O = NoOverlap>
+__device__ __forceinline__ void mma_round(uint64_t* bar, uint32_t& phase, F issue,
+                                          const O& overlap = O(), int round = 0) {
   fence_async_smem();
   tc_fence_before();
   __syncthreads();
@@ -205,6 +214,7 @@ __device__ __forceinline__ void mma_round(uint64_t* bar, uint32_t& phase, F issu
     issue();
     mma_commit(bar);
   }
+  overlap(round);
   mbar_wait(bar, phase);
   phase ^= 1u;
   __syncwarp();
@@ -218,12 +228,12 @@ struct FwdRow {
 // Forward chain of one tile.  X0 = enc (pre-staged); activations go to X1 (h1d),
 // X2 (cin), X3 (h1c), X4 (h2c) — X2 may alias X0, X3 may alias X1, X4 may alias X2.
 // d0: 64 scratch columns, d1: 16 scratch columns.
-template <int TPR>
+template <int TPR, class O = NoOverlap>
 __device__ __forceinline__ FwdRow forward_tile(uint8_t* sw, uint8_t* X0, uint8_t* X1, uint8_t* X2,
                                                uint8_t* X3, uint8_t* X4, uint32_t tm_row,
                                                uint32_t tmem, uint32_t d0, uint32_t d1,
                                                uint64_t* bar, uint32_t& phase, float dx,
-                                               float dy, float dz) {
+                                               float dy, float dz, const O& ov = O()) {
   using G = Geo<TPR>;
   const int r = G::row(), part = G::part();
   constexpr int C64 = 64 / TPR;  // columns of a 64-wide layer per thread
@@ -231,7 +241,7 @@ __device__ __forceinline__ FwdRow forward_tile(uint8_t* sw, uint8_t* X0, uint8_t
   float v[16];
   FwdRow out = {0.f, 0.f, {0.f, 0.f, 0.f}};
   // L1d
-  mma_round(bar, phase, [&] { issue_fwd(smem_u32(X0), 32, sW + OW1D, 64, tmem + d0); });
+  mma_round(bar, phase, [&] { issue_fwd(smem_u32(X0), 32, sW + OW1D, 64, tmem + d0); }, ov, 0);
 #pragma unroll
   for (int c = part * C64; c < (part + 1) * C64; c += 16) {
     tmem_ld16(tm_row + d0 + c, v);
@@ -239,7 +249,7 @@ __device__ __forceinline__ FwdRow forward_tile(uint8_t* sw, uint8_t* X0, uint8_t
     put_relu8(X1, r, c / 8 + 1, v + 8);
   }
   // L2d -> sigma, geo (part 0) ; SH(d) (last part)
-  mma_round(bar, phase, [&] { issue_fwd(smem_u32(X1), 64, sW + OW2D, 16, tmem + d1); });
+  mma_round(bar, phase, [&] { issue_fwd(smem_u32(X1), 64, sW + OW2D, 16, tmem + d1); }, ov, 1);
   if (part == 0) {
     tmem_ld16(tm_row + d1, v);
     out.od0 = v[0];
@@ -253,7 +263,7 @@ __device__ __forceinline__ FwdRow forward_tile(uint8_t* sw, uint8_t* X0, uint8_t
     put8(X2, r, 3, v + 8);
   }
   // L1c
-  mma_round(bar, phase, [&] { issue_fwd(smem_u32(X2), 32, sW + OW1C, 64, tmem + d0); });
+  mma_round(bar, phase, [&] { issue_fwd(smem_u32(X2), 32, sW + OW1C, 64, tmem + d0); }, ov, 2);
 #pragma unroll
   for (int c = part * C64; c < (part + 1) * C64; c += 16) {
     tmem_ld16(tm_row + d0 + c, v);
@@ -261,7 +271,7 @@ __device__ __forceinline__ FwdRow forward_tile(uint8_t* sw, uint8_t* X0, uint8_t
     put_relu8(X3, r, c / 8 + 1, v + 8);
   }
   // L2c
-  mma_round(bar, phase, [&] { issue_fwd(smem_u32(X3), 64, sW + OW2C, 64, tmem + d0); });
+  mma_round(bar, phase, [&] { issue_fwd(smem_u32(X3), 64, sW + OW2C, 64, tmem + d0); }, ov, 3);
 #pragma unroll
   for (int c = part * C64; c < (part + 1) * C64; c += 16) {
     tmem_ld16(tm_row + d0 + c, v);
@@ -269,7 +279,7 @@ __device__ __forceinline__ FwdRow forward_tile(uint8_t* sw, uint8_t* X0, uint8_t
     put_relu8(X4, r, c / 8 + 1, v + 8);
   }
   // L3c
-  mma_round(bar, phase, [&] { issue_fwd(smem_u32(X4), 64, sW + OW3C, 16, tmem + d1); });
+  mma_round(bar, phase, [&] { issue_fwd(smem_u32(X4), 64, sW + OW3C, 16, tmem + d1); }, ov, 4);
   if (part == 0) {
     tmem_ld16(tm_row + d1, v);
 #pragma unroll
@@ -295,10 +305,62 @@ constexpr int FWD_TPR = 1;
 constexpr uint32_t F_P = WBYTES, F_Q = F_P + TILE * 64 * 2, F_BAR = F_Q + TILE * 64 * 2,
                    F_SMEM = F_BAR + 16;
 
+// Hash-grid encoding of this thread's row (FUSED forward): 16 levels gathered from the
+// region's table, rounded to fp16, staged into tile P and (optionally) written to enc_out
+// for the backward.  dir returned as float for the SH encoding.
+__device__ __forceinline__ void encode_row(const VrHashGridDesc& g, const float2* __restrict__ table,
+                                           const double* __restrict__ rays, int64_t stride,
+                                           const double* __restrict__ t0,
+                                           const double* __restrict__ t1,
+                                           const int32_t* __restrict__ rid, int64_t n, int64_t i,
+                                           bool valid, uint8_t* P, int r,
+                                           __half2* __restrict__ enc_out, float& dx, float& dy,
+                                           float& dz) {
+  uint4 q[4];
+  __half2* h = reinterpret_cast<__half2*>(q);
+  dx = dy = dz = 0.f;
+  if (valid) {
+    const int64_t ray = rid[i];
+    const double m = sample_mid(t0[i], t1[i]);
+    double o[3], d[3];
+#pragma unroll
+    for (int a = 0; a < 3; ++a) {
+      o[a] = __ldg(rays + a * stride + ray);
+      d[a] = __ldg(rays + (3 + a) * stride + ray);
+    }
+    dx = (float)d[0];
+    dy = (float)d[1];
+    dz = (float)d[2];
+    float u[3];
+    norm_pos_od(g, o, d, m, u);
+#pragma unroll
+    for (int l = 0; l < 16; ++l) {
+      Corners c;
+      level_corners(g, l, u, c);
+      const float2 f = gather_level(table + g.offset[l], c);
+      h[l] = __floats2half2_rn(f.x, f.y);
+    }
+    if (enc_out) {
+#pragma unroll
+      for (int l = 0; l < 16; ++l) enc_out[(int64_t)l * n + i] = h[l];
+    }
+  } else {
+#pragma unroll
+    for (int l = 0; l < 16; ++l) h[l] = __floats2half2_rn(0.f, 0.f);
+  }
+#pragma unroll
+  for (int c = 0; c < 4; ++c) *reinterpret_cast<uint4*>(P + tile_off(TILE, r, c * 8)) = q[c];
+}
+
+// FUSED = true: the kernel computes the hash encoding itself (K2 + K3 in one pass);
+// otherwise it reads enc (level-major half2) produced by vr_hash_fwd.
+template <bool FUSED>
 __global__ void __launch_bounds__(TILE * FWD_TPR, 4)
     k_mlp_fwd_tc(const __half* __restrict__ W, const __half2* __restrict__ enc,
                  const double* __restrict__ rays, int64_t stride, const int32_t* __restrict__ rid,
-                 int64_t n, float4* __restrict__ out) {
+                 int64_t n, float4* __restrict__ out, const VrHashGridDesc g,
+                 const float2* __restrict__ table, const double* __restrict__ t0,
+                 const double* __restrict__ t1, __half2* __restrict__ enc_out) {
   using G = Geo<FWD_TPR>;
   extern __shared__ __align__(1024) uint8_t smem[];
   uint8_t* sw = smem;
@@ -323,9 +385,13 @@ __global__ void __launch_bounds__(TILE * FWD_TPR, 4)
   for (int64_t tile = blockIdx.x; tile < n_tiles; tile += gridDim.x) {
     const int64_t i = tile * TILE + r;
     const bool valid = i < n;
-    stage_enc<FWD_TPR>(P, r, part, enc, n, i, valid);
     float dx, dy, dz;
-    load_dir(rays, stride, rid, i, valid, dx, dy, dz);
+    if (FUSED) {
+      encode_row(g, table, rays, stride, t0, t1, rid, n, i, valid, P, r, enc_out, dx, dy, dz);
+    } else {
+      stage_enc<FWD_TPR>(P, r, part, enc, n, i, valid);
+      load_dir(rays, stride, rid, i, valid, dx, dy, dz);
+    }
     // P(enc) -> Q(h1d) -> P(cin) -> Q(h1c) -> P(h2c)
     const FwdRow f =
         forward_tile<FWD_TPR>(sw, P, Q, P, Q, P, tm_row, tmem, 0, 64, bar, phase, dx, dy, dz);
@@ -355,21 +421,39 @@ constexpr uint32_t T_W1D = 0, T_W2DT = 32, T_W1C = 48, T_W2C = 80, T_W3CT = 144,
 struct RowIn {
   __half2 enc[16 / BWD_TPR];
   float dx, dy, dz;
+  float u[3];  // normalised hash-grid position (FUSED backward only)
   float4 gin;
 };
 
+template <bool FUSED>
 __device__ __forceinline__ void fetch_row(RowIn& x, const __half2* __restrict__ enc,
                                           const double* __restrict__ rays, int64_t stride,
                                           const int32_t* __restrict__ rid,
                                           const float4* __restrict__ dsr, int64_t n, int64_t i,
-                                          int part) {
+                                          int part, const VrHashGridDesc& g,
+                                          const double* __restrict__ t0,
+                                          const double* __restrict__ t1) {
   constexpr int LV = 16 / BWD_TPR;
   const bool valid = i < n;
 #pragma unroll
   for (int l = 0; l < LV; ++l)
     x.enc[l] = valid ? enc[(int64_t)(part * LV + l) * n + i] : __floats2half2_rn(0.f, 0.f);
-  load_dir(rays, stride, rid, i, valid, x.dx, x.dy, x.dz);
   x.gin = (valid && part == 0) ? dsr[i] : make_float4(0.f, 0.f, 0.f, 0.f);
+  x.dx = x.dy = x.dz = 0.f;
+  x.u[0] = x.u[1] = x.u[2] = 0.f;
+  if (valid) {
+    const int64_t ray = rid[i];
+    double o[3], d[3];
+#pragma unroll
+    for (int a = 0; a < 3; ++a) {
+      d[a] = __ldg(rays + (3 + a) * stride + ray);
+      if (FUSED) o[a] = __ldg(rays + a * stride + ray);
+    }
+    x.dx = (float)d[0];
+    x.dy = (float)d[1];
+    x.dz = (float)d[2];
+    if (FUSED) norm_pos_od(g, o, d, sample_mid(t0[i], t1[i]), x.u);
+  }
 }
 
 __device__ __forceinline__ void put_enc(uint8_t* tile, int r, int part, const RowIn& x) {
@@ -380,11 +464,18 @@ __device__ __forceinline__ void put_enc(uint8_t* tile, int r, int part, const Ro
     *reinterpret_cast<uint4*>(tile + tile_off(TILE, r, (part * LV / 4 + c) * 8)) = q[c];
 }
 
+// FUSED = true: instead of writing d(enc) to global memory, each thread scatters its
+// row's hash-grid gradients (its 8 levels) straight from the last epilogue (K3 + K2
+// backward in one pass); the atomics overlap other tiles' tensor-core rounds.
+template <bool FUSED>
 __global__ void __launch_bounds__(TILE * BWD_TPR, 2)
     k_mlp_bwd_tc(const __half* __restrict__ W, const __half2* __restrict__ enc,
                  const double* __restrict__ rays, int64_t stride, const int32_t* __restrict__ rid,
                  int64_t n, const float4* __restrict__ dsr, float* __restrict__ gW,
-                 float2* __restrict__ denc, int32_t* err, int use_lo) {
+                 float2* __restrict__ denc, int32_t* err, int use_lo, const VrHashGridDesc hg,
+                 const RepPlan plan, const double* __restrict__ t0,
+                 const double* __restrict__ t1, float2* __restrict__ grad_table,
+                 float2* __restrict__ rep_ws) {
   using G = Geo<BWD_TPR>;
   extern __shared__ __align__(1024) uint8_t smem[];
   uint8_t* sw = smem;
@@ -450,15 +541,38 @@ __global__ void __launch_bounds__(TILE * BWD_TPR, 2)
     tc_fence_after();
   };
 
+  // deferred hash-grid scatter of the previous tile (FUSED): this thread's 8 levels are
+  // spread over the 5 forward rounds of the next tile (2, 2, 2, 1, 1)
+  bool pending = false;
+  const int gwarp = blockIdx.x * (TILE * BWD_TPR / 32) + (threadIdx.x >> 5);
+  auto scatter_levels = [&](int j0, int j1) {
+    const float* pv = reinterpret_cast<const float*>(Gl) + threadIdx.x * 16;
+    const float4 uu = *reinterpret_cast<const float4*>(reinterpret_cast<const float*>(Gh) +
+                                                       threadIdx.x * 4);
+    const float u[3] = {uu.x, uu.y, uu.z};
+    for (int j = j0; j < j1; ++j)
+      scatter_level(hg, plan, 8 * part + j, u, make_float2(pv[2 * j], pv[2 * j + 1]), gwarp,
+                    grad_table, rep_ws);
+  };
+  auto scatter_ov = [&](int round) {
+    if (FUSED && pending) {
+      const int j0 = round < 3 ? 2 * round : 6 + (round - 3);
+      scatter_levels(j0, round < 3 ? j0 + 2 : j0 + 1);
+      if (round == 4) pending = false;
+    }
+  };
+
   RowIn nxt;
   if ((int64_t)blockIdx.x < n_tiles)
-    fetch_row(nxt, enc, rays, stride, rid, dsr, n, (int64_t)blockIdx.x * TILE + r, part);
+    fetch_row<FUSED>(nxt, enc, rays, stride, rid, dsr, n, (int64_t)blockIdx.x * TILE + r, part,
+                     hg, t0, t1);
   for (int64_t tile = blockIdx.x; tile < n_tiles; tile += gridDim.x) {
     const int64_t i = tile * TILE + r;
     const bool valid = i < n;
     const RowIn cur = nxt;
     if (tile + gridDim.x < n_tiles)  // prefetch the next tile's inputs
-      fetch_row(nxt, enc, rays, stride, rid, dsr, n, (tile + gridDim.x) * TILE + r, part);
+      fetch_row<FUSED>(nxt, enc, rays, stride, rid, dsr, n, (tile + gridDim.x) * TILE + r, part,
+                       hg, t0, t1);
     if (wgrad_pending) {  // the previous tile's last wgrad reads X4/Gh/Gl
       mbar_wait(barB, phB);
       phB ^= 1u;
@@ -467,7 +581,7 @@ __global__ void __launch_bounds__(TILE * BWD_TPR, 2)
     put_enc(A, r, part, cur);
     // forward recompute: A(enc) -> X1(h1d) -> A(cin) -> X3(h1c) -> X4(h2c)
     const FwdRow f = forward_tile<BWD_TPR>(sw, A, X1, A, X3, X4, tm_row, tmem, T_D0, T_D1, barA,
-                                           phA, cur.dx, cur.dy, cur.dz);
+                                           phA, cur.dx, cur.dy, cur.dz, scatter_ov);
     const float4 gin = cur.gin;
     float g[C64];
     float v[16];
@@ -555,9 +669,24 @@ __global__ void __launch_bounds__(TILE * BWD_TPR, 2)
             issue_wgrad(sGh, sX4, 32, tmem + T_W1D, a_w);  // dW1d += dh1d^T enc
             if (use_lo) issue_wgrad(sGl, sX4, 32, tmem + T_W1D, true);
           });
-    // denc -> global, level-major float2 (this thread: levels part*8 .. part*8+7)
+    // d(enc) of this thread's levels part*8 .. part*8+7
     tmem_ld16(tm_row + T_D0 + 16 * part, v);
-    if (valid) {
+    if (FUSED) {
+      // park them in smem (Gl/Gh are free until the next tile's first backward stage,
+      // once this tile's last wgrad has finished reading them); the hash-grid scatter
+      // then runs while the next tile's forward MMAs execute (see scatter_ov)
+      mbar_wait(barB, phB);
+      phB ^= 1u;
+      wgrad_pending = false;
+      float* pv = reinterpret_cast<float*>(Gl) + threadIdx.x * 16;
+#pragma unroll
+      for (int j = 0; j < 16; j += 4)
+        *reinterpret_cast<float4*>(pv + j) = valid ? make_float4(v[j], v[j + 1], v[j + 2], v[j + 3])
+                                                   : make_float4(0.f, 0.f, 0.f, 0.f);
+      float* pu = reinterpret_cast<float*>(Gh) + threadIdx.x * 4;
+      *reinterpret_cast<float4*>(pu) = make_float4(cur.u[0], cur.u[1], cur.u[2], 0.f);
+      pending = true;
+    } else if (valid) {
 #pragma unroll
       for (int j = 0; j < 16; j += 2)
         denc[(int64_t)(8 * part + j / 2) * n + i] = make_float2(v[j], v[j + 1]);
@@ -568,6 +697,7 @@ __global__ void __launch_bounds__(TILE * BWD_TPR, 2)
     mbar_wait(barB, phB);
     phB ^= 1u;
   }
+  if (FUSED && pending) scatter_levels(0, 8);  // the CTA's last tile
   // ---- flush the weight-gradient accumulators (M = 64: row 16q+t at lane 32q+t) -----
   tc_fence_before();
   __syncthreads();
@@ -613,6 +743,82 @@ __global__ void __launch_bounds__(TILE * BWD_TPR, 2)
 
 using namespace vr;
 
+namespace {
+
+template <class K>
+int set_smem(K kernel, uint32_t bytes, bool& done, const char* who) {
+  if (done) return VR_OK;
+  if (cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes) !=
+      cudaSuccess) {
+    set_error(who);
+    return VR_ERR_CUDA;
+  }
+  done = true;
+  return VR_OK;
+}
+
+// VR_MLP_BWD_LO=0 drops the fp16 lo correction of the upstream gradients (half the
+// backward MMAs; gradients then carry fp16 rounding, ~1e-4 relative)
+int bwd_use_lo() {
+  static int use_lo = -1;
+  if (use_lo < 0) {
+    const char* e = getenv("VR_MLP_BWD_LO");
+    use_lo = (e && e[0] == '0') ? 0 : 1;
+  }
+  return use_lo;
+}
+
+template <bool FUSED>
+int launch_fwd(const void* w, const void* enc, const double* rays, int64_t stride,
+               const int32_t* rid, int64_t n, float* out, const VrHashGridDesc* g,
+               const float* table, const double* t0, const double* t1, void* enc_out,
+               void* stream) {
+  static bool attr = false;
+  int rc = set_smem(mlp::k_mlp_fwd_tc<FUSED>, mlp::F_SMEM, attr, "mlp fwd: smem attribute");
+  if (rc != VR_OK) return rc;
+  VrHashGridDesc gd;
+  if (g) gd = *g; else memset(&gd, 0, sizeof(gd));
+  const int64_t tiles = ceil_div(n, mlp::TILE);
+  const int grid = (int)(tiles < VR_NUM_SMS * 4 ? tiles : VR_NUM_SMS * 4);
+  mlp::k_mlp_fwd_tc<FUSED><<<grid, mlp::TILE * mlp::FWD_TPR, mlp::F_SMEM, (cudaStream_t)stream>>>(
+      (const __half*)w, (const __half2*)enc, rays, stride, rid, n, reinterpret_cast<float4*>(out),
+      gd, reinterpret_cast<const float2*>(table), t0, t1, (__half2*)enc_out);
+  return check_launch("vr_mlp_fwd_tc");
+}
+
+template <bool FUSED>
+int launch_bwd(const void* w, const void* enc, const double* rays, int64_t stride,
+               const int32_t* rid, int64_t n, const float* dsr, float* gW, float* denc,
+               int32_t* err, const VrHashGridDesc* g, const double* t0, const double* t1,
+               float* grad_table, void* ws, size_t ws_bytes, void* stream) {
+  static bool attr = false;
+  int rc = set_smem(mlp::k_mlp_bwd_tc<FUSED>, mlp::B_SMEM, attr, "mlp bwd: smem attribute");
+  if (rc != VR_OK) return rc;
+  VrHashGridDesc gd;
+  RepPlan plan;
+  int64_t ws_entries = 0, red = 0;
+  memset(&plan, 0, sizeof(plan));
+  if (g) {
+    gd = *g;
+    plan = hash_rep_plan(g, &ws_entries, &red);
+    if (!ws || ws_bytes < (size_t)ws_entries * sizeof(float2)) plan.n_rep = 0;
+  } else {
+    memset(&gd, 0, sizeof(gd));
+  }
+  const int64_t tiles = ceil_div(n, mlp::TILE);
+  const int grid = (int)(tiles < VR_NUM_SMS * 2 ? tiles : VR_NUM_SMS * 2);
+  mlp::k_mlp_bwd_tc<FUSED><<<grid, mlp::TILE * mlp::BWD_TPR, mlp::B_SMEM, (cudaStream_t)stream>>>(
+      (const __half*)w, (const __half2*)enc, rays, stride, rid, n,
+      reinterpret_cast<const float4*>(dsr), gW, reinterpret_cast<float2*>(denc), err,
+      bwd_use_lo(), gd, plan, t0, t1, reinterpret_cast<float2*>(grad_table),
+      reinterpret_cast<float2*>(ws));
+  rc = check_launch("vr_mlp_bwd_tc");
+  if (rc != VR_OK || !FUSED) return rc;
+  return hash_rep_reduce(&gd, plan, red, grad_table, ws, stream);
+}
+
+}  // namespace
+
 extern "C" int vr_mlp_fwd_tc(const void* w, const void* enc, const double* rays, int64_t stride,
                              const int32_t* rid, int64_t n, float* out, void* stream) {
   if (n < 0 || !w) {
@@ -620,20 +826,8 @@ extern "C" int vr_mlp_fwd_tc(const void* w, const void* enc, const double* rays,
     return VR_ERR_BAD_ARG;
   }
   if (n == 0) return VR_OK;
-  static bool attr = false;
-  if (!attr) {
-    if (cudaFuncSetAttribute(mlp::k_mlp_fwd_tc, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                             (int)mlp::F_SMEM) != cudaSuccess) {
-      set_error("vr_mlp_fwd_tc: smem attribute");
-      return VR_ERR_CUDA;
-    }
-    attr = true;
-  }
-  const int64_t tiles = ceil_div(n, mlp::TILE);
-  const int grid = (int)(tiles < VR_NUM_SMS * 4 ? tiles : VR_NUM_SMS * 4);
-  mlp::k_mlp_fwd_tc<<<grid, mlp::TILE * mlp::FWD_TPR, mlp::F_SMEM, (cudaStream_t)stream>>>(
-      (const __half*)w, (const __half2*)enc, rays, stride, rid, n, reinterpret_cast<float4*>(out));
-  return check_launch("vr_mlp_fwd_tc");
+  return launch_fwd<false>(w, enc, rays, stride, rid, n, out, nullptr, nullptr, nullptr, nullptr,
+                           nullptr, stream);
 }
 
 extern "C" int vr_mlp_bwd_tc(const void* w, const void* enc, const double* rays, int64_t stride,
@@ -644,26 +838,33 @@ extern "C" int vr_mlp_bwd_tc(const void* w, const void* enc, const double* rays,
     return VR_ERR_BAD_ARG;
   }
   if (n == 0) return VR_OK;
-  static bool attr = false;
-  if (!attr) {
-    if (cudaFuncSetAttribute(mlp::k_mlp_bwd_tc, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                             (int)mlp::B_SMEM) != cudaSuccess) {
-      set_error("vr_mlp_bwd_tc: smem attribute");
-      return VR_ERR_CUDA;
-    }
-    attr = true;
+  return launch_bwd<false>(w, enc, rays, stride, rid, n, dsr, gW, denc, err, nullptr, nullptr,
+                           nullptr, nullptr, nullptr, 0, stream);
+}
+
+extern "C" int vr_field_fwd_tc(const VrHashGridDesc* g, const float* table, const void* w,
+                               const double* rays, int64_t stride, const double* t0,
+                               const double* t1, const int32_t* rid, int64_t n, void* enc_out,
+                               float* out, void* stream) {
+  if (!valid_grid(g) || g->n_levels != 16 || n < 0 || !w || !table) {
+    set_error("vr_field_fwd_tc: bad argument");
+    return VR_ERR_BAD_ARG;
   }
-  // VR_MLP_BWD_LO=0 drops the fp16 lo correction of the upstream gradients (half the
-  // backward MMAs; gradients then carry fp16 rounding, ~1e-4 relative)
-  static int use_lo = -1;
-  if (use_lo < 0) {
-    const char* e = getenv("VR_MLP_BWD_LO");
-    use_lo = (e && e[0] == '0') ? 0 : 1;
+  if (n == 0) return VR_OK;
+  return launch_fwd<true>(w, nullptr, rays, stride, rid, n, out, g, table, t0, t1, enc_out,
+                          stream);
+}
+
+extern "C" int vr_field_bwd_tc(const VrHashGridDesc* g, const void* w, const void* enc,
+                               const double* rays, int64_t stride, const double* t0,
+                               const double* t1, const int32_t* rid, int64_t n, const float* dsr,
+                               float* gW, float* grad_table, void* ws, size_t ws_bytes,
+                               int32_t* err, void* stream) {
+  if (!valid_grid(g) || g->n_levels != 16 || n < 0 || !w || !enc || !gW || !grad_table || !err) {
+    set_error("vr_field_bwd_tc: bad argument");
+    return VR_ERR_BAD_ARG;
   }
-  const int64_t tiles = ceil_div(n, mlp::TILE);
-  const int grid = (int)(tiles < VR_NUM_SMS * 2 ? tiles : VR_NUM_SMS * 2);
-  mlp::k_mlp_bwd_tc<<<grid, mlp::TILE * mlp::BWD_TPR, mlp::B_SMEM, (cudaStream_t)stream>>>(
-      (const __half*)w, (const __half2*)enc, rays, stride, rid, n,
-      reinterpret_cast<const float4*>(dsr), gW, reinterpret_cast<float2*>(denc), err, use_lo);
-  return check_launch("vr_mlp_bwd_tc");
+  if (n == 0) return VR_OK;
+  return launch_bwd<true>(w, enc, rays, stride, rid, n, dsr, gW, nullptr, err, g, t0, t1,
+                          grad_table, ws, ws_bytes, stream);
 }

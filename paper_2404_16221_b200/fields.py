@@ -276,9 +276,12 @@ class HashGridMLP(RegionField):
     trainable = True
 
     def __init__(self, cfg: HashGridConfig, box: Aabb, device, seed=0, table_init=1e-4,
-                 table=None, weights=None, mlp_impl: str = "tc"):
-        if mlp_impl not in ("tc", "cuda"):
-            raise ValueError("mlp_impl must be 'tc' (tcgen05 tensor cores) or 'cuda' (reference)")
+                 table=None, weights=None, mlp_impl: str = "fused"):
+        if mlp_impl not in ("fused", "fused_fwd", "tc", "cuda"):
+            raise ValueError(
+                "mlp_impl: 'fused' (default: gather kernel + tcgen05 MLP forward, hash-grid "
+                "backward fused into the tcgen05 MLP backward), 'fused_fwd' (also the forward "
+                "in one kernel), 'tc' (separate kernels) or 'cuda' (CUDA-core reference MLP)")
         self.mlp_impl = mlp_impl
         self.err = torch.zeros(1, dtype=torch.int32, device=device)  # replaced by the pool's
         self.cfg = cfg
@@ -313,14 +316,28 @@ class HashGridMLP(RegionField):
             self._enc = torch.empty(need, dtype=torch.float32, device=dev)  # half2 = 4 B
         return self._enc
 
+    def _workspace(self, dev):
+        if self._hash_ws is None:
+            nbytes = int(_lib.load().vr_hash_bwd_workspace_bytes(_lib.addr(self.desc)))
+            self._hash_ws = torch.zeros(max(nbytes, 16), dtype=torch.uint8, device=dev)
+        return self._hash_ws
+
     def forward(self, rays, t0, t1, ray_id, n, sig_rgb, stream):
         if n == 0:
             return
         enc = self._enc_buf(n, rays.device)
+        if self.mlp_impl == "fused_fwd":  # K2 + K3 in one tensor-core kernel
+            _lib.call("vr_field_fwd_tc", _lib.addr(self.desc), _lib.ptr(self.table),
+                      _lib.ptr(self.weights16), _lib.ptr(rays), rays.shape[1], _lib.ptr(t0),
+                      _lib.ptr(t1), _lib.ptr(ray_id), n, _lib.ptr(enc), _lib.ptr(sig_rgb),
+                      stream)
+            return
+        # measured (c3): the standalone gather kernel (2048 threads/SM) + the tensor-core
+        # MLP beat the fused forward (512 threads/SM left the gathers latency-bound)
         _lib.call("vr_hash_fwd", _lib.addr(self.desc), _lib.ptr(self.table), _lib.ptr(rays),
                   rays.shape[1], _lib.ptr(t0), _lib.ptr(t1), _lib.ptr(ray_id), n,
                   _lib.ptr(enc), stream)
-        _lib.call("vr_mlp_fwd_tc" if self.mlp_impl == "tc" else "vr_mlp_fwd",
+        _lib.call("vr_mlp_fwd" if self.mlp_impl == "cuda" else "vr_mlp_fwd_tc",
                   _lib.ptr(self.weights16), _lib.ptr(enc), _lib.ptr(rays), rays.shape[1],
                   _lib.ptr(ray_id), n, _lib.ptr(sig_rgb), stream)
 
@@ -328,6 +345,14 @@ class HashGridMLP(RegionField):
         if n == 0:
             return
         enc = self._enc  # written by the forward of the same step
+        if self.mlp_impl in ("fused", "fused_fwd"):
+            ws = self._workspace(rays.device)
+            _lib.call("vr_field_bwd_tc", _lib.addr(self.desc), _lib.ptr(self.weights16),
+                      _lib.ptr(enc), _lib.ptr(rays), rays.shape[1], _lib.ptr(t0), _lib.ptr(t1),
+                      _lib.ptr(ray_id), n, _lib.ptr(dsig_rgb), _lib.ptr(self.grad_weights),
+                      _lib.ptr(self.grad_table), _lib.ptr(ws), ws.numel(), _lib.ptr(self.err),
+                      stream)
+            return
         denc = torch.empty(16 * n * 2, dtype=torch.float32, device=rays.device)
         if self.mlp_impl == "tc":
             _lib.call("vr_mlp_bwd_tc", _lib.ptr(self.weights16), _lib.ptr(enc), _lib.ptr(rays),
@@ -337,13 +362,10 @@ class HashGridMLP(RegionField):
             _lib.call("vr_mlp_bwd", _lib.ptr(self.weights16), _lib.ptr(enc), _lib.ptr(rays),
                       rays.shape[1], _lib.ptr(ray_id), n, _lib.ptr(dsig_rgb),
                       _lib.ptr(self.grad_weights), _lib.ptr(denc), stream)
-        if self._hash_ws is None:
-            nbytes = int(_lib.load().vr_hash_bwd_workspace_bytes(_lib.addr(self.desc)))
-            self._hash_ws = torch.zeros(max(nbytes, 16), dtype=torch.uint8, device=rays.device)
+        ws = self._workspace(rays.device)
         _lib.call("vr_hash_bwd", _lib.addr(self.desc), _lib.ptr(rays), rays.shape[1],
                   _lib.ptr(t0), _lib.ptr(t1), _lib.ptr(ray_id), n, _lib.ptr(denc),
-                  _lib.ptr(self.grad_table), _lib.ptr(self._hash_ws), self._hash_ws.numel(),
-                  stream)
+                  _lib.ptr(self.grad_table), _lib.ptr(ws), ws.numel(), stream)
 
     def zero_grad(self):
         self.grad_table.zero_()

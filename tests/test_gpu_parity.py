@@ -237,7 +237,7 @@ def test_nonfinite_packet_raises():
 
 # ---- hash grid + MLP (parity unpinned: checked against oracle/hashmlp_oracle.py) ------
 
-def _hash_setup(log2_T=14, K=2, n_rays=48, seed=0, restriction=False):
+def _hash_setup(log2_T=14, K=2, n_rays=48, seed=0, restriction=False, mlp_impl="fused"):
     rng = np.random.default_rng(seed)
     root = vr.Aabb([-1, -1, -1], [1, 1, 1])
     tree = vr.grid_tree(root, "x" * int(np.log2(K))) if K > 1 else vr.grid_tree(root, "")
@@ -254,7 +254,7 @@ def _hash_setup(log2_T=14, K=2, n_rays=48, seed=0, restriction=False):
                                     (9216, 3, 64)):
                 w[off:off + rows * cols] = rng.normal(size=rows * cols) / np.sqrt(cols)
             weights0 = w
-        f = vr.HashGridMLP(cfg, box, DEV, table=torch.from_numpy(table0.copy()),
+        f = vr.HashGridMLP(cfg, box, DEV, mlp_impl=mlp_impl, table=torch.from_numpy(table0.copy()),
                            weights=torch.from_numpy(weights0.copy()))
         fields.append(f)
         models.append(hmo.HashMLPModel(table0, weights0, log2_T, box.mn, box.mx, max_res=256))
@@ -296,9 +296,11 @@ def test_hash_indices_bit_exact():
         assert np.array_equal(idx.cpu().numpy().astype(np.int64), want)
 
 
+@pytest.mark.parametrize("mlp_impl", ["fused", "fused_fwd", "tc", "cuda"])
 @pytest.mark.parametrize("restriction", [False, True])
-def test_hashmlp_loss_and_grads_match_oracle(restriction):
-    pool, tree, models, rays, targets = _hash_setup(log2_T=14, K=2, restriction=restriction)
+def test_hashmlp_loss_and_grads_match_oracle(restriction, mlp_impl):
+    pool, tree, models, rays, targets = _hash_setup(log2_T=14, K=2, restriction=restriction,
+                                                    mlp_impl=mlp_impl)
     dt = 0.04
     pool.zero_grad()
     loss, out, b = pool.loss_and_grad(rays, targets, dt)
