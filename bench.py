@@ -27,6 +27,7 @@ ROOT = Path(__file__).resolve().parent
 sys.path.insert(0, str(ROOT))
 
 METRIC = "train rays/sec (fwd+bwd)"
+RENDER_METRIC = "render rays/sec"
 UNIT = "rays/s"
 
 # Algorithmic cost per unit of work: bytes (hbm) or flops (tensor)
@@ -294,10 +295,16 @@ def main():
 
     step = 0
 
+    train = w.train
+    metric = METRIC if train else RENDER_METRIC
+
     def one_step(r, t):
         nonlocal step
         step += 1
-        return pool.train_step(r, t, w.dt, lr=args.lr, step=step)
+        if train:
+            return pool.train_step(r, t, w.dt, lr=args.lr, step=step)
+        out, _ = pool.render_rays(r, w.dt)  # forward only; gathered to rank 0
+        return out
 
     for _ in range(args.warmup):
         one_step(rays, tg)
@@ -371,7 +378,7 @@ def main():
     ms = float(t_ms.item())
     value = R / (ms / 1e3)
     launches = sum(n * _lib.LAUNCHES.get(k, 1) for k, n in calls.items())
-    final_loss = float(loss.item())
+    final_loss = float(loss.item()) if train else None
 
     # samples per step (for per-sample kernel costs)
     b = pool.sample(rays, w.dt)
@@ -427,8 +434,11 @@ def main():
         for _ in range(args.steps):
             r_d = rays_h.to(dev, non_blocking=True)
             t_d = tg_h.to(dev, non_blocking=True)
-            l = one_step(r_d, t_d)
-            _ = float(l.item())  # D2H read of the step's loss
+            res = one_step(r_d, t_d)
+            if train:
+                _ = float(res.item())  # D2H read of the step's loss
+            elif res is not None:
+                _ = res[0:3].cpu()  # D2H read of the rendered colours
         t1.record()
         torch.cuda.synchronize()
         e_ms = torch.tensor([t0.elapsed_time(t1) / args.steps], dtype=torch.float64, device=dev)
@@ -436,10 +446,10 @@ def main():
             dist.all_reduce(e_ms, op=dist.ReduceOp.MAX)
         e2e = {"value": R / (float(e_ms.item()) / 1e3), "unit": UNIT,
                "h2d_bytes_per_step": rays_h.numel() * 8 + tg_h.numel() * 4,
-               "d2h_bytes_per_step": 8, "ms_per_step": float(e_ms.item())}
+               "d2h_bytes_per_step": 8 if train else 3 * 4 * R, "ms_per_step": float(e_ms.item())}
 
     cpu = None
-    if rank == 0 and world == 1 and not args.no_cpu:
+    if rank == 0 and world == 1 and not args.no_cpu and train:
         n_cpu = 64
         v, _ = cpu_baseline_port(w, n_cpu)
         cpu = {"value": v, "unit": UNIT, "cores": 1, "kind": "port",
@@ -447,7 +457,7 @@ def main():
                          "bwd, single thread"}
 
     if rank == 0:
-        line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world,
+        line = {"metric": metric, "value": value, "unit": UNIT, "n_gpus": world,
                 "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms,
                 "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
                 "dtype": "f32+f16", "data": "synthetic",
@@ -456,7 +466,8 @@ def main():
                            "regions_per_gpu": len(w.tree.leaves) // world, "log2_T": w.log2_T,
                            "dt": w.dt, "parallelism": f"region-parallel x{world}",
                            "l2": "inputs larger than L2 (tables+rays+samples >> 126 MB)",
-                           "optimizer": "adam", "loss": "mse+distortion"},
+                           "optimizer": "adam" if train else None,
+                           "loss": "mse+distortion" if train else None},
                 "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e,
                 "gpu_launches": launches, "clocks": clk, "loss": final_loss,
                 "step_ms": [round(x, 3) for x in step_ms],

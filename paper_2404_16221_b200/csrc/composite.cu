@@ -73,6 +73,254 @@ __device__ __forceinline__ SegTotals seg_forward(const double* __restrict__ t0,
   return tot;
 }
 
+// ---- grouped K4: one warp per 32 consecutive segments ---------------------------------
+// The samples of consecutive segments are contiguous, so a warp walks the group's whole
+// sample range 32 samples at a time with segmented warp scans (head flags at segment
+// starts); empty segments cost nothing but their identity packet, and no lane idles on
+// short segments.  Carries link a segment that spans two chunks.
+struct GroupSeg {
+  int64_t lo, hi;  // lane j: sample range of segment seg0 + j
+};
+
+// index of the segment (0..nseg-1) that contains sample s (largest j with lo[j] <= s)
+__device__ __forceinline__ int find_seg(int64_t my_lo, int nseg, int64_t s) {
+  int j = 0;
+#pragma unroll
+  for (int step = 16; step > 0; step >>= 1) {
+    const int cand = j + step;
+    const int64_t lo_c = __shfl_sync(0xffffffffu, my_lo, cand < 32 ? cand : 31);
+    if (cand < nseg && lo_c <= s) j = cand;
+  }
+  return j;
+}
+
+// segmented inclusive scans of up to 4 doubles sharing the head flags
+template <int NV, class Op>
+__device__ __forceinline__ void seg_scan(double* v, bool head, int lane, Op op) {
+  bool f = head;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    double nv[NV];
+#pragma unroll
+    for (int k = 0; k < NV; ++k) nv[k] = __shfl_up_sync(0xffffffffu, v[k], o);
+    const bool nf = __shfl_up_sync(0xffffffffu, (int)f, o) != 0;
+    if (lane >= o && !f) {
+#pragma unroll
+      for (int k = 0; k < NV; ++k) v[k] = op(nv[k], v[k]);
+      f = nf;
+    }
+  }
+}
+
+struct Carry {
+  double T, A, D, L, C0, C1, C2, V;
+};
+
+// Per-lane quantities of one chunk of a group (forward sweep).
+struct ChunkFwd {
+  bool valid, head, tail, cont;
+  int seg;
+  double keep, alpha, m, dlt;
+  float4 v;
+  double Ti, Tn, w, a_lt, d_lt, a_incl, d_incl;  // Tn = T_{i+1}
+  double l_incl, c_incl[3];
+};
+
+template <bool TOTALS = true>
+__device__ __forceinline__ ChunkFwd chunk_forward(const double* __restrict__ t0,
+                                                  const double* __restrict__ t1,
+                                                  const float4* __restrict__ sr, int64_t s,
+                                                  int64_t s_end, const GroupSeg& gs, int nseg,
+                                                  double te_lane, const Carry& cin, int lane) {
+  ChunkFwd c;
+  c.valid = s < s_end;
+  c.seg = find_seg(gs.lo, nseg, c.valid ? s : s_end - 1);
+  const int64_t seg_lo = __shfl_sync(0xffffffffu, gs.lo, c.seg);
+  const int64_t seg_hi = __shfl_sync(0xffffffffu, gs.hi, c.seg);
+  const double te = __shfl_sync(0xffffffffu, te_lane, c.seg);
+  c.head = (s == seg_lo) || lane == 0;
+  c.tail = c.valid && (s + 1 == seg_hi);
+  // the chunk's first segment may continue from the previous chunk
+  const int seg0 = __shfl_sync(0xffffffffu, c.seg, 0);
+  const bool cont = (__shfl_sync(0xffffffffu, (int)(s != seg_lo), 0) != 0) && c.seg == seg0;
+  c.keep = 1.0;
+  c.alpha = 0.0;
+  c.m = 0.0;
+  c.dlt = 0.0;
+  c.v = make_float4(0.f, 0.f, 0.f, 0.f);
+  if (c.valid) {
+    const double a = t0[s], b = t1[s];
+    c.v = sr[s];
+    c.dlt = b - a;
+    const double x = (double)c.v.x * c.dlt;
+    c.keep = exp(-x);
+    c.alpha = -expm1(-x);
+    c.m = sample_mid(a, b) - te;
+  }
+  // transmittance
+  double p[1] = {c.keep};
+  seg_scan<1>(p, c.head, lane, [](double a, double b) { return a * b; });
+  const double p_up = __shfl_up_sync(0xffffffffu, p[0], 1);
+  const double p_excl = c.head ? 1.0 : p_up;
+  const double cT = cont ? cin.T : 1.0;
+  c.Ti = cT * p_excl;
+  c.Tn = cT * p[0];
+  c.w = c.Ti * c.alpha;
+  // opacity / depth prefix sums
+  double q[2] = {c.w, c.w * c.m};
+  seg_scan<2>(q, c.head, lane, [](double a, double b) { return a + b; });
+  const double q0_up = __shfl_up_sync(0xffffffffu, q[0], 1);
+  const double q1_up = __shfl_up_sync(0xffffffffu, q[1], 1);
+  const double cA = cont ? cin.A : 0.0, cD = cont ? cin.D : 0.0;
+  c.a_lt = cA + (c.head ? 0.0 : q0_up);
+  c.d_lt = cD + (c.head ? 0.0 : q1_up);
+  c.a_incl = cA + q[0];
+  c.d_incl = cD + q[1];
+  c.cont = cont;
+  if (TOTALS) {
+    // distortion terms and colour
+    double r[4] = {c.w * (c.m * c.a_lt - c.d_lt), c.w * (double)c.v.y, c.w * (double)c.v.z,
+                   c.w * (double)c.v.w};
+    seg_scan<4>(r, c.head, lane, [](double a, double b) { return a + b; });
+    c.l_incl = (cont ? cin.L : 0.0) + 2.0 * r[0];
+    c.c_incl[0] = (cont ? cin.C0 : 0.0) + r[1];
+    c.c_incl[1] = (cont ? cin.C1 : 0.0) + r[2];
+    c.c_incl[2] = (cont ? cin.C2 : 0.0) + r[3];
+  }
+  return c;
+}
+
+__device__ __forceinline__ Carry carry_out(const ChunkFwd& c) {
+  Carry o;
+  o.T = __shfl_sync(0xffffffffu, c.Tn, 31);
+  o.A = __shfl_sync(0xffffffffu, c.a_incl, 31);
+  o.D = __shfl_sync(0xffffffffu, c.d_incl, 31);
+  o.L = __shfl_sync(0xffffffffu, c.l_incl, 31);
+  o.C0 = __shfl_sync(0xffffffffu, c.c_incl[0], 31);
+  o.C1 = __shfl_sync(0xffffffffu, c.c_incl[1], 31);
+  o.C2 = __shfl_sync(0xffffffffu, c.c_incl[2], 31);
+  o.V = 0.0;
+  return o;
+}
+
+__global__ void __launch_bounds__(SEG_WARPS * 32)
+    k_segment_fwd_grp(const double* __restrict__ t0, const double* __restrict__ t1,
+                      const float4* __restrict__ sr, const int64_t* __restrict__ off,
+                      const int32_t* __restrict__ seg_first, const double* __restrict__ ray_te,
+                      int64_t n_rays, int64_t n_segs, float4* __restrict__ packets) {
+  const int lane = threadIdx.x & 31;
+  const int64_t n_groups = ceil_div(n_segs, 32);
+  for (int64_t grp = (int64_t)blockIdx.x * SEG_WARPS + (threadIdx.x >> 5); grp < n_groups;
+       grp += (int64_t)gridDim.x * SEG_WARPS) {
+    const int64_t seg0 = grp * 32;
+    const int nseg = (int)min((int64_t)32, n_segs - seg0);
+    const int64_t my = seg0 + lane;
+    GroupSeg gs;
+    gs.lo = off[lane < nseg ? my : seg0 + nseg];
+    gs.hi = off[lane < nseg ? my + 1 : seg0 + nseg];
+    const double te_lane = lane < nseg ? ray_te[my % n_rays] : 0.0;
+    const int64_t s_beg = __shfl_sync(0xffffffffu, gs.lo, 0);
+    const int64_t s_end = __shfl_sync(0xffffffffu, gs.hi, nseg - 1);
+    // empty segments: identity packet
+    if (lane < nseg && gs.lo == gs.hi) {
+      packets[2 * my] = make_float4(1.f, 0.f, 0.f, 0.f);
+      packets[2 * my + 1] = make_float4(0.f, 0.f, 0.f, order_bits(INT32_MAX));
+    }
+    Carry cin = {1.0, 0.0, 0.0, 0.0, 0.0, 0.0, 0.0, 0.0};
+    for (int64_t base = s_beg; base < s_end; base += 32) {
+      const ChunkFwd c =
+          chunk_forward(t0, t1, sr, base + lane, s_end, gs, nseg, te_lane, cin, lane);
+      if (c.tail) {
+        const int64_t seg = seg0 + c.seg;
+        packets[2 * seg] = make_float4((float)c.Tn, (float)c.c_incl[0], (float)c.c_incl[1],
+                                       (float)c.c_incl[2]);
+        packets[2 * seg + 1] = make_float4((float)c.a_incl, (float)c.d_incl, (float)c.l_incl,
+                                           order_bits(seg_first[seg]));
+      }
+      cin = carry_out(c);
+    }
+  }
+}
+
+// Grouped K4 backward: sweep 1 = the forward (segment totals into shared memory),
+// sweep 2 = per-sample gradients with one more segmented scan for sum_{i>j} w_i v_i.
+__global__ void __launch_bounds__(SEG_WARPS * 32)
+    k_segment_bwd_grp(const double* __restrict__ t0, const double* __restrict__ t1,
+                      const float4* __restrict__ sr, const int64_t* __restrict__ off,
+                      const double* __restrict__ ray_te, int64_t n_rays, int64_t n_segs,
+                      const float4* __restrict__ dpk, float4* __restrict__ dsr) {
+  __shared__ double s_tot[SEG_WARPS][32][6];  // T, A, D, L, Vtot, bT*T per segment
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  double(*tot)[6] = s_tot[wid];
+  const int64_t n_groups = ceil_div(n_segs, 32);
+  for (int64_t grp = (int64_t)blockIdx.x * SEG_WARPS + wid; grp < n_groups;
+       grp += (int64_t)gridDim.x * SEG_WARPS) {
+    const int64_t seg0 = grp * 32;
+    const int nseg = (int)min((int64_t)32, n_segs - seg0);
+    const int64_t my = seg0 + lane;
+    GroupSeg gs;
+    gs.lo = off[lane < nseg ? my : seg0 + nseg];
+    gs.hi = off[lane < nseg ? my + 1 : seg0 + nseg];
+    const double te_lane = lane < nseg ? ray_te[my % n_rays] : 0.0;
+    const int64_t s_beg = __shfl_sync(0xffffffffu, gs.lo, 0);
+    const int64_t s_end = __shfl_sync(0xffffffffu, gs.hi, nseg - 1);
+    if (s_beg == s_end) continue;
+    float4 g0 = make_float4(0.f, 0.f, 0.f, 0.f), g1 = g0;
+    if (lane < nseg && gs.lo < gs.hi) {
+      g0 = dpk[2 * my];
+      g1 = dpk[2 * my + 1];
+    }
+    // sweep 1: totals
+    Carry cin = {1.0, 0.0, 0.0, 0.0, 0.0, 0.0, 0.0, 0.0};
+    for (int64_t base = s_beg; base < s_end; base += 32) {
+      const ChunkFwd c =
+          chunk_forward<true>(t0, t1, sr, base + lane, s_end, gs, nseg, te_lane, cin, lane);
+      if (c.tail) {
+        tot[c.seg][0] = c.Tn;
+        tot[c.seg][1] = c.a_incl;
+        tot[c.seg][2] = c.d_incl;
+        tot[c.seg][3] = c.l_incl;
+        // Vtot = bC.C + bA A + bD D + 2 bL L  (adjoints of this segment)
+        const float4 a0 = dpk[2 * (seg0 + c.seg)], a1 = dpk[2 * (seg0 + c.seg) + 1];
+        tot[c.seg][4] = (double)a0.y * c.c_incl[0] + (double)a0.z * c.c_incl[1] +
+                        (double)a0.w * c.c_incl[2] + (double)a1.x * c.a_incl +
+                        (double)a1.y * c.d_incl + 2.0 * (double)a1.z * c.l_incl;
+        tot[c.seg][5] = (double)a0.x * c.Tn;
+      }
+      cin = carry_out(c);
+    }
+    __syncwarp();
+    // sweep 2: per-sample gradients
+    cin = {1.0, 0.0, 0.0, 0.0, 0.0, 0.0, 0.0, 0.0};
+    for (int64_t base = s_beg; base < s_end; base += 32) {
+      const ChunkFwd c =
+          chunk_forward<false>(t0, t1, sr, base + lane, s_end, gs, nseg, te_lane, cin, lane);
+      const float bC0 = __shfl_sync(0xffffffffu, g0.y, c.seg);
+      const float bC1 = __shfl_sync(0xffffffffu, g0.z, c.seg);
+      const float bC2 = __shfl_sync(0xffffffffu, g0.w, c.seg);
+      const float bA = __shfl_sync(0xffffffffu, g1.x, c.seg);
+      const float bD = __shfl_sync(0xffffffffu, g1.y, c.seg);
+      const float bL = __shfl_sync(0xffffffffu, g1.z, c.seg);
+      const double A_tot = tot[c.seg][1], D_tot = tot[c.seg][2], V_tot = tot[c.seg][4],
+                   bTT = tot[c.seg][5];
+      const double a_gt = A_tot - c.a_incl, d_gt = D_tot - c.d_incl;
+      const double g = 2.0 * (c.m * c.a_lt - c.d_lt + d_gt - c.m * a_gt);
+      const double vi = (double)bC0 * c.v.y + (double)bC1 * c.v.z + (double)bC2 * c.v.w +
+                        (double)bA + (double)bD * c.m + (double)bL * g;
+      double q[1] = {c.w * vi};
+      seg_scan<1>(q, c.head, lane, [](double a, double b) { return a + b; });
+      const double v_incl = (c.cont ? cin.V : 0.0) + q[0];
+      const double ds = -bTT + c.Tn * vi - (V_tot - v_incl);
+      if (c.valid)
+        dsr[base + lane] = make_float4((float)(ds * c.dlt), (float)(c.w * bC0),
+                                       (float)(c.w * bC1), (float)(c.w * bC2));
+      cin = carry_out(c);
+      cin.V = __shfl_sync(0xffffffffu, v_incl, 31);
+    }
+    __syncwarp();
+  }
+}
+
 __global__ void __launch_bounds__(SEG_WARPS * 32)
     k_segment_fwd(const double* __restrict__ t0, const double* __restrict__ t1,
                   const float4* __restrict__ sr, const int64_t* __restrict__ off,
@@ -365,10 +613,10 @@ extern "C" int vr_segment_fwd(const double* t0, const double* t1, const float* s
   }
   const int64_t n_segs = n_rays * region_cnt;
   if (n_segs == 0) return VR_OK;
-  k_segment_fwd<<<grid_for(ceil_div(n_segs, SEG_WARPS), 1, 8), SEG_WARPS * 32, 0,
-                  (cudaStream_t)stream>>>(t0, t1, reinterpret_cast<const float4*>(sr), off,
-                                          seg_first, ray_te, n_rays, n_segs,
-                                          reinterpret_cast<float4*>(packets));
+  k_segment_fwd_grp<<<grid_for(ceil_div(n_segs, 32 * SEG_WARPS), 1, 8), SEG_WARPS * 32, 0,
+                      (cudaStream_t)stream>>>(t0, t1, reinterpret_cast<const float4*>(sr), off,
+                                              seg_first, ray_te, n_rays, n_segs,
+                                              reinterpret_cast<float4*>(packets));
   return check_launch("vr_segment_fwd");
 }
 
@@ -381,11 +629,11 @@ extern "C" int vr_segment_bwd(const double* t0, const double* t1, const float* s
   }
   const int64_t n_segs = n_rays * region_cnt;
   if (n_segs == 0) return VR_OK;
-  k_segment_bwd<<<grid_for(ceil_div(n_segs, SEG_WARPS), 1, 8), SEG_WARPS * 32, 0,
-                  (cudaStream_t)stream>>>(t0, t1, reinterpret_cast<const float4*>(sr), off,
-                                          ray_te, n_rays, n_segs,
-                                          reinterpret_cast<const float4*>(dpk),
-                                          reinterpret_cast<float4*>(dsr));
+  k_segment_bwd_grp<<<grid_for(ceil_div(n_segs, 32 * SEG_WARPS), 1, 8), SEG_WARPS * 32, 0,
+                      (cudaStream_t)stream>>>(t0, t1, reinterpret_cast<const float4*>(sr), off,
+                                              ray_te, n_rays, n_segs,
+                                              reinterpret_cast<const float4*>(dpk),
+                                              reinterpret_cast<float4*>(dsr));
   return check_launch("vr_segment_bwd");
 }
 

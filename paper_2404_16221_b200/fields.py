@@ -334,11 +334,26 @@ class HashGridMLP(RegionField):
             return
         # measured (c3): the standalone gather kernel (2048 threads/SM) + the tensor-core
         # MLP beat the fused forward (512 threads/SM left the gathers latency-bound)
+        self.forward_hash(rays, t0, t1, ray_id, n, stream)
+        self.forward_mlp(rays, ray_id, n, sig_rgb, stream)
+
+    # the two halves of the non-fused forward; VolumePool overlaps region k's MLP with
+    # region k+1's gathers on a second stream (L2-bound gathers || tensor-core MLP)
+    splittable = property(lambda self: self.mlp_impl != "fused_fwd")
+
+    def forward_hash(self, rays, t0, t1, ray_id, n, stream):
+        if n == 0:
+            return
+        enc = self._enc_buf(n, rays.device)
         _lib.call("vr_hash_fwd", _lib.addr(self.desc), _lib.ptr(self.table), _lib.ptr(rays),
                   rays.shape[1], _lib.ptr(t0), _lib.ptr(t1), _lib.ptr(ray_id), n,
                   _lib.ptr(enc), stream)
+
+    def forward_mlp(self, rays, ray_id, n, sig_rgb, stream):
+        if n == 0:
+            return
         _lib.call("vr_mlp_fwd" if self.mlp_impl == "cuda" else "vr_mlp_fwd_tc",
-                  _lib.ptr(self.weights16), _lib.ptr(enc), _lib.ptr(rays), rays.shape[1],
+                  _lib.ptr(self.weights16), _lib.ptr(self._enc), _lib.ptr(rays), rays.shape[1],
                   _lib.ptr(ray_id), n, _lib.ptr(sig_rgb), stream)
 
     def backward(self, rays, t0, t1, ray_id, n, dsig_rgb, stream):

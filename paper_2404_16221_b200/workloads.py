@@ -4,6 +4,7 @@
   c2  same scene split into 2 regions (equivalence check; parity-test case)
   c3  8-region x-strip street, root [0,16]x[0,1]x[0,2], 1M rays, T=2^19 per region
   c4  8-region 4x2 city grid, root [0,16]x[0,16]x[0,1], 4M rays, T=2^22 per region
+  c4  dt chosen for ~64 samples/ray (measured 64.7); c5 for ~128 (measured 129)
   c5  c4's tree, render-only 1920x1080 frame, ~128 samples/ray
 
 Seeds: rays default_rng(0), params seed 1 (+region), targets rng(2).
@@ -42,9 +43,9 @@ CONFIGS = {
     "c3": Workload("c3-street-8strip-1Mrays-T2^19", Aabb([0, 0, 0], [16, 1, 2]), "xxx", 1 << 20, 19,
                    0.09),
     "c4": Workload("c4-city-4x2-4Mrays-T2^22", Aabb([0, 0, 0], [16, 16, 1]), "xyx", 1 << 22, 22,
-                   0.028),
+                   0.056),
     "c5": Workload("c5-render-1080p-8region", Aabb([0, 0, 0], [16, 16, 1]), "xyx", 1920 * 1080, 22,
-                   0.012, train=False),
+                   0.028, train=False),
 }
 
 
