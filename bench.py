@@ -263,6 +263,9 @@ def main():
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--rays", type=int, default=None, help="override rays per step")
+    ap.add_argument("--backend", default="nccl", choices=["nccl", "gloo"],
+                    help="gloo + --same-device: exercise the multi-rank path on one GPU")
+    ap.add_argument("--same-device", action="store_true", help="all ranks on cuda:0 (testing)")
     args = ap.parse_args()
     rank, world, local = dist_env()
 
@@ -277,12 +280,18 @@ def main():
     from paper_2404_16221_b200 import _lib
     from paper_2404_16221_b200.workloads import CONFIGS, make_rays, make_targets
 
+    if args.same_device:
+        local = 0
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
     group = None
     if world > 1:
-        dist.init_process_group("nccl", device_id=dev)
+        if args.backend == "nccl":
+            dist.init_process_group("nccl", device_id=dev)
+        else:
+            dist.init_process_group("gloo")
         group = dist.group.WORLD
+    red_dev = dev if args.backend == "nccl" else torch.device("cpu")
     w = CONFIGS[args.config]
     if args.rays:
         w.n_rays = args.rays
@@ -372,7 +381,7 @@ def main():
     _lib.TIMER = None
     ms_instrumented = p0.elapsed_time(p1) / args.steps
     ms = start.elapsed_time(end) / args.steps
-    t_ms = torch.tensor([ms], dtype=torch.float64, device=dev)
+    t_ms = torch.tensor([ms], dtype=torch.float64, device=red_dev)
     if world > 1:
         dist.all_reduce(t_ms, op=dist.ReduceOp.MAX)
     ms = float(t_ms.item())
@@ -383,7 +392,7 @@ def main():
     # samples per step (for per-sample kernel costs)
     b = pool.sample(rays, w.dt)
     n_samples_rank = b.n_samples
-    n_samples = torch.tensor([n_samples_rank], dtype=torch.int64, device=dev)
+    n_samples = torch.tensor([n_samples_rank], dtype=torch.int64, device=red_dev)
     if world > 1:
         dist.all_reduce(n_samples)
     n_samples = int(n_samples.item())
@@ -441,7 +450,8 @@ def main():
                 _ = res[0:3].cpu()  # D2H read of the rendered colours
         t1.record()
         torch.cuda.synchronize()
-        e_ms = torch.tensor([t0.elapsed_time(t1) / args.steps], dtype=torch.float64, device=dev)
+        e_ms = torch.tensor([t0.elapsed_time(t1) / args.steps], dtype=torch.float64,
+                            device=red_dev)
         if world > 1:
             dist.all_reduce(e_ms, op=dist.ReduceOp.MAX)
         e2e = {"value": R / (float(e_ms.item()) / 1e3), "unit": UNIT,

@@ -21,13 +21,25 @@ def owned_regions(n_regions: int, rank: int, world: int) -> tuple[int, int]:
     return rank * cnt, cnt
 
 
+def _host_staged(group, t: torch.Tensor) -> bool:
+    """gloo moves host memory: stage CUDA tensors through the CPU (tests / single-GPU
+    multi-rank runs); NCCL moves device memory over NVLink directly."""
+    return t.is_cuda and dist.get_backend(group) == "gloo"
+
+
 def all_gather_packets(local: torch.Tensor, group=None, world: int = 1) -> torch.Tensor:
     """[K_own, R, 8] on every rank -> [world*K_own, R, 8] on every rank (training)."""
     if world == 1:
         return local
+    src = local.contiguous()
+    if _host_staged(group, src):
+        cpu = src.cpu()
+        parts = [torch.empty_like(cpu) for _ in range(world)]
+        dist.all_gather(parts, cpu, group=group)
+        return torch.cat(parts, dim=0).to(local.device)
     out = torch.empty((world * local.shape[0],) + tuple(local.shape[1:]), dtype=local.dtype,
                       device=local.device)
-    dist.all_gather_into_tensor(out, local.contiguous(), group=group)
+    dist.all_gather_into_tensor(out, src, group=group)
     return out
 
 
@@ -35,11 +47,15 @@ def gather_packets(local: torch.Tensor, group=None, world: int = 1, rank: int = 
     """Inference: packets only need to reach one compositor rank."""
     if world == 1:
         return local
+    src = local.contiguous()
+    staged = _host_staged(group, src)
+    if staged:
+        src = src.cpu()
     if rank == dst:
-        parts = [torch.empty_like(local) for _ in range(world)]
-        dist.gather(local.contiguous(), gather_list=parts, dst=dst, group=group)
-        return torch.cat(parts, dim=0)
-    dist.gather(local.contiguous(), gather_list=None, dst=dst, group=group)
+        parts = [torch.empty_like(src) for _ in range(world)]
+        dist.gather(src, gather_list=parts, dst=dst, group=group)
+        return torch.cat(parts, dim=0).to(local.device)
+    dist.gather(src, gather_list=None, dst=dst, group=group)
     return None
 
 
