@@ -168,7 +168,13 @@ def build_pool(w, rank, world, dev, group, seed_base=1):
     cfg = vr.HashGridConfig(log2_T=w.log2_T, max_res=w.max_res)
     fields = [vr.HashGridMLP(cfg, tree.leaves[k].box, dev, seed=seed_base + k)
               for k in range(lo, lo + cnt)]
-    return vr.VolumePool(tree, fields, (0.05, 0.05, 0.08), dev, rank, world, group)
+    props = None
+    if w.interlevel > 0:  # config 4: proposal fields for the interlevel loss
+        pcfg = vr.HashGridConfig(log2_T=w.prop_log2_T, max_res=w.prop_max_res)
+        props = [vr.HashGridMLP(pcfg, tree.leaves[k].box, dev, seed=1000 + k)
+                 for k in range(lo, lo + cnt)]
+    return vr.VolumePool(tree, fields, (0.05, 0.05, 0.08), dev, rank, world, group,
+                         proposals=props)
 
 
 def cpu_baseline_port(w, n_rays: int, seed: int = 0, reps: int = 1):
@@ -311,7 +317,8 @@ def main():
         nonlocal step
         step += 1
         if train:
-            return pool.train_step(r, t, w.dt, lr=args.lr, step=step)
+            return pool.train_step(r, t, w.dt, lr=args.lr, step=step,
+                                   lambda_interlevel=w.interlevel)
         out, _ = pool.render_rays(r, w.dt)  # forward only; gathered to rank 0
         return out
 
@@ -327,13 +334,14 @@ def main():
     def f_state(f):
         return [f.table, f.weights] + list(f.adam or [])
 
-    snap = [[t.clone() for t in f_state(f)] for f in pool.fields]
+    all_fields = pool.fields + (pool.proposals or [])
+    snap = [[t.clone() for t in f_state(f)] for f in all_fields]
     snap_step = step
     one_step(rays, tg)  # absorbs the allocator's reaction to the snapshot copies
 
     def restore():
         nonlocal step
-        for f, ts in zip(pool.fields, snap):
+        for f, ts in zip(all_fields, snap):
             for dst, src in zip(f_state(f), ts):
                 dst.copy_(src)
             f.refresh_weights()
@@ -477,7 +485,8 @@ def main():
                            "dt": w.dt, "parallelism": f"region-parallel x{world}",
                            "l2": "inputs larger than L2 (tables+rays+samples >> 126 MB)",
                            "optimizer": "adam" if train else None,
-                           "loss": "mse+distortion" if train else None},
+                           "loss": (("mse+distortion+interlevel" if w.interlevel else
+                                     "mse+distortion") if train else None)},
                 "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e,
                 "gpu_launches": launches, "clocks": clk, "loss": final_loss,
                 "step_ms": [round(x, 3) for x in step_ms],

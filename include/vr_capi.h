@@ -264,6 +264,20 @@ int vr_global_train(const float* packets_dev, int32_t n_regions, int64_t n_rays,
                     const float* targets_dev /*[n_rays][3]*/, float lambda_dist, int32_t own_lo,
                     int32_t own_cnt, float* out_dev, double* ray_loss_dev, float* dpackets_dev,
                     int32_t* err_dev, void* stream);
+/* ---- interlevel (proposal) loss — no reference code (spec in
+ * csrc/interlevel.cu and oracle/grad_oracle.py).  vr_prefix_train: NeRF and proposal
+ * transmittance in front of each owned segment, prefix [own_cnt][n_rays][2] float32,
+ * from the exchanged packets and the exchanged proposal transmittances prop_T
+ * [n_regions][n_rays].  vr_interlevel: per-segment loss (float64 [region_cnt][n_rays])
+ * and d(loss)/d(proposal sigma) into dsig_prop[i].x (float4, other lanes zero). */
+int vr_prefix_train(const float* packets_dev, const float* prop_T_dev, int32_t n_regions,
+                    int64_t n_rays, int32_t own_lo, int32_t own_cnt, float* prefix_dev,
+                    void* stream);
+int vr_interlevel(const double* t0_dev, const double* t1_dev, const float* sig_rgb_dev,
+                  const float* sig_prop_dev, const int64_t* offsets_dev, const float* prefix_dev,
+                  int64_t n_rays, int32_t region_cnt, float lambda_interlevel, float eps,
+                  double* seg_loss_dev, float* dsig_prop_dev, void* stream);
+
 /* deterministic float64 sum (fixed reduction tree) */
 int vr_sum_f64(const double* x_dev, int64_t n, double* out_dev, void* stream);
 

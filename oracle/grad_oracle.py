@@ -103,6 +103,48 @@ def field_loss(tree: vo.Tree, eval_t, rays, targets, bg, dt, lambda_dist=1.0):
     return total, outs
 
 
+def field_loss_interlevel(tree: vo.Tree, eval_t, prop_t, rays, targets, bg, dt,
+                          lambda_dist=1.0, lambda_int=1.0, eps=1e-7):
+    """field_loss plus the interlevel (proposal) loss of csrc/interlevel.cu — PARITY
+    UNPINNED (no reference code).  ``prop_t`` has eval_t's signature (its sigma is used).
+
+        L_int = lambda_int * sum_i max(0, w_i - wh_i)^2 / (w_i + eps)
+        w_i  = sg(P_s) T_i alpha_i   (stop-gradient: trains the proposal only)
+        wh_i = sg(Ph_s) Th_i alphah_i
+    P_s / Ph_s: NeRF / proposal transmittance in front of segment s (constants, like
+    peers' packets in NeRF-XL).  Returns (main + interlevel loss, outs, interlevel part)."""
+    main, outs = field_loss(tree, eval_t, rays, targets, bg, dt, lambda_dist)
+    total = torch.zeros((), dtype=torch.float64)
+    for r in rays:
+        o, d, tn, tf = r[0:3], r[3:6], r[6], r[7]
+        t0, t1, tile = vo.sample_ray(tree, o, d, tn, tf, dt)
+        segs = []
+        for k in sorted(set(tile.tolist())):
+            sel = np.nonzero(tile == k)[0]
+            segs.append((float(t0[sel[0]]), k, sel))
+        segs.sort(key=lambda x: (x[0], x[1]))
+        P = 1.0
+        Ph = 1.0
+        for _, k, sel in segs:
+            a, b = t0[sel], t1[sel]
+            mids = 0.5 * (a + b)
+            pts = np.asarray(o) + mids[:, None] * np.asarray(d)
+            sig, _ = eval_t(k, pts, np.asarray(d))
+            sigh, _ = prop_t(k, pts, np.asarray(d))
+            dl = torch.from_numpy(b - a)
+            alpha = 1.0 - torch.exp(-sig.detach() * dl)
+            Tl = torch.cumprod(torch.cat([torch.ones(1, dtype=torch.float64), 1.0 - alpha]), 0)
+            w = P * Tl[:-1] * alpha
+            alphah = 1.0 - torch.exp(-sigh * dl)
+            Thl = torch.cumprod(torch.cat([torch.ones(1, dtype=torch.float64), 1.0 - alphah]), 0)
+            wh = Ph * Thl[:-1] * alphah
+            dd = torch.clamp(w - wh, min=0.0)
+            total = total + lambda_int * (dd * dd / (w + eps)).sum()
+            P = P * float(Tl[-1])
+            Ph = Ph * float(Thl[-1].detach())
+    return main + total, outs, total
+
+
 def voxel_loss(tree: vo.Tree, grid_doc: dict, region_dens, rays, targets, bg, dt,
                lambda_dist=1.0):
     """Loss with a private density copy per region (segrender.py:175-178);

@@ -129,6 +129,8 @@ SIGNATURES = {
     "vr_segment_bwd": [P, P, P, P, P, I64, I32, P, P, P],
     "vr_global_fwd": [P, I32, I64, P, P, I32, P, P, P],
     "vr_global_train": [P, I32, I64, P, P, P, F32, I32, I32, P, P, P, P, P],
+    "vr_prefix_train": [P, P, I32, I64, I32, I32, P, P],
+    "vr_interlevel": [P, P, P, P, P, P, I64, I32, F32, F32, P, P, P],
     "vr_sum_f64": [P, I64, P, P],
     "vr_adam_step": [P, P, P, P, I64, F32, F32, F32, F32, I32, P],
     "vr_cast_f32_f16": [P, P, I64, P],

@@ -17,7 +17,8 @@ PKG = HERE.parent
 ROOT = PKG.parent
 OUT = PKG / "libvolray_b200.so"
 BUILD = ROOT / "build" / "csrc"
-SOURCES = ["capi.cu", "sampler.cu", "fields.cu", "composite.cu", "hashgrid.cu", "mlp.cu", "mlp_tc.cu"]
+SOURCES = ["capi.cu", "sampler.cu", "fields.cu", "composite.cu", "hashgrid.cu", "mlp.cu", "mlp_tc.cu",
+           "interlevel.cu"]
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 FLAGS = ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC", "--expt-relaxed-constexpr",
          f"-I{ROOT / 'include'}"]

@@ -82,7 +82,7 @@ class VolumePool:
     """GPU-resident analogue of WorkerPool (distsim.py:347-364) for one rank."""
 
     def __init__(self, tree: PartitionTree, fields, background=(0.0, 0.0, 0.0), device=None,
-                 rank: int = 0, world: int = 1, group=None):
+                 rank: int = 0, world: int = 1, group=None, proposals=None):
         self.tree = tree
         self.tree_c = tree.to_c()
         self.n_regions = len(tree.leaves)
@@ -91,10 +91,14 @@ class VolumePool:
         if len(fields) != self.region_cnt:
             raise ValueError(f"need {self.region_cnt} region fields, got {len(fields)}")
         self.fields = list(fields)
+        # optional per-region proposal (density) fields for the interlevel loss
+        self.proposals = list(proposals) if proposals is not None else None
+        if self.proposals is not None and len(self.proposals) != self.region_cnt:
+            raise ValueError("one proposal field per owned region")
         self.background = np.asarray(background, dtype=np.float64)
         self.device = torch.device(device) if device is not None else torch.device("cuda")
         self.err = torch.zeros(1, dtype=torch.int32, device=self.device)
-        for f in self.fields:
+        for f in self.fields + (self.proposals or []):
             if hasattr(f, "err"):
                 f.err = self.err  # kernels of the fields report into the pool's flag word
         self._ws = None
@@ -169,15 +173,16 @@ class VolumePool:
                            ray_total, t0, t1, ray_id, [int(b) for b in bounds])
 
     # ---- fields -------------------------------------------------------------------------
-    def evaluate(self, rays: torch.Tensor, b: SampleBatch) -> torch.Tensor:
+    def evaluate(self, rays: torch.Tensor, b: SampleBatch, fields=None) -> torch.Tensor:
+        fields = self.fields if fields is None else fields
         sig_rgb = torch.empty((max(b.n_samples, 1), 4), dtype=torch.float32, device=self.device)
         s = self._stream()
         # Off by default: measured on c3 the concurrent MLP CTAs (52 KB smem each) shrink the
         # L1 the gathers live on and the step got slower (76.7 vs 67.6 ms).
-        split = (self.overlap_regions and len(self.fields) > 1
-                 and all(getattr(f, "splittable", False) for f in self.fields))
+        split = (self.overlap_regions and len(fields) > 1
+                 and all(getattr(f, "splittable", False) for f in fields))
         if not split:
-            for kk, f in enumerate(self.fields):
+            for kk, f in enumerate(fields):
                 lo, hi = b.region_slice(kk)
                 if hi > lo:
                     f.forward(rays, b.t0[lo:], b.t1[lo:], b.ray_id[lo:], hi - lo, sig_rgb[lo:], s)
@@ -189,7 +194,7 @@ class VolumePool:
             self._side = torch.cuda.Stream(device=self.device)
         side = self._side
         side.wait_stream(main)
-        for kk, f in enumerate(self.fields):
+        for kk, f in enumerate(fields):
             lo, hi = b.region_slice(kk)
             if hi <= lo:
                 continue
@@ -202,9 +207,9 @@ class VolumePool:
         main.wait_stream(side)
         return sig_rgb
 
-    def field_backward(self, rays, b: SampleBatch, dsig_rgb: torch.Tensor) -> None:
+    def field_backward(self, rays, b: SampleBatch, dsig_rgb: torch.Tensor, fields=None) -> None:
         s = self._stream()
-        for kk, f in enumerate(self.fields):
+        for kk, f in enumerate(self.fields if fields is None else fields):
             lo, hi = b.region_slice(kk)
             if hi > lo and f.trainable:
                 f.backward(rays, b.t0[lo:], b.t1[lo:], b.ray_id[lo:], hi - lo, dsig_rgb[lo:], s)
@@ -246,11 +251,13 @@ class VolumePool:
         return self.compose(allp, b, background, clip), b
 
     def loss_and_grad(self, rays, targets, dt: float, lambda_dist: float = 1.0,
-                      background=None):
+                      background=None, lambda_interlevel: float = 0.0, eps: float = 1e-7):
         """Forward + backward of the NeRF-XL loss (segrender.py:198-207 definition:
-        sum over rays of |C + T*bg - target|^2 + lambda * distortion).  Gradients
-        accumulate into the owned region fields; returns (loss [1] float64 device
-        tensor, out [7][R], batch)."""
+        sum over rays of |C + T*bg - target|^2 + lambda * distortion), plus, with
+        proposal fields and lambda_interlevel > 0, the interlevel loss of csrc/interlevel.cu
+        (this rank's segments; multi-rank totals need one scalar all-reduce for logging).
+        Gradients accumulate into the owned region fields; returns (loss [1] float64
+        device tensor, out [7][R], batch)."""
         rays = self.rays_to_device(rays)
         tg = torch.as_tensor(targets, dtype=torch.float32).to(self.device, non_blocking=True)
         tg = tg.reshape(-1, 3).contiguous()
@@ -261,6 +268,12 @@ class VolumePool:
         sig_rgb = self.evaluate(rays, b)
         local = self.local_packets(b, sig_rgb)
         allp = comm.all_gather_packets(local, self.group, self.world)
+        interlevel = self.proposals is not None and lambda_interlevel > 0.0
+        if interlevel:
+            sig_prop = self.evaluate(rays, b, self.proposals)
+            # only the proposal transmittance of each segment crosses the link
+            prop_T = self.local_packets(b, sig_prop)[:, :, 0].contiguous()
+            all_T = comm.all_gather_packets(prop_T, self.group, self.world)
         R = b.n_rays
         out = torch.empty((7, R), dtype=torch.float32, device=self.device)
         ray_loss = torch.empty(R, dtype=torch.float64, device=self.device)
@@ -271,6 +284,21 @@ class VolumePool:
                   _lib.ptr(self.err), s)
         loss = torch.empty(1, dtype=torch.float64, device=self.device)
         _lib.call("vr_sum_f64", _lib.ptr(ray_loss), R, _lib.ptr(loss), s)
+        if interlevel:
+            prefix = torch.empty((b.region_cnt, R, 2), dtype=torch.float32, device=self.device)
+            _lib.call("vr_prefix_train", _lib.ptr(allp), _lib.ptr(all_T), allp.shape[0], R,
+                      self.region_lo, self.region_cnt, _lib.ptr(prefix), s)
+            seg_loss = torch.empty(b.region_cnt * R, dtype=torch.float64, device=self.device)
+            dsig_prop = torch.zeros((max(b.n_samples, 1), 4), dtype=torch.float32,
+                                    device=self.device)
+            _lib.call("vr_interlevel", _lib.ptr(b.t0), _lib.ptr(b.t1), _lib.ptr(sig_rgb),
+                      _lib.ptr(sig_prop), _lib.ptr(b.offsets), _lib.ptr(prefix), R,
+                      b.region_cnt, float(lambda_interlevel), float(eps), _lib.ptr(seg_loss),
+                      _lib.ptr(dsig_prop), s)
+            il = torch.empty(1, dtype=torch.float64, device=self.device)
+            _lib.call("vr_sum_f64", _lib.ptr(seg_loss), seg_loss.numel(), _lib.ptr(il), s)
+            loss = loss + il
+            self.field_backward(rays, b, dsig_prop, self.proposals)
         dsig = torch.zeros((max(b.n_samples, 1), 4), dtype=torch.float32, device=self.device)
         _lib.call("vr_segment_bwd", _lib.ptr(b.t0), _lib.ptr(b.t1), _lib.ptr(sig_rgb),
                   _lib.ptr(b.offsets), _lib.ptr(b.ray_te), R, b.region_cnt, _lib.ptr(dpk),
@@ -279,15 +307,16 @@ class VolumePool:
         return loss, out, b
 
     def zero_grad(self):
-        for f in self.fields:
+        for f in self.fields + (self.proposals or []):
             f.zero_grad()
 
     def train_step(self, rays, targets, dt: float, lr: float = 1e-2, step: int = 1,
-                   lambda_dist: float = 1.0, background=None):
+                   lambda_dist: float = 1.0, background=None, lambda_interlevel: float = 0.0):
         """One training iteration: zero grads, fwd+bwd, Adam.  Returns the device loss."""
         self.zero_grad()
-        loss, _, _ = self.loss_and_grad(rays, targets, dt, lambda_dist, background)
-        for f in self.fields:
+        loss, _, _ = self.loss_and_grad(rays, targets, dt, lambda_dist, background,
+                                        lambda_interlevel)
+        for f in self.fields + (self.proposals or []):
             if f.trainable:
                 f.step(lr, step)
         return loss

@@ -29,6 +29,9 @@ class Workload:
     dt: float
     max_res: int = 2048
     train: bool = True
+    interlevel: float = 0.0  # > 0: per-region proposal fields + interlevel loss weight
+    prop_log2_T: int = 17
+    prop_max_res: int = 512
 
     @property
     def tree(self):
@@ -43,7 +46,7 @@ CONFIGS = {
     "c3": Workload("c3-street-8strip-1Mrays-T2^19", Aabb([0, 0, 0], [16, 1, 2]), "xxx", 1 << 20, 19,
                    0.09),
     "c4": Workload("c4-city-4x2-4Mrays-T2^22", Aabb([0, 0, 0], [16, 16, 1]), "xyx", 1 << 22, 22,
-                   0.056),
+                   0.056, interlevel=1.0),
     "c5": Workload("c5-render-1080p-8region", Aabb([0, 0, 0], [16, 16, 1]), "xyx", 1920 * 1080, 22,
                    0.028, train=False),
 }

@@ -381,3 +381,43 @@ def test_mlp_tensor_core_matches_cuda_core(n):
     assert ((gw_a - gw_b).norm() / gw_a.norm()).item() < 5e-3
     assert ((de_a - de_b).norm() / de_a.norm()).item() < 5e-3
     assert gw_b[_lib.VR_MLP_W3C + 3 * 64:].abs().max().item() == 0.0
+
+
+def test_interlevel_loss_and_proposal_grads_match_oracle():
+    """Interlevel (proposal) loss — parity against oracle/grad_oracle.field_loss_interlevel
+    (parity unpinned: no reference code).  NeRF gradients must be unaffected (w is
+    stop-gradient in the interlevel term)."""
+    rng = np.random.default_rng(7)
+    pool, tree, models, rays, targets = _hash_setup(log2_T=14, K=2, seed=3)
+    cfg = vr.HashGridConfig(log2_T=12, max_res=128)
+    props, pmodels = [], []
+    for k in range(len(tree.leaves)):
+        _, n_entries = hmo.levels(12, max_res=128)
+        table = rng.uniform(-0.3, 0.3, size=(n_entries, 2)).astype(np.float32)
+        w = np.zeros(hmo.NPARAMS, dtype=np.float32)
+        for off, rows, cols in ((0, 64, 32), (2048, 16, 64), (3072, 64, 32), (5120, 64, 64),
+                                (9216, 3, 64)):
+            w[off:off + rows * cols] = rng.normal(size=rows * cols) / np.sqrt(cols)
+        box = tree.leaves[k].box
+        props.append(vr.HashGridMLP(cfg, box, DEV, table=torch.from_numpy(table),
+                                    weights=torch.from_numpy(w)))
+        pmodels.append(hmo.HashMLPModel(table, w, 12, box.mn, box.mx, max_res=128))
+    pool2 = vr.VolumePool(tree, pool.fields, (0.2, 0.3, 0.4), DEV, proposals=props)
+    dt = 0.04
+    pool2.zero_grad()
+    loss, out, b = pool2.loss_and_grad(rays, targets, dt, lambda_interlevel=0.5)
+    torch.cuda.synchronize()
+    pool2.check()
+    otree = vo.Tree(vr.tree_to_json(tree))
+    oloss, oout, oil = grad_oracle.field_loss_interlevel(
+        otree, lambda k, p, d: models[k].eval_t(p, d), lambda k, p, d: pmodels[k].eval_t(p, d),
+        rays.T, targets, (0.2, 0.3, 0.4), dt, 1.0, 0.5)
+    oloss.backward()
+    assert oil.item() > 0.0
+    assert loss.item() == pytest.approx(oloss.item(), rel=1e-5)
+    for kk in range(len(tree.leaves)):
+        for f, m in ((pool2.fields[kk], models[kk]), (props[kk], pmodels[kk])):
+            gt, gw = m.grads()
+            rel_t = np.linalg.norm(f.grad_table.cpu().numpy() - gt) / max(np.linalg.norm(gt), 1e-30)
+            rel_w = np.linalg.norm(f.grad_weights.cpu().numpy() - gw) / max(np.linalg.norm(gw), 1e-30)
+            assert rel_t <= 1e-3 and rel_w <= 1e-3, (kk, rel_t, rel_w)
