@@ -166,7 +166,8 @@ def build_pool(w, rank, world, dev, group, seed_base=1):
     tree = w.tree
     lo, cnt = vr.owned_regions(len(tree.leaves), rank, world)
     cfg = vr.HashGridConfig(log2_T=w.log2_T, max_res=w.max_res)
-    fields = [vr.HashGridMLP(cfg, tree.leaves[k].box, dev, seed=seed_base + k)
+    impl = os.environ.get("VR_BENCH_MLP_IMPL", "fused")  # kernel experiments only
+    fields = [vr.HashGridMLP(cfg, tree.leaves[k].box, dev, seed=seed_base + k, mlp_impl=impl)
               for k in range(lo, lo + cnt)]
     props = None
     if w.interlevel > 0:  # config 4: proposal fields for the interlevel loss

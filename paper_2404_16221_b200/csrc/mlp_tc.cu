@@ -20,9 +20,15 @@
 //   recompute the forward keeping h1d, cin, h1c, h2c in smem (enc is re-staged from
 //   global memory for the last stage, so its slot is reused for cin);
 //   for each layer the upstream gradient G (fp32 registers) is written to smem as an
-//   fp16 hi tile and an fp16 lo tile (G = hi + lo to ~22 bits) and ONE round issues
-//       dW += Ghi^T X + Glo^T X    (M = 64, both operands MN-major, K = 128 samples)
-//       dX  = Ghi . W  + Glo . W   (M = 128, A K-major, B = W read MN-major).
+//   fp16 hi part and an fp16 lo part (G = hi + lo to ~22 bits) and ONE round issues
+//       dX  = Ghi . W  + Glo . W   (M = 128, A K-major, B = W read MN-major)
+//       dW += [Ghi | Glo]^T X      (one MMA, both operands MN-major, K = 128 samples).
+//   The weight-gradient MMA stacks hi and lo instead of issuing two M = 64 MMAs (an
+//   M = 64 dispatch costs as much as M = 128): for 64-wide G the hi and lo tiles are
+//   adjacent in smem and form one M = 128 A operand (accumulator rows 64..127 hold the lo
+//   products); for 16-wide G the lo part sits in columns 16..31 of the hi tile and the
+//   stacked operand is B with N = 32.  The halves are summed when the accumulators are
+//   flushed.
 //   Activations and weights are exactly fp16 by definition of the model, so the
 //   backward is accurate to fp32 accumulation.  |g| >= 65504 raises VR_FLAG_OVERFLOW.
 #include <stdlib.h>
@@ -80,11 +86,12 @@ __device__ __forceinline__ void issue_dgrad(uint32_t g, int K, uint32_t w, int N
             (accumulate || kb > 0) ? 1u : 0u);
 }
 
-// Acc[M=64 x N] (+)= A^T . B over the 128 samples: A tile [128 x 64] (cols = M),
-// B tile [128 x N] (cols = N), both MN-major with K = rows.
-__device__ __forceinline__ void issue_wgrad(uint32_t a, uint32_t b, int N, uint32_t d,
+// Acc[M x N] (+)= A^T . B over the 128 samples: A tile [128 x M] (cols = M), B tile
+// [128 x N] (cols = N), both MN-major with K = rows (an M = 128 A spans two adjacent
+// 64-column tiles, an N = 32 B the first 32 columns of one tile).
+__device__ __forceinline__ void issue_wgrad(uint32_t a, int M, uint32_t b, int N, uint32_t d,
                                             bool accumulate) {
-  const uint32_t id = idesc_f16(64, N, 1, 1);
+  const uint32_t id = idesc_f16(M, N, 1, 1);
   for (int kb = 0; kb < TILE / 16; ++kb)
     mma_f16(d, desc_mn(a, TILE, 2 * kb), desc_mn(b, TILE, 2 * kb), id,
             (accumulate || kb > 0) ? 1u : 0u);
@@ -138,7 +145,7 @@ __device__ __forceinline__ void relu_mask8(const uint8_t* tile, int r, int cb, c
 }
 // fp16 hi/lo split of 8 gradients into Gh / Gl (column block cb)
 __device__ __forceinline__ void put_grad8(uint8_t* Gh, uint8_t* Gl, int r, int cb, const float* g,
-                                          uint32_t& inf_bits, int use_lo) {
+                                          uint32_t& inf_bits) {
   uint4 qh, ql;
   __half2* hh = reinterpret_cast<__half2*>(&qh);
   __half2* hl = reinterpret_cast<__half2*>(&ql);
@@ -152,7 +159,7 @@ __device__ __forceinline__ void put_grad8(uint8_t* Gh, uint8_t* Gl, int r, int c
     inf_bits |= ((u & 0x7C00u) == 0x7C00u) | ((u & 0x7C000000u) == 0x7C000000u);
   }
   *reinterpret_cast<uint4*>(Gh + tile_off(TILE, r, cb * 8)) = qh;
-  if (use_lo) *reinterpret_cast<uint4*>(Gl + tile_off(TILE, r, cb * 8)) = ql;
+  *reinterpret_cast<uint4*>(Gl + tile_off(TILE, r, cb * 8)) = ql;
 }
 
 __device__ __forceinline__ void tmem_ld8(uint32_t taddr, float* v) {
@@ -413,9 +420,13 @@ constexpr uint32_t B_A = WBYTES, B_X1 = B_A + TILE * 32 * 2, B_X3 = B_X1 + TILE 
                    B_X4 = B_X3 + TILE * 64 * 2, B_GH = B_X4 + TILE * 64 * 2,
                    B_GL = B_GH + TILE * 64 * 2, B_BAR = B_GL + TILE * 64 * 2,
                    B_SMEM = B_BAR + 32;
-// TMEM columns: weight-gradient accumulators (M = 64) then scratch
-constexpr uint32_t T_W1D = 0, T_W2DT = 32, T_W1C = 48, T_W2C = 80, T_W3CT = 144, T_D0 = 160,
-                   T_D1 = 224, T_COLS = 256;
+// TMEM columns: weight-gradient accumulators, then scratch.  W1d, W1c, W2c: M = 128
+// (rows 0..63 hi, 64..127 lo products); W2d^T, W3c^T: M = 64, columns [hi 16 | lo 16].
+// The forward's second scratch slice aliases the first (its results are consumed before
+// the next round is issued).
+constexpr uint32_t T_W1D = 0, T_W2DT = 32, T_W1C = 64, T_W2C = 96, T_W3CT = 160, T_D0 = 192,
+                   T_D1 = T_D0, T_COLS = 256;
+static_assert(B_GL == B_GH + TILE * 64 * 2, "stacked wgrad operand needs Gl right after Gh");
 
 // Inputs of one row for one tile, prefetched into registers one tile ahead.
 struct RowIn {
@@ -472,10 +483,10 @@ __global__ void __launch_bounds__(TILE * BWD_TPR, 2)
     k_mlp_bwd_tc(const __half* __restrict__ W, const __half2* __restrict__ enc,
                  const double* __restrict__ rays, int64_t stride, const int32_t* __restrict__ rid,
                  int64_t n, const float4* __restrict__ dsr, float* __restrict__ gW,
-                 float2* __restrict__ denc, int32_t* err, int use_lo, const VrHashGridDesc hg,
+                 float2* __restrict__ denc, int32_t* err, const VrHashGridDesc hg,
                  const RepPlan plan, const double* __restrict__ t0,
                  const double* __restrict__ t1, float2* __restrict__ grad_table,
-                 float2* __restrict__ rep_ws) {
+                 float2* __restrict__ rep_ws, int do_scatter) {
   using G = Geo<BWD_TPR>;
   extern __shared__ __align__(1024) uint8_t smem[];
   uint8_t* sw = smem;
@@ -504,7 +515,7 @@ __global__ void __launch_bounds__(TILE * BWD_TPR, 2)
   const uint32_t tm_row = tmem + G::lane_base();
   const uint32_t sW = smem_u32(sw);
   const uint32_t sA = smem_u32(A), sX1 = smem_u32(X1), sX3 = smem_u32(X3), sX4 = smem_u32(X4),
-                 sGh = smem_u32(Gh), sGl = smem_u32(Gl);
+                 sGh = smem_u32(Gh), sGl = smem_u32(Gl), sGh16 = sGh + 2 * TILE * 16;
   uint32_t phA = 0, phB = 0;
   bool wgrad_pending = false;
   uint32_t inf_bits = 0;
@@ -516,14 +527,14 @@ __global__ void __launch_bounds__(TILE * BWD_TPR, 2)
   // one backward stage: wait until the previous wgrad released G, write G = hi + lo,
   // issue dX = G.W (commit -> barA) then dW += G^T X (commit -> barB), wait for dX only;
   // the wgrad MMAs overlap the following epilogue.
-  auto stage = [&](const float* g, int width_here, int col0, auto issue_dgrad_fn,
-                   auto issue_wgrad_fn) {
+  auto stage = [&](const float* g, int width_here, int col0, bool total16, auto issue_dgrad_fn,
+                   auto issue_wgrad_fn, auto overlap_fn) {
     if (wgrad_pending) {
       mbar_wait(barB, phB);
       phB ^= 1u;
     }
-    for (int c = 0; c < width_here; c += 8)
-      put_grad8(Gh, Gl, r, (col0 + c) / 8, g + c, inf_bits, use_lo);
+    for (int c = 0; c < width_here; c += 8)  // 16-wide G: lo part -> Gh columns 16..31
+      put_grad8(Gh, total16 ? Gh + 2 * TILE * 16 : Gl, r, (col0 + c) / 8, g + c, inf_bits);
     fence_async_smem();
     tc_fence_before();
     __syncthreads();
@@ -535,32 +546,26 @@ __global__ void __launch_bounds__(TILE * BWD_TPR, 2)
       mma_commit(barB);
     }
     wgrad_pending = true;
+    overlap_fn();
     mbar_wait(barA, phA);
     phA ^= 1u;
     __syncwarp();
     tc_fence_after();
   };
 
-  // deferred hash-grid scatter of the previous tile (FUSED): this thread's 8 levels are
-  // spread over the 5 forward rounds of the next tile (2, 2, 2, 1, 1)
+  // deferred hash-grid scatter of the previous tile (FUSED): its d(enc) (this thread's
+  // 8 levels) and position are parked in registers and one level is scattered in each of
+  // the next tile's first 8 tensor-core waits (5 forward rounds, backward stages 1-3), so
+  // the atomics stream through the whole tile instead of bunching up
   bool pending = false;
+  float pk[16], pu[3];
   const int gwarp = blockIdx.x * (TILE * BWD_TPR / 32) + (threadIdx.x >> 5);
-  auto scatter_levels = [&](int j0, int j1) {
-    const float* pv = reinterpret_cast<const float*>(Gl) + threadIdx.x * 16;
-    const float4 uu = *reinterpret_cast<const float4*>(reinterpret_cast<const float*>(Gh) +
-                                                       threadIdx.x * 4);
-    const float u[3] = {uu.x, uu.y, uu.z};
-    for (int j = j0; j < j1; ++j)
-      scatter_level(hg, plan, 8 * part + j, u, make_float2(pv[2 * j], pv[2 * j + 1]), gwarp,
+  auto scatter_one = [&](int j) {
+    if (FUSED && pending && do_scatter)
+      scatter_level(hg, plan, 8 * part + j, pu, make_float2(pk[2 * j], pk[2 * j + 1]), gwarp,
                     grad_table, rep_ws);
   };
-  auto scatter_ov = [&](int round) {
-    if (FUSED && pending) {
-      const int j0 = round < 3 ? 2 * round : 6 + (round - 3);
-      scatter_levels(j0, round < 3 ? j0 + 2 : j0 + 1);
-      if (round == 4) pending = false;
-    }
-  };
+  auto scatter_ov = [&](int round) { scatter_one(round); };
 
   RowIn nxt;
   if ((int64_t)blockIdx.x < n_tiles)
@@ -595,15 +600,13 @@ __global__ void __launch_bounds__(TILE * BWD_TPR, 2)
       g[1] = gin.z * f.rgb[1] * (1.f - f.rgb[1]);
       g[2] = gin.w * f.rgb[2] * (1.f - f.rgb[2]);
     }
-    stage(g, C16, c16,
+    stage(g, C16, c16, true,
           [&] {
             issue_dgrad(sGh, 16, sW + OW3C, 64, tmem + T_D0, false);  // g_o . W3c
-            if (use_lo) issue_dgrad(sGl, 16, sW + OW3C, 64, tmem + T_D0, true);
+            issue_dgrad(sGh16, 16, sW + OW3C, 64, tmem + T_D0, true);
           },
-          [&] {
-            issue_wgrad(sX4, sGh, 16, tmem + T_W3CT, a_w);  // dW3c^T += h2c^T g_o
-            if (use_lo) issue_wgrad(sX4, sGl, 16, tmem + T_W3CT, true);
-          });
+          [&] { issue_wgrad(sX4, 64, sGh, 32, tmem + T_W3CT, a_w); },  // dW3c^T += h2c^T g_o
+          [&] { scatter_one(5); });
     // dh2c = (g_o . W3c) * relu'(h2c)
 #pragma unroll
     for (int c = 0; c < C64; c += 16) {
@@ -611,15 +614,13 @@ __global__ void __launch_bounds__(TILE * BWD_TPR, 2)
       relu_mask8(X4, r, (c64 + c) / 8, v, g + c);
       relu_mask8(X4, r, (c64 + c) / 8 + 1, v + 8, g + c + 8);
     }
-    stage(g, C64, c64,
+    stage(g, C64, c64, false,
           [&] {
             issue_dgrad(sGh, 64, sW + OW2C, 64, tmem + T_D0, false);  // dh2c . W2c
-            if (use_lo) issue_dgrad(sGl, 64, sW + OW2C, 64, tmem + T_D0, true);
+            issue_dgrad(sGl, 64, sW + OW2C, 64, tmem + T_D0, true);
           },
-          [&] {
-            issue_wgrad(sGh, sX3, 64, tmem + T_W2C, a_w);  // dW2c += dh2c^T h1c
-            if (use_lo) issue_wgrad(sGl, sX3, 64, tmem + T_W2C, true);
-          });
+          [&] { issue_wgrad(sGh, 128, sX3, 64, tmem + T_W2C, a_w); },  // dW2c += dh2c^T h1c
+          [&] { scatter_one(6); });
     // dh1c = (dh2c . W2c) * relu'(h1c)
 #pragma unroll
     for (int c = 0; c < C64; c += 16) {
@@ -629,30 +630,26 @@ __global__ void __launch_bounds__(TILE * BWD_TPR, 2)
     }
     // the stage-1 wgrad (reads X4) is complete once stage() below has waited on barB;
     // enc is re-staged into X4 after that, before stage 5 needs it
-    stage(g, C64, c64,
+    stage(g, C64, c64, false,
           [&] {
             issue_dgrad(sGh, 64, sW + OW1C, 32, tmem + T_D0, false);  // dh1c . W1c
-            if (use_lo) issue_dgrad(sGl, 64, sW + OW1C, 32, tmem + T_D0, true);
+            issue_dgrad(sGl, 64, sW + OW1C, 32, tmem + T_D0, true);
           },
-          [&] {
-            issue_wgrad(sGh, sA, 32, tmem + T_W1C, a_w);  // dW1c += dh1c^T cin
-            if (use_lo) issue_wgrad(sGl, sA, 32, tmem + T_W1C, true);
-          });
+          [&] { issue_wgrad(sGh, 128, sA, 32, tmem + T_W1C, a_w); },  // dW1c += dh1c^T cin
+          [&] { scatter_one(7); });
     put_enc(X4, r, part, cur);
     // d od = dcin[0:16]; + dsigma * sigma on od0 (trunc-exp inside the clamp range)
     tmem_ld8(tm_row + T_D0 + c16, v);
 #pragma unroll
     for (int j = 0; j < C16; ++j) g[j] = v[j];
     if (part == 0 && f.od0 > -15.f && f.od0 < 15.f) g[0] += gin.x * f.sigma;
-    stage(g, C16, c16,
+    stage(g, C16, c16, true,
           [&] {
             issue_dgrad(sGh, 16, sW + OW2D, 64, tmem + T_D0, false);  // dod . W2d
-            if (use_lo) issue_dgrad(sGl, 16, sW + OW2D, 64, tmem + T_D0, true);
+            issue_dgrad(sGh16, 16, sW + OW2D, 64, tmem + T_D0, true);
           },
-          [&] {
-            issue_wgrad(sX1, sGh, 16, tmem + T_W2DT, a_w);  // dW2d^T += h1d^T dod
-            if (use_lo) issue_wgrad(sX1, sGl, 16, tmem + T_W2DT, true);
-          });
+          [&] { issue_wgrad(sX1, 64, sGh, 32, tmem + T_W2DT, a_w); },  // dW2d^T += h1d^T dod
+          [] {});
     // dh1d = (dod . W2d) * relu'(h1d)
 #pragma unroll
     for (int c = 0; c < C64; c += 16) {
@@ -660,31 +657,21 @@ __global__ void __launch_bounds__(TILE * BWD_TPR, 2)
       relu_mask8(X1, r, (c64 + c) / 8, v, g + c);
       relu_mask8(X1, r, (c64 + c) / 8 + 1, v + 8, g + c + 8);
     }
-    stage(g, C64, c64,
+    stage(g, C64, c64, false,
           [&] {
             issue_dgrad(sGh, 64, sW + OW1D, 32, tmem + T_D0, false);  // denc = dh1d . W1d
-            if (use_lo) issue_dgrad(sGl, 64, sW + OW1D, 32, tmem + T_D0, true);
+            issue_dgrad(sGl, 64, sW + OW1D, 32, tmem + T_D0, true);
           },
-          [&] {
-            issue_wgrad(sGh, sX4, 32, tmem + T_W1D, a_w);  // dW1d += dh1d^T enc
-            if (use_lo) issue_wgrad(sGl, sX4, 32, tmem + T_W1D, true);
-          });
+          [&] { issue_wgrad(sGh, 128, sX4, 32, tmem + T_W1D, a_w); },  // dW1d += dh1d^T enc
+          [] {});
     // d(enc) of this thread's levels part*8 .. part*8+7
     tmem_ld16(tm_row + T_D0 + 16 * part, v);
     if (FUSED) {
-      // park them in smem (Gl/Gh are free until the next tile's first backward stage,
-      // once this tile's last wgrad has finished reading them); the hash-grid scatter
-      // then runs while the next tile's forward MMAs execute (see scatter_ov)
-      mbar_wait(barB, phB);
-      phB ^= 1u;
-      wgrad_pending = false;
-      float* pv = reinterpret_cast<float*>(Gl) + threadIdx.x * 16;
 #pragma unroll
-      for (int j = 0; j < 16; j += 4)
-        *reinterpret_cast<float4*>(pv + j) = valid ? make_float4(v[j], v[j + 1], v[j + 2], v[j + 3])
-                                                   : make_float4(0.f, 0.f, 0.f, 0.f);
-      float* pu = reinterpret_cast<float*>(Gh) + threadIdx.x * 4;
-      *reinterpret_cast<float4*>(pu) = make_float4(cur.u[0], cur.u[1], cur.u[2], 0.f);
+      for (int j = 0; j < 16; ++j) pk[j] = valid ? v[j] : 0.f;
+      pu[0] = cur.u[0];
+      pu[1] = cur.u[1];
+      pu[2] = cur.u[2];
       pending = true;
     } else if (valid) {
 #pragma unroll
@@ -697,35 +684,39 @@ __global__ void __launch_bounds__(TILE * BWD_TPR, 2)
     mbar_wait(barB, phB);
     phB ^= 1u;
   }
-  if (FUSED && pending) scatter_levels(0, 8);  // the CTA's last tile
+  if (FUSED && pending) {  // the CTA's last tile
+#pragma unroll
+    for (int j = 0; j < 8; ++j) scatter_one(j);
+  }
   // ---- flush the weight-gradient accumulators (M = 64: row 16q+t at lane 32q+t) -----
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
   if (acc) {
+    // M = 128 accumulators: row 32*wq + lane (rows >= 64 hold the lo products of row - 64)
+    const int m2 = (wq * 32 + lane) & 63;
+    // M = 64 accumulators: row 16q+t at lane 32q+t; columns [hi 16 | lo 16]
     const int m = wq * 16 + lane;  // valid for lane < 16
-    float v[16];
+    float v[16], w[16];
     // this warp's column half of each accumulator
     tmem_ld16(tm_row + T_W1D + 16 * part, v);
-    if (lane < 16)
-      for (int j = 0; j < 16; ++j) atomicAdd(gW + VR_MLP_W1D + m * 32 + 16 * part + j, v[j]);
+    for (int j = 0; j < 16; ++j) atomicAdd(gW + VR_MLP_W1D + m2 * 32 + 16 * part + j, v[j]);
     tmem_ld8(tm_row + T_W2DT + 8 * part, v);
+    tmem_ld8(tm_row + T_W2DT + 16 + 8 * part, w);
     if (lane < 16)
-      for (int j = 0; j < 8; ++j) atomicAdd(gW + VR_MLP_W2D + (8 * part + j) * 64 + m, v[j]);
+      for (int j = 0; j < 8; ++j) atomicAdd(gW + VR_MLP_W2D + (8 * part + j) * 64 + m, v[j] + w[j]);
     tmem_ld16(tm_row + T_W1C + 16 * part, v);
-    if (lane < 16)
-      for (int j = 0; j < 16; ++j) atomicAdd(gW + VR_MLP_W1C + m * 32 + 16 * part + j, v[j]);
+    for (int j = 0; j < 16; ++j) atomicAdd(gW + VR_MLP_W1C + m2 * 32 + 16 * part + j, v[j]);
 #pragma unroll
     for (int c = 0; c < 32; c += 16) {
       tmem_ld16(tm_row + T_W2C + 32 * part + c, v);
-      if (lane < 16)
-        for (int j = 0; j < 16; ++j)
-          atomicAdd(gW + VR_MLP_W2C + m * 64 + 32 * part + c + j, v[j]);
+      for (int j = 0; j < 16; ++j) atomicAdd(gW + VR_MLP_W2C + m2 * 64 + 32 * part + c + j, v[j]);
     }
     if (part == 0) {
       tmem_ld8(tm_row + T_W3CT, v);
+      tmem_ld8(tm_row + T_W3CT + 16, w);
       if (lane < 16)
-        for (int j = 0; j < 3; ++j) atomicAdd(gW + VR_MLP_W3C + j * 64 + m, v[j]);
+        for (int j = 0; j < 3; ++j) atomicAdd(gW + VR_MLP_W3C + j * 64 + m, v[j] + w[j]);
     }
   }
   const int flags = inf_bits ? VR_FLAG_OVERFLOW : 0;
@@ -755,17 +746,6 @@ int set_smem(K kernel, uint32_t bytes, bool& done, const char* who) {
   }
   done = true;
   return VR_OK;
-}
-
-// VR_MLP_BWD_LO=0 drops the fp16 lo correction of the upstream gradients (half the
-// backward MMAs; gradients then carry fp16 rounding, ~1e-4 relative)
-int bwd_use_lo() {
-  static int use_lo = -1;
-  if (use_lo < 0) {
-    const char* e = getenv("VR_MLP_BWD_LO");
-    use_lo = (e && e[0] == '0') ? 0 : 1;
-  }
-  return use_lo;
 }
 
 template <bool FUSED>
@@ -809,9 +789,8 @@ int launch_bwd(const void* w, const void* enc, const double* rays, int64_t strid
   const int grid = (int)(tiles < VR_NUM_SMS * 2 ? tiles : VR_NUM_SMS * 2);
   mlp::k_mlp_bwd_tc<FUSED><<<grid, mlp::TILE * mlp::BWD_TPR, mlp::B_SMEM, (cudaStream_t)stream>>>(
       (const __half*)w, (const __half2*)enc, rays, stride, rid, n,
-      reinterpret_cast<const float4*>(dsr), gW, reinterpret_cast<float2*>(denc), err,
-      bwd_use_lo(), gd, plan, t0, t1, reinterpret_cast<float2*>(grad_table),
-      reinterpret_cast<float2*>(ws));
+      reinterpret_cast<const float4*>(dsr), gW, reinterpret_cast<float2*>(denc), err, gd, plan, t0, t1, reinterpret_cast<float2*>(grad_table),
+      reinterpret_cast<float2*>(ws), getenv("VR_DEBUG_NOSCATTER") ? 0 : 1);
   rc = check_launch("vr_mlp_bwd_tc");
   if (rc != VR_OK || !FUSED) return rc;
   return hash_rep_reduce(&gd, plan, red, grad_table, ws, stream);
