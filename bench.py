@@ -32,23 +32,31 @@ UNIT = "rays/s"
 
 # Algorithmic cost per unit of work: bytes (hbm) or flops (tensor)
 # per sample for the per-sample kernels.
+# entry point -> (bound, algorithmic bytes or flops per sample, index of the sample-count
+# argument in the C-ABI call); bench sums the samples each launch processed
 KERNEL_COST = {
     # t0,t1 (16) + ray id (4) + 16 levels x 8 corners x float2 (1024) + enc fp16 (64)
-    "vr_hash_fwd": ("hbm", 1108.0),
+    "vr_hash_fwd": ("hbm", 1108.0, 7),
     # t0,t1,ray id (20) + denc f32 (128) + 16 x 8 float2 atomics (1024)
-    "vr_hash_bwd": ("hbm", 1172.0),
+    "vr_hash_bwd": ("hbm", 1172.0, 6),
+    # level-major: pos (12 per level read) + 8 float2 gathers (64) + enc (4), x 16 levels
+    "vr_hash_fwd_lm": ("hbm", 16 * (12 + 64 + 4.0), 3),
+    # level-major: pos (12) + denc (8) + 8 float2 atomics (64), x 16 levels
+    "vr_hash_bwd_lm": ("hbm", 16 * (12 + 8 + 64.0), 2),
     # 2 * (32*64 + 64*16 + 32*64 + 64*64 + 64*3)
-    "vr_mlp_fwd": ("tensor", 18816.0),
+    "vr_mlp_fwd": ("tensor", 18816.0, 5),
+    "vr_mlp_fwd_tc": ("tensor", 18816.0, 5),
     # recomputed forward + activation grads + weight grads
-    "vr_mlp_bwd": ("tensor", 3 * 18816.0),
+    "vr_mlp_bwd": ("tensor", 3 * 18816.0, 5),
+    "vr_mlp_bwd_tc": ("tensor", 3 * 18816.0, 5),
     # fused K2+K3 forward: t0,t1,id (20) + 128 corner gathers (1024) + enc out (64) + sig_rgb (16)
-    "vr_field_fwd_tc": ("hbm", 1124.0),
+    "vr_field_fwd_tc": ("hbm", 1124.0, 8),
     # fused K3+K2 backward: enc (64) + dsig_rgb (16) + t0,t1,id (20) + 1024 atomic payload
-    "vr_field_bwd_tc": ("hbm", 1124.0),
+    "vr_field_bwd_tc": ("hbm", 1124.0, 8),
     # t0,t1 (16) + sig_rgb (16); packets amortised
-    "vr_segment_fwd": ("hbm", 32.0),
+    "vr_segment_fwd": ("hbm", 32.0, None),
     # t0,t1 (16) + sig_rgb (16) + dsig_rgb (16)
-    "vr_segment_bwd": ("hbm", 48.0),
+    "vr_segment_bwd": ("hbm", 48.0, None),
 }
 
 
@@ -72,11 +80,15 @@ class EventTimer:
         self.torch = torch
         self.pending = []
         self.open = {}
+        self.samples = {}
 
-    def before(self, name):
+    def before(self, name, args=()):
         e = self.torch.cuda.Event(enable_timing=True)
         e.record()
         self.open[name] = e
+        cost = KERNEL_COST.get(name)
+        if cost and cost[2] is not None:  # samples this launch processes
+            self.samples[name] = self.samples.get(name, 0) + int(args[cost[2]])
 
     def after(self, name):
         e = self.torch.cuda.Event(enable_timing=True)
@@ -413,9 +425,12 @@ def main():
     dom = max((k for k in totals if k in KERNEL_COST), key=lambda k: totals[k][0], default=None)
     roofline = None
     if dom:
-        bound, per_unit = KERNEL_COST[dom]
+        bound, per_unit, _ = KERNEL_COST[dom]
         t_total, n_launch = totals[dom]
-        work = per_unit * n_samples_rank * args.steps  # bytes or flops over the region
+        # bytes or flops over the timed steps: the samples the kernel's launches processed
+        # (K4 kernels: the rank's samples once per step)
+        units = timer.samples.get(dom, n_samples_rank * args.steps)
+        work = per_unit * units
         avg_s = (t_total / 1e3) / n_launch
         per_launch = work / n_launch
         if bound == "hbm":
@@ -431,7 +446,7 @@ def main():
         if tp.exists():  # DRAM bytes/sample from the committed ncu --set full capture
             per_sample = json.loads(tp.read_text()).get(dom)
             if per_sample:
-                traffic = per_sample * n_samples_rank * args.steps / n_launch
+                traffic = per_sample * units / n_launch
         roofline = {"kernel": dom, "bound": bound, "achieved": achieved, "peak": peak,
                     "unit": unit, "frac": achieved / peak, "traffic": traffic,
                     "algorithmic_per_launch": per_launch, "peak_source": peaks["source"],

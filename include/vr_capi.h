@@ -186,6 +186,19 @@ int vr_hash_bwd(const VrHashGridDesc* g, const double* rays_dev, int64_t ray_str
                 const double* t0_dev, const double* t1_dev, const int32_t* ray_id_dev, int64_t n,
                 const float* denc_dev, float* grad_table_dev, void* workspace_dev,
                 size_t workspace_bytes, void* stream);
+/* Level-major variants for tables larger than L2 (T = 2^22: ~0.5 GB per region): the
+ * samples are walked once per level so only one level's slice is live in L2.
+ * vr_hash_positions writes the normalised positions pos[3][n] float32 (computed exactly
+ * as inside vr_hash_fwd); vr_hash_fwd_lm / vr_hash_bwd_lm then produce the same enc and
+ * the same gradient sums as vr_hash_fwd / vr_hash_bwd (same replica workspace). */
+int vr_hash_positions(const VrHashGridDesc* g, const double* rays_dev, int64_t ray_stride,
+                      const double* t0_dev, const double* t1_dev, const int32_t* ray_id_dev,
+                      int64_t n, float* pos_dev, void* stream);
+int vr_hash_fwd_lm(const VrHashGridDesc* g, const float* table_dev, const float* pos_dev,
+                   int64_t n, void* enc_dev, void* stream);
+int vr_hash_bwd_lm(const VrHashGridDesc* g, const float* pos_dev, int64_t n,
+                   const float* denc_dev, float* grad_table_dev, void* workspace_dev,
+                   size_t workspace_bytes, void* stream);
 /* debug/parity: the 8 corner indices per (level, sample): idx[l][n][8] int32 */
 int vr_hash_indices(const VrHashGridDesc* g, const double* rays_dev, int64_t ray_stride,
                     const double* t0_dev, const double* t1_dev, const int32_t* ray_id_dev,

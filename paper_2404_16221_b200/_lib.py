@@ -119,6 +119,9 @@ SIGNATURES = {
     "vr_hash_bwd_workspace_bytes": [P],
     "vr_hash_bwd": [P, P, I64, P, P, P, I64, P, P, P, C.c_size_t, P],
     "vr_hash_indices": [P, P, I64, P, P, P, I64, P, P],
+    "vr_hash_positions": [P, P, I64, P, P, P, I64, P, P],
+    "vr_hash_fwd_lm": [P, P, P, I64, P, P],
+    "vr_hash_bwd_lm": [P, P, I64, P, P, P, C.c_size_t, P],
     "vr_mlp_fwd": [P, P, P, I64, P, I64, P, P],
     "vr_mlp_bwd": [P, P, P, I64, P, I64, P, P, P, P],
     "vr_mlp_fwd_tc": [P, P, P, I64, P, I64, P, P],
@@ -168,7 +171,7 @@ def load(path: str | os.PathLike | None = None) -> C.CDLL:
 
 
 # Optional per-entry-point CUDA-event timer (bench.py's kernel roofline): an object with
-# before(name) / after(name), both recording events on the current stream.
+# before(name, args) / after(name), both recording events on the current stream.
 TIMER = None
 # kernel launches per entry point (for bench.py's gpu_launches count)
 LAUNCHES = {"vr_scan_offsets": 3, "vr_sum_f64": 2, "vr_adam_step": 2}
@@ -180,7 +183,7 @@ def call(name: str, *args) -> None:
     lib = load()
     CALLS[name] = CALLS.get(name, 0) + 1
     if TIMER is not None:
-        TIMER.before(name)
+        TIMER.before(name, args)
     rc = getattr(lib, name)(*args)
     if TIMER is not None:
         TIMER.after(name)

@@ -58,6 +58,55 @@ __global__ void __launch_bounds__(HASH_THREADS)
   }
 }
 
+// ---- level-major variants (tables larger than L2) ---------------------------------------
+// With T = 2^22 a region's table is ~0.5 GB: per-sample loops over all 16 levels turn every
+// corner access into a DRAM sector read-modify-write.  Level-major kernels walk the
+// samples once per level (grid.y = level, so the block scheduler finishes level l before
+// level l+1 starts): only one level's slice (<= 32 MB) is live, it stays in L2, and the
+// DRAM traffic becomes the streaming of u / enc / d(enc) (16 B per sample and level).
+// The normalised positions are computed once (k_hash_pos) and reused by the backward.
+__global__ void __launch_bounds__(HASH_THREADS)
+    k_hash_pos(const VrHashGridDesc g, const double* __restrict__ rays, int64_t stride,
+               const double* __restrict__ t0, const double* __restrict__ t1,
+               const int32_t* __restrict__ rid, int64_t n, float* __restrict__ pos) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    float u[3];
+    norm_pos(g, rays, stride, t0, t1, rid, i, u);
+    pos[i] = u[0];
+    pos[n + i] = u[1];
+    pos[2 * n + i] = u[2];
+  }
+}
+
+__global__ void __launch_bounds__(HASH_THREADS)
+    k_hash_fwd_lm(const VrHashGridDesc g, const float2* __restrict__ table,
+                  const float* __restrict__ pos, int64_t n, __half2* __restrict__ enc) {
+  const int l = blockIdx.y;
+  const float2* tl = table + g.offset[l];
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    const float u[3] = {__ldg(pos + i), __ldg(pos + n + i), __ldg(pos + 2 * n + i)};
+    Corners c;
+    level_corners(g, l, u, c);
+    const float2 f = gather_level(tl, c);
+    enc[(int64_t)l * n + i] = __floats2half2_rn(f.x, f.y);
+  }
+}
+
+__global__ void __launch_bounds__(HASH_THREADS)
+    k_hash_bwd_lm(const VrHashGridDesc g, const RepPlan plan, const float* __restrict__ pos,
+                  int64_t n, const float2* __restrict__ denc, float2* __restrict__ grad,
+                  float2* __restrict__ ws) {
+  const int l = blockIdx.y;
+  const int gwarp = blockIdx.x * (HASH_THREADS / 32) + (threadIdx.x >> 5);
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    const float u[3] = {__ldg(pos + i), __ldg(pos + n + i), __ldg(pos + 2 * n + i)};
+    scatter_level(g, plan, l, u, denc[(int64_t)l * n + i], gwarp, grad, ws);
+  }
+}
+
 // grad[level l entry e] += sum_r ws[l][r][e]; the replicas are zeroed for the next use
 __global__ void k_hash_rep_reduce(const VrHashGridDesc g, const RepPlan plan,
                                   float2* __restrict__ grad, float2* __restrict__ ws,
@@ -194,4 +243,53 @@ extern "C" int vr_hash_indices(const VrHashGridDesc* g, const double* rays, int6
   k_hash_idx<<<grid_for(n, 256), 256, 0, (cudaStream_t)stream>>>(*g, rays, stride, t0, t1, rid,
                                                                    n, out);
   return check_launch("vr_hash_indices");
+}
+
+extern "C" int vr_hash_positions(const VrHashGridDesc* g, const double* rays, int64_t stride,
+                                 const double* t0, const double* t1, const int32_t* rid,
+                                 int64_t n, float* pos, void* stream) {
+  if (!valid_grid(g) || n < 0 || (n > 0 && !pos)) {
+    set_error("vr_hash_positions: bad argument");
+    return VR_ERR_BAD_ARG;
+  }
+  if (n == 0) return VR_OK;
+  k_hash_pos<<<grid_for(n, HASH_THREADS, 8), HASH_THREADS, 0, (cudaStream_t)stream>>>(
+      *g, rays, stride, t0, t1, rid, n, pos);
+  return check_launch("vr_hash_positions");
+}
+
+static dim3 lm_grid(const VrHashGridDesc* g, int64_t n) {
+  const int64_t blocks = ceil_div(n, HASH_THREADS);
+  return dim3((unsigned)(blocks < VR_NUM_SMS * 8 ? blocks : VR_NUM_SMS * 8), (unsigned)g->n_levels);
+}
+
+extern "C" int vr_hash_fwd_lm(const VrHashGridDesc* g, const float* table, const float* pos,
+                              int64_t n, void* enc, void* stream) {
+  if (!valid_grid(g) || n < 0 || (n > 0 && (!table || !pos || !enc))) {
+    set_error("vr_hash_fwd_lm: bad argument");
+    return VR_ERR_BAD_ARG;
+  }
+  if (n == 0) return VR_OK;
+  k_hash_fwd_lm<<<lm_grid(g, n), HASH_THREADS, 0, (cudaStream_t)stream>>>(
+      *g, reinterpret_cast<const float2*>(table), pos, n, reinterpret_cast<__half2*>(enc));
+  return check_launch("vr_hash_fwd_lm");
+}
+
+extern "C" int vr_hash_bwd_lm(const VrHashGridDesc* g, const float* pos, int64_t n,
+                              const float* denc, float* grad, void* ws, size_t ws_bytes,
+                              void* stream) {
+  if (!valid_grid(g) || n < 0 || (n > 0 && (!pos || !denc || !grad))) {
+    set_error("vr_hash_bwd_lm: bad argument");
+    return VR_ERR_BAD_ARG;
+  }
+  if (n == 0) return VR_OK;
+  int64_t ws_entries = 0, red = 0;
+  RepPlan plan = hash_rep_plan(g, &ws_entries, &red);
+  if (!ws || ws_bytes < (size_t)ws_entries * sizeof(float2)) plan.n_rep = 0;
+  k_hash_bwd_lm<<<lm_grid(g, n), HASH_THREADS, 0, (cudaStream_t)stream>>>(
+      *g, plan, pos, n, reinterpret_cast<const float2*>(denc), reinterpret_cast<float2*>(grad),
+      reinterpret_cast<float2*>(ws));
+  const int rc = check_launch("vr_hash_bwd_lm");
+  if (rc != VR_OK) return rc;
+  return hash_rep_reduce(g, plan, red, grad, ws, stream);
 }

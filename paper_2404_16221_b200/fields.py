@@ -275,13 +275,21 @@ class HashGridMLP(RegionField):
 
     trainable = True
 
+    # tables larger than this are walked level-major (one level's slice live in L2)
+    LEVEL_MAJOR_BYTES = 64 << 20
+
     def __init__(self, cfg: HashGridConfig, box: Aabb, device, seed=0, table_init=1e-4,
-                 table=None, weights=None, mlp_impl: str = "fused"):
+                 table=None, weights=None, mlp_impl: str = "fused", hash_order: str = "auto"):
         if mlp_impl not in ("fused", "fused_fwd", "tc", "cuda"):
             raise ValueError(
                 "mlp_impl: 'fused' (default: gather kernel + tcgen05 MLP forward, hash-grid "
                 "backward fused into the tcgen05 MLP backward), 'fused_fwd' (also the forward "
                 "in one kernel), 'tc' (separate kernels) or 'cuda' (CUDA-core reference MLP)")
+        if hash_order not in ("auto", "sample", "level"):
+            raise ValueError("hash_order: 'auto', 'sample' (all levels per sample) or 'level' "
+                             "(level-major kernels for tables larger than L2)")
+        if hash_order == "level" and mlp_impl == "fused_fwd":
+            raise ValueError("hash_order='level' needs a separate hash-grid forward")
         self.mlp_impl = mlp_impl
         self.err = torch.zeros(1, dtype=torch.int32, device=device)  # replaced by the pool's
         self.cfg = cfg
@@ -289,6 +297,11 @@ class HashGridMLP(RegionField):
         self.desc = hash_desc(cfg, box)
         n_entries = int(self.desc.offset[cfg.n_levels])
         self.n_entries = n_entries
+        if hash_order == "auto":
+            hash_order = ("level" if n_entries * 8 > self.LEVEL_MAJOR_BYTES
+                          and mlp_impl != "fused_fwd" else "sample")
+        self.hash_order = hash_order
+        self._pos = None
         g = torch.Generator(device="cpu").manual_seed(seed)
         if table is None:
             dg = torch.Generator(device=device).manual_seed(seed)
@@ -345,6 +358,15 @@ class HashGridMLP(RegionField):
         if n == 0:
             return
         enc = self._enc_buf(n, rays.device)
+        if self.hash_order == "level":
+            if self._pos is None or self._pos.numel() < 3 * n:
+                self._pos = torch.empty(3 * n, dtype=torch.float32, device=rays.device)
+            _lib.call("vr_hash_positions", _lib.addr(self.desc), _lib.ptr(rays), rays.shape[1],
+                      _lib.ptr(t0), _lib.ptr(t1), _lib.ptr(ray_id), n, _lib.ptr(self._pos),
+                      stream)
+            _lib.call("vr_hash_fwd_lm", _lib.addr(self.desc), _lib.ptr(self.table),
+                      _lib.ptr(self._pos), n, _lib.ptr(enc), stream)
+            return
         _lib.call("vr_hash_fwd", _lib.addr(self.desc), _lib.ptr(self.table), _lib.ptr(rays),
                   rays.shape[1], _lib.ptr(t0), _lib.ptr(t1), _lib.ptr(ray_id), n,
                   _lib.ptr(enc), stream)
@@ -360,7 +382,7 @@ class HashGridMLP(RegionField):
         if n == 0:
             return
         enc = self._enc  # written by the forward of the same step
-        if self.mlp_impl in ("fused", "fused_fwd"):
+        if self.mlp_impl in ("fused", "fused_fwd") and self.hash_order == "sample":
             ws = self._workspace(rays.device)
             _lib.call("vr_field_bwd_tc", _lib.addr(self.desc), _lib.ptr(self.weights16),
                       _lib.ptr(enc), _lib.ptr(rays), rays.shape[1], _lib.ptr(t0), _lib.ptr(t1),
@@ -369,7 +391,7 @@ class HashGridMLP(RegionField):
                       stream)
             return
         denc = torch.empty(16 * n * 2, dtype=torch.float32, device=rays.device)
-        if self.mlp_impl == "tc":
+        if self.mlp_impl != "cuda":
             _lib.call("vr_mlp_bwd_tc", _lib.ptr(self.weights16), _lib.ptr(enc), _lib.ptr(rays),
                       rays.shape[1], _lib.ptr(ray_id), n, _lib.ptr(dsig_rgb),
                       _lib.ptr(self.grad_weights), _lib.ptr(denc), _lib.ptr(self.err), stream)
@@ -378,6 +400,11 @@ class HashGridMLP(RegionField):
                       rays.shape[1], _lib.ptr(ray_id), n, _lib.ptr(dsig_rgb),
                       _lib.ptr(self.grad_weights), _lib.ptr(denc), stream)
         ws = self._workspace(rays.device)
+        if self.hash_order == "level":  # positions of the same step's forward
+            _lib.call("vr_hash_bwd_lm", _lib.addr(self.desc), _lib.ptr(self._pos), n,
+                      _lib.ptr(denc), _lib.ptr(self.grad_table), _lib.ptr(ws), ws.numel(),
+                      stream)
+            return
         _lib.call("vr_hash_bwd", _lib.addr(self.desc), _lib.ptr(rays), rays.shape[1],
                   _lib.ptr(t0), _lib.ptr(t1), _lib.ptr(ray_id), n, _lib.ptr(denc),
                   _lib.ptr(self.grad_table), _lib.ptr(ws), ws.numel(), stream)

@@ -237,7 +237,8 @@ def test_nonfinite_packet_raises():
 
 # ---- hash grid + MLP (parity unpinned: checked against oracle/hashmlp_oracle.py) ------
 
-def _hash_setup(log2_T=14, K=2, n_rays=48, seed=0, restriction=False, mlp_impl="fused"):
+def _hash_setup(log2_T=14, K=2, n_rays=48, seed=0, restriction=False, mlp_impl="fused",
+                hash_order="auto"):
     rng = np.random.default_rng(seed)
     root = vr.Aabb([-1, -1, -1], [1, 1, 1])
     tree = vr.grid_tree(root, "x" * int(np.log2(K))) if K > 1 else vr.grid_tree(root, "")
@@ -255,7 +256,7 @@ def _hash_setup(log2_T=14, K=2, n_rays=48, seed=0, restriction=False, mlp_impl="
                 w[off:off + rows * cols] = rng.normal(size=rows * cols) / np.sqrt(cols)
             weights0 = w
         f = vr.HashGridMLP(cfg, box, DEV, mlp_impl=mlp_impl, table=torch.from_numpy(table0.copy()),
-                           weights=torch.from_numpy(weights0.copy()))
+                           weights=torch.from_numpy(weights0.copy()), hash_order=hash_order)
         fields.append(f)
         models.append(hmo.HashMLPModel(table0, weights0, log2_T, box.mn, box.mx, max_res=256))
     pool = vr.VolumePool(tree, fields, (0.2, 0.3, 0.4), DEV)
@@ -296,11 +297,13 @@ def test_hash_indices_bit_exact():
         assert np.array_equal(idx.cpu().numpy().astype(np.int64), want)
 
 
-@pytest.mark.parametrize("mlp_impl", ["fused", "fused_fwd", "tc", "cuda"])
+@pytest.mark.parametrize("mlp_impl,hash_order", [("fused", "sample"), ("fused_fwd", "sample"),
+                                                 ("tc", "sample"), ("cuda", "sample"),
+                                                 ("fused", "level"), ("cuda", "level")])
 @pytest.mark.parametrize("restriction", [False, True])
-def test_hashmlp_loss_and_grads_match_oracle(restriction, mlp_impl):
+def test_hashmlp_loss_and_grads_match_oracle(restriction, mlp_impl, hash_order):
     pool, tree, models, rays, targets = _hash_setup(log2_T=14, K=2, restriction=restriction,
-                                                    mlp_impl=mlp_impl)
+                                                    mlp_impl=mlp_impl, hash_order=hash_order)
     dt = 0.04
     pool.zero_grad()
     loss, out, b = pool.loss_and_grad(rays, targets, dt)
@@ -323,6 +326,48 @@ def test_hashmlp_loss_and_grads_match_oracle(restriction, mlp_impl):
         print(f"region {kk}: grad rel err table {rel_t:.2e} weights {rel_w:.2e}")
         assert rel_t <= 1e-3, rel_t
         assert rel_w <= 1e-3, rel_w
+
+
+def test_level_major_hash_kernels_match_sample_major():
+    """vr_hash_positions + vr_hash_fwd_lm == vr_hash_fwd bit for bit; vr_hash_bwd_lm sums the
+    same contributions as vr_hash_bwd (float atomics: order-dependent rounding only)."""
+    from paper_2404_16221_b200 import _lib
+    pool, tree, models, rays, _ = _hash_setup(log2_T=16, K=1, n_rays=3000)
+    f = pool.fields[0]
+    rd = pool.rays_to_device(rays)
+    b = pool.sample(rd, 0.01)
+    n = b.n_samples
+    assert n > 100000
+    s = _lib.stream_ptr()
+    enc_a = torch.empty((16, n), dtype=torch.float32, device=DEV)
+    enc_b = torch.empty((16, n), dtype=torch.float32, device=DEV)
+    pos = torch.empty((3, n), dtype=torch.float32, device=DEV)
+    args = (_lib.ptr(rd), rd.shape[1], _lib.ptr(b.t0), _lib.ptr(b.t1), _lib.ptr(b.ray_id), n)
+    _lib.call("vr_hash_fwd", _lib.addr(f.desc), _lib.ptr(f.table), *args, _lib.ptr(enc_a), s)
+    _lib.call("vr_hash_positions", _lib.addr(f.desc), *args, _lib.ptr(pos), s)
+    _lib.call("vr_hash_fwd_lm", _lib.addr(f.desc), _lib.ptr(f.table), _lib.ptr(pos), n,
+              _lib.ptr(enc_b), s)
+    assert torch.equal(enc_a.view(torch.int32), enc_b.view(torch.int32))
+    denc = torch.randn((16, n, 2), device=DEV)
+    ga = torch.zeros_like(f.table)
+    gb = torch.zeros_like(f.table)
+    ws = f._workspace(rd.device)
+    _lib.call("vr_hash_bwd", _lib.addr(f.desc), *args, _lib.ptr(denc), _lib.ptr(ga), _lib.ptr(ws),
+              ws.numel(), s)
+    _lib.call("vr_hash_bwd_lm", _lib.addr(f.desc), _lib.ptr(pos), n, _lib.ptr(denc),
+              _lib.ptr(gb), _lib.ptr(ws), ws.numel(), s)
+    torch.cuda.synchronize()
+    assert torch.count_nonzero(ga) > 1000
+    rel = ((ga - gb).norm() / ga.norm()).item()
+    assert rel < 1e-5, rel
+
+
+def test_hash_order_auto_picks_level_major_for_tables_larger_than_l2():
+    cfg_small = vr.HashGridConfig(log2_T=19, max_res=2048)
+    cfg_big = vr.HashGridConfig(log2_T=22, max_res=2048)
+    box = vr.Aabb([0, 0, 0], [1, 1, 1])
+    assert vr.HashGridMLP(cfg_small, box, DEV).hash_order == "sample"
+    assert vr.HashGridMLP(cfg_big, box, DEV).hash_order == "level"
 
 
 def test_train_step_decreases_loss():
