@@ -178,9 +178,11 @@ def build_pool(w, rank, world, dev, group, seed_base=1):
     tree = w.tree
     lo, cnt = vr.owned_regions(len(tree.leaves), rank, world)
     cfg = vr.HashGridConfig(log2_T=w.log2_T, max_res=w.max_res)
-    impl = os.environ.get("VR_BENCH_MLP_IMPL", "fused")  # kernel experiments only
-    fields = [vr.HashGridMLP(cfg, tree.leaves[k].box, dev, seed=seed_base + k, mlp_impl=impl)
-              for k in range(lo, lo + cnt)]
+    # kernel experiments only: force an MLP implementation / hash-grid traversal order
+    impl = os.environ.get("VR_BENCH_MLP_IMPL", "fused")
+    order = os.environ.get("VR_BENCH_HASH_ORDER", "auto")
+    fields = [vr.HashGridMLP(cfg, tree.leaves[k].box, dev, seed=seed_base + k, mlp_impl=impl,
+                             hash_order=order) for k in range(lo, lo + cnt)]
     props = None
     if w.interlevel > 0:  # config 4: proposal fields for the interlevel loss
         pcfg = vr.HashGridConfig(log2_T=w.prop_log2_T, max_res=w.prop_max_res)

@@ -64,7 +64,9 @@ __global__ void __launch_bounds__(HASH_THREADS)
 // samples once per level (grid.y = level, so the block scheduler finishes level l before
 // level l+1 starts): only one level's slice (<= 32 MB) is live, it stays in L2, and the
 // DRAM traffic becomes the streaming of u / enc / d(enc) (16 B per sample and level).
-// The normalised positions are computed once (k_hash_pos) and reused by the backward.
+// The normalised positions are computed once (k_hash_pos) and reused by the backward;
+// the streamed pos / enc / d(enc) use evict-first accesses so they do not push the live
+// table slice out of L2.
 __global__ void __launch_bounds__(HASH_THREADS)
     k_hash_pos(const VrHashGridDesc g, const double* __restrict__ rays, int64_t stride,
                const double* __restrict__ t0, const double* __restrict__ t1,
@@ -86,25 +88,52 @@ __global__ void __launch_bounds__(HASH_THREADS)
   const float2* tl = table + g.offset[l];
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
        i += (int64_t)gridDim.x * blockDim.x) {
-    const float u[3] = {__ldg(pos + i), __ldg(pos + n + i), __ldg(pos + 2 * n + i)};
+    const float u[3] = {__ldcs(pos + i), __ldcs(pos + n + i), __ldcs(pos + 2 * n + i)};
     Corners c;
     level_corners(g, l, u, c);
     const float2 f = gather_level(tl, c);
-    enc[(int64_t)l * n + i] = __floats2half2_rn(f.x, f.y);
+    __stcs(enc + (int64_t)l * n + i, __floats2half2_rn(f.x, f.y));
   }
 }
 
+// Backward passes group consecutive levels (pass p = levels [first[p], first[p+1])): the
+// small coarse levels share one pass, so their atomics are diluted among several levels'
+// (one coarse level alone would put every SM's atomics on a few thousand addresses).
+struct LmPasses {
+  int32_t n;
+  int32_t first[VR_MAX_LEVELS + 1];
+};
+
 __global__ void __launch_bounds__(HASH_THREADS)
-    k_hash_bwd_lm(const VrHashGridDesc g, const RepPlan plan, const float* __restrict__ pos,
-                  int64_t n, const float2* __restrict__ denc, float2* __restrict__ grad,
-                  float2* __restrict__ ws) {
-  const int l = blockIdx.y;
+    k_hash_bwd_lm(const VrHashGridDesc g, const RepPlan plan, const LmPasses passes,
+                  const float* __restrict__ pos, int64_t n, const float2* __restrict__ denc,
+                  float2* __restrict__ grad, float2* __restrict__ ws) {
+  const int l0 = passes.first[blockIdx.y], l1 = passes.first[blockIdx.y + 1];
   const int gwarp = blockIdx.x * (HASH_THREADS / 32) + (threadIdx.x >> 5);
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
        i += (int64_t)gridDim.x * blockDim.x) {
-    const float u[3] = {__ldg(pos + i), __ldg(pos + n + i), __ldg(pos + 2 * n + i)};
-    scatter_level(g, plan, l, u, denc[(int64_t)l * n + i], gwarp, grad, ws);
+    const float u[3] = {__ldcs(pos + i), __ldcs(pos + n + i), __ldcs(pos + 2 * n + i)};
+    for (int l = l0; l < l1; ++l)
+      scatter_level(g, plan, l, u, __ldcs(denc + (int64_t)l * n + i), gwarp, grad, ws);
   }
+}
+
+// greedy: consecutive levels share a pass while their slices total <= 48 MB
+static LmPasses lm_passes(const VrHashGridDesc* g) {
+  LmPasses p;
+  memset(&p, 0, sizeof(p));
+  const int64_t budget = (int64_t)48 << 20;
+  int64_t bytes = 0;
+  for (int l = 0; l < g->n_levels; ++l) {
+    const int64_t b = (g->offset[l + 1] - g->offset[l]) * (int64_t)sizeof(float2);
+    if (l == 0 || bytes + b > budget) {
+      p.first[p.n++] = l;
+      bytes = 0;
+    }
+    bytes += b;
+  }
+  p.first[p.n] = g->n_levels;
+  return p;
 }
 
 // grad[level l entry e] += sum_r ws[l][r][e]; the replicas are zeroed for the next use
@@ -286,8 +315,11 @@ extern "C" int vr_hash_bwd_lm(const VrHashGridDesc* g, const float* pos, int64_t
   int64_t ws_entries = 0, red = 0;
   RepPlan plan = hash_rep_plan(g, &ws_entries, &red);
   if (!ws || ws_bytes < (size_t)ws_entries * sizeof(float2)) plan.n_rep = 0;
-  k_hash_bwd_lm<<<lm_grid(g, n), HASH_THREADS, 0, (cudaStream_t)stream>>>(
-      *g, plan, pos, n, reinterpret_cast<const float2*>(denc), reinterpret_cast<float2*>(grad),
+  const LmPasses passes = lm_passes(g);
+  dim3 grid = lm_grid(g, n);
+  grid.y = passes.n;
+  k_hash_bwd_lm<<<grid, HASH_THREADS, 0, (cudaStream_t)stream>>>(
+      *g, plan, passes, pos, n, reinterpret_cast<const float2*>(denc), reinterpret_cast<float2*>(grad),
       reinterpret_cast<float2*>(ws));
   const int rc = check_launch("vr_hash_bwd_lm");
   if (rc != VR_OK) return rc;
