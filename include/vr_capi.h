@@ -173,10 +173,12 @@ int vr_voxel_bwd(const VrVoxelDesc* g, const double* rays_dev, int64_t ray_strid
                  const float* dsig_rgb_dev, double* grad_densities_dev, void* stream);
 
 /* ---- K2: hash-grid encoding ---------------------------------------------------- */
-/* enc layout: [n_levels][n] half2 (level-major, coalesced on samples). */
+/* enc layout: [n_levels][n] half2 (level-major, coalesced on samples).  pos_dev (may be
+ * NULL) receives the normalised positions [3][n] float32 for the fused backward. */
 int vr_hash_fwd(const VrHashGridDesc* g, const float* table_dev, const double* rays_dev,
                 int64_t ray_stride, const double* t0_dev, const double* t1_dev,
-                const int32_t* ray_id_dev, int64_t n, void* enc_dev, void* stream);
+                const int32_t* ray_id_dev, int64_t n, void* enc_dev, float* pos_dev,
+                void* stream);
 /* denc layout: [n_levels][n] float2; grad_table float2 scatter-add.  workspace: zero-
  * initialised device buffer of vr_hash_bwd_workspace_bytes() (left zeroed on return)
  * holding per-warp replicas of the small dense levels, whose atomics would otherwise
@@ -199,6 +201,14 @@ int vr_hash_fwd_lm(const VrHashGridDesc* g, const float* table_dev, const float*
 int vr_hash_bwd_lm(const VrHashGridDesc* g, const float* pos_dev, int64_t n,
                    const float* denc_dev, float* grad_table_dev, void* workspace_dev,
                    size_t workspace_bytes, void* stream);
+/* General scatter from stored positions: level_major = 0 walks all levels per sample
+ * (tables that fit L2), 1 as vr_hash_bwd_lm.  max_blocks > 0 launches that many 128-thread
+ * blocks per pass, sized to run concurrently with the tensor-core MLP backward of the next
+ * region on another stream (dedicated scatter warps next to the MLP's CTAs). */
+int vr_hash_scatter(const VrHashGridDesc* g, const float* pos_dev, int64_t n,
+                    const float* denc_dev, float* grad_table_dev, void* workspace_dev,
+                    size_t workspace_bytes, int32_t level_major, int32_t max_blocks,
+                    void* stream);
 /* debug/parity: the 8 corner indices per (level, sample): idx[l][n][8] int32 */
 int vr_hash_indices(const VrHashGridDesc* g, const double* rays_dev, int64_t ray_stride,
                     const double* t0_dev, const double* t1_dev, const int32_t* ray_id_dev,
@@ -237,7 +247,8 @@ int vr_mlp_bwd_tc(const void* weights_dev, const void* enc_dev, const double* ra
  * encoding round trip through HBM before the MLP) and, if enc_out != NULL, writes it
  * (level-major half2) for the backward.  Backward: the MLP backward scatters the
  * hash-grid gradients straight from its last epilogue (no d(enc) round trip);
- * workspace as for vr_hash_bwd. */
+ * workspace as for vr_hash_bwd; pos_dev (may be NULL: recomputed from the rays) are the
+ * normalised positions written by vr_hash_fwd / vr_hash_positions for these samples. */
 int vr_field_fwd_tc(const VrHashGridDesc* g, const float* table_dev, const void* weights_dev,
                     const double* rays_dev, int64_t ray_stride, const double* t0_dev,
                     const double* t1_dev, const int32_t* ray_id_dev, int64_t n, void* enc_out_dev,
@@ -246,7 +257,8 @@ int vr_field_bwd_tc(const VrHashGridDesc* g, const void* weights_dev, const void
                     const double* rays_dev, int64_t ray_stride, const double* t0_dev,
                     const double* t1_dev, const int32_t* ray_id_dev, int64_t n,
                     const float* dsig_rgb_dev, float* grad_weights_dev, float* grad_table_dev,
-                    void* workspace_dev, size_t workspace_bytes, int32_t* err_dev, void* stream);
+                    void* workspace_dev, size_t workspace_bytes, int32_t* err_dev,
+                    const float* pos_dev, void* stream);
 
 /* ---- K4: per-segment front-to-back composite (composite_samples quadrature.py:141-165,
  * aggregate_segment segrender.py:71-90, process_inbox distsim.py:318-329) ------------- */

@@ -115,19 +115,20 @@ SIGNATURES = {
     "vr_field_analytic_fwd": [P, P, I64, P, P, P, I64, P, P],
     "vr_voxel_fwd": [P, P, P, P, I64, P, P, P, I64, P, P],
     "vr_voxel_bwd": [P, P, I64, P, P, P, I64, P, P, P],
-    "vr_hash_fwd": [P, P, P, I64, P, P, P, I64, P, P],
+    "vr_hash_fwd": [P, P, P, I64, P, P, P, I64, P, P, P],
     "vr_hash_bwd_workspace_bytes": [P],
     "vr_hash_bwd": [P, P, I64, P, P, P, I64, P, P, P, C.c_size_t, P],
     "vr_hash_indices": [P, P, I64, P, P, P, I64, P, P],
     "vr_hash_positions": [P, P, I64, P, P, P, I64, P, P],
     "vr_hash_fwd_lm": [P, P, P, I64, P, P],
     "vr_hash_bwd_lm": [P, P, I64, P, P, P, C.c_size_t, P],
+    "vr_hash_scatter": [P, P, I64, P, P, P, C.c_size_t, I32, I32, P],
     "vr_mlp_fwd": [P, P, P, I64, P, I64, P, P],
     "vr_mlp_bwd": [P, P, P, I64, P, I64, P, P, P, P],
     "vr_mlp_fwd_tc": [P, P, P, I64, P, I64, P, P],
     "vr_mlp_bwd_tc": [P, P, P, I64, P, I64, P, P, P, P, P],
     "vr_field_fwd_tc": [P, P, P, P, I64, P, P, P, I64, P, P, P],
-    "vr_field_bwd_tc": [P, P, P, P, I64, P, P, P, I64, P, P, P, P, C.c_size_t, P, P],
+    "vr_field_bwd_tc": [P, P, P, P, I64, P, P, P, I64, P, P, P, P, C.c_size_t, P, P, P],
     "vr_segment_fwd": [P, P, P, P, P, P, I64, I32, P, P, P],
     "vr_segment_bwd": [P, P, P, P, P, I64, I32, P, P, P],
     "vr_global_fwd": [P, I32, I64, P, P, I32, P, P, P],

@@ -27,11 +27,16 @@ __global__ void __launch_bounds__(HASH_THREADS)
     k_hash_fwd(const VrHashGridDesc g, const float2* __restrict__ table,
                const double* __restrict__ rays, int64_t stride, const double* __restrict__ t0,
                const double* __restrict__ t1, const int32_t* __restrict__ rid, int64_t n,
-               __half2* __restrict__ enc) {
+               __half2* __restrict__ enc, float* __restrict__ pos) {
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
        i += (int64_t)gridDim.x * blockDim.x) {
     float u[3];
     norm_pos(g, rays, stride, t0, t1, rid, i, u);
+    if (pos) {
+      pos[i] = u[0];
+      pos[n + i] = u[1];
+      pos[2 * n + i] = u[2];
+    }
 #pragma unroll 2
     for (int l = 0; l < g.n_levels; ++l) {
       Corners c;
@@ -109,7 +114,7 @@ __global__ void __launch_bounds__(HASH_THREADS)
                   const float* __restrict__ pos, int64_t n, const float2* __restrict__ denc,
                   float2* __restrict__ grad, float2* __restrict__ ws) {
   const int l0 = passes.first[blockIdx.y], l1 = passes.first[blockIdx.y + 1];
-  const int gwarp = blockIdx.x * (HASH_THREADS / 32) + (threadIdx.x >> 5);
+  const int gwarp = blockIdx.x * (blockDim.x / 32) + (threadIdx.x >> 5);
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
        i += (int64_t)gridDim.x * blockDim.x) {
     const float u[3] = {__ldcs(pos + i), __ldcs(pos + n + i), __ldcs(pos + 2 * n + i)};
@@ -222,7 +227,7 @@ using namespace vr;
 
 extern "C" int vr_hash_fwd(const VrHashGridDesc* g, const float* table, const double* rays,
                            int64_t stride, const double* t0, const double* t1, const int32_t* rid,
-                           int64_t n, void* enc, void* stream) {
+                           int64_t n, void* enc, float* pos, void* stream) {
   if (!valid_grid(g) || n < 0) {
     set_error("vr_hash_fwd: bad argument");
     return VR_ERR_BAD_ARG;
@@ -230,7 +235,7 @@ extern "C" int vr_hash_fwd(const VrHashGridDesc* g, const float* table, const do
   if (n == 0) return VR_OK;
   k_hash_fwd<<<grid_for(n, HASH_THREADS, 8), HASH_THREADS, 0, (cudaStream_t)stream>>>(
       *g, reinterpret_cast<const float2*>(table), rays, stride, t0, t1, rid, n,
-      reinterpret_cast<__half2*>(enc));
+      reinterpret_cast<__half2*>(enc), pos);
   return check_launch("vr_hash_fwd");
 }
 
@@ -304,24 +309,42 @@ extern "C" int vr_hash_fwd_lm(const VrHashGridDesc* g, const float* table, const
   return check_launch("vr_hash_fwd_lm");
 }
 
-extern "C" int vr_hash_bwd_lm(const VrHashGridDesc* g, const float* pos, int64_t n,
-                              const float* denc, float* grad, void* ws, size_t ws_bytes,
-                              void* stream) {
-  if (!valid_grid(g) || n < 0 || (n > 0 && (!pos || !denc || !grad))) {
-    set_error("vr_hash_bwd_lm: bad argument");
+extern "C" int vr_hash_scatter(const VrHashGridDesc* g, const float* pos, int64_t n,
+                               const float* denc, float* grad, void* ws, size_t ws_bytes,
+                               int32_t level_major, int32_t max_blocks, void* stream) {
+  if (!valid_grid(g) || n < 0 || max_blocks < 0 || (n > 0 && (!pos || !denc || !grad))) {
+    set_error("vr_hash_scatter: bad argument");
     return VR_ERR_BAD_ARG;
   }
   if (n == 0) return VR_OK;
   int64_t ws_entries = 0, red = 0;
   RepPlan plan = hash_rep_plan(g, &ws_entries, &red);
   if (!ws || ws_bytes < (size_t)ws_entries * sizeof(float2)) plan.n_rep = 0;
-  const LmPasses passes = lm_passes(g);
+  LmPasses passes;
+  if (level_major) {
+    passes = lm_passes(g);
+  } else {  // one pass over all levels: sample order
+    memset(&passes, 0, sizeof(passes));
+    passes.n = 1;
+    passes.first[1] = g->n_levels;
+  }
   dim3 grid = lm_grid(g, n);
   grid.y = passes.n;
-  k_hash_bwd_lm<<<grid, HASH_THREADS, 0, (cudaStream_t)stream>>>(
-      *g, plan, passes, pos, n, reinterpret_cast<const float2*>(denc), reinterpret_cast<float2*>(grad),
-      reinterpret_cast<float2*>(ws));
-  const int rc = check_launch("vr_hash_bwd_lm");
+  int threads = HASH_THREADS;
+  if (max_blocks > 0) {  // co-resident with another kernel: few small blocks per level pass
+    threads = 128;
+    grid.x = (unsigned)max_blocks;
+  }
+  k_hash_bwd_lm<<<grid, threads, 0, (cudaStream_t)stream>>>(
+      *g, plan, passes, pos, n, reinterpret_cast<const float2*>(denc),
+      reinterpret_cast<float2*>(grad), reinterpret_cast<float2*>(ws));
+  const int rc = check_launch("vr_hash_scatter");
   if (rc != VR_OK) return rc;
   return hash_rep_reduce(g, plan, red, grad, ws, stream);
+}
+
+extern "C" int vr_hash_bwd_lm(const VrHashGridDesc* g, const float* pos, int64_t n,
+                              const float* denc, float* grad, void* ws, size_t ws_bytes,
+                              void* stream) {
+  return vr_hash_scatter(g, pos, n, denc, grad, ws, ws_bytes, 1, 0, stream);
 }

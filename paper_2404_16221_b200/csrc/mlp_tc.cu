@@ -443,7 +443,8 @@ __device__ __forceinline__ void fetch_row(RowIn& x, const __half2* __restrict__ 
                                           const float4* __restrict__ dsr, int64_t n, int64_t i,
                                           int part, const VrHashGridDesc& g,
                                           const double* __restrict__ t0,
-                                          const double* __restrict__ t1) {
+                                          const double* __restrict__ t1,
+                                          const float* __restrict__ pos) {
   constexpr int LV = 16 / BWD_TPR;
   const bool valid = i < n;
 #pragma unroll
@@ -454,16 +455,23 @@ __device__ __forceinline__ void fetch_row(RowIn& x, const __half2* __restrict__ 
   x.u[0] = x.u[1] = x.u[2] = 0.f;
   if (valid) {
     const int64_t ray = rid[i];
+    const bool own_pos = FUSED && pos == nullptr;
     double o[3], d[3];
 #pragma unroll
     for (int a = 0; a < 3; ++a) {
       d[a] = __ldg(rays + (3 + a) * stride + ray);
-      if (FUSED) o[a] = __ldg(rays + a * stride + ray);
+      if (own_pos) o[a] = __ldg(rays + a * stride + ray);
     }
     x.dx = (float)d[0];
     x.dy = (float)d[1];
     x.dz = (float)d[2];
-    if (FUSED) norm_pos_od(g, o, d, sample_mid(t0[i], t1[i]), x.u);
+    if (own_pos) {
+      norm_pos_od(g, o, d, sample_mid(t0[i], t1[i]), x.u);
+    } else if (FUSED) {  // positions written by the hash-grid forward
+      x.u[0] = __ldcs(pos + i);
+      x.u[1] = __ldcs(pos + n + i);
+      x.u[2] = __ldcs(pos + 2 * n + i);
+    }
   }
 }
 
@@ -486,7 +494,7 @@ __global__ void __launch_bounds__(TILE * BWD_TPR, 2)
                  float2* __restrict__ denc, int32_t* err, const VrHashGridDesc hg,
                  const RepPlan plan, const double* __restrict__ t0,
                  const double* __restrict__ t1, float2* __restrict__ grad_table,
-                 float2* __restrict__ rep_ws, int do_scatter) {
+                 float2* __restrict__ rep_ws, int do_scatter, const float* __restrict__ pos) {
   using G = Geo<BWD_TPR>;
   extern __shared__ __align__(1024) uint8_t smem[];
   uint8_t* sw = smem;
@@ -570,14 +578,14 @@ __global__ void __launch_bounds__(TILE * BWD_TPR, 2)
   RowIn nxt;
   if ((int64_t)blockIdx.x < n_tiles)
     fetch_row<FUSED>(nxt, enc, rays, stride, rid, dsr, n, (int64_t)blockIdx.x * TILE + r, part,
-                     hg, t0, t1);
+                     hg, t0, t1, pos);
   for (int64_t tile = blockIdx.x; tile < n_tiles; tile += gridDim.x) {
     const int64_t i = tile * TILE + r;
     const bool valid = i < n;
     const RowIn cur = nxt;
     if (tile + gridDim.x < n_tiles)  // prefetch the next tile's inputs
       fetch_row<FUSED>(nxt, enc, rays, stride, rid, dsr, n, (tile + gridDim.x) * TILE + r, part,
-                       hg, t0, t1);
+                       hg, t0, t1, pos);
     if (wgrad_pending) {  // the previous tile's last wgrad reads X4/Gh/Gl
       mbar_wait(barB, phB);
       phB ^= 1u;
@@ -770,7 +778,7 @@ template <bool FUSED>
 int launch_bwd(const void* w, const void* enc, const double* rays, int64_t stride,
                const int32_t* rid, int64_t n, const float* dsr, float* gW, float* denc,
                int32_t* err, const VrHashGridDesc* g, const double* t0, const double* t1,
-               float* grad_table, void* ws, size_t ws_bytes, void* stream) {
+               float* grad_table, void* ws, size_t ws_bytes, const float* pos, void* stream) {
   static bool attr = false;
   int rc = set_smem(mlp::k_mlp_bwd_tc<FUSED>, mlp::B_SMEM, attr, "mlp bwd: smem attribute");
   if (rc != VR_OK) return rc;
@@ -790,7 +798,7 @@ int launch_bwd(const void* w, const void* enc, const double* rays, int64_t strid
   mlp::k_mlp_bwd_tc<FUSED><<<grid, mlp::TILE * mlp::BWD_TPR, mlp::B_SMEM, (cudaStream_t)stream>>>(
       (const __half*)w, (const __half2*)enc, rays, stride, rid, n,
       reinterpret_cast<const float4*>(dsr), gW, reinterpret_cast<float2*>(denc), err, gd, plan, t0, t1, reinterpret_cast<float2*>(grad_table),
-      reinterpret_cast<float2*>(ws), getenv("VR_DEBUG_NOSCATTER") ? 0 : 1);
+      reinterpret_cast<float2*>(ws), getenv("VR_DEBUG_NOSCATTER") ? 0 : 1, pos);
   rc = check_launch("vr_mlp_bwd_tc");
   if (rc != VR_OK || !FUSED) return rc;
   return hash_rep_reduce(&gd, plan, red, grad_table, ws, stream);
@@ -818,7 +826,7 @@ extern "C" int vr_mlp_bwd_tc(const void* w, const void* enc, const double* rays,
   }
   if (n == 0) return VR_OK;
   return launch_bwd<false>(w, enc, rays, stride, rid, n, dsr, gW, denc, err, nullptr, nullptr,
-                           nullptr, nullptr, nullptr, 0, stream);
+                           nullptr, nullptr, nullptr, 0, nullptr, stream);
 }
 
 extern "C" int vr_field_fwd_tc(const VrHashGridDesc* g, const float* table, const void* w,
@@ -838,12 +846,12 @@ extern "C" int vr_field_bwd_tc(const VrHashGridDesc* g, const void* w, const voi
                                const double* rays, int64_t stride, const double* t0,
                                const double* t1, const int32_t* rid, int64_t n, const float* dsr,
                                float* gW, float* grad_table, void* ws, size_t ws_bytes,
-                               int32_t* err, void* stream) {
+                               int32_t* err, const float* pos, void* stream) {
   if (!valid_grid(g) || g->n_levels != 16 || n < 0 || !w || !enc || !gW || !grad_table || !err) {
     set_error("vr_field_bwd_tc: bad argument");
     return VR_ERR_BAD_ARG;
   }
   if (n == 0) return VR_OK;
   return launch_bwd<true>(w, enc, rays, stride, rid, n, dsr, gW, nullptr, err, g, t0, t1,
-                          grad_table, ws, ws_bytes, stream);
+                          grad_table, ws, ws_bytes, pos, stream);
 }

@@ -329,6 +329,11 @@ class HashGridMLP(RegionField):
             self._enc = torch.empty(need, dtype=torch.float32, device=dev)  # half2 = 4 B
         return self._enc
 
+    def _pos_buf(self, n, dev):
+        if self._pos is None or self._pos.numel() < 3 * n:
+            self._pos = torch.empty(3 * max(n, 1), dtype=torch.float32, device=dev)
+        return self._pos
+
     def _workspace(self, dev):
         if self._hash_ws is None:
             nbytes = int(_lib.load().vr_hash_bwd_workspace_bytes(_lib.addr(self.desc)))
@@ -359,17 +364,17 @@ class HashGridMLP(RegionField):
             return
         enc = self._enc_buf(n, rays.device)
         if self.hash_order == "level":
-            if self._pos is None or self._pos.numel() < 3 * n:
-                self._pos = torch.empty(3 * n, dtype=torch.float32, device=rays.device)
+            self._pos_buf(n, rays.device)
             _lib.call("vr_hash_positions", _lib.addr(self.desc), _lib.ptr(rays), rays.shape[1],
                       _lib.ptr(t0), _lib.ptr(t1), _lib.ptr(ray_id), n, _lib.ptr(self._pos),
                       stream)
             _lib.call("vr_hash_fwd_lm", _lib.addr(self.desc), _lib.ptr(self.table),
                       _lib.ptr(self._pos), n, _lib.ptr(enc), stream)
             return
+        # the positions are kept for the fused backward of the same step
         _lib.call("vr_hash_fwd", _lib.addr(self.desc), _lib.ptr(self.table), _lib.ptr(rays),
                   rays.shape[1], _lib.ptr(t0), _lib.ptr(t1), _lib.ptr(ray_id), n,
-                  _lib.ptr(enc), stream)
+                  _lib.ptr(enc), _lib.ptr(self._pos_buf(n, rays.device)), stream)
 
     def forward_mlp(self, rays, ray_id, n, sig_rgb, stream):
         if n == 0:
@@ -388,7 +393,7 @@ class HashGridMLP(RegionField):
                       _lib.ptr(enc), _lib.ptr(rays), rays.shape[1], _lib.ptr(t0), _lib.ptr(t1),
                       _lib.ptr(ray_id), n, _lib.ptr(dsig_rgb), _lib.ptr(self.grad_weights),
                       _lib.ptr(self.grad_table), _lib.ptr(ws), ws.numel(), _lib.ptr(self.err),
-                      stream)
+                      _lib.ptr(self._pos) if self.mlp_impl == "fused" else None, stream)
             return
         denc = torch.empty(16 * n * 2, dtype=torch.float32, device=rays.device)
         if self.mlp_impl != "cuda":
@@ -408,6 +413,37 @@ class HashGridMLP(RegionField):
         _lib.call("vr_hash_bwd", _lib.addr(self.desc), _lib.ptr(rays), rays.shape[1],
                   _lib.ptr(t0), _lib.ptr(t1), _lib.ptr(ray_id), n, _lib.ptr(denc),
                   _lib.ptr(self.grad_table), _lib.ptr(ws), ws.numel(), stream)
+
+    # ---- split backward: the MLP part and the hash-grid scatter as separate launches, so
+    # VolumePool can run region k's scatter (L2-atomic bound) on a side stream while the
+    # tensor-core MLP backward of region k+1 runs on the main stream
+    # measured: split + side-stream scatter beats the fused kernel for level-major tables
+    # (c4 NeRF) and for small tables (c4 proposals, 12 MB: 549 -> 535 ms per c4 step); the
+    # fused kernel wins for mid-size L2-resident tables (c3, 49 MB: 61.3 vs 64.8 ms)
+    SPLIT_BELOW_BYTES = 16 << 20
+
+    @property
+    def split_backward(self):
+        return self.mlp_impl in ("fused", "tc") and (
+            self.hash_order == "level" or self.n_entries * 8 < self.SPLIT_BELOW_BYTES)
+
+    def backward_mlp(self, rays, ray_id, n, dsig_rgb, stream):
+        """MLP backward of the step's samples; returns d(enc) [16][n] float2 (float32)."""
+        denc = torch.empty(16 * max(n, 1) * 2, dtype=torch.float32, device=rays.device)
+        if n:
+            _lib.call("vr_mlp_bwd_tc", _lib.ptr(self.weights16), _lib.ptr(self._enc),
+                      _lib.ptr(rays), rays.shape[1], _lib.ptr(ray_id), n, _lib.ptr(dsig_rgb),
+                      _lib.ptr(self.grad_weights), _lib.ptr(denc), _lib.ptr(self.err), stream)
+        return denc
+
+    def backward_scatter(self, denc, n, stream, max_blocks=0):
+        """Hash-grid scatter of d(enc) at the positions stored by the forward."""
+        if n == 0:
+            return
+        ws = self._workspace(denc.device)
+        _lib.call("vr_hash_scatter", _lib.addr(self.desc), _lib.ptr(self._pos), n,
+                  _lib.ptr(denc), _lib.ptr(self.grad_table), _lib.ptr(ws), ws.numel(),
+                  1 if self.hash_order == "level" else 0, int(max_blocks), stream)
 
     def zero_grad(self):
         self.grad_table.zero_()

@@ -42,7 +42,7 @@ for nl in (1, 2, 4, 8, 12, 16):
     d = L.VrHashGridDesc.from_buffer_copy(f.desc)
     d.n_levels = nl
     tf = timeit(lambda: L.call("vr_hash_fwd", L.addr(d), L.ptr(f.table), L.ptr(rays), rays.shape[1],
-                               L.ptr(b.t0[lo:]), L.ptr(b.t1[lo:]), L.ptr(b.ray_id[lo:]), n, L.ptr(enc), s))
+                               L.ptr(b.t0[lo:]), L.ptr(b.t1[lo:]), L.ptr(b.ray_id[lo:]), n, L.ptr(enc), None, s))
     nb = int(L.load().vr_hash_bwd_workspace_bytes(L.addr(d)))
     ws = torch.zeros(max(nb, 16), dtype=torch.uint8, device=DEV)
     tb = timeit(lambda: L.call("vr_hash_bwd", L.addr(d), L.ptr(rays), rays.shape[1], L.ptr(b.t0[lo:]),

@@ -297,13 +297,17 @@ def test_hash_indices_bit_exact():
         assert np.array_equal(idx.cpu().numpy().astype(np.int64), want)
 
 
-@pytest.mark.parametrize("mlp_impl,hash_order", [("fused", "sample"), ("fused_fwd", "sample"),
-                                                 ("tc", "sample"), ("cuda", "sample"),
-                                                 ("fused", "level"), ("cuda", "level")])
+# overlap: split backward (MLP on the main stream, scatter on the side stream) vs the
+# fused tensor-core backward / per-field backward
+@pytest.mark.parametrize("mlp_impl,hash_order,overlap", [
+    ("fused", "sample", False), ("fused", "sample", True), ("fused_fwd", "sample", False),
+    ("tc", "sample", False), ("cuda", "sample", False), ("fused", "level", True),
+    ("fused", "level", False), ("cuda", "level", False)])
 @pytest.mark.parametrize("restriction", [False, True])
-def test_hashmlp_loss_and_grads_match_oracle(restriction, mlp_impl, hash_order):
+def test_hashmlp_loss_and_grads_match_oracle(restriction, mlp_impl, hash_order, overlap):
     pool, tree, models, rays, targets = _hash_setup(log2_T=14, K=2, restriction=restriction,
                                                     mlp_impl=mlp_impl, hash_order=hash_order)
+    pool.overlap_backward = overlap  # the split pipeline applies to level-major fields
     dt = 0.04
     pool.zero_grad()
     loss, out, b = pool.loss_and_grad(rays, targets, dt)
@@ -343,11 +347,14 @@ def test_level_major_hash_kernels_match_sample_major():
     enc_b = torch.empty((16, n), dtype=torch.float32, device=DEV)
     pos = torch.empty((3, n), dtype=torch.float32, device=DEV)
     args = (_lib.ptr(rd), rd.shape[1], _lib.ptr(b.t0), _lib.ptr(b.t1), _lib.ptr(b.ray_id), n)
-    _lib.call("vr_hash_fwd", _lib.addr(f.desc), _lib.ptr(f.table), *args, _lib.ptr(enc_a), s)
+    pos_a = torch.empty((3, n), dtype=torch.float32, device=DEV)
+    _lib.call("vr_hash_fwd", _lib.addr(f.desc), _lib.ptr(f.table), *args, _lib.ptr(enc_a),
+              _lib.ptr(pos_a), s)
     _lib.call("vr_hash_positions", _lib.addr(f.desc), *args, _lib.ptr(pos), s)
     _lib.call("vr_hash_fwd_lm", _lib.addr(f.desc), _lib.ptr(f.table), _lib.ptr(pos), n,
               _lib.ptr(enc_b), s)
     assert torch.equal(enc_a.view(torch.int32), enc_b.view(torch.int32))
+    assert torch.equal(pos_a.view(torch.int32), pos.view(torch.int32))
     denc = torch.randn((16, n, 2), device=DEV)
     ga = torch.zeros_like(f.table)
     gb = torch.zeros_like(f.table)
@@ -356,10 +363,14 @@ def test_level_major_hash_kernels_match_sample_major():
               ws.numel(), s)
     _lib.call("vr_hash_bwd_lm", _lib.addr(f.desc), _lib.ptr(pos), n, _lib.ptr(denc),
               _lib.ptr(gb), _lib.ptr(ws), ws.numel(), s)
+    gc = torch.zeros_like(f.table)  # sample order from stored positions, co-resident grid
+    _lib.call("vr_hash_scatter", _lib.addr(f.desc), _lib.ptr(pos), n, _lib.ptr(denc),
+              _lib.ptr(gc), _lib.ptr(ws), ws.numel(), 0, 148, s)
     torch.cuda.synchronize()
     assert torch.count_nonzero(ga) > 1000
-    rel = ((ga - gb).norm() / ga.norm()).item()
-    assert rel < 1e-5, rel
+    for g in (gb, gc):
+        rel = ((ga - g).norm() / ga.norm()).item()
+        assert rel < 1e-5, rel
 
 
 def test_hash_order_auto_picks_level_major_for_tables_larger_than_l2():
