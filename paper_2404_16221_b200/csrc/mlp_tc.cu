@@ -494,7 +494,7 @@ __global__ void __launch_bounds__(TILE * BWD_TPR, 2)
                  float2* __restrict__ denc, int32_t* err, const VrHashGridDesc hg,
                  const RepPlan plan, const double* __restrict__ t0,
                  const double* __restrict__ t1, float2* __restrict__ grad_table,
-                 float2* __restrict__ rep_ws, int do_scatter, const float* __restrict__ pos) {
+                 float2* __restrict__ rep_ws, const float* __restrict__ pos) {
   using G = Geo<BWD_TPR>;
   extern __shared__ __align__(1024) uint8_t smem[];
   uint8_t* sw = smem;
@@ -569,7 +569,7 @@ __global__ void __launch_bounds__(TILE * BWD_TPR, 2)
   float pk[16], pu[3];
   const int gwarp = blockIdx.x * (TILE * BWD_TPR / 32) + (threadIdx.x >> 5);
   auto scatter_one = [&](int j) {
-    if (FUSED && pending && do_scatter)
+    if (FUSED && pending)
       scatter_level(hg, plan, 8 * part + j, pu, make_float2(pk[2 * j], pk[2 * j + 1]), gwarp,
                     grad_table, rep_ws);
   };
@@ -798,7 +798,7 @@ int launch_bwd(const void* w, const void* enc, const double* rays, int64_t strid
   mlp::k_mlp_bwd_tc<FUSED><<<grid, mlp::TILE * mlp::BWD_TPR, mlp::B_SMEM, (cudaStream_t)stream>>>(
       (const __half*)w, (const __half2*)enc, rays, stride, rid, n,
       reinterpret_cast<const float4*>(dsr), gW, reinterpret_cast<float2*>(denc), err, gd, plan, t0, t1, reinterpret_cast<float2*>(grad_table),
-      reinterpret_cast<float2*>(ws), getenv("VR_DEBUG_NOSCATTER") ? 0 : 1, pos);
+      reinterpret_cast<float2*>(ws), pos);
   rc = check_launch("vr_mlp_bwd_tc");
   if (rc != VR_OK || !FUSED) return rc;
   return hash_rep_reduce(&gd, plan, red, grad_table, ws, stream);
