@@ -266,6 +266,14 @@ int vr_segment_fwd(const double* t0_dev, const double* t1_dev, const float* sig_
                    const int64_t* offsets_dev, const int32_t* seg_first_dev,
                    const double* ray_te_dev, int64_t n_rays, int32_t region_cnt,
                    float* packets_dev, int32_t* err_dev, void* stream);
+/* Sample-broadcast protocol (distsim.py:311-316, _compose_samples distsim.py:385-392):
+ * move per-sample elements (4, 8 or 16 bytes) between the region-major K1 layout and a
+ * ray-major layout (ray_off = exclusive scan of per-ray totals, a ray's segments in t
+ * order via seg_first), so vr_segment_fwd/bwd with region_cnt = 1 composite whole rays. */
+int vr_segment_permute(const int64_t* offsets_dev, const int32_t* seg_first_dev,
+                       const int64_t* ray_offsets_dev, int64_t n_rays, int32_t n_regions,
+                       const void* src_dev, void* dst_dev, int32_t elem_bytes,
+                       int32_t to_ray_major, void* stream);
 /* analytic backward: dpackets [region_cnt][n_rays][8] = adjoints of {T,C,A,D',L};
  * writes dsig_rgb[i] = {dL/dsigma, dL/dr, dL/dg, dL/db}. */
 int vr_segment_bwd(const double* t0_dev, const double* t1_dev, const float* sig_rgb_dev,

@@ -350,6 +350,24 @@ def render_ray_tile(tree: Tree, field_eval, o, d, tn, tf, dt):
     return fold_packets([s[2] for s in segs])
 
 
+def render_ray_samples(tree: Tree, field_eval, o, d, tn, tf, dt):
+    """(C, A, D, T, L) under the sample-broadcast / mono protocols: every bin, owner-
+    evaluated, in t0 order, one composite_samples over the whole ray (_compose_samples
+    distsim.py:385-392, mono distsim.py:398-404)."""
+    t0, t1, tile = sample_ray(tree, o, d, tn, tf, dt)
+    if len(t0) == 0:
+        return np.zeros(3), 0.0, 0.0, 1.0, 0.0
+    sig = np.zeros(len(t0))
+    rgb = np.zeros((len(t0), 3))
+    for k in sorted(set(tile.tolist())):
+        sel = np.nonzero(tile == k)[0]
+        mids = 0.5 * (t0[sel] + t1[sel])
+        sig[sel], rgb[sel] = field_eval(k, np.asarray(o) + mids[:, None] * np.asarray(d), d)
+    order = np.argsort(t0, kind="stable")
+    T, C, A, D, L = segment_packet(t0[order], t1[order], sig[order], rgb[order])
+    return C, A, D, T, L
+
+
 def ray_loss(C, T, L, bg, target, lambda_dist=1.0):
     pix = np.asarray(C) + T * np.asarray(bg)
     err = pix - np.asarray(target)

@@ -43,6 +43,46 @@ def all_gather_packets(local: torch.Tensor, group=None, world: int = 1) -> torch
     return out
 
 
+def exchange_samples(sig_rgb: torch.Tensor, bounds, n_regions: int, group=None, world: int = 1,
+                     rank: int = 0, dst=None):
+    """Sample-broadcast protocol (distsim.py:311-316): every rank sampled all regions and
+    evaluated its own block [bounds[lo], bounds[lo+cnt]) of the region-major [N, 4]
+    (sigma, r, g, b) array; the other ranks' blocks are filled in place.  dst=None:
+    all-gather (training, every rank composes); dst=r: gather to rank r only (render).
+    16 B per sample cross the link (t0/t1 are recomputed by every rank's K1).  Returns
+    False on ranks that did not receive (gather)."""
+    if world == 1:
+        return True
+    per = n_regions // world
+    blocks = [(int(bounds[r * per]), int(bounds[(r + 1) * per])) for r in range(world)]
+    m = max(1, max(hi - lo for lo, hi in blocks))
+    lo, hi = blocks[rank]
+    mine = torch.zeros((m, 4), dtype=sig_rgb.dtype, device=sig_rgb.device)
+    mine[: hi - lo] = sig_rgb[lo:hi]
+    staged = _host_staged(group, mine)
+    src = mine.cpu() if staged else mine
+    if dst is None:
+        if staged:
+            parts = [torch.empty_like(src) for _ in range(world)]
+            dist.all_gather(parts, src, group=group)
+            allp = torch.cat(parts, dim=0).to(sig_rgb.device)
+        else:
+            allp = torch.empty((world * m, 4), dtype=sig_rgb.dtype, device=sig_rgb.device)
+            dist.all_gather_into_tensor(allp, src, group=group)
+    else:
+        if rank == dst:
+            parts = [torch.empty_like(src) for _ in range(world)]
+            dist.gather(src, gather_list=parts, dst=dst, group=group)
+            allp = torch.cat(parts, dim=0).to(sig_rgb.device)
+        else:
+            dist.gather(src, gather_list=None, dst=dst, group=group)
+            return False
+    for r, (blo, bhi) in enumerate(blocks):
+        if r != rank and bhi > blo:
+            sig_rgb[blo:bhi] = allp[r * m: r * m + (bhi - blo)]
+    return True
+
+
 def gather_packets(local: torch.Tensor, group=None, world: int = 1, rank: int = 0, dst: int = 0):
     """Inference: packets only need to reach one compositor rank."""
     if world == 1:

@@ -667,6 +667,57 @@ extern "C" int vr_global_train(const float* pk, int32_t n_regions, int64_t n_ray
   return check_launch("vr_global_train");
 }
 
+// ---- sample-broadcast protocol: region-major <-> ray-major sample order ---------------
+// Segment (k, r) occupies [off[k*R + r], off[k*R + r + 1]) in the region-major layout and
+// [ray_off[r] + seg_first[k*R + r], ...) in the ray-major one (seg_first = index along the
+// ray of the segment's first sample, so a ray's segments land in t order).  Warp per
+// segment, lanes copy consecutive elements of ELEM bytes.
+template <typename T>
+__global__ void k_segment_permute(const int64_t* __restrict__ off,
+                                  const int32_t* __restrict__ seg_first,
+                                  const int64_t* __restrict__ ray_off, int64_t n_rays,
+                                  int64_t n_segs, const T* __restrict__ src, T* __restrict__ dst,
+                                  int to_ray_major) {
+  const int lane = threadIdx.x & 31;
+  for (int64_t sg = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5); sg < n_segs;
+       sg += (int64_t)gridDim.x * (blockDim.x >> 5)) {
+    const int64_t b = off[sg], e = off[sg + 1];
+    if (b == e) continue;
+    const int64_t rm = ray_off[sg % n_rays] + seg_first[sg];
+    for (int64_t j = lane; j < e - b; j += 32) {
+      if (to_ray_major)
+        dst[rm + j] = src[b + j];
+      else
+        dst[b + j] = src[rm + j];
+    }
+  }
+}
+
+extern "C" int vr_segment_permute(const int64_t* off, const int32_t* seg_first,
+                                  const int64_t* ray_off, int64_t n_rays, int32_t n_regions,
+                                  const void* src, void* dst, int32_t elem_bytes,
+                                  int32_t to_ray_major, void* stream) {
+  if (n_rays < 0 || n_regions < 1 || n_regions > VR_MAX_REGIONS ||
+      (elem_bytes != 4 && elem_bytes != 8 && elem_bytes != 16)) {
+    set_error("vr_segment_permute: bad argument");
+    return VR_ERR_BAD_ARG;
+  }
+  const int64_t n_segs = n_rays * n_regions;
+  if (n_segs == 0) return VR_OK;
+  const int grid = grid_for(ceil_div(n_segs, 8), 1, 16);
+  cudaStream_t s = (cudaStream_t)stream;
+  if (elem_bytes == 4)
+    k_segment_permute<<<grid, 256, 0, s>>>(off, seg_first, ray_off, n_rays, n_segs,
+                                           (const float*)src, (float*)dst, to_ray_major);
+  else if (elem_bytes == 8)
+    k_segment_permute<<<grid, 256, 0, s>>>(off, seg_first, ray_off, n_rays, n_segs,
+                                           (const double*)src, (double*)dst, to_ray_major);
+  else
+    k_segment_permute<<<grid, 256, 0, s>>>(off, seg_first, ray_off, n_rays, n_segs,
+                                           (const float4*)src, (float4*)dst, to_ray_major);
+  return check_launch("vr_segment_permute");
+}
+
 extern "C" int vr_sum_f64(const double* x, int64_t n, double* out, void* stream) {
   if (n < 0 || !out) {
     set_error("vr_sum_f64: bad argument");

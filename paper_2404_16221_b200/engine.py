@@ -28,7 +28,7 @@ from .errors import ProtocolMismatchError
 from .fields import RegionField, Scene, region_field_for
 from .geometry import Aabb, Camera, Ray, camera_rays, rays_to_soa, vec3
 from .partition import PartitionTree
-from .stats import COMPOSITOR, SCALARS_PER_TILE_PACKET, CommStats
+from .stats import COMPOSITOR, SCALARS_PER_SAMPLE, SCALARS_PER_TILE_PACKET, CommStats
 
 PROTOCOLS = ("mono", "sample_broadcast", "tile_aggregate")
 _ALIASES = {"sample": "sample_broadcast", "tile": "tile_aggregate"}
@@ -150,11 +150,13 @@ class VolumePool:
         return self._ws
 
     # ---- K1 ----------------------------------------------------------------------------
-    def sample(self, rays: torch.Tensor, dt: float) -> SampleBatch:
+    def sample(self, rays: torch.Tensor, dt: float, all_regions: bool = False) -> SampleBatch:
+        """K1 for the owned regions (or every region: sample-broadcast protocol)."""
         if not dt > 0.0:
             raise ValueError("dt must be > 0")
         R = rays.shape[1]
-        cnt = self.region_cnt
+        region_lo, cnt = (0, self.n_regions) if all_regions else (self.region_lo,
+                                                                  self.region_cnt)
         dev = self.device
         s = self._stream()
         counts = torch.empty(cnt * R, dtype=torch.int32, device=dev)
@@ -164,7 +166,7 @@ class VolumePool:
         ray_total = torch.empty(R, dtype=torch.int32, device=dev)
         tc = _lib.addr(self.tree_c)
         _lib.call("vr_sample_count", tc, _lib.ptr(rays), rays.shape[1], R, float(dt),
-                  self.region_lo, cnt, _lib.ptr(counts), _lib.ptr(seg_first), _lib.ptr(ray_te),
+                  region_lo, cnt, _lib.ptr(counts), _lib.ptr(seg_first), _lib.ptr(ray_te),
                   _lib.ptr(ray_part), _lib.ptr(ray_total), _lib.ptr(self.err), s)
         offsets = torch.empty(cnt * R + 1, dtype=torch.int64, device=dev)
         ws = self._workspace(cnt * R)
@@ -179,15 +181,18 @@ class VolumePool:
         ray_id = torch.empty(max(N, 1), dtype=torch.int32, device=dev)
         if N:
             _lib.call("vr_sample_fill", tc, _lib.ptr(rays), rays.shape[1], R, float(dt),
-                      self.region_lo, cnt, _lib.ptr(offsets), _lib.ptr(seg_first), _lib.ptr(t0),
+                      region_lo, cnt, _lib.ptr(offsets), _lib.ptr(seg_first), _lib.ptr(t0),
                       _lib.ptr(t1), _lib.ptr(ray_id), _lib.ptr(self.err), s)
-        return SampleBatch(R, self.region_lo, cnt, counts, seg_first, offsets, ray_te, ray_part,
+        return SampleBatch(R, region_lo, cnt, counts, seg_first, offsets, ray_te, ray_part,
                            ray_total, t0, t1, ray_id, [int(b) for b in bounds])
 
     # ---- fields -------------------------------------------------------------------------
     def evaluate(self, rays: torch.Tensor, b: SampleBatch, fields=None) -> torch.Tensor:
         fields = self.fields if fields is None else fields
-        sig_rgb = torch.empty((max(b.n_samples, 1), 4), dtype=torch.float32, device=self.device)
+        base = self.region_lo - b.region_lo  # an all-region batch: skip the peers' regions
+        # (an all-region batch leaves the peers' rows zero until the exchange fills them)
+        alloc = torch.zeros if base or len(fields) < b.region_cnt else torch.empty
+        sig_rgb = alloc((max(b.n_samples, 1), 4), dtype=torch.float32, device=self.device)
         s = self._stream()
         # Off by default: measured on c3 the concurrent MLP CTAs (52 KB smem each) shrink the
         # L1 the gathers live on and the step got slower (76.7 vs 67.6 ms).
@@ -195,7 +200,7 @@ class VolumePool:
                  and all(getattr(f, "splittable", False) for f in fields))
         if not split:
             for kk, f in enumerate(fields):
-                lo, hi = b.region_slice(kk)
+                lo, hi = b.region_slice(base + kk)
                 if hi > lo:
                     f.forward(rays, b.t0[lo:], b.t1[lo:], b.ray_id[lo:], hi - lo, sig_rgb[lo:], s)
             return sig_rgb
@@ -205,7 +210,7 @@ class VolumePool:
         side = self._side_stream()
         side.wait_stream(main)
         for kk, f in enumerate(fields):
-            lo, hi = b.region_slice(kk)
+            lo, hi = b.region_slice(base + kk)
             if hi <= lo:
                 continue
             f.forward_hash(rays, b.t0[lo:], b.t1[lo:], b.ray_id[lo:], hi - lo, s)
@@ -224,6 +229,7 @@ class VolumePool:
     def field_backward(self, rays, b: SampleBatch, dsig_rgb: torch.Tensor, fields=None) -> None:
         s = self._stream()
         fields = self.fields if fields is None else fields
+        base = self.region_lo - b.region_lo  # an all-region batch: skip the peers' regions
         if self.overlap_backward and all(getattr(f, "split_backward", False)
                                          for f in fields if f.trainable):
             # region k's hash-grid scatter (L2-atomic bound) runs on the side stream while
@@ -233,7 +239,7 @@ class VolumePool:
             side = self._side_stream()
             side.wait_stream(main)
             for kk, f in enumerate(fields):
-                lo, hi = b.region_slice(kk)
+                lo, hi = b.region_slice(base + kk)
                 if hi <= lo or not f.trainable:
                     continue
                 denc = f.backward_mlp(rays, b.ray_id[lo:], hi - lo, dsig_rgb[lo:], s)
@@ -246,7 +252,7 @@ class VolumePool:
             main.wait_stream(side)
             return
         for kk, f in enumerate(fields):
-            lo, hi = b.region_slice(kk)
+            lo, hi = b.region_slice(base + kk)
             if hi > lo and f.trainable:
                 f.backward(rays, b.t0[lo:], b.t1[lo:], b.ray_id[lo:], hi - lo, dsig_rgb[lo:], s)
 
@@ -274,10 +280,21 @@ class VolumePool:
         return out
 
     # ---- entry points ------------------------------------------------------------------
-    def render_rays(self, rays, dt: float, background=None, clip: bool = True):
+    def render_rays(self, rays, dt: float, background=None, clip: bool = True,
+                    protocol: str = "tile"):
         """Batched render.  Returns (out [7][R] on rank 0 / None elsewhere, batch);
-        out rows: r, g, b (C + T*bg clipped, or raw C if clip=False), alpha, depth, T, L."""
+        out rows: r, g, b (C + T*bg clipped, or raw C if clip=False), alpha, depth, T, L.
+        protocol: "tile" (segment packets, the NeRF-XL path), "sample" (per-sample
+        broadcast) or "mono" (one composite over the whole ray, no exchange)."""
         rays = self.rays_to_device(rays)
+        protocol = canonical_protocol(protocol)
+        if protocol != "tile_aggregate":
+            b, res = self._sample_protocol_forward(rays, dt, train=False)
+            if res is None:
+                return None, b
+            _, ray_off, (t0r, t1r, srr) = res
+            pk = self._whole_ray_packets(b, ray_off, t0r, t1r, srr)
+            return self.compose(pk, b, background, clip), b
         b = self.sample(rays, dt)
         sig_rgb = self.evaluate(rays, b)
         local = self.local_packets(b, sig_rgb)
@@ -286,8 +303,52 @@ class VolumePool:
             return None, b
         return self.compose(allp, b, background, clip), b
 
+    # ---- sample-broadcast / mono protocols --------------------------------------------
+    # The reference's per-sample protocols (distsim.py:311-316, _compose_samples
+    # distsim.py:385-392, mono distsim.py:398-404): every rank samples every region, its
+    # own regions' (sigma, rgb) cross the link (16 B per sample instead of 32 B per
+    # (ray, region) packet), and whole rays are composited in t order — the region-major
+    # samples are permuted ray-major so K4 (region_cnt = 1) sees one segment per ray.
+    def _ray_major(self, b: SampleBatch):
+        R = b.n_rays
+        s = self._stream()
+        ray_off = torch.empty(R + 1, dtype=torch.int64, device=self.device)
+        ws = self._workspace(R)
+        _lib.call("vr_scan_offsets", _lib.ptr(b.ray_total), R, _lib.ptr(ray_off), _lib.ptr(ws),
+                  ws.numel(), s)
+        return ray_off
+
+    def _permute(self, b: SampleBatch, ray_off, src: torch.Tensor, to_ray_major: bool):
+        dst = torch.empty_like(src)
+        _lib.call("vr_segment_permute", _lib.ptr(b.offsets), _lib.ptr(b.seg_first),
+                  _lib.ptr(ray_off), b.n_rays, b.region_cnt, _lib.ptr(src), _lib.ptr(dst),
+                  src.element_size() * (src.shape[1] if src.dim() == 2 else 1),
+                  1 if to_ray_major else 0, self._stream())
+        return dst
+
+    def _whole_ray_packets(self, b: SampleBatch, ray_off, t0r, t1r, srr):
+        R = b.n_rays
+        pk = torch.empty((1, R, 8), dtype=torch.float32, device=self.device)
+        first = torch.zeros(R, dtype=torch.int32, device=self.device)  # one packet per ray
+        _lib.call("vr_segment_fwd", _lib.ptr(t0r), _lib.ptr(t1r), _lib.ptr(srr),
+                  _lib.ptr(ray_off), _lib.ptr(first), _lib.ptr(b.ray_te), R, 1, _lib.ptr(pk),
+                  _lib.ptr(self.err), self._stream())
+        return pk
+
+    def _sample_protocol_forward(self, rays, dt: float, train: bool):
+        b = self.sample(rays, dt, all_regions=True)
+        sig_rgb = self.evaluate(rays, b)
+        got = comm.exchange_samples(sig_rgb, b.region_bounds, self.n_regions, self.group,
+                                    self.world, self.rank, None if train else 0)
+        if not got:
+            return b, None
+        ray_off = self._ray_major(b)
+        rm = [self._permute(b, ray_off, x, True) for x in (b.t0, b.t1, sig_rgb)]
+        return b, (sig_rgb, ray_off, rm)
+
     def loss_and_grad(self, rays, targets, dt: float, lambda_dist: float = 1.0,
-                      background=None, lambda_interlevel: float = 0.0, eps: float = 1e-7):
+                      background=None, lambda_interlevel: float = 0.0, eps: float = 1e-7,
+                      protocol: str = "tile"):
         """Forward + backward of the NeRF-XL loss (segrender.py:198-207 definition:
         sum over rays of |C + T*bg - target|^2 + lambda * distortion), plus, with
         proposal fields and lambda_interlevel > 0, the interlevel loss of csrc/interlevel.cu
@@ -300,6 +361,11 @@ class VolumePool:
         if tg.shape[0] != rays.shape[1]:
             raise ValueError("targets must be (R, 3)")
         s = self._stream()
+        protocol = canonical_protocol(protocol)
+        if protocol != "tile_aggregate":
+            if lambda_interlevel > 0.0:
+                raise ValueError("the interlevel loss is defined on the tile protocol")
+            return self._sample_protocol_train(rays, tg, dt, lambda_dist, background)
         b = self.sample(rays, dt)
         sig_rgb = self.evaluate(rays, b)
         local = self.local_packets(b, sig_rgb)
@@ -342,6 +408,29 @@ class VolumePool:
         self.field_backward(rays, b, dsig)
         return loss, out, b
 
+    def _sample_protocol_train(self, rays, tg, dt, lambda_dist, background):
+        """Training through the sample-broadcast protocol: every rank composites whole rays
+        from all samples, takes the gradients of its own samples (no gradient exchange
+        either way)."""
+        s = self._stream()
+        b, (sig_rgb, ray_off, (t0r, t1r, srr)) = self._sample_protocol_forward(rays, dt, True)
+        R = b.n_rays
+        pk = self._whole_ray_packets(b, ray_off, t0r, t1r, srr)
+        out = torch.empty((7, R), dtype=torch.float32, device=self.device)
+        ray_loss = torch.empty(R, dtype=torch.float64, device=self.device)
+        dpk = torch.empty((1, R, 8), dtype=torch.float32, device=self.device)
+        _lib.call("vr_global_train", _lib.ptr(pk), 1, R, _lib.ptr(b.ray_te),
+                  _lib.addr(self._set_bg(background)), _lib.ptr(tg), float(lambda_dist), 0, 1,
+                  _lib.ptr(out), _lib.ptr(ray_loss), _lib.ptr(dpk), _lib.ptr(self.err), s)
+        loss = torch.empty(1, dtype=torch.float64, device=self.device)
+        _lib.call("vr_sum_f64", _lib.ptr(ray_loss), R, _lib.ptr(loss), s)
+        dsr = torch.zeros_like(srr)
+        _lib.call("vr_segment_bwd", _lib.ptr(t0r), _lib.ptr(t1r), _lib.ptr(srr), _lib.ptr(ray_off),
+                  _lib.ptr(b.ray_te), R, 1, _lib.ptr(dpk), _lib.ptr(dsr), s)
+        dsig = self._permute(b, ray_off, dsr, False)
+        self.field_backward(rays, b, dsig)
+        return loss, out, b
+
     def zero_grad(self):
         for f in self.fields + (self.proposals or []):
             f.zero_grad()
@@ -358,14 +447,32 @@ class VolumePool:
         return loss
 
     # ---- accounting ----------------------------------------------------------------------
-    def comm_stats(self, b: SampleBatch, broadcast_all: bool = False) -> CommStats:
+    def comm_stats(self, b: SampleBatch, broadcast_all: bool = False,
+                   protocol: str = "tile") -> CommStats:
         """Reference-style scalar counts (distsim.py:415-446) from the K1 outputs."""
+        protocol = canonical_protocol(protocol)
         st = CommStats()
         st.rays = b.n_rays
+        if protocol == "mono":  # one field, no workers (distsim.py:398-404)
+            return st
         part = b.ray_part.to(torch.int64) & 0xFFFFFFFF
         per_leaf = [int(((part >> k) & 1).sum().item()) for k in range(self.n_regions)]
         st.participations = int(sum(per_leaf))
         st.samples_assigned = int(b.ray_total.to(torch.int64).sum().item())
+        if protocol == "sample_broadcast":
+            # one SamplePayload per participation: 1 + 6 scalars per bin (distsim.py:151)
+            for k, n in enumerate(per_leaf):
+                if n:
+                    bins = b.region_bounds[k + 1] - b.region_bounds[k]
+                    st.record(k, COMPOSITOR, n + SCALARS_PER_SAMPLE * bins, n)
+            if self.world > 1:
+                per = self.n_regions // self.world
+                blk = [b.region_bounds[(r + 1) * per] - b.region_bounds[r * per]
+                       for r in range(self.world)]
+                st.link_bytes = (self.world - 1) * max(blk) * 16
+            else:
+                st.link_bytes = 0
+            return st
         for k, n in enumerate(per_leaf):
             if n:
                 st.record(k, COMPOSITOR, SCALARS_PER_TILE_PACKET * n, n)
@@ -408,10 +515,8 @@ def render_ray(pool: VolumePool, ray: Ray, protocol: str, dt: float, rng=None,
     if pool.num_workers == 0:
         raise ProtocolMismatchError("worker pool is empty")
     protocol = canonical_protocol(protocol)
-    if protocol != "tile_aggregate":
-        raise NotImplementedError(f"protocol {protocol!r} is not on the B200 path (SURVEY §8(f))")
-    out, b = pool.render_rays(rays_to_soa([ray]), dt, clip=False)
-    st = pool.comm_stats(b, broadcast_all)
+    out, b = pool.render_rays(rays_to_soa([ray]), dt, clip=False, protocol=protocol)
+    st = pool.comm_stats(b, broadcast_all, protocol)
     if out is None:
         return None, st
     return _aggregate_from_out(out.cpu().numpy(), 0), st
@@ -425,12 +530,10 @@ def render_image(pool: VolumePool, camera: Camera, protocol: str, dt: float, bac
     if pool.num_workers == 0:
         raise ProtocolMismatchError("worker pool is empty")
     protocol = canonical_protocol(protocol)
-    if protocol != "tile_aggregate":
-        raise NotImplementedError(f"protocol {protocol!r} is not on the B200 path (SURVEY §8(f))")
     t0 = time.perf_counter()
     rays = camera_rays(camera, pool.tree.root_box)
-    out, b = pool.render_rays(rays, dt, background=background, clip=True)
-    st = pool.comm_stats(b, broadcast_all)
+    out, b = pool.render_rays(rays, dt, background=background, clip=True, protocol=protocol)
+    st = pool.comm_stats(b, broadcast_all, protocol)
     if out is None:
         return None, st
     img = out[0:3].T.contiguous().cpu().numpy().astype(np.float64)

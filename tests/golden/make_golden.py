@@ -11,6 +11,9 @@ Fixtures
                   distsim.py:369-373, :406-419)
   render_*.npz    per-ray RayAggregate of distsim.render_ray(..., "tile_aggregate")
   image_three_blobs.npz   distsim.render_image of the builtin 64x64 camera, K=4
+  image_three_blobs_{sample,mono}.npz   the same image and CommStats under the
+                  sample-broadcast and mono protocols (distsim.py:311-316, :385-404);
+                  `make_golden.py protocols` regenerates only these two files
   grad_voxel_room.json    DistributedLossProbe.gradient_pair (local, global) FD
                   gradients of the voxel_room loss (segrender.py:153-251)
 """
@@ -221,5 +224,25 @@ def main():
     print("grad_voxel_room:", len(entries), "entries, loss", base_loss)
 
 
+def protocols():
+    """render_image of the builtin three_blobs camera under the per-sample protocols."""
+    b = scenes.three_blobs()
+    tree_tb = partitioner.build_tree(b.points, b.scene.root_box, b.depth)
+    for proto in ("sample_broadcast", "mono"):
+        pool = distsim.spawn(tree_tb, b.scene)
+        img, st = distsim.render_image(pool, b.camera, proto, b.dt)
+        short = "sample" if proto == "sample_broadcast" else proto
+        np.savez_compressed(OUT / f"image_three_blobs_{short}.npz", image=img,
+                            tree=json.dumps(partitioner.tree_to_json(tree_tb)),
+                            scene=json.dumps(scene_to_json(b.scene)),
+                            camera=json.dumps(b.camera.to_json()), dt=np.float64(b.dt),
+                            stats=json.dumps(distsim.stats_json(st, proto, 4)))
+        print(f"image_three_blobs_{short}: scalars", st.scalars_sent_total)
+
+
 if __name__ == "__main__":
-    main()
+    if sys.argv[1:] == ["protocols"]:
+        protocols()
+    else:
+        main()
+        protocols()

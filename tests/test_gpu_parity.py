@@ -102,11 +102,14 @@ def _scene_pool(g, world=1, rank=0):
     return vr.spawn(tree, scene, DEV, rank, world), tree, scene
 
 
+# the reference's protocols all integrate the same bins and agree within 1e-10
+# (distsim.render_ray docstring), so every protocol is checked against the tile golden
+@pytest.mark.parametrize("protocol", ["tile", "sample", "mono"])
 @pytest.mark.parametrize("name", render_fixtures())
-def test_render_matches_reference(name):
+def test_render_matches_reference(name, protocol):
     g = load_npz(name)
     pool, tree, scene = _scene_pool(g)
-    out, b = pool.render_rays(_soa(g["rays"]), float(g["dt"]), clip=False)
+    out, b = pool.render_rays(_soa(g["rays"]), float(g["dt"]), clip=False, protocol=protocol)
     torch.cuda.synchronize()
     pool.check()
     got = out.cpu().numpy().T.astype(np.float64)  # (R, 7): C, A, depth, T, L
@@ -130,6 +133,45 @@ def test_render_image_matches_reference():
     assert st.scalars_sent_total == g["stats"]["scalars_sent_total"]
     assert [w["scalars_sent"] for w in vr.stats_json(st, "tile_aggregate", 4)["per_worker"]] == \
         [w["scalars_sent"] for w in g["stats"]["per_worker"]]
+
+
+@pytest.mark.parametrize("proto", ["sample", "mono"])
+def test_render_image_other_protocols_match_reference(proto):
+    """render_image under the sample-broadcast / mono protocols: image and the reference's
+    CommStats scalar counts (1 + 6 per bin per participation; nothing for mono)."""
+    g = load_npz(f"image_three_blobs_{proto}.npz")
+    pool, tree, scene = _scene_pool(g)
+    cam = vr.Camera.from_json(g["camera"])
+    img, st = vr.render_image(pool, cam, proto, float(g["dt"]))
+    np.testing.assert_allclose(img, g["image"], atol=1e-4, rtol=0)
+    assert st.rays == g["stats"]["rays"]
+    assert st.scalars_sent_total == g["stats"]["scalars_sent_total"]
+    mine = vr.stats_json(st, g["stats"]["protocol"], 4)["per_worker"]
+    ref = g["stats"]["per_worker"]
+    assert [(w["scalars_sent"], w["messages_sent"]) for w in mine] == \
+        [(w["scalars_sent"], w["messages_sent"]) for w in ref]
+
+
+def test_sample_protocol_multi_rank_exchange_is_bitwise_identical():
+    """Sample-broadcast with 2 simulated ranks: each evaluates only its own regions of the
+    all-region batch; the filled-in array (what the all-gather delivers) composes exactly
+    the single-rank image."""
+    g = load_npz("render_three_blobs_k4.npz")
+    rays = _soa(g["rays"])
+    dt = float(g["dt"])
+    pool1, _, _ = _scene_pool(g)
+    out1, _ = pool1.render_rays(rays, dt, protocol="sample")
+    full = None
+    for rank in range(2):
+        p, _, _ = _scene_pool(g, world=2, rank=rank)
+        rd = p.rays_to_device(rays)
+        b = p.sample(rd, dt, all_regions=True)
+        sr = p.evaluate(rd, b)
+        full = sr if full is None else full + sr  # disjoint blocks, zeros elsewhere
+    ray_off = p._ray_major(b)
+    rm = [p._permute(b, ray_off, x, True) for x in (b.t0, b.t1, full)]
+    out2 = p.compose(p._whole_ray_packets(b, ray_off, *rm), b)
+    assert torch.equal(out1, out2)
 
 
 def test_multi_rank_composite_is_bitwise_identical():
@@ -163,11 +205,12 @@ def _grad_setup():
     return doc, tree, scene, rays, targets
 
 
-def test_voxel_gradients_match_reference_fd():
+@pytest.mark.parametrize("protocol", ["tile", "sample"])
+def test_voxel_gradients_match_reference_fd(protocol):
     doc, tree, scene, rays, targets = _grad_setup()
     pool = vr.spawn(tree, scene, DEV)
     pool.zero_grad()
-    loss, out, b = pool.loss_and_grad(rays, targets, doc["dt"])
+    loss, out, b = pool.loss_and_grad(rays, targets, doc["dt"], protocol=protocol)
     torch.cuda.synchronize()
     pool.check()
     assert loss.item() == pytest.approx(doc["loss"], rel=1e-5)

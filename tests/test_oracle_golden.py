@@ -57,6 +57,25 @@ def test_image_matches_reference():
         np.testing.assert_allclose(img[i], g["image"].reshape(-1, 3)[i], atol=1e-12)
 
 
+@pytest.mark.parametrize("proto", ["sample", "mono"])
+def test_sample_protocol_image_matches_reference(proto):
+    """The per-sample protocols (one composite over all of a ray's bins) against the
+    reference's render_image under that protocol; they agree with the tile image to
+    ~1e-10 as the reference promises (distsim.render_ray docstring)."""
+    g = load_npz(f"image_three_blobs_{proto}.npz")
+    tile = load_npz("image_three_blobs.npz")
+    np.testing.assert_allclose(g["image"], tile["image"], rtol=0, atol=1e-9)
+    tree = vo.Tree(g["tree"])
+    ev = vo.scene_field_eval(g["scene"])
+    rays = vo.camera_rays(g["camera"], g["scene"]["root_box"]["min"], g["scene"]["root_box"]["max"])
+    bg = np.array(g["scene"]["background"])
+    for i in range(0, rays.shape[0], 11):
+        r = rays[i]
+        C, A, D, T, L = vo.render_ray_samples(tree, ev, r[0:3], r[3:6], r[6], r[7], float(g["dt"]))
+        np.testing.assert_allclose(np.clip(C + T * bg, 0.0, 1.0), g["image"].reshape(-1, 3)[i],
+                                   atol=1e-12)
+
+
 def test_voxel_grad_oracle_matches_reference_fd():
     doc = json.loads((GOLDEN / "grad_voxel_room.json").read_text())
     tree = vo.Tree(doc["tree"])
