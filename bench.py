@@ -287,6 +287,8 @@ def main():
     ap.add_argument("--backend", default="nccl", choices=["nccl", "gloo"],
                     help="gloo + --same-device: exercise the multi-rank path on one GPU")
     ap.add_argument("--same-device", action="store_true", help="all ranks on cuda:0 (testing)")
+    ap.add_argument("--protocol", default="tile", choices=["tile", "sample"],
+                    help="tile: NeRF-XL segment packets; sample: per-sample broadcast baseline")
     args = ap.parse_args()
     rank, world, local = dist_env()
 
@@ -327,14 +329,16 @@ def main():
 
     train = w.train
     metric = METRIC if train else RENDER_METRIC
+    # the interlevel loss is defined on the tile protocol's segments
+    interlevel = w.interlevel if args.protocol == "tile" else 0.0
 
     def one_step(r, t):
         nonlocal step
         step += 1
         if train:
             return pool.train_step(r, t, w.dt, lr=args.lr, step=step,
-                                   lambda_interlevel=w.interlevel)
-        out, _ = pool.render_rays(r, w.dt)  # forward only; gathered to rank 0
+                                   lambda_interlevel=interlevel, protocol=args.protocol)
+        out, _ = pool.render_rays(r, w.dt, protocol=args.protocol)  # gathered to rank 0
         return out
 
     for _ in range(args.warmup):
@@ -503,8 +507,19 @@ def main():
                            "dt": w.dt, "parallelism": f"region-parallel x{world}",
                            "l2": "inputs larger than L2 (tables+rays+samples >> 126 MB)",
                            "optimizer": "adam" if train else None,
-                           "loss": (("mse+distortion+interlevel" if w.interlevel else
-                                     "mse+distortion") if train else None)},
+                           "loss": (("mse+distortion+interlevel" if interlevel else
+                                     "mse+distortion") if train else None),
+                           "protocol": args.protocol},
+                "exchange": {
+                    "protocol": args.protocol,
+                    # data that crosses the link when every region is on its own GPU:
+                    # tile = one 32 B packet per (ray, region); sample = 16 B per sample
+                    "wire": "32 B/(ray, region) packet" if args.protocol == "tile"
+                            else "16 B/sample (sigma, rgb)",
+                    "bytes_per_step_1_region_per_gpu": (len(w.tree.leaves) * R * 32
+                                                        if args.protocol == "tile"
+                                                        else n_samples * 16),
+                    "tile_vs_sample_bytes": (len(w.tree.leaves) * R * 32) / max(1, n_samples * 16)},
                 "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e,
                 "gpu_launches": launches, "clocks": clk, "loss": final_loss,
                 "step_ms": [round(x, 3) for x in step_ms],

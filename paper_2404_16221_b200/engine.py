@@ -436,11 +436,12 @@ class VolumePool:
             f.zero_grad()
 
     def train_step(self, rays, targets, dt: float, lr: float = 1e-2, step: int = 1,
-                   lambda_dist: float = 1.0, background=None, lambda_interlevel: float = 0.0):
+                   lambda_dist: float = 1.0, background=None, lambda_interlevel: float = 0.0,
+                   protocol: str = "tile"):
         """One training iteration: zero grads, fwd+bwd, Adam.  Returns the device loss."""
         self.zero_grad()
         loss, _, _ = self.loss_and_grad(rays, targets, dt, lambda_dist, background,
-                                        lambda_interlevel)
+                                        lambda_interlevel, protocol=protocol)
         for f in self.fields + (self.proposals or []):
             if f.trainable:
                 f.step(lr, step)
