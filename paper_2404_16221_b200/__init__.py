@@ -48,10 +48,14 @@ from .geometry import Aabb, Camera, Ray, camera_ray_dirs, camera_rays, rays_to_s
 from .partition import (
     LeafNode,
     PartitionTree,
+    PointCloud,
     SplitNode,
+    balance_report,
     build_tree,
     choose_split,
+    default_root_box,
     grid_tree,
+    rays_to_points,
     load_tree,
     locate,
     locate_many,

@@ -15,8 +15,8 @@ from pathlib import Path
 import numpy as np
 
 from . import _lib
-from .errors import DegenerateSplitError, InsufficientPointsError, OutOfBoundsError
-from .geometry import Aabb, vec3
+from .errors import DegenerateSplitError, InsufficientPointsError, NoPointsError, OutOfBoundsError
+from .geometry import Aabb, rays_to_soa, vec3
 
 AXES = "xyz"
 
@@ -201,6 +201,115 @@ def locate_many(tree: PartitionTree, pts, device=None) -> np.ndarray:
               _lib.ptr(err), _lib.stream_ptr())
     _lib.raise_flags(int(err.item()), "in locate_many")
     return out.cpu().numpy().astype(np.int64)
+
+
+# ---- sample-balanced partitioning --------------------------------
+
+@dataclass(frozen=True)
+class PointCloud:
+    """partitioner.PointCloud: points (n, 3) float64 and their source tag."""
+
+    points: np.ndarray
+    source: str
+
+
+def _k1_all_leaves(tree: PartitionTree, rays, dt: float, device=None):
+    """K1 (vr_sample_count / vr_scan_offsets / vr_sample_fill) over every leaf of ``tree``;
+    returns (rays_dev, t0, t1, ray_id, per-leaf sample totals) on the device."""
+    import torch
+
+    if not dt > 0.0:
+        raise ValueError("dt must be > 0")
+    if not isinstance(rays, (np.ndarray, torch.Tensor)):
+        rays = rays_to_soa(list(rays))
+    dev = torch.device(device or "cuda")
+    r = torch.as_tensor(np.ascontiguousarray(rays, dtype=np.float64) if isinstance(rays, np.ndarray)
+                        else rays, dtype=torch.float64).to(dev).contiguous()
+    R, K = r.shape[1], len(tree.leaves)
+    s = _lib.stream_ptr()
+    tc = tree.to_c()
+    err = torch.zeros(1, dtype=torch.int32, device=dev)
+    counts = torch.empty(K * R, dtype=torch.int32, device=dev)
+    first = torch.empty(K * R, dtype=torch.int32, device=dev)
+    te = torch.empty(R, dtype=torch.float64, device=dev)
+    _lib.call("vr_sample_count", _lib.addr(tc), _lib.ptr(r), R, R, float(dt), 0, K,
+              _lib.ptr(counts), _lib.ptr(first), _lib.ptr(te), None, None, _lib.ptr(err), s)
+    off = torch.empty(K * R + 1, dtype=torch.int64, device=dev)
+    ws = torch.empty(int(_lib.load().vr_scan_workspace_bytes(K * R)), dtype=torch.uint8, device=dev)
+    _lib.call("vr_scan_offsets", _lib.ptr(counts), K * R, _lib.ptr(off), _lib.ptr(ws), ws.numel(),
+              s)
+    bounds = off[torch.arange(K + 1, device=dev) * R].cpu().numpy().astype(np.int64)
+    n = int(bounds[-1])
+    t0 = torch.empty(max(n, 1), dtype=torch.float64, device=dev)
+    t1 = torch.empty(max(n, 1), dtype=torch.float64, device=dev)
+    rid = torch.empty(max(n, 1), dtype=torch.int32, device=dev)
+    if n:
+        _lib.call("vr_sample_fill", _lib.addr(tc), _lib.ptr(r), R, R, float(dt), 0, K,
+                  _lib.ptr(off), _lib.ptr(first), _lib.ptr(t0), _lib.ptr(t1), _lib.ptr(rid),
+                  _lib.ptr(err), s)
+    # an out-of-root midpoint (rounding at a grazing exit) only matters to owner lookup
+    flags = int(err.item()) & ~_lib.VR_FLAG_OOB
+    _lib.raise_flags(flags, "in sampling")
+    return r, t0[:n], t1[:n], rid[:n], np.diff(bounds)
+
+
+def rays_to_points(rays, root: Aabb, dt: float, max_points: int, seed: int,
+                   device=None) -> PointCloud:
+    """Discretize rays on the global dt grid (generate_samples, quadrature.py:66-88, as
+    K1 over a one-leaf tree) and subsample the midpoints (partitioner.py:209-229): same
+    points, same numpy subsample as the reference.  Raises NoPointsError when no ray
+    intersects the root box."""
+    if max_points <= 0:
+        raise ValueError("max_points must be > 0")
+    r, t0, t1, rid, _ = _k1_all_leaves(grid_tree(root, ""), rays, dt, device)
+    if t0.numel() == 0:
+        raise NoPointsError("no ray intersects the root box")
+    t0n, t1n, idx = t0.cpu().numpy(), t1.cpu().numpy(), rid.cpu().numpy().astype(np.int64)
+    rn = r.cpu().numpy()
+    m = 0.5 * (t0n + t1n)  # SampleInterval.m (quadrature.py:40)
+    arr = rn[0:3, idx].T + m[:, None] * rn[3:6, idx].T  # Ray.points_at (geometry.py:96-97)
+    if arr.shape[0] > max_points:
+        rng = np.random.default_rng(seed)
+        keep = np.sort(rng.choice(arr.shape[0], size=max_points, replace=False))
+        arr = arr[keep]
+    return PointCloud(arr, "ray_discretized")
+
+
+def default_root_box(points: np.ndarray) -> Aabb:
+    """Point-cloud bounding box inflated by 1% per axis about its centre
+    (partitioner.py:232-239)."""
+    pts = np.asarray(points, dtype=np.float64).reshape(-1, 3)
+    mn = pts.min(axis=0)
+    mx = pts.max(axis=0)
+    extent = mx - mn
+    pad = np.where(extent > 0.0, 0.005 * extent, 1e-3)
+    return Aabb(mn - pad, mx + pad)
+
+
+def balance_report(tree: PartitionTree, points, rays=None, dt: float = None,
+                   device=None) -> dict:
+    """Per-leaf point counts and, with rays, per-leaf render-time sample counts
+    (partitioner.py:242-271): owner lookup by the vr_locate kernel, sample counts from K1
+    over all leaves.  Ratios are max/min, or None when some leaf is empty."""
+    pts = np.asarray(points, dtype=np.float64).reshape(-1, 3)
+    mn, mx = tree.root_box.mn, tree.root_box.mx
+    inside = np.all((pts >= mn) & (pts <= mx), axis=1)
+    tids = locate_many(tree, pts[inside], device) if inside.any() else np.zeros(0, np.int64)
+    counts = np.bincount(tids, minlength=len(tree.leaves))
+    report = {
+        "num_tiles": len(tree.leaves),
+        "leaf_point_counts": [int(c) for c in counts],
+        "points_outside_root": int(np.count_nonzero(~inside)),
+        "point_max_min_ratio": float(counts.max() / counts.min()) if counts.min() > 0 else None,
+    }
+    if rays is not None:
+        if dt is None or dt <= 0.0:
+            raise ValueError("sample counting needs dt > 0")
+        _, _, _, _, per_leaf = _k1_all_leaves(tree, rays, dt, device)
+        report["leaf_sample_counts"] = [int(c) for c in per_leaf]
+        report["sample_max_min_ratio"] = (
+            float(per_leaf.max() / per_leaf.min()) if per_leaf.min() > 0 else None)
+    return report
 
 
 def _node_to_json(node) -> dict:

@@ -18,7 +18,7 @@ def pytest_configure(config):
 def load_npz(name):
     d = np.load(GOLDEN / name, allow_pickle=False)
     out = {k: d[k] for k in d.files}
-    for k in ("tree", "scene", "camera", "stats"):
+    for k in ("tree", "scene", "camera", "stats", "report", "root"):
         if k in out:
             out[k] = json.loads(str(out[k]))
     return out

@@ -14,6 +14,8 @@ Fixtures
   image_three_blobs_{sample,mono}.npz   the same image and CommStats under the
                   sample-broadcast and mono protocols (distsim.py:311-316, :385-404);
                   `make_golden.py protocols` regenerates only these two files
+  partition_*.npz rays_to_points + build_tree + balance_report (partitioner.py:
+                  209-271) on the street and voxel_room scenes (`make_golden.py partition`)
   grad_voxel_room.json    DistributedLossProbe.gradient_pair (local, global) FD
                   gradients of the voxel_room loss (segrender.py:153-251)
 """
@@ -240,9 +242,30 @@ def protocols():
         print(f"image_three_blobs_{short}: scalars", st.scalars_sent_total)
 
 
+def partition():
+    """Sample-balanced partitioning from ray-discretized points."""
+    s = scenes.street()
+    v = scenes.voxel_room()
+    for name, sc, rays, dt, n_pts, depth in (("street", s.scene, list(s.rays), s.dt, 4000, 3),
+                                             ("voxel_room", v.scene, list(v.rays), v.dt, 10 ** 6,
+                                              2)):
+        pc = partitioner.rays_to_points(rays, sc.root_box, dt, n_pts, seed=3)
+        tree = partitioner.build_tree(pc.points, sc.root_box, depth)
+        rep = partitioner.balance_report(tree, pc.points, rays, dt)
+        np.savez_compressed(OUT / f"partition_{name}.npz", points=pc.points,
+                            rays=np.array([ray_row(r) for r in rays]), dt=np.float64(dt),
+                            root=json.dumps(sc.root_box.to_json()), max_points=n_pts,
+                            tree=json.dumps(partitioner.tree_to_json(tree)),
+                            report=json.dumps(rep))
+        print(f"partition_{name}: {len(pc.points)} points, report {rep}")
+
+
 if __name__ == "__main__":
     if sys.argv[1:] == ["protocols"]:
         protocols()
+    elif sys.argv[1:] == ["partition"]:
+        partition()
     else:
         main()
         protocols()
+        partition()

@@ -196,6 +196,21 @@ def test_multi_rank_composite_is_bitwise_identical():
     assert torch.equal(out1, out2)
 
 
+@pytest.mark.parametrize("name", ["partition_street.npz", "partition_voxel_room.npz"])
+def test_rays_to_points_and_balance_report_match_reference(name):
+    """rays_to_points (K1 on a one-leaf tree + the reference's numpy subsample) gives the
+    reference's points bit for bit; balance_report's point and sample counts match."""
+    g = load_npz(name)
+    root = vr.Aabb.from_json(g["root"])
+    rays = _soa(g["rays"])
+    pc = vr.rays_to_points(rays, root, float(g["dt"]), int(g["max_points"]), seed=3, device=DEV)
+    assert pc.source == "ray_discretized"
+    assert np.array_equal(pc.points, g["points"])
+    tree = vr.tree_from_json(g["tree"])
+    rep = vr.balance_report(tree, pc.points, rays, float(g["dt"]), device=DEV)
+    assert rep == g["report"]
+
+
 def _grad_setup():
     doc = json.loads((GOLDEN / "grad_voxel_room.json").read_text())
     tree = vr.tree_from_json(doc["tree"])

@@ -134,3 +134,16 @@ def test_geometry_validation():
         vr.soa_rays([[0, 0, 0]], [[1, 0, 0]], 1.0, 0.5)
     soa = vr.rays_to_soa([vr.Ray([0, 0, 0], [0, 0, 1], 0.5, 2.0)])
     assert soa.shape == (8, 1) and soa[5, 0] == 1.0 and soa[6, 0] == 0.5
+
+
+@pytest.mark.parametrize("name", ["partition_street.npz", "partition_voxel_room.npz"])
+def test_build_tree_from_ray_points_matches_reference(name):
+    """Sample-balanced partitioning: the median-split tree built from
+    the reference's ray-discretized points is the reference's tree."""
+    g = load_npz(name)
+    root = vr.Aabb.from_json(g["root"])
+    depth = {"partition_street.npz": 3, "partition_voxel_room.npz": 2}[name]
+    tree = vr.build_tree(g["points"], root, depth)
+    assert vr.tree_to_json(tree) == g["tree"]
+    box = vr.default_root_box(g["points"])
+    assert np.all(box.mn <= g["points"].min(axis=0)) and np.all(box.mx >= g["points"].max(axis=0))
