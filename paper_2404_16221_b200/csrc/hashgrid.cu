@@ -15,6 +15,7 @@
 // goes through per-warp replicas (see RepPlan in hashgrid.cuh).
 // The production training path fuses both directions into the tensor-core MLP kernels
 // (mlp_tc.cu); these standalone kernels serve inference-only callers and the tests.
+#include <stdlib.h>
 #include <string.h>
 
 #include "hashgrid.cuh"
@@ -86,28 +87,29 @@ __global__ void __launch_bounds__(HASH_THREADS)
   }
 }
 
-__global__ void __launch_bounds__(HASH_THREADS)
-    k_hash_fwd_lm(const VrHashGridDesc g, const float2* __restrict__ table,
-                  const float* __restrict__ pos, int64_t n, __half2* __restrict__ enc) {
-  const int l = blockIdx.y;
-  const float2* tl = table + g.offset[l];
-  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
-       i += (int64_t)gridDim.x * blockDim.x) {
-    const float u[3] = {__ldcs(pos + i), __ldcs(pos + n + i), __ldcs(pos + 2 * n + i)};
-    Corners c;
-    level_corners(g, l, u, c);
-    const float2 f = gather_level(tl, c);
-    __stcs(enc + (int64_t)l * n + i, __floats2half2_rn(f.x, f.y));
-  }
-}
-
-// Backward passes group consecutive levels (pass p = levels [first[p], first[p+1])): the
+// Passes group consecutive levels (pass p = levels [first[p], first[p+1])): the
 // small coarse levels share one pass, so their atomics are diluted among several levels'
 // (one coarse level alone would put every SM's atomics on a few thousand addresses).
 struct LmPasses {
   int32_t n;
   int32_t first[VR_MAX_LEVELS + 1];
 };
+
+__global__ void __launch_bounds__(HASH_THREADS)
+    k_hash_fwd_lm(const VrHashGridDesc g, const LmPasses passes, const float2* __restrict__ table,
+                  const float* __restrict__ pos, int64_t n, __half2* __restrict__ enc) {
+  const int l0 = passes.first[blockIdx.y], l1 = passes.first[blockIdx.y + 1];
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    const float u[3] = {__ldcs(pos + i), __ldcs(pos + n + i), __ldcs(pos + 2 * n + i)};
+    for (int l = l0; l < l1; ++l) {
+      Corners c;
+      level_corners(g, l, u, c);
+      const float2 f = gather_level(table + g.offset[l], c);
+      __stcs(enc + (int64_t)l * n + i, __floats2half2_rn(f.x, f.y));
+    }
+  }
+}
 
 __global__ void __launch_bounds__(HASH_THREADS)
     k_hash_bwd_lm(const VrHashGridDesc g, const RepPlan plan, const LmPasses passes,
@@ -123,7 +125,9 @@ __global__ void __launch_bounds__(HASH_THREADS)
   }
 }
 
-// greedy: consecutive levels share a pass while their slices total <= 48 MB
+// greedy: consecutive levels share a pass while their slices total <= 48 MB (the streamed
+// positions are re-read once per pass, the live slices must stay in L2; measured on c4/c5:
+// 64 MB passes — two 32 MB hashed levels — thrash L2, c5 97 -> 111 ms)
 static LmPasses lm_passes(const VrHashGridDesc* g) {
   LmPasses p;
   memset(&p, 0, sizeof(p));
@@ -304,8 +308,11 @@ extern "C" int vr_hash_fwd_lm(const VrHashGridDesc* g, const float* table, const
     return VR_ERR_BAD_ARG;
   }
   if (n == 0) return VR_OK;
-  k_hash_fwd_lm<<<lm_grid(g, n), HASH_THREADS, 0, (cudaStream_t)stream>>>(
-      *g, reinterpret_cast<const float2*>(table), pos, n, reinterpret_cast<__half2*>(enc));
+  const LmPasses passes = lm_passes(g);
+  dim3 grid = lm_grid(g, n);
+  grid.y = passes.n;
+  k_hash_fwd_lm<<<grid, HASH_THREADS, 0, (cudaStream_t)stream>>>(
+      *g, passes, reinterpret_cast<const float2*>(table), pos, n, reinterpret_cast<__half2*>(enc));
   return check_launch("vr_hash_fwd_lm");
 }
 
