@@ -49,6 +49,9 @@ KERNEL_COST = {
     # recomputed forward + activation grads + weight grads
     "vr_mlp_bwd": ("tensor", 3 * 18816.0, 5),
     "vr_mlp_bwd_tc": ("tensor", 3 * 18816.0, 5),
+    # density branch only: 2 * (32*64 + 64*16) fwd, x3 with the backward
+    "vr_mlp_fwd_tc_density": ("tensor", 6144.0, 2),
+    "vr_mlp_bwd_tc_density": ("tensor", 3 * 6144.0, 5),
     # fused K2+K3 forward: t0,t1,id (20) + 128 corner gathers (1024) + enc out (64) + sig_rgb (16)
     "vr_field_fwd_tc": ("hbm", 1124.0, 8),
     # fused K3+K2 backward: enc (64) + dsig_rgb (16) + t0,t1,id (20) + 1024 atomic payload
@@ -186,7 +189,8 @@ def build_pool(w, rank, world, dev, group, seed_base=1):
     props = None
     if w.interlevel > 0:  # config 4: proposal fields for the interlevel loss
         pcfg = vr.HashGridConfig(log2_T=w.prop_log2_T, max_res=w.prop_max_res)
-        props = [vr.HashGridMLP(pcfg, tree.leaves[k].box, dev, seed=1000 + k)
+        # the proposal's colour head is never read: density branch only
+        props = [vr.HashGridMLP(pcfg, tree.leaves[k].box, dev, seed=1000 + k, density_only=True)
                  for k in range(lo, lo + cnt)]
     return vr.VolumePool(tree, fields, (0.05, 0.05, 0.08), dev, rank, world, group,
                          proposals=props)

@@ -242,6 +242,16 @@ int vr_mlp_bwd_tc(const void* weights_dev, const void* enc_dev, const double* ra
                   const float* dsig_rgb_dev, float* grad_weights_dev, float* denc_dev,
                   int32_t* err_dev, void* stream);
 
+/* Density branch only (proposal fields of the interlevel loss, whose colour head is never
+ * read): out[i] = {sigma, 0, 0, 0}; the backward reads dL/dsigma (dsig_rgb[i].x), writes
+ * d(enc) and accumulates the W1d / W2d gradients only. */
+int vr_mlp_fwd_tc_density(const void* weights_dev, const void* enc_dev, int64_t n,
+                          float* sig_rgb_dev, void* stream);
+int vr_mlp_bwd_tc_density(const void* weights_dev, const void* enc_dev, const double* rays_dev,
+                          int64_t ray_stride, const int32_t* ray_id_dev, int64_t n,
+                          const float* dsig_rgb_dev, float* grad_weights_dev, float* denc_dev,
+                          int32_t* err_dev, void* stream);
+
 /* ---- K2 + K3 fused (production training path) ------------------------------------
  * Forward: the tensor-core MLP kernel computes each row's hash encoding itself (no
  * encoding round trip through HBM before the MLP) and, if enc_out != NULL, writes it

@@ -235,7 +235,9 @@ struct FwdRow {
 // Forward chain of one tile.  X0 = enc (pre-staged); activations go to X1 (h1d),
 // X2 (cin), X3 (h1c), X4 (h2c) — X2 may alias X0, X3 may alias X1, X4 may alias X2.
 // d0: 64 scratch columns, d1: 16 scratch columns.
-template <int TPR, class O = NoOverlap>
+// DENS: density branch only (a proposal field: its colour head is never used) — rounds
+// L1d and L2d, no cin.
+template <int TPR, bool DENS = false, class O = NoOverlap>
 __device__ __forceinline__ FwdRow forward_tile(uint8_t* sw, uint8_t* X0, uint8_t* X1, uint8_t* X2,
                                                uint8_t* X3, uint8_t* X4, uint32_t tm_row,
                                                uint32_t tmem, uint32_t d0, uint32_t d1,
@@ -261,9 +263,12 @@ __device__ __forceinline__ FwdRow forward_tile(uint8_t* sw, uint8_t* X0, uint8_t
     tmem_ld16(tm_row + d1, v);
     out.od0 = v[0];
     out.sigma = expf(fminf(fmaxf(v[0], -15.f), 15.f));
-    put8(X2, r, 0, v);
-    put8(X2, r, 1, v + 8);
+    if (!DENS) {
+      put8(X2, r, 0, v);
+      put8(X2, r, 1, v + 8);
+    }
   }
+  if (DENS) return out;
   if (part == TPR - 1) {
     sh16f(dx, dy, dz, v);
     put8(X2, r, 2, v);
@@ -361,7 +366,7 @@ __device__ __forceinline__ void encode_row(const VrHashGridDesc& g, const float2
 
 // FUSED = true: the kernel computes the hash encoding itself (K2 + K3 in one pass);
 // otherwise it reads enc (level-major half2) produced by vr_hash_fwd.
-template <bool FUSED>
+template <bool FUSED, bool DENS = false>
 __global__ void __launch_bounds__(TILE * FWD_TPR, 4)
     k_mlp_fwd_tc(const __half* __restrict__ W, const __half2* __restrict__ enc,
                  const double* __restrict__ rays, int64_t stride, const int32_t* __restrict__ rid,
@@ -397,11 +402,14 @@ __global__ void __launch_bounds__(TILE * FWD_TPR, 4)
       encode_row(g, table, rays, stride, t0, t1, rid, n, i, valid, P, r, enc_out, dx, dy, dz);
     } else {
       stage_enc<FWD_TPR>(P, r, part, enc, n, i, valid);
-      load_dir(rays, stride, rid, i, valid, dx, dy, dz);
+      if (DENS)
+        dx = dy = dz = 0.f;
+      else
+        load_dir(rays, stride, rid, i, valid, dx, dy, dz);
     }
     // P(enc) -> Q(h1d) -> P(cin) -> Q(h1c) -> P(h2c)
-    const FwdRow f =
-        forward_tile<FWD_TPR>(sw, P, Q, P, Q, P, tm_row, tmem, 0, 64, bar, phase, dx, dy, dz);
+    const FwdRow f = forward_tile<FWD_TPR, DENS>(sw, P, Q, P, Q, P, tm_row, tmem, 0, 64, bar,
+                                                 phase, dx, dy, dz);
     if (valid && part == 0) out[i] = make_float4(f.sigma, f.rgb[0], f.rgb[1], f.rgb[2]);
   }
   tc_fence_before();
@@ -486,7 +494,7 @@ __device__ __forceinline__ void put_enc(uint8_t* tile, int r, int part, const Ro
 // FUSED = true: instead of writing d(enc) to global memory, each thread scatters its
 // row's hash-grid gradients (its 8 levels) straight from the last epilogue (K3 + K2
 // backward in one pass); the atomics overlap other tiles' tensor-core rounds.
-template <bool FUSED>
+template <bool FUSED, bool DENS = false>
 __global__ void __launch_bounds__(TILE * BWD_TPR, 2)
     k_mlp_bwd_tc(const __half* __restrict__ W, const __half2* __restrict__ enc,
                  const double* __restrict__ rays, int64_t stride, const int32_t* __restrict__ rid,
@@ -593,12 +601,43 @@ __global__ void __launch_bounds__(TILE * BWD_TPR, 2)
     }
     put_enc(A, r, part, cur);
     // forward recompute: A(enc) -> X1(h1d) -> A(cin) -> X3(h1c) -> X4(h2c)
-    const FwdRow f = forward_tile<BWD_TPR>(sw, A, X1, A, X3, X4, tm_row, tmem, T_D0, T_D1, barA,
-                                           phA, cur.dx, cur.dy, cur.dz, scatter_ov);
+    const FwdRow f = forward_tile<BWD_TPR, DENS>(sw, A, X1, A, X3, X4, tm_row, tmem, T_D0, T_D1,
+                                                 barA, phA, cur.dx, cur.dy, cur.dz, scatter_ov);
     const float4 gin = cur.gin;
     float g[C64];
     float v[16];
     const bool a_w = acc;
+    if (DENS) {  // density branch only: no colour-head stages, enc still in A
+#pragma unroll
+      for (int j = 0; j < C16; ++j) g[j] = 0.f;
+      if (part == 0 && f.od0 > -15.f && f.od0 < 15.f) g[0] = gin.x * f.sigma;
+      stage(g, C16, c16, true,
+            [&] {
+              issue_dgrad(sGh, 16, sW + OW2D, 64, tmem + T_D0, false);  // dod . W2d
+              issue_dgrad(sGh16, 16, sW + OW2D, 64, tmem + T_D0, true);
+            },
+            [&] { issue_wgrad(sX1, 64, sGh, 32, tmem + T_W2DT, a_w); }, [] {});
+#pragma unroll
+      for (int c = 0; c < C64; c += 16) {
+        tmem_ld16(tm_row + T_D0 + c64 + c, v);
+        relu_mask8(X1, r, (c64 + c) / 8, v, g + c);
+        relu_mask8(X1, r, (c64 + c) / 8 + 1, v + 8, g + c + 8);
+      }
+      stage(g, C64, c64, false,
+            [&] {
+              issue_dgrad(sGh, 64, sW + OW1D, 32, tmem + T_D0, false);  // denc = dh1d . W1d
+              issue_dgrad(sGl, 64, sW + OW1D, 32, tmem + T_D0, true);
+            },
+            [&] { issue_wgrad(sGh, 128, sA, 32, tmem + T_W1D, a_w); }, [] {});
+      tmem_ld16(tm_row + T_D0 + 16 * part, v);
+      if (valid) {
+#pragma unroll
+        for (int j = 0; j < 16; j += 2)
+          denc[(int64_t)(8 * part + j / 2) * n + i] = make_float2(v[j], v[j + 1]);
+      }
+      acc = true;
+      continue;
+    }
 
     // stage 1, colour head: g_o = drgb * rgb (1 - rgb) padded to 16 columns
 #pragma unroll
@@ -713,18 +752,21 @@ __global__ void __launch_bounds__(TILE * BWD_TPR, 2)
     tmem_ld8(tm_row + T_W2DT + 16 + 8 * part, w);
     if (lane < 16)
       for (int j = 0; j < 8; ++j) atomicAdd(gW + VR_MLP_W2D + (8 * part + j) * 64 + m, v[j] + w[j]);
-    tmem_ld16(tm_row + T_W1C + 16 * part, v);
-    for (int j = 0; j < 16; ++j) atomicAdd(gW + VR_MLP_W1C + m2 * 32 + 16 * part + j, v[j]);
+    if (!DENS) {  // the colour accumulators (never written in a density-only kernel)
+      tmem_ld16(tm_row + T_W1C + 16 * part, v);
+      for (int j = 0; j < 16; ++j) atomicAdd(gW + VR_MLP_W1C + m2 * 32 + 16 * part + j, v[j]);
 #pragma unroll
-    for (int c = 0; c < 32; c += 16) {
-      tmem_ld16(tm_row + T_W2C + 32 * part + c, v);
-      for (int j = 0; j < 16; ++j) atomicAdd(gW + VR_MLP_W2C + m2 * 64 + 32 * part + c + j, v[j]);
-    }
-    if (part == 0) {
-      tmem_ld8(tm_row + T_W3CT, v);
-      tmem_ld8(tm_row + T_W3CT + 16, w);
-      if (lane < 16)
-        for (int j = 0; j < 3; ++j) atomicAdd(gW + VR_MLP_W3C + j * 64 + m, v[j] + w[j]);
+      for (int c = 0; c < 32; c += 16) {
+        tmem_ld16(tm_row + T_W2C + 32 * part + c, v);
+        for (int j = 0; j < 16; ++j)
+          atomicAdd(gW + VR_MLP_W2C + m2 * 64 + 32 * part + c + j, v[j]);
+      }
+      if (part == 0) {
+        tmem_ld8(tm_row + T_W3CT, v);
+        tmem_ld8(tm_row + T_W3CT + 16, w);
+        if (lane < 16)
+          for (int j = 0; j < 3; ++j) atomicAdd(gW + VR_MLP_W3C + j * 64 + m, v[j] + w[j]);
+      }
     }
   }
   const int flags = inf_bits ? VR_FLAG_OVERFLOW : 0;
@@ -756,31 +798,32 @@ int set_smem(K kernel, uint32_t bytes, bool& done, const char* who) {
   return VR_OK;
 }
 
-template <bool FUSED>
+template <bool FUSED, bool DENS = false>
 int launch_fwd(const void* w, const void* enc, const double* rays, int64_t stride,
                const int32_t* rid, int64_t n, float* out, const VrHashGridDesc* g,
                const float* table, const double* t0, const double* t1, void* enc_out,
                void* stream) {
   static bool attr = false;
-  int rc = set_smem(mlp::k_mlp_fwd_tc<FUSED>, mlp::F_SMEM, attr, "mlp fwd: smem attribute");
+  int rc = set_smem(mlp::k_mlp_fwd_tc<FUSED, DENS>, mlp::F_SMEM, attr, "mlp fwd: smem attribute");
   if (rc != VR_OK) return rc;
   VrHashGridDesc gd;
   if (g) gd = *g; else memset(&gd, 0, sizeof(gd));
   const int64_t tiles = ceil_div(n, mlp::TILE);
   const int grid = (int)(tiles < VR_NUM_SMS * 4 ? tiles : VR_NUM_SMS * 4);
-  mlp::k_mlp_fwd_tc<FUSED><<<grid, mlp::TILE * mlp::FWD_TPR, mlp::F_SMEM, (cudaStream_t)stream>>>(
+  mlp::k_mlp_fwd_tc<FUSED, DENS><<<grid, mlp::TILE * mlp::FWD_TPR, mlp::F_SMEM,
+                                   (cudaStream_t)stream>>>(
       (const __half*)w, (const __half2*)enc, rays, stride, rid, n, reinterpret_cast<float4*>(out),
       gd, reinterpret_cast<const float2*>(table), t0, t1, (__half2*)enc_out);
   return check_launch("vr_mlp_fwd_tc");
 }
 
-template <bool FUSED>
+template <bool FUSED, bool DENS = false>
 int launch_bwd(const void* w, const void* enc, const double* rays, int64_t stride,
                const int32_t* rid, int64_t n, const float* dsr, float* gW, float* denc,
                int32_t* err, const VrHashGridDesc* g, const double* t0, const double* t1,
                float* grad_table, void* ws, size_t ws_bytes, const float* pos, void* stream) {
   static bool attr = false;
-  int rc = set_smem(mlp::k_mlp_bwd_tc<FUSED>, mlp::B_SMEM, attr, "mlp bwd: smem attribute");
+  int rc = set_smem(mlp::k_mlp_bwd_tc<FUSED, DENS>, mlp::B_SMEM, attr, "mlp bwd: smem attribute");
   if (rc != VR_OK) return rc;
   VrHashGridDesc gd;
   RepPlan plan;
@@ -795,7 +838,8 @@ int launch_bwd(const void* w, const void* enc, const double* rays, int64_t strid
   }
   const int64_t tiles = ceil_div(n, mlp::TILE);
   const int grid = (int)(tiles < VR_NUM_SMS * 2 ? tiles : VR_NUM_SMS * 2);
-  mlp::k_mlp_bwd_tc<FUSED><<<grid, mlp::TILE * mlp::BWD_TPR, mlp::B_SMEM, (cudaStream_t)stream>>>(
+  mlp::k_mlp_bwd_tc<FUSED, DENS><<<grid, mlp::TILE * mlp::BWD_TPR, mlp::B_SMEM,
+                                   (cudaStream_t)stream>>>(
       (const __half*)w, (const __half2*)enc, rays, stride, rid, n,
       reinterpret_cast<const float4*>(dsr), gW, reinterpret_cast<float2*>(denc), err, gd, plan, t0, t1, reinterpret_cast<float2*>(grad_table),
       reinterpret_cast<float2*>(ws), pos);
@@ -827,6 +871,32 @@ extern "C" int vr_mlp_bwd_tc(const void* w, const void* enc, const double* rays,
   if (n == 0) return VR_OK;
   return launch_bwd<false>(w, enc, rays, stride, rid, n, dsr, gW, denc, err, nullptr, nullptr,
                            nullptr, nullptr, nullptr, 0, nullptr, stream);
+}
+
+// density branch only (proposal fields): sigma of the same MLP, rgb = 0; the backward takes
+// dL/dsigma (dsig_rgb[i].x) and writes d(enc) and the density weights' gradients only
+extern "C" int vr_mlp_fwd_tc_density(const void* w, const void* enc, int64_t n, float* out,
+                                     void* stream) {
+  if (n < 0 || !w || (n > 0 && (!enc || !out))) {
+    set_error("vr_mlp_fwd_tc_density: bad argument");
+    return VR_ERR_BAD_ARG;
+  }
+  if (n == 0) return VR_OK;
+  return launch_fwd<false, true>(w, enc, nullptr, 0, nullptr, n, out, nullptr, nullptr, nullptr,
+                                 nullptr, nullptr, stream);
+}
+
+extern "C" int vr_mlp_bwd_tc_density(const void* w, const void* enc, const double* rays,
+                                     int64_t stride, const int32_t* rid, int64_t n,
+                                     const float* dsr, float* gW, float* denc, int32_t* err,
+                                     void* stream) {
+  if (n < 0 || !w || !gW || !denc || !err) {
+    set_error("vr_mlp_bwd_tc_density: bad argument");
+    return VR_ERR_BAD_ARG;
+  }
+  if (n == 0) return VR_OK;
+  return launch_bwd<false, true>(w, enc, rays, stride, rid, n, dsr, gW, denc, err, nullptr,
+                                 nullptr, nullptr, nullptr, nullptr, 0, nullptr, stream);
 }
 
 extern "C" int vr_field_fwd_tc(const VrHashGridDesc* g, const float* table, const void* w,

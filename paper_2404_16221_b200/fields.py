@@ -279,7 +279,8 @@ class HashGridMLP(RegionField):
     LEVEL_MAJOR_BYTES = 64 << 20
 
     def __init__(self, cfg: HashGridConfig, box: Aabb, device, seed=0, table_init=1e-4,
-                 table=None, weights=None, mlp_impl: str = "fused", hash_order: str = "auto"):
+                 table=None, weights=None, mlp_impl: str = "fused", hash_order: str = "auto",
+                 density_only: bool = False):
         if mlp_impl not in ("fused", "fused_fwd", "tc", "cuda"):
             raise ValueError(
                 "mlp_impl: 'fused' (default: gather kernel + tcgen05 MLP forward, hash-grid "
@@ -290,7 +291,12 @@ class HashGridMLP(RegionField):
                              "(level-major kernels for tables larger than L2)")
         if hash_order == "level" and mlp_impl == "fused_fwd":
             raise ValueError("hash_order='level' needs a separate hash-grid forward")
+        if density_only and mlp_impl not in ("fused", "tc"):
+            raise ValueError("density_only runs on the tensor-core kernels (mlp_impl fused/tc)")
         self.mlp_impl = mlp_impl
+        # density branch only (a proposal field: sigma is all the interlevel loss reads, so
+        # the colour head is neither evaluated nor trained); rgb outputs are 0
+        self.density_only = bool(density_only)
         self.err = torch.zeros(1, dtype=torch.int32, device=device)  # replaced by the pool's
         self.cfg = cfg
         self.box = box
@@ -379,6 +385,10 @@ class HashGridMLP(RegionField):
     def forward_mlp(self, rays, ray_id, n, sig_rgb, stream):
         if n == 0:
             return
+        if self.density_only:
+            _lib.call("vr_mlp_fwd_tc_density", _lib.ptr(self.weights16), _lib.ptr(self._enc), n,
+                      _lib.ptr(sig_rgb), stream)
+            return
         _lib.call("vr_mlp_fwd" if self.mlp_impl == "cuda" else "vr_mlp_fwd_tc",
                   _lib.ptr(self.weights16), _lib.ptr(self._enc), _lib.ptr(rays), rays.shape[1],
                   _lib.ptr(ray_id), n, _lib.ptr(sig_rgb), stream)
@@ -387,6 +397,10 @@ class HashGridMLP(RegionField):
         if n == 0:
             return
         enc = self._enc  # written by the forward of the same step
+        if self.density_only:
+            self.backward_scatter(self.backward_mlp(rays, ray_id, n, dsig_rgb, stream), n,
+                                  stream)
+            return
         if self.mlp_impl in ("fused", "fused_fwd") and self.hash_order == "sample":
             ws = self._workspace(rays.device)
             _lib.call("vr_field_bwd_tc", _lib.addr(self.desc), _lib.ptr(self.weights16),
@@ -425,13 +439,15 @@ class HashGridMLP(RegionField):
     @property
     def split_backward(self):
         return self.mlp_impl in ("fused", "tc") and (
-            self.hash_order == "level" or self.n_entries * 8 < self.SPLIT_BELOW_BYTES)
+            self.density_only or self.hash_order == "level"
+            or self.n_entries * 8 < self.SPLIT_BELOW_BYTES)
 
     def backward_mlp(self, rays, ray_id, n, dsig_rgb, stream):
         """MLP backward of the step's samples; returns d(enc) [16][n] float2 (float32)."""
         denc = torch.empty(16 * max(n, 1) * 2, dtype=torch.float32, device=rays.device)
         if n:
-            _lib.call("vr_mlp_bwd_tc", _lib.ptr(self.weights16), _lib.ptr(self._enc),
+            _lib.call("vr_mlp_bwd_tc_density" if self.density_only else "vr_mlp_bwd_tc",
+                      _lib.ptr(self.weights16), _lib.ptr(self._enc),
                       _lib.ptr(rays), rays.shape[1], _lib.ptr(ray_id), n, _lib.ptr(dsig_rgb),
                       _lib.ptr(self.grad_weights), _lib.ptr(denc), _lib.ptr(self.err), stream)
         return denc

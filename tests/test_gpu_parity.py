@@ -497,10 +497,12 @@ def test_mlp_tensor_core_matches_cuda_core(n):
     assert gw_b[_lib.VR_MLP_W3C + 3 * 64:].abs().max().item() == 0.0
 
 
-def test_interlevel_loss_and_proposal_grads_match_oracle():
+@pytest.mark.parametrize("density_only", [False, True])
+def test_interlevel_loss_and_proposal_grads_match_oracle(density_only):
     """Interlevel (proposal) loss — parity against oracle/grad_oracle.field_loss_interlevel
     (parity unpinned: no reference code).  NeRF gradients must be unaffected (w is
-    stop-gradient in the interlevel term)."""
+    stop-gradient in the interlevel term).  density_only: the proposal runs only its
+    density branch (its colour head gets zero gradient either way)."""
     rng = np.random.default_rng(7)
     pool, tree, models, rays, targets = _hash_setup(log2_T=14, K=2, seed=3)
     cfg = vr.HashGridConfig(log2_T=12, max_res=128)
@@ -514,7 +516,7 @@ def test_interlevel_loss_and_proposal_grads_match_oracle():
             w[off:off + rows * cols] = rng.normal(size=rows * cols) / np.sqrt(cols)
         box = tree.leaves[k].box
         props.append(vr.HashGridMLP(cfg, box, DEV, table=torch.from_numpy(table),
-                                    weights=torch.from_numpy(w)))
+                                    weights=torch.from_numpy(w), density_only=density_only))
         pmodels.append(hmo.HashMLPModel(table, w, 12, box.mn, box.mx, max_res=128))
     pool2 = vr.VolumePool(tree, pool.fields, (0.2, 0.3, 0.4), DEV, proposals=props)
     dt = 0.04
