@@ -13,6 +13,7 @@
 //   dL/dsh_j = Ph_s (Th_{j+1} e_j - sum_{i>j} wh_loc_i e_i),  e_i = dL/dwh_i
 //            = -2 lambda max(0, w_i - wh_i) / (w_i + eps)
 #include "common.cuh"
+#include "segscan.cuh"
 
 namespace vr {
 
@@ -52,24 +53,50 @@ __global__ void k_prefix(const float4* __restrict__ pk, const float* __restrict_
   }
 }
 
-struct IlSample {
-  double keep, alpha, keeph, alphah, dlt;
+// Grouped like K4 (segscan.cuh): one warp per 32 consecutive (region, ray) segments walks
+// their contiguous sample range 32 samples at a time with segmented scans, so no lane
+// idles on short segments.  Sweep 1: local transmittances (NeRF, proposal), per-segment
+// loss L and S = sum_i wh_loc_i e_i; sweep 2: per-sample proposal gradients.
+struct IlChunk {
+  bool valid, head, tail, cont;
+  int seg;
+  double dlt, keep, alpha, alphah, keeph;
+  double T, Th;  // local exclusive transmittances (NeRF, proposal)
 };
 
-__device__ __forceinline__ IlSample il_load(const double* __restrict__ t0,
+__device__ __forceinline__ IlChunk il_chunk(const double* __restrict__ t0,
                                             const double* __restrict__ t1,
                                             const float4* __restrict__ sr,
-                                            const float4* __restrict__ sp, int64_t i, bool valid) {
-  IlSample s = {1.0, 0.0, 1.0, 0.0, 0.0};
-  if (valid) {
-    s.dlt = t1[i] - t0[i];
-    const double x = (double)sr[i].x * s.dlt, xh = (double)sp[i].x * s.dlt;
-    s.keep = exp(-x);
-    s.alpha = -expm1(-x);
-    s.keeph = exp(-xh);
-    s.alphah = -expm1(-xh);
+                                            const float4* __restrict__ sp, int64_t s,
+                                            int64_t s_end, const GroupSeg& gs, int nseg,
+                                            double cT, double cTh, int lane) {
+  IlChunk c;
+  c.valid = s < s_end;
+  c.seg = find_seg(gs.lo, nseg, c.valid ? s : s_end - 1);
+  const int64_t seg_lo = __shfl_sync(0xffffffffu, gs.lo, c.seg);
+  const int64_t seg_hi = __shfl_sync(0xffffffffu, gs.hi, c.seg);
+  c.head = (s == seg_lo) || lane == 0;
+  c.tail = c.valid && (s + 1 == seg_hi);
+  const int seg0 = __shfl_sync(0xffffffffu, c.seg, 0);
+  c.cont = (__shfl_sync(0xffffffffu, (int)(s != seg_lo), 0) != 0) && c.seg == seg0;
+  c.keep = 1.0;
+  c.keeph = 1.0;
+  c.dlt = c.alpha = c.alphah = 0.0;
+  if (c.valid) {
+    c.dlt = t1[s] - t0[s];
+    const double x = (double)sr[s].x * c.dlt, xh = (double)sp[s].x * c.dlt;
+    c.keep = exp(-x);
+    c.alpha = -expm1(-x);
+    c.keeph = exp(-xh);
+    c.alphah = -expm1(-xh);
   }
-  return s;
+  double p[2] = {c.keep, c.keeph};
+  seg_scan<2>(p, c.head, lane, [](double a, double b) { return a * b; });
+  const double pu0 = __shfl_up_sync(0xffffffffu, p[0], 1);
+  const double pu1 = __shfl_up_sync(0xffffffffu, p[1], 1);
+  c.T = (c.cont ? cT : 1.0) * (c.head ? 1.0 : pu0);
+  c.Th = (c.cont ? cTh : 1.0) * (c.head ? 1.0 : pu1);
+  return c;
 }
 
 __global__ void __launch_bounds__(IL_WARPS * 32)
@@ -78,58 +105,75 @@ __global__ void __launch_bounds__(IL_WARPS * 32)
                  const int64_t* __restrict__ off, const float2* __restrict__ prefix,
                  int64_t n_segs, float lambda, float eps, double* __restrict__ seg_loss,
                  float4* __restrict__ dsp) {
-  const int lane = threadIdx.x & 31;
-  for (int64_t seg = (int64_t)blockIdx.x * IL_WARPS + (threadIdx.x >> 5); seg < n_segs;
-       seg += (int64_t)gridDim.x * IL_WARPS) {
-    const int64_t b = off[seg], e = off[seg + 1];
-    if (b == e) {
-      if (lane == 0) seg_loss[seg] = 0.0;
-      continue;
+  __shared__ double s_S[IL_WARPS][32];
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  double* Sseg = s_S[wid];
+  const double lam = lambda, ep = eps;
+  const int64_t n_groups = ceil_div(n_segs, 32);
+  for (int64_t grp = (int64_t)blockIdx.x * IL_WARPS + wid; grp < n_groups;
+       grp += (int64_t)gridDim.x * IL_WARPS) {
+    const int64_t seg0 = grp * 32;
+    const int nseg = (int)min((int64_t)32, n_segs - seg0);
+    const int64_t my = seg0 + lane;
+    GroupSeg gs;
+    gs.lo = off[lane < nseg ? my : seg0 + nseg];
+    gs.hi = off[lane < nseg ? my + 1 : seg0 + nseg];
+    float2 pre = make_float2(1.f, 1.f);
+    if (lane < nseg) {
+      pre = prefix[my];
+      if (gs.lo == gs.hi) seg_loss[my] = 0.0;  // empty segment
     }
-    const float2 pre = prefix[seg];
-    const double P = pre.x, Ph = pre.y;
-    // sweep 1: loss and S = sum_i wh_loc_i e_i
-    double Tc = 1.0, Thc = 1.0, L = 0.0, S = 0.0;
-    for (int64_t i0 = b; i0 < e; i0 += 32) {
-      const int64_t i = i0 + lane;
-      const IlSample s = il_load(t0, t1, sr, sp, i, i < e);
-      const double p = warp_incl_prod(s.keep, lane), ph = warp_incl_prod(s.keeph, lane);
-      double pe = __shfl_up_sync(0xffffffffu, p, 1), phe = __shfl_up_sync(0xffffffffu, ph, 1);
-      if (lane == 0) pe = phe = 1.0;
-      const double w = P * Tc * pe * s.alpha;
-      const double whl = Thc * phe * s.alphah;
+    const int64_t s_beg = __shfl_sync(0xffffffffu, gs.lo, 0);
+    const int64_t s_end = __shfl_sync(0xffffffffu, gs.hi, nseg - 1);
+    if (s_beg == s_end) continue;
+    // sweep 1: L and S per segment
+    double cT = 1.0, cTh = 1.0, cL = 0.0, cS = 0.0;
+    for (int64_t base = s_beg; base < s_end; base += 32) {
+      const IlChunk c = il_chunk(t0, t1, sr, sp, base + lane, s_end, gs, nseg, cT, cTh, lane);
+      const double P = __shfl_sync(0xffffffffu, (double)pre.x, c.seg);
+      const double Ph = __shfl_sync(0xffffffffu, (double)pre.y, c.seg);
+      const double w = P * c.T * c.alpha;
+      const double whl = c.Th * c.alphah;
       const double d = fmax(w - Ph * whl, 0.0);
-      const double inv = 1.0 / (w + (double)eps);
-      L += warp_sum((double)lambda * d * d * inv);
-      S += warp_sum(whl * (-2.0 * (double)lambda * d * inv));
-      Tc *= __shfl_sync(0xffffffffu, p, 31);
-      Thc *= __shfl_sync(0xffffffffu, ph, 31);
+      const double inv = 1.0 / (w + ep);
+      double q[2] = {c.valid ? lam * d * d * inv : 0.0, c.valid ? whl * (-2.0 * lam * d * inv) : 0.0};
+      seg_scan<2>(q, c.head, lane, [](double a, double b) { return a + b; });
+      const double L = (c.cont ? cL : 0.0) + q[0];
+      const double S = (c.cont ? cS : 0.0) + q[1];
+      if (c.tail) {
+        seg_loss[seg0 + c.seg] = L;
+        Sseg[c.seg] = S;
+      }
+      cT = __shfl_sync(0xffffffffu, c.T * c.keep, 31);
+      cTh = __shfl_sync(0xffffffffu, c.Th * c.keeph, 31);
+      cL = __shfl_sync(0xffffffffu, L, 31);
+      cS = __shfl_sync(0xffffffffu, S, 31);
     }
-    if (lane == 0) seg_loss[seg] = L;
-    // sweep 2: per-sample proposal gradients
-    Tc = 1.0;
-    Thc = 1.0;
-    double Sc = 0.0;
-    for (int64_t i0 = b; i0 < e; i0 += 32) {
-      const int64_t i = i0 + lane;
-      const IlSample s = il_load(t0, t1, sr, sp, i, i < e);
-      const double p = warp_incl_prod(s.keep, lane), ph = warp_incl_prod(s.keeph, lane);
-      double pe = __shfl_up_sync(0xffffffffu, p, 1), phe = __shfl_up_sync(0xffffffffu, ph, 1);
-      if (lane == 0) pe = phe = 1.0;
-      const double w = P * Tc * pe * s.alpha;
-      const double whl = Thc * phe * s.alphah;
+    __syncwarp();
+    // sweep 2: dL/dsigma_prop per sample
+    cT = 1.0;
+    cTh = 1.0;
+    double cSc = 0.0;
+    for (int64_t base = s_beg; base < s_end; base += 32) {
+      const IlChunk c = il_chunk(t0, t1, sr, sp, base + lane, s_end, gs, nseg, cT, cTh, lane);
+      const double P = __shfl_sync(0xffffffffu, (double)pre.x, c.seg);
+      const double Ph = __shfl_sync(0xffffffffu, (double)pre.y, c.seg);
+      const double w = P * c.T * c.alpha;
+      const double whl = c.Th * c.alphah;
       const double d = fmax(w - Ph * whl, 0.0);
-      const double ei = -2.0 * (double)lambda * d / (w + (double)eps);
-      const double we = whl * ei;
-      const double incl = warp_incl_sum(we, lane);
-      const double s_gt = S - (Sc + incl);
-      const double Thn = Thc * ph;  // local proposal transmittance after sample i
+      const double ei = -2.0 * lam * d / (w + ep);
+      double q[1] = {c.valid ? whl * ei : 0.0};
+      seg_scan<1>(q, c.head, lane, [](double a, double b) { return a + b; });
+      const double incl = (c.cont ? cSc : 0.0) + q[0];
+      const double s_gt = Sseg[c.seg] - incl;
+      const double Thn = c.Th * c.keeph;  // local proposal transmittance after sample i
       const double ds = Ph * (Thn * ei - s_gt);
-      if (i < e) dsp[i] = make_float4((float)(ds * s.dlt), 0.f, 0.f, 0.f);
-      Tc *= __shfl_sync(0xffffffffu, p, 31);
-      Thc *= __shfl_sync(0xffffffffu, ph, 31);
-      Sc += __shfl_sync(0xffffffffu, incl, 31);
+      if (c.valid) dsp[base + lane] = make_float4((float)(ds * c.dlt), 0.f, 0.f, 0.f);
+      cT = __shfl_sync(0xffffffffu, c.T * c.keep, 31);
+      cTh = __shfl_sync(0xffffffffu, Thn, 31);
+      cSc = __shfl_sync(0xffffffffu, incl, 31);
     }
+    __syncwarp();
   }
 }
 
@@ -163,7 +207,7 @@ extern "C" int vr_interlevel(const double* t0, const double* t1, const float* si
   }
   const int64_t n_segs = n_rays * region_cnt;
   if (n_segs == 0) return VR_OK;
-  k_interlevel<<<grid_for(ceil_div(n_segs, IL_WARPS), 1, 8), IL_WARPS * 32, 0,
+  k_interlevel<<<grid_for(ceil_div(n_segs, 32 * IL_WARPS), 1, 8), IL_WARPS * 32, 0,
                  (cudaStream_t)stream>>>(t0, t1, reinterpret_cast<const float4*>(sig_rgb),
                                          reinterpret_cast<const float4*>(sig_prop), off,
                                          reinterpret_cast<const float2*>(prefix), n_segs, lambda,
