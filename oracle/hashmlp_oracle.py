@@ -79,6 +79,20 @@ def corners(u32, scale, res, dense, log2_T):
     return idx, w
 
 
+def feature32(w, vals):
+    """The kernel's float32 feature of one level: corners with cx = 0 (c = 0, 2, 4, 6) and
+    cx = 1 (c = 1, 3, 5, 7) each summed in that order from 0 (round-to-nearest, no FMA),
+    then added (csrc/hashgrid.cuh gather_half / gather_level).  w (n, 8) float32, vals
+    (n, 8, 2) float32."""
+    halves = []
+    for p in (0, 1):
+        acc = np.zeros((w.shape[0], 2), dtype=np.float32)
+        for c in range(p, 8, 2):
+            acc = (acc + (w[:, c:c + 1] * vals[:, c]).astype(np.float32)).astype(np.float32)
+        halves.append(acc)
+    return (halves[0] + halves[1]).astype(np.float32)
+
+
 def all_indices(pts, box_mn, box_mx, log2_T, max_res=2048):
     """Per-level corner indices [L][n][8] int64 (for the bit-exact parity test)."""
     lv, _ = levels(log2_T, max_res=max_res)
@@ -126,11 +140,9 @@ class HashMLPModel:
             gidx = idx.astype(np.int64) + off
             rows = self.table[torch.from_numpy(gidx)]  # (n, 8, 2)
             f = (rows * torch.from_numpy(w.astype(np.float64))[:, :, None]).sum(1)
-            # forward value: the kernel's float32 sum in corner order (bit-exact);
+            # forward value: the kernel's float32 sum (bit-exact, feature32 order);
             # gradient: the exact linear map
-            f32 = np.zeros((u.shape[0], 2), dtype=np.float32)
-            for c in range(8):
-                f32 = (f32 + (w[:, c:c + 1] * tab32[gidx[:, c]]).astype(np.float32)).astype(np.float32)
+            f32 = feature32(w, tab32[gidx])
             f = f + (torch.from_numpy(f32.astype(np.float64)) - f).detach()
             feats.append(f)
         return _q16(torch.cat(feats, dim=1))
@@ -194,9 +206,7 @@ class CompactHashMLPModel(HashMLPModel):
             loc = np.searchsorted(self.uniq, idx.astype(np.int64) + off)
             rows = self.table[torch.from_numpy(loc)]
             f = (rows * torch.from_numpy(w.astype(np.float64))[:, :, None]).sum(1)
-            f32 = np.zeros((u.shape[0], 2), dtype=np.float32)
-            for c in range(8):
-                f32 = (f32 + (w[:, c:c + 1] * tab32[loc[:, c]]).astype(np.float32)).astype(np.float32)
+            f32 = feature32(w, tab32[loc])
             f = f + (torch.from_numpy(f32.astype(np.float64)) - f).detach()
             feats.append(f)
         return _q16(torch.cat(feats, dim=1))

@@ -7,8 +7,8 @@
 //   g   = clamp(floor(pos), 0, res_l - 2),  f = pos - g
 //   corner c = (cx, cy, cz):  idx = dense_l ? x + res*(y + res*z)
 //                                           : (x ^ y*2654435761 ^ z*805459861) & (T-1)
-//   w_c = (wx * wy) * wz,  feat_l = sum_c w_c * table[offset_l + idx_c]   (F = 2,
-//   float32, corner order c = 0..7, no FMA)
+//   w_c = (wx * wy) * wz,  feat_l = sum_{c even} w_c t_c + sum_{c odd} w_c t_c   (F = 2,
+//   float32, each half summed in increasing c from 0, no FMA; t_c = table[offset_l + idx_c])
 // Encodings are written level-major enc[l][n] as half2 so both the gather kernel
 // and the MLP read them coalesced.  The backward scatters w_c * dfeat with vector
 // atomics (float4 for x-adjacent pairs, float2 otherwise); the coarsest dense level
@@ -24,26 +24,36 @@ namespace vr {
 
 constexpr int HASH_THREADS = 256;
 
+// Lane pairs: a warp covers 16 samples per step; lane 2j+p gathers half p of sample j's
+// corners (gather_half), the partner's half arrives by one shuffle.
 __global__ void __launch_bounds__(HASH_THREADS)
     k_hash_fwd(const VrHashGridDesc g, const float2* __restrict__ table,
                const double* __restrict__ rays, int64_t stride, const double* __restrict__ t0,
                const double* __restrict__ t1, const int32_t* __restrict__ rid, int64_t n,
                __half2* __restrict__ enc, float* __restrict__ pos) {
-  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
-       i += (int64_t)gridDim.x * blockDim.x) {
-    float u[3];
-    norm_pos(g, rays, stride, t0, t1, rid, i, u);
-    if (pos) {
+  const int lane = threadIdx.x & 31, p = lane & 1;
+  const int64_t warp0 = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int64_t n_warps = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  for (int64_t s0 = warp0 * 16; s0 < n; s0 += n_warps * 16) {
+    const int64_t i = s0 + (lane >> 1);
+    const bool valid = i < n;
+    float u[3] = {0.f, 0.f, 0.f};
+    if (valid && p == 0) norm_pos(g, rays, stride, t0, t1, rid, i, u);
+#pragma unroll
+    for (int a = 0; a < 3; ++a) u[a] = __shfl_sync(0xffffffffu, u[a], lane & ~1);
+    if (pos && valid && p == 1) {
       pos[i] = u[0];
       pos[n + i] = u[1];
       pos[2 * n + i] = u[2];
     }
 #pragma unroll 2
     for (int l = 0; l < g.n_levels; ++l) {
-      Corners c;
-      level_corners(g, l, u, c);
-      const float2 f = gather_level(table + g.offset[l], c);
-      enc[(int64_t)l * n + i] = __floats2half2_rn(f.x, f.y);
+      float2 h = make_float2(0.f, 0.f);
+      if (valid) h = gather_half(g, l, table + g.offset[l], u, p);
+      const float2 o = make_float2(__shfl_xor_sync(0xffffffffu, h.x, 1),
+                                   __shfl_xor_sync(0xffffffffu, h.y, 1));
+      if (valid && p == 0)
+        enc[(int64_t)l * n + i] = __floats2half2_rn(__fadd_rn(h.x, o.x), __fadd_rn(h.y, o.y));
     }
   }
 }
@@ -99,14 +109,26 @@ __global__ void __launch_bounds__(HASH_THREADS)
     k_hash_fwd_lm(const VrHashGridDesc g, const LmPasses passes, const float2* __restrict__ table,
                   const float* __restrict__ pos, int64_t n, __half2* __restrict__ enc) {
   const int l0 = passes.first[blockIdx.y], l1 = passes.first[blockIdx.y + 1];
-  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
-       i += (int64_t)gridDim.x * blockDim.x) {
-    const float u[3] = {__ldcs(pos + i), __ldcs(pos + n + i), __ldcs(pos + 2 * n + i)};
+  const int lane = threadIdx.x & 31, p = lane & 1;  // lane pairs as in k_hash_fwd
+  const int64_t warp0 = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int64_t n_warps = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  for (int64_t s0 = warp0 * 16; s0 < n; s0 += n_warps * 16) {
+    const int64_t i = s0 + (lane >> 1);
+    const bool valid = i < n;
+    float u[3] = {0.f, 0.f, 0.f};
+    if (valid) {
+      u[0] = __ldcs(pos + i);
+      u[1] = __ldcs(pos + n + i);
+      u[2] = __ldcs(pos + 2 * n + i);
+    }
     for (int l = l0; l < l1; ++l) {
-      Corners c;
-      level_corners(g, l, u, c);
-      const float2 f = gather_level(table + g.offset[l], c);
-      __stcs(enc + (int64_t)l * n + i, __floats2half2_rn(f.x, f.y));
+      float2 h = make_float2(0.f, 0.f);
+      if (valid) h = gather_half(g, l, table + g.offset[l], u, p);
+      const float2 o = make_float2(__shfl_xor_sync(0xffffffffu, h.x, 1),
+                                   __shfl_xor_sync(0xffffffffu, h.y, 1));
+      if (valid && p == 0)
+        __stcs(enc + (int64_t)l * n + i,
+               __floats2half2_rn(__fadd_rn(h.x, o.x), __fadd_rn(h.y, o.y)));
     }
   }
 }
@@ -237,7 +259,7 @@ extern "C" int vr_hash_fwd(const VrHashGridDesc* g, const float* table, const do
     return VR_ERR_BAD_ARG;
   }
   if (n == 0) return VR_OK;
-  k_hash_fwd<<<grid_for(n, HASH_THREADS, 8), HASH_THREADS, 0, (cudaStream_t)stream>>>(
+  k_hash_fwd<<<grid_for(2 * n, HASH_THREADS, 8), HASH_THREADS, 0, (cudaStream_t)stream>>>(
       *g, reinterpret_cast<const float2*>(table), rays, stride, t0, t1, rid, n,
       reinterpret_cast<__half2*>(enc), pos);
   return check_launch("vr_hash_fwd");
@@ -297,7 +319,7 @@ extern "C" int vr_hash_positions(const VrHashGridDesc* g, const double* rays, in
 }
 
 static dim3 lm_grid(const VrHashGridDesc* g, int64_t n) {
-  const int64_t blocks = ceil_div(n, HASH_THREADS);
+  const int64_t blocks = ceil_div(2 * n, HASH_THREADS);  // lane pairs (forward) fit too
   return dim3((unsigned)(blocks < VR_NUM_SMS * 8 ? blocks : VR_NUM_SMS * 8), (unsigned)g->n_levels);
 }
 

@@ -37,12 +37,11 @@ struct Corners {
   float w[8];
 };
 
-__device__ __forceinline__ void level_corners(const VrHashGridDesc& g, int l, const float u[3],
-                                              Corners& c) {
+// cell of level l: lower corner gi and fractions fr (two float32 roundings, no FMA)
+__device__ __forceinline__ void level_cell(const VrHashGridDesc& g, int l, const float u[3],
+                                           int gi[3], float fr[3]) {
   const float scale = g.scale[l];
   const int res = g.res[l];
-  int gi[3];
-  float fr[3];
 #pragma unroll
   for (int a = 0; a < 3; ++a) {
     const float pos = __fadd_rn(__fmul_rn(u[a], scale), 0.5f);
@@ -51,20 +50,56 @@ __device__ __forceinline__ void level_corners(const VrHashGridDesc& g, int l, co
     gi[a] = gg;
     fr[a] = __fsub_rn(pos, (float)gg);
   }
-  const uint32_t mask = (1u << g.log2_T) - 1u;
-  const bool dense = g.dense[l] != 0;
+}
+
+// table index and trilinear weight of corner c8 = cx + 2 cy + 4 cz
+__device__ __forceinline__ void corner(const VrHashGridDesc& g, int l, const int gi[3],
+                                       const float fr[3], int c8, uint32_t& idx, float& w) {
+  const int res = g.res[l];
+  const int cx = c8 & 1, cy = (c8 >> 1) & 1, cz = (c8 >> 2) & 1;
+  const uint32_t x = (uint32_t)(gi[0] + cx), y = (uint32_t)(gi[1] + cy),
+                 z = (uint32_t)(gi[2] + cz);
+  idx = g.dense[l] ? x + (uint32_t)res * (y + (uint32_t)res * z)
+                   : (x ^ (y * 2654435761u) ^ (z * 805459861u)) & ((1u << g.log2_T) - 1u);
+  const float wx = cx ? fr[0] : __fsub_rn(1.f, fr[0]);
+  const float wy = cy ? fr[1] : __fsub_rn(1.f, fr[1]);
+  const float wz = cz ? fr[2] : __fsub_rn(1.f, fr[2]);
+  w = __fmul_rn(__fmul_rn(wx, wy), wz);
+}
+
+__device__ __forceinline__ void level_corners(const VrHashGridDesc& g, int l, const float u[3],
+                                              Corners& c) {
+  int gi[3];
+  float fr[3];
+  level_cell(g, l, u, gi, fr);
 #pragma unroll
-  for (int c8 = 0; c8 < 8; ++c8) {
-    const int cx = c8 & 1, cy = (c8 >> 1) & 1, cz = (c8 >> 2) & 1;
-    const uint32_t x = (uint32_t)(gi[0] + cx), y = (uint32_t)(gi[1] + cy),
-                   z = (uint32_t)(gi[2] + cz);
-    c.idx[c8] = dense ? x + (uint32_t)res * (y + (uint32_t)res * z)
-                      : (x ^ (y * 2654435761u) ^ (z * 805459861u)) & mask;
-    const float wx = cx ? fr[0] : __fsub_rn(1.f, fr[0]);
-    const float wy = cy ? fr[1] : __fsub_rn(1.f, fr[1]);
-    const float wz = cz ? fr[2] : __fsub_rn(1.f, fr[2]);
-    c.w[c8] = __fmul_rn(__fmul_rn(wx, wy), wz);
+  for (int c8 = 0; c8 < 8; ++c8) corner(g, l, gi, fr, c8, c.idx[c8], c.w[c8]);
+}
+
+// Half of a level's feature: the corners with cx = p (c8 = p, p+2, p+4, p+6), accumulated
+// in that order from 0 with round-to-nearest mul/add (no FMA).  feature = half(0) + half(1)
+// — the accumulation order every gather implements and oracle/hashmlp_oracle.py restates.
+// Lane-pair gathers: lanes 2j and 2j+1 take the two halves of one sample, so the x-adjacent
+// corners of a row are read by the same 8-byte load instruction and merge into one L2
+// sector request whenever their entries share a 32-byte sector (x mod 4 != 3 on hashed
+// levels; measured 2.5x the per-lane rate of 16-byte loads in scripts/micro/gather_bench.cu).
+__device__ __forceinline__ float2 gather_half(const VrHashGridDesc& g, int l,
+                                              const float2* __restrict__ tl, const float u[3],
+                                              int p) {
+  int gi[3];
+  float fr[3];
+  level_cell(g, l, u, gi, fr);
+  float a0 = 0.f, a1 = 0.f;
+#pragma unroll
+  for (int k = 0; k < 4; ++k) {
+    uint32_t idx;
+    float w;
+    corner(g, l, gi, fr, p + 2 * k, idx, w);
+    const float2 v = __ldg(tl + idx);
+    a0 = __fadd_rn(a0, __fmul_rn(w, v.x));
+    a1 = __fadd_rn(a1, __fmul_rn(w, v.y));
   }
+  return make_float2(a0, a1);
 }
 
 // Feature of one level.  x-adjacent corners whose entries differ only in bit 0 share
@@ -86,13 +121,16 @@ __device__ __forceinline__ float2 gather_level(const float2* __restrict__ tl, co
       v[k + 1] = __ldg(tl + b);
     }
   }
-  float a0 = 0.f, a1 = 0.f;
+  // even corners, odd corners, then their sum (the order gather_half pairs implement)
+  float e0 = 0.f, e1 = 0.f, o0 = 0.f, o1 = 0.f;
 #pragma unroll
-  for (int k = 0; k < 8; ++k) {
-    a0 = __fadd_rn(a0, __fmul_rn(c.w[k], v[k].x));
-    a1 = __fadd_rn(a1, __fmul_rn(c.w[k], v[k].y));
+  for (int k = 0; k < 8; k += 2) {
+    e0 = __fadd_rn(e0, __fmul_rn(c.w[k], v[k].x));
+    e1 = __fadd_rn(e1, __fmul_rn(c.w[k], v[k].y));
+    o0 = __fadd_rn(o0, __fmul_rn(c.w[k + 1], v[k + 1].x));
+    o1 = __fadd_rn(o1, __fmul_rn(c.w[k + 1], v[k + 1].y));
   }
-  return make_float2(a0, a1);
+  return make_float2(__fadd_rn(e0, o0), __fadd_rn(e1, o1));
 }
 
 // Branch-free: one 16-byte vector atomic on a's aligned entry pair (carrying b's gradient
