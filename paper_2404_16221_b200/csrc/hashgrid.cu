@@ -139,11 +139,17 @@ __global__ void __launch_bounds__(HASH_THREADS)
                   float2* __restrict__ grad, float2* __restrict__ ws) {
   const int l0 = passes.first[blockIdx.y], l1 = passes.first[blockIdx.y + 1];
   const int gwarp = blockIdx.x * (blockDim.x / 32) + (threadIdx.x >> 5);
-  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
-       i += (int64_t)gridDim.x * blockDim.x) {
+  const int lane = threadIdx.x & 31, p = lane & 1;  // lane pairs (scatter_half)
+  const int64_t warp0 = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int64_t n_warps = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  for (int64_t s0 = warp0 * 16; s0 < n; s0 += n_warps * 16) {
+    const int64_t i = s0 + (lane >> 1);
+    if (i >= n) continue;  // no shuffles below: lanes may leave independently
     const float u[3] = {__ldcs(pos + i), __ldcs(pos + n + i), __ldcs(pos + 2 * n + i)};
-    for (int l = l0; l < l1; ++l)
-      scatter_level(g, plan, l, u, __ldcs(denc + (int64_t)l * n + i), gwarp, grad, ws);
+    for (int l = l0; l < l1; ++l) {
+      const float2 d = __ldcs(denc + (int64_t)l * n + i);
+      if (d.x != 0.f || d.y != 0.f) scatter_half(g, plan, l, u, d, p, gwarp, grad, ws);
+    }
   }
 }
 
@@ -359,6 +365,7 @@ extern "C" int vr_hash_scatter(const VrHashGridDesc* g, const float* pos, int64_
   }
   dim3 grid = lm_grid(g, n);
   grid.y = passes.n;
+  grid.x = (unsigned)grid_for(2 * n, HASH_THREADS, 8);  // lane pairs
   int threads = HASH_THREADS;
   if (max_blocks > 0) {  // co-resident with another kernel: few small blocks per level pass
     threads = 128;

@@ -172,6 +172,29 @@ __device__ __forceinline__ void scatter_level(const VrHashGridDesc& g, const Rep
                  make_float2(c.w[k + 1] * d.x, c.w[k + 1] * d.y));
 }
 
+// Half of a level's scatter for lane pairs (as gather_half): lane p adds w_c * d to the
+// corners with cx = p.  The partner lane adds the x+1 corner of each row in the same
+// 8-byte RED instruction, so entries in one 32-byte sector (x mod 4 != 3) cost one L2
+// request (measured: two lanes' 8-byte adds into one sector run at the 16-byte-RED rate,
+// scripts/micro/atom_bench.cu modes 4/7) — 1.25 requests per row instead of 1.5.
+__device__ __forceinline__ void scatter_half(const VrHashGridDesc& g, const RepPlan& plan, int l,
+                                             const float u[3], float2 d, int p, int gwarp,
+                                             float2* __restrict__ grad, float2* __restrict__ ws) {
+  int gi[3];
+  float fr[3];
+  level_cell(g, l, u, gi, fr);
+  const int64_t size_l = g.offset[l + 1] - g.offset[l];
+  float2* gl = (l < plan.n_rep) ? ws + plan.off[l] + (int64_t)(gwarp % plan.R[l]) * size_l
+                                : grad + g.offset[l];
+#pragma unroll
+  for (int k = 0; k < 4; ++k) {
+    uint32_t idx;
+    float w;
+    corner(g, l, gi, fr, p + 2 * k, idx, w);
+    atomicAdd(gl + idx, make_float2(w * d.x, w * d.y));
+  }
+}
+
 // host: replica plan + workspace / reduction sizes (entries)
 RepPlan hash_rep_plan(const VrHashGridDesc* g, int64_t* ws_entries, int64_t* red_entries);
 // host: sum the replicas into grad and zero them (enqueued on stream)

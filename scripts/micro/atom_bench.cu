@@ -23,7 +23,7 @@ __global__ void __launch_bounds__(256) k(float* tab, uint32_t mask_pairs, int it
     bool use_bulk = MODE == 1 || (MODE == 2 && (it & 1));
     if (MODE >= 4) {
       // lanes cooperating on one sector: the group leader's random pair index is shared
-      const int gs = MODE == 4 ? 2 : (MODE == 5 ? 4 : 2);
+      const int gs = MODE == 5 ? 4 : 2;
       const uint32_t lane = threadIdx.x & 31, lead = lane & ~(uint32_t)(gs - 1);
       const uint32_t sl = __shfl_sync(0xffffffffu, s, lead);
       float* base = tab + (size_t)((sl & mask_pairs) & ~1u) * 4;  // 32-byte aligned
@@ -31,8 +31,10 @@ __global__ void __launch_bounds__(256) k(float* tab, uint32_t mask_pairs, int it
         asm volatile("red.global.add.v2.f32 [%0], {%1, %1};" ::"l"(base + 2 * (lane & 1)), "f"(v) : "memory");
       } else if (MODE == 5) {  // 4 lanes x v2 into one 32-byte sector
         asm volatile("red.global.add.v2.f32 [%0], {%1, %1};" ::"l"(base + 2 * (lane & 3)), "f"(v) : "memory");
-      } else {  // 2 lanes x v4 into one 32-byte sector
+      } else if (MODE == 6) {  // 2 lanes x v4 into one 32-byte sector
         asm volatile("red.global.add.v4.f32 [%0], {%1, %1, %1, %1};" ::"l"(base + 4 * (lane & 1)), "f"(v) : "memory");
+      } else {  // MODE 7: 2 lanes x v2 straddling the sector's 16-byte halves (bytes 8..23)
+        asm volatile("red.global.add.v2.f32 [%0], {%1, %1};" ::"l"(base + 2 + 2 * (lane & 1)), "f"(v) : "memory");
       }
     } else if (MODE == 3) {
       asm volatile("red.global.add.v2.f32 [%0], {%1, %1};" ::"l"(dst), "f"(v) : "memory");
@@ -65,7 +67,7 @@ int main() {
   const int blocks_per_sm = 8;
   {
     const int grid = sms * blocks_per_sm;
-    for (int mode = 0; mode < 7; ++mode) {
+    for (int mode = 0; mode < 8; ++mode) {
       auto launch = [&] {
         if (mode == 0) k<0><<<grid, 256>>>(tab, np - 1, iters);
         if (mode == 1) k<1><<<grid, 256>>>(tab, np - 1, iters);
@@ -74,6 +76,7 @@ int main() {
         if (mode == 4) k<4><<<grid, 256>>>(tab, np - 1, iters);
         if (mode == 5) k<5><<<grid, 256>>>(tab, np - 1, iters);
         if (mode == 6) k<6><<<grid, 256>>>(tab, np - 1, iters);
+        if (mode == 7) k<7><<<grid, 256>>>(tab, np - 1, iters);
       };
       launch();
       cudaEvent_t a, b;
@@ -86,7 +89,7 @@ int main() {
       float ms;
       cudaEventElapsedTime(&ms, a, b);
       // 16-byte adds: modes 4/5 move 8 B per lane
-      const double ops = 5.0 * grid * 256.0 * iters * ((mode == 4 || mode == 5) ? 0.5 : 1.0);
+      const double ops = 5.0 * grid * 256.0 * iters * ((mode == 4 || mode == 5 || mode == 7) ? 0.5 : 1.0);
       printf("table %zu MB mode %d: %.2f ms  %.1f G 16B-adds/s  (%.3f per SM-clk @1.965GHz) err=%s\n",
              np * 16 >> 20, mode, ms / 5, ops / (ms * 1e6), ops / (ms * 1e-3) / sms / 1.965e9,
              cudaGetErrorString(cudaGetLastError()));
