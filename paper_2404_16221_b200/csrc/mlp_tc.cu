@@ -576,10 +576,27 @@ __global__ void __launch_bounds__(TILE * BWD_TPR, 2)
   bool pending = false;
   float pk[16], pu[3];
   const int gwarp = blockIdx.x * (TILE * BWD_TPR / 32) + (threadIdx.x >> 5);
+  // lane pairs (scatter_half): lanes 2j, 2j+1 hold rows r, r+1; each of the rows is
+  // scattered by both lanes, lane p adding the corners with cx = p
   auto scatter_one = [&](int j) {
-    if (FUSED && pending)
-      scatter_level(hg, plan, 8 * part + j, pu, make_float2(pk[2 * j], pk[2 * j + 1]), gwarp,
-                    grad_table, rep_ws);
+    if (FUSED && pending) {
+      const int p = lane & 1;
+      const float2 mine = make_float2(pk[2 * j], pk[2 * j + 1]);
+      const float2 other = make_float2(__shfl_xor_sync(0xffffffffu, mine.x, 1),
+                                       __shfl_xor_sync(0xffffffffu, mine.y, 1));
+      float uo[3];
+#pragma unroll
+      for (int a = 0; a < 3; ++a) uo[a] = __shfl_xor_sync(0xffffffffu, pu[a], 1);
+      // pass 0: the even lane's row, pass 1: the odd lane's row
+      const float2 d0 = p ? other : mine, d1 = p ? mine : other;
+      const float* u0 = p ? uo : pu;
+      const float* u1 = p ? pu : uo;
+      const int l = 8 * part + j;
+      if (d0.x != 0.f || d0.y != 0.f)
+        scatter_half(hg, plan, l, u0, d0, p, gwarp, grad_table, rep_ws);
+      if (d1.x != 0.f || d1.y != 0.f)
+        scatter_half(hg, plan, l, u1, d1, p, gwarp, grad_table, rep_ws);
+    }
   };
   auto scatter_ov = [&](int round) { scatter_one(round); };
 
