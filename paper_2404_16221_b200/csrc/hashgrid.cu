@@ -10,9 +10,10 @@
 //   w_c = (wx * wy) * wz,  feat_l = sum_{c even} w_c t_c + sum_{c odd} w_c t_c   (F = 2,
 //   float32, each half summed in increasing c from 0, no FMA; t_c = table[offset_l + idx_c])
 // Encodings are written level-major enc[l][n] as half2 so both the gather kernel
-// and the MLP read them coalesced.  The backward scatters w_c * dfeat with vector
-// atomics (float4 for x-adjacent pairs, float2 otherwise); the coarsest dense level
-// goes through per-warp replicas (see RepPlan in hashgrid.cuh).
+// and the MLP read them coalesced.  Gathers and the backward's float2 atomics run in lane
+// pairs (two lanes per sample, one per x side of the cell: gather_half / scatter_half in
+// hashgrid.cuh); the coarsest dense level's atomics go through per-warp replicas
+// (RepPlan).
 // The production training path fuses both directions into the tensor-core MLP kernels
 // (mlp_tc.cu); these standalone kernels serve inference-only callers and the tests.
 #include <stdlib.h>
@@ -64,13 +65,22 @@ __global__ void __launch_bounds__(HASH_THREADS)
                const int32_t* __restrict__ rid, int64_t n, const float2* __restrict__ denc,
                float2* __restrict__ grad, float2* __restrict__ ws) {
   const int gwarp = blockIdx.x * (HASH_THREADS / 32) + (threadIdx.x >> 5);
-  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
-       i += (int64_t)gridDim.x * blockDim.x) {
-    float u[3];
-    norm_pos(g, rays, stride, t0, t1, rid, i, u);
+  const int lane = threadIdx.x & 31, p = lane & 1;  // lane pairs (scatter_half)
+  const int64_t warp0 = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int64_t n_warps = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  for (int64_t s0 = warp0 * 16; s0 < n; s0 += n_warps * 16) {
+    const int64_t i = s0 + (lane >> 1);
+    const bool valid = i < n;
+    float u[3] = {0.f, 0.f, 0.f};
+    if (valid && p == 0) norm_pos(g, rays, stride, t0, t1, rid, i, u);
+#pragma unroll
+    for (int a = 0; a < 3; ++a) u[a] = __shfl_sync(0xffffffffu, u[a], lane & ~1);
+    if (!valid) continue;
 #pragma unroll 2
-    for (int l = 0; l < g.n_levels; ++l)
-      scatter_level(g, plan, l, u, denc[(int64_t)l * n + i], gwarp, grad, ws);
+    for (int l = 0; l < g.n_levels; ++l) {
+      const float2 d = denc[(int64_t)l * n + i];
+      if (d.x != 0.f || d.y != 0.f) scatter_half(g, plan, l, u, d, p, gwarp, grad, ws);
+    }
   }
 }
 
@@ -290,7 +300,7 @@ extern "C" int vr_hash_bwd(const VrHashGridDesc* g, const double* rays, int64_t 
   int64_t ws_entries = 0, red = 0;
   RepPlan plan = hash_rep_plan(g, &ws_entries, &red);
   if (!ws || ws_bytes < (size_t)ws_entries * sizeof(float2)) plan.n_rep = 0;  // plain atomics
-  k_hash_bwd<<<grid_for(n, HASH_THREADS, 8), HASH_THREADS, 0, (cudaStream_t)stream>>>(
+  k_hash_bwd<<<grid_for(2 * n, HASH_THREADS, 8), HASH_THREADS, 0, (cudaStream_t)stream>>>(
       *g, plan, rays, stride, t0, t1, rid, n, reinterpret_cast<const float2*>(denc),
       reinterpret_cast<float2*>(grad), reinterpret_cast<float2*>(ws));
   const int rc = check_launch("vr_hash_bwd");

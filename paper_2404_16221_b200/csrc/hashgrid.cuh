@@ -133,20 +133,6 @@ __device__ __forceinline__ float2 gather_level(const float2* __restrict__ tl, co
   return make_float2(__fadd_rn(e0, o0), __fadd_rn(e1, o1));
 }
 
-// Branch-free: one 16-byte vector atomic on a's aligned entry pair (carrying b's gradient
-// when b is a's partner, zeros otherwise) plus a predicated 8-byte atomic for a b outside
-// that pair.  Same L2 requests as a divergent pair / two-singles version, but a warp
-// issues 2 RED instructions per row instead of 3.
-__device__ __forceinline__ void scatter_pair(float2* gl, uint32_t a, uint32_t b, float2 ga,
-                                             float2 gb) {
-  const bool pair = (a ^ b) == 1u;
-  const float2 gp = pair ? gb : make_float2(0.f, 0.f);
-  const float4 q =
-      (a & 1u) ? make_float4(gp.x, gp.y, ga.x, ga.y) : make_float4(ga.x, ga.y, gp.x, gp.y);
-  atomicAdd(reinterpret_cast<float4*>(gl + (a & ~1u)), q);
-  if (!pair) atomicAdd(gl + b, gb);
-}
-
 // Coarse dense levels (a few thousand entries hit by every sample of the region) are
 // contention-bound under global atomics: their gradients go to R private replicas
 // (picked per warp) in a workspace, summed into the table by k_hash_rep_reduce.
@@ -155,22 +141,6 @@ struct RepPlan {
   int32_t R[VR_MAX_LEVELS];
   int64_t off[VR_MAX_LEVELS];  // workspace offset (entries) of level l's replicas
 };
-
-// scatter d(feature) of level l for one sample
-__device__ __forceinline__ void scatter_level(const VrHashGridDesc& g, const RepPlan& plan,
-                                              int l, const float u[3], float2 d, int gwarp,
-                                              float2* __restrict__ grad, float2* __restrict__ ws) {
-  if (d.x == 0.f && d.y == 0.f) return;
-  Corners c;
-  level_corners(g, l, u, c);
-  const int64_t size_l = g.offset[l + 1] - g.offset[l];
-  float2* gl = (l < plan.n_rep) ? ws + plan.off[l] + (int64_t)(gwarp % plan.R[l]) * size_l
-                                : grad + g.offset[l];
-#pragma unroll
-  for (int k = 0; k < 8; k += 2)
-    scatter_pair(gl, c.idx[k], c.idx[k + 1], make_float2(c.w[k] * d.x, c.w[k] * d.y),
-                 make_float2(c.w[k + 1] * d.x, c.w[k + 1] * d.y));
-}
 
 // Half of a level's scatter for lane pairs (as gather_half): lane p adds w_c * d to the
 // corners with cx = p.  The partner lane adds the x+1 corner of each row in the same
