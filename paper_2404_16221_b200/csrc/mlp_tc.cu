@@ -313,22 +313,116 @@ __device__ __forceinline__ void load_dir(const double* __restrict__ rays, int64_
 }
 
 // ---- forward kernel ---------------------------------------------------------------------
+// The forward keeps its activations in TMEM: every layer's A operand is written there by
+// the epilogue (tcgen05.st, lane = row, 32-bit column j = features 2j, 2j+1) and read by a
+// "TS" tcgen05.mma (A from TMEM, weights from shared memory) — no activation round trip
+// through shared memory, whose bandwidth the small-K SS MMAs were bound by (ncu: tensor
+// pipe ~50 % active at 16 % of peak FLOP/s).  TMEM per CTA (128 columns, 4 CTAs/SM):
+// D [0,64) accumulator, A1 [64,96) and A2 [96,128) activation buffers.
 constexpr int FWD_TPR = 1;
-constexpr uint32_t F_P = WBYTES, F_Q = F_P + TILE * 64 * 2, F_BAR = F_Q + TILE * 64 * 2,
-                   F_SMEM = F_BAR + 16;
+constexpr uint32_t F_BAR = WBYTES, F_SMEM = F_BAR + 16;
+constexpr uint32_t TF_D = 0, TF_A1 = 64, TF_A2 = 96, TF_COLS = 128;
+
+__device__ __forceinline__ void tmem_st8(uint32_t taddr, const uint32_t* r) {
+  asm volatile("tcgen05.st.sync.aligned.32x32b.x8.b32 [%0], {%1, %2, %3, %4, %5, %6, %7, %8};"
+               ::"r"(taddr), "r"(r[0]), "r"(r[1]), "r"(r[2]), "r"(r[3]), "r"(r[4]), "r"(r[5]),
+                 "r"(r[6]), "r"(r[7])
+               : "memory");
+}
+__device__ __forceinline__ void tmem_st_wait() {
+  asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
+}
+__device__ __forceinline__ uint32_t h2bits(__half2 h) { return *reinterpret_cast<uint32_t*>(&h); }
+
+// D[128 x N] = A[128 x K] . B^T with A in TMEM (K/2 columns at a_tmem), B a weight tile
+__device__ __forceinline__ void issue_fwd_ts(uint32_t a_tmem, int K, uint32_t b, int N,
+                                             uint32_t d) {
+  const uint32_t id = idesc_f16(TILE, N, 0, 0);
+  for (int kb = 0; kb < K / 16; ++kb) {
+    const uint64_t bd = desc_k(b, N, 2 * kb);
+    const uint32_t acc = kb > 0 ? 1u : 0u;
+    asm volatile("{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
+                 "tcgen05.mma.cta_group::1.kind::f16 [%0], [%1], %2, %3, p;\n\t}\n"
+                 ::"r"(d), "r"(a_tmem + (uint32_t)(kb * 8)), "l"(bd), "r"(id), "r"(acc));
+  }
+}
+
+// one TS round: the TMEM stores of every thread are complete and visible, thread 0 issues
+__device__ __forceinline__ void ts_round(uint64_t* bar, uint32_t& phase, uint32_t a, int K,
+                                         uint32_t b, int N, uint32_t d) {
+  tmem_st_wait();
+  tc_fence_before();
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    tc_fence_after();
+    issue_fwd_ts(a, K, b, N, d);
+    mma_commit(bar);
+  }
+  mbar_wait(bar, phase);
+  phase ^= 1u;
+  __syncwarp();
+  tc_fence_after();
+}
+
+// ReLU + fp16 of the 64-wide D into an activation buffer (32 TMEM columns)
+__device__ __forceinline__ void epi_relu64(uint32_t tm_row, uint32_t dst) {
+  float v[16];
+  uint32_t q[8];
+#pragma unroll
+  for (int c = 0; c < 64; c += 16) {
+    tmem_ld16(tm_row + TF_D + c, v);
+#pragma unroll
+    for (int j = 0; j < 8; ++j)
+      q[j] = h2bits(__floats2half2_rn(fmaxf(v[2 * j], 0.f), fmaxf(v[2 * j + 1], 0.f)));
+    tmem_st8(tm_row + dst + c / 2, q);
+  }
+}
+
+// Forward chain of one 128-sample tile; enc (K = 32) is already in A2.
+template <bool DENS>
+__device__ __forceinline__ FwdRow forward_tile_ts(uint32_t sW, uint32_t tmem, uint32_t tm_row,
+                                                  uint64_t* bar, uint32_t& phase, float dx,
+                                                  float dy, float dz) {
+  FwdRow out = {0.f, 0.f, {0.f, 0.f, 0.f}};
+  float v[16];
+  uint32_t q[8];
+  ts_round(bar, phase, tmem + TF_A2, 32, sW + OW1D, 64, tmem + TF_D);  // L1d
+  epi_relu64(tm_row, TF_A1);
+  ts_round(bar, phase, tmem + TF_A1, 64, sW + OW2D, 16, tmem + TF_D);  // L2d
+  tmem_ld16(tm_row + TF_D, v);
+  out.od0 = v[0];
+  out.sigma = expf(fminf(fmaxf(v[0], -15.f), 15.f));
+  if (DENS) return out;
+  // cin = [geo (16) | SH(d) (16)] -> A2
+#pragma unroll
+  for (int j = 0; j < 8; ++j) q[j] = h2bits(__floats2half2_rn(v[2 * j], v[2 * j + 1]));
+  tmem_st8(tm_row + TF_A2, q);
+  sh16f(dx, dy, dz, v);
+#pragma unroll
+  for (int j = 0; j < 8; ++j) q[j] = h2bits(__floats2half2_rn(v[2 * j], v[2 * j + 1]));
+  tmem_st8(tm_row + TF_A2 + 8, q);
+  ts_round(bar, phase, tmem + TF_A2, 32, sW + OW1C, 64, tmem + TF_D);  // L1c
+  epi_relu64(tm_row, TF_A1);
+  ts_round(bar, phase, tmem + TF_A1, 64, sW + OW2C, 64, tmem + TF_D);  // L2c
+  epi_relu64(tm_row, TF_A2);
+  ts_round(bar, phase, tmem + TF_A2, 64, sW + OW3C, 16, tmem + TF_D);  // L3c
+  tmem_ld8(tm_row + TF_D, v);
+#pragma unroll
+  for (int c = 0; c < 3; ++c) out.rgb[c] = 1.f / (1.f + expf(-v[c]));
+  return out;
+}
 
 // Hash-grid encoding of this thread's row (FUSED forward): 16 levels gathered from the
-// region's table, rounded to fp16, staged into tile P and (optionally) written to enc_out
-// for the backward.  dir returned as float for the SH encoding.
+// region's table, rounded to fp16, returned packed (16 half2) and (optionally) written
+// to enc_out for the backward.  dir returned as float for the SH encoding.
 __device__ __forceinline__ void encode_row(const VrHashGridDesc& g, const float2* __restrict__ table,
                                            const double* __restrict__ rays, int64_t stride,
                                            const double* __restrict__ t0,
                                            const double* __restrict__ t1,
                                            const int32_t* __restrict__ rid, int64_t n, int64_t i,
-                                           bool valid, uint8_t* P, int r,
+                                           bool valid, uint32_t* q,
                                            __half2* __restrict__ enc_out, float& dx, float& dy,
                                            float& dz) {
-  uint4 q[4];
   __half2* h = reinterpret_cast<__half2*>(q);
   dx = dy = dz = 0.f;
   if (valid) {
@@ -360,12 +454,11 @@ __device__ __forceinline__ void encode_row(const VrHashGridDesc& g, const float2
 #pragma unroll
     for (int l = 0; l < 16; ++l) h[l] = __floats2half2_rn(0.f, 0.f);
   }
-#pragma unroll
-  for (int c = 0; c < 4; ++c) *reinterpret_cast<uint4*>(P + tile_off(TILE, r, c * 8)) = q[c];
 }
 
 // FUSED = true: the kernel computes the hash encoding itself (K2 + K3 in one pass);
-// otherwise it reads enc (level-major half2) produced by vr_hash_fwd.
+// otherwise it reads enc (level-major half2) produced by vr_hash_fwd.  DENS: density
+// branch only.
 template <bool FUSED, bool DENS = false>
 __global__ void __launch_bounds__(TILE * FWD_TPR, 4)
     k_mlp_fwd_tc(const __half* __restrict__ W, const __half2* __restrict__ enc,
@@ -376,47 +469,47 @@ __global__ void __launch_bounds__(TILE * FWD_TPR, 4)
   using G = Geo<FWD_TPR>;
   extern __shared__ __align__(1024) uint8_t smem[];
   uint8_t* sw = smem;
-  uint8_t* P = smem + F_P;
-  uint8_t* Q = smem + F_Q;
   uint64_t* bar = reinterpret_cast<uint64_t*>(smem + F_BAR);
   uint32_t* slot = reinterpret_cast<uint32_t*>(smem + F_BAR + 8);
   stage_weights(W, sw);
-  if (threadIdx.x < 32) tmem_alloc(slot, 128);
+  if (threadIdx.x < 32) tmem_alloc(slot, TF_COLS);
   if (threadIdx.x == 0) {
     mbar_init(bar, 1);
     fence_barrier_init();
   }
+  fence_async_smem();  // weights visible to the tensor core
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem = *slot;
   const uint32_t tm_row = tmem + G::lane_base();
-  const int r = G::row(), part = G::part();
+  const uint32_t sW = smem_u32(sw);
+  const int r = G::row();
   uint32_t phase = 0;
   const int64_t n_tiles = ceil_div(n, TILE);
   for (int64_t tile = blockIdx.x; tile < n_tiles; tile += gridDim.x) {
     const int64_t i = tile * TILE + r;
     const bool valid = i < n;
-    float dx, dy, dz;
+    float dx = 0.f, dy = 0.f, dz = 0.f;
+    uint32_t q[16];
     if (FUSED) {
-      encode_row(g, table, rays, stride, t0, t1, rid, n, i, valid, P, r, enc_out, dx, dy, dz);
+      encode_row(g, table, rays, stride, t0, t1, rid, n, i, valid, q, enc_out, dx, dy, dz);
     } else {
-      stage_enc<FWD_TPR>(P, r, part, enc, n, i, valid);
-      if (DENS)
-        dx = dy = dz = 0.f;
-      else
-        load_dir(rays, stride, rid, i, valid, dx, dy, dz);
+#pragma unroll
+      for (int l = 0; l < 16; ++l)
+        q[l] = valid ? h2bits(enc[(int64_t)l * n + i]) : 0u;
+      if (!DENS) load_dir(rays, stride, rid, i, valid, dx, dy, dz);
     }
-    // P(enc) -> Q(h1d) -> P(cin) -> Q(h1c) -> P(h2c)
-    const FwdRow f = forward_tile<FWD_TPR, DENS>(sw, P, Q, P, Q, P, tm_row, tmem, 0, 64, bar,
-                                                 phase, dx, dy, dz);
-    if (valid && part == 0) out[i] = make_float4(f.sigma, f.rgb[0], f.rgb[1], f.rgb[2]);
+    tmem_st8(tm_row + TF_A2, q);  // enc -> A2 (the previous tile's last MMA is complete)
+    tmem_st8(tm_row + TF_A2 + 8, q + 8);
+    const FwdRow f = forward_tile_ts<DENS>(sW, tmem, tm_row, bar, phase, dx, dy, dz);
+    if (valid) out[i] = make_float4(f.sigma, f.rgb[0], f.rgb[1], f.rgb[2]);
   }
   tc_fence_before();
   __syncthreads();
   if (threadIdx.x < 32) {
     tc_fence_after();
-    tmem_dealloc(tmem, 128);
+    tmem_dealloc(tmem, TF_COLS);
   }
 }
 
