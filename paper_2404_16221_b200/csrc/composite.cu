@@ -88,12 +88,30 @@ struct ChunkFwd {
   double l_incl, c_incl[3];
 };
 
+// One lane's sample of a chunk, loaded one chunk ahead by the kernels (the scans of the
+// current chunk hide the next chunk's load latency).
+struct ChunkIn {
+  double a, b;
+  float4 v;
+};
+
+__device__ __forceinline__ ChunkIn chunk_load(const double* __restrict__ t0,
+                                              const double* __restrict__ t1,
+                                              const float4* __restrict__ sr, int64_t s,
+                                              int64_t s_end) {
+  ChunkIn in = {0.0, 0.0, make_float4(0.f, 0.f, 0.f, 0.f)};
+  if (s < s_end) {
+    in.a = t0[s];
+    in.b = t1[s];
+    in.v = sr[s];
+  }
+  return in;
+}
+
 template <bool TOTALS = true>
-__device__ __forceinline__ ChunkFwd chunk_forward(const double* __restrict__ t0,
-                                                  const double* __restrict__ t1,
-                                                  const float4* __restrict__ sr, int64_t s,
-                                                  int64_t s_end, const GroupSeg& gs, int nseg,
-                                                  double te_lane, const Carry& cin, int lane) {
+__device__ __forceinline__ ChunkFwd chunk_forward(const ChunkIn& in, int64_t s, int64_t s_end,
+                                                  const GroupSeg& gs, int nseg, double te_lane,
+                                                  const Carry& cin, int lane) {
   ChunkFwd c;
   c.valid = s < s_end;
   c.seg = find_seg(gs.lo, nseg, c.valid ? s : s_end - 1);
@@ -111,8 +129,8 @@ __device__ __forceinline__ ChunkFwd chunk_forward(const double* __restrict__ t0,
   c.dlt = 0.0;
   c.v = make_float4(0.f, 0.f, 0.f, 0.f);
   if (c.valid) {
-    const double a = t0[s], b = t1[s];
-    c.v = sr[s];
+    const double a = in.a, b = in.b;
+    c.v = in.v;
     c.dlt = b - a;
     const double x = (double)c.v.x * c.dlt;
     c.keep = exp(-x);
@@ -189,9 +207,11 @@ __global__ void __launch_bounds__(SEG_WARPS * 32)
       packets[2 * my + 1] = make_float4(0.f, 0.f, 0.f, order_bits(INT32_MAX));
     }
     Carry cin = {1.0, 0.0, 0.0, 0.0, 0.0, 0.0, 0.0, 0.0};
+    ChunkIn nxt = chunk_load(t0, t1, sr, s_beg + lane, s_end);
     for (int64_t base = s_beg; base < s_end; base += 32) {
-      const ChunkFwd c =
-          chunk_forward(t0, t1, sr, base + lane, s_end, gs, nseg, te_lane, cin, lane);
+      const ChunkIn cur = nxt;
+      nxt = chunk_load(t0, t1, sr, base + 32 + lane, s_end);
+      const ChunkFwd c = chunk_forward(cur, base + lane, s_end, gs, nseg, te_lane, cin, lane);
       if (c.tail) {
         const int64_t seg = seg0 + c.seg;
         packets[2 * seg] = make_float4((float)c.Tn, (float)c.c_incl[0], (float)c.c_incl[1],
@@ -234,9 +254,12 @@ __global__ void __launch_bounds__(SEG_WARPS * 32)
     }
     // sweep 1: totals
     Carry cin = {1.0, 0.0, 0.0, 0.0, 0.0, 0.0, 0.0, 0.0};
+    ChunkIn nxt = chunk_load(t0, t1, sr, s_beg + lane, s_end);
     for (int64_t base = s_beg; base < s_end; base += 32) {
+      const ChunkIn cur = nxt;
+      nxt = chunk_load(t0, t1, sr, base + 32 + lane, s_end);
       const ChunkFwd c =
-          chunk_forward<true>(t0, t1, sr, base + lane, s_end, gs, nseg, te_lane, cin, lane);
+          chunk_forward<true>(cur, base + lane, s_end, gs, nseg, te_lane, cin, lane);
       if (c.tail) {
         tot[c.seg][0] = c.Tn;
         tot[c.seg][1] = c.a_incl;
@@ -254,9 +277,12 @@ __global__ void __launch_bounds__(SEG_WARPS * 32)
     __syncwarp();
     // sweep 2: per-sample gradients
     cin = {1.0, 0.0, 0.0, 0.0, 0.0, 0.0, 0.0, 0.0};
+    nxt = chunk_load(t0, t1, sr, s_beg + lane, s_end);
     for (int64_t base = s_beg; base < s_end; base += 32) {
+      const ChunkIn cur = nxt;
+      nxt = chunk_load(t0, t1, sr, base + 32 + lane, s_end);
       const ChunkFwd c =
-          chunk_forward<false>(t0, t1, sr, base + lane, s_end, gs, nseg, te_lane, cin, lane);
+          chunk_forward<false>(cur, base + lane, s_end, gs, nseg, te_lane, cin, lane);
       const float bC0 = __shfl_sync(0xffffffffu, g0.y, c.seg);
       const float bC1 = __shfl_sync(0xffffffffu, g0.z, c.seg);
       const float bC2 = __shfl_sync(0xffffffffu, g0.w, c.seg);
