@@ -64,12 +64,29 @@ struct IlChunk {
   double T, Th;  // local exclusive transmittances (NeRF, proposal)
 };
 
-__device__ __forceinline__ IlChunk il_chunk(const double* __restrict__ t0,
-                                            const double* __restrict__ t1,
-                                            const float4* __restrict__ sr,
-                                            const float4* __restrict__ sp, int64_t s,
-                                            int64_t s_end, const GroupSeg& gs, int nseg,
-                                            double cT, double cTh, int lane) {
+// one lane's inputs of a chunk, loaded one chunk ahead
+struct IlIn {
+  double a, b;
+  float sig, sigh;
+};
+
+__device__ __forceinline__ IlIn il_load(const double* __restrict__ t0,
+                                        const double* __restrict__ t1,
+                                        const float4* __restrict__ sr,
+                                        const float4* __restrict__ sp, int64_t s, int64_t s_end) {
+  IlIn in = {0.0, 0.0, 0.f, 0.f};
+  if (s < s_end) {
+    in.a = t0[s];
+    in.b = t1[s];
+    in.sig = sr[s].x;
+    in.sigh = sp[s].x;
+  }
+  return in;
+}
+
+__device__ __forceinline__ IlChunk il_chunk(const IlIn& in, int64_t s, int64_t s_end,
+                                            const GroupSeg& gs, int nseg, double cT, double cTh,
+                                            int lane) {
   IlChunk c;
   c.valid = s < s_end;
   c.seg = find_seg(gs.lo, nseg, c.valid ? s : s_end - 1);
@@ -83,8 +100,8 @@ __device__ __forceinline__ IlChunk il_chunk(const double* __restrict__ t0,
   c.keeph = 1.0;
   c.dlt = c.alpha = c.alphah = 0.0;
   if (c.valid) {
-    c.dlt = t1[s] - t0[s];
-    const double x = (double)sr[s].x * c.dlt, xh = (double)sp[s].x * c.dlt;
+    c.dlt = in.b - in.a;
+    const double x = (double)in.sig * c.dlt, xh = (double)in.sigh * c.dlt;
     c.keep = exp(-x);
     c.alpha = -expm1(-x);
     c.keeph = exp(-xh);
@@ -128,8 +145,11 @@ __global__ void __launch_bounds__(IL_WARPS * 32)
     if (s_beg == s_end) continue;
     // sweep 1: L and S per segment
     double cT = 1.0, cTh = 1.0, cL = 0.0, cS = 0.0;
+    IlIn nxt = il_load(t0, t1, sr, sp, s_beg + lane, s_end);
     for (int64_t base = s_beg; base < s_end; base += 32) {
-      const IlChunk c = il_chunk(t0, t1, sr, sp, base + lane, s_end, gs, nseg, cT, cTh, lane);
+      const IlIn cur = nxt;
+      nxt = il_load(t0, t1, sr, sp, base + 32 + lane, s_end);
+      const IlChunk c = il_chunk(cur, base + lane, s_end, gs, nseg, cT, cTh, lane);
       const double P = __shfl_sync(0xffffffffu, (double)pre.x, c.seg);
       const double Ph = __shfl_sync(0xffffffffu, (double)pre.y, c.seg);
       const double w = P * c.T * c.alpha;
@@ -154,8 +174,11 @@ __global__ void __launch_bounds__(IL_WARPS * 32)
     cT = 1.0;
     cTh = 1.0;
     double cSc = 0.0;
+    nxt = il_load(t0, t1, sr, sp, s_beg + lane, s_end);
     for (int64_t base = s_beg; base < s_end; base += 32) {
-      const IlChunk c = il_chunk(t0, t1, sr, sp, base + lane, s_end, gs, nseg, cT, cTh, lane);
+      const IlIn cur = nxt;
+      nxt = il_load(t0, t1, sr, sp, base + 32 + lane, s_end);
+      const IlChunk c = il_chunk(cur, base + lane, s_end, gs, nseg, cT, cTh, lane);
       const double P = __shfl_sync(0xffffffffu, (double)pre.x, c.seg);
       const double Ph = __shfl_sync(0xffffffffu, (double)pre.y, c.seg);
       const double w = P * c.T * c.alpha;
