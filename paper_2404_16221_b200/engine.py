@@ -227,34 +227,45 @@ class VolumePool:
     SCATTER_BLOCKS = int(os.environ.get("VR_SCATTER_BLOCKS", "0"))
 
     def field_backward(self, rays, b: SampleBatch, dsig_rgb: torch.Tensor, fields=None) -> None:
+        self.field_backward_jobs(rays, b, [(self.fields if fields is None else fields, dsig_rgb)])
+
+    def field_backward_jobs(self, rays, b: SampleBatch, jobs) -> None:
+        """Backward of several field sets of the same batch ([(fields, dsig_rgb), ...]: the
+        NeRF fields and the proposals) as one pipeline."""
         s = self._stream()
-        fields = self.fields if fields is None else fields
         base = self.region_lo - b.region_lo  # an all-region batch: skip the peers' regions
-        if self.overlap_backward and all(getattr(f, "split_backward", False)
-                                         for f in fields if f.trainable):
+        split = [all(getattr(f, "split_backward", False) for f in fields if f.trainable)
+                 for fields, _ in jobs]
+        if self.overlap_backward and any(split):
             # region k's hash-grid scatter (L2-atomic bound) runs on the side stream while
-            # the tensor-core MLP backward of region k+1 runs here: the scatter warps are
-            # dedicated instead of sharing the MLP's warps (vr_field_bwd_tc)
+            # the tensor-core MLP backward of the next region (of any field set) runs here
             main = torch.cuda.current_stream()
             side = self._side_stream()
             side.wait_stream(main)
-            for kk, f in enumerate(fields):
-                lo, hi = b.region_slice(base + kk)
-                if hi <= lo or not f.trainable:
-                    continue
-                denc = f.backward_mlp(rays, b.ray_id[lo:], hi - lo, dsig_rgb[lo:], s)
-                ev = torch.cuda.Event()
-                ev.record(main)
-                with torch.cuda.stream(side):
-                    side.wait_event(ev)
-                    denc.record_stream(side)
-                    f.backward_scatter(denc, hi - lo, _lib.stream_ptr(), self.SCATTER_BLOCKS)
+            for (fields, dsig_rgb), sp in zip(jobs, split):
+                for kk, f in enumerate(fields):
+                    lo, hi = b.region_slice(base + kk)
+                    if hi <= lo or not f.trainable:
+                        continue
+                    if not sp:
+                        f.backward(rays, b.t0[lo:], b.t1[lo:], b.ray_id[lo:], hi - lo,
+                                   dsig_rgb[lo:], s)
+                        continue
+                    denc = f.backward_mlp(rays, b.ray_id[lo:], hi - lo, dsig_rgb[lo:], s)
+                    ev = torch.cuda.Event()
+                    ev.record(main)
+                    with torch.cuda.stream(side):
+                        side.wait_event(ev)
+                        denc.record_stream(side)
+                        f.backward_scatter(denc, hi - lo, _lib.stream_ptr(), self.SCATTER_BLOCKS)
             main.wait_stream(side)
             return
-        for kk, f in enumerate(fields):
-            lo, hi = b.region_slice(base + kk)
-            if hi > lo and f.trainable:
-                f.backward(rays, b.t0[lo:], b.t1[lo:], b.ray_id[lo:], hi - lo, dsig_rgb[lo:], s)
+        for fields, dsig_rgb in jobs:
+            for kk, f in enumerate(fields):
+                lo, hi = b.region_slice(base + kk)
+                if hi > lo and f.trainable:
+                    f.backward(rays, b.t0[lo:], b.t1[lo:], b.ray_id[lo:], hi - lo,
+                               dsig_rgb[lo:], s)
 
     # ---- K4 ----------------------------------------------------------------------------
     def local_packets(self, b: SampleBatch, sig_rgb: torch.Tensor) -> torch.Tensor:
@@ -400,12 +411,16 @@ class VolumePool:
             il = torch.empty(1, dtype=torch.float64, device=self.device)
             _lib.call("vr_sum_f64", _lib.ptr(seg_loss), seg_loss.numel(), _lib.ptr(il), s)
             loss = loss + il
-            self.field_backward(rays, b, dsig_prop, self.proposals)
         dsig = torch.zeros((max(b.n_samples, 1), 4), dtype=torch.float32, device=self.device)
         _lib.call("vr_segment_bwd", _lib.ptr(b.t0), _lib.ptr(b.t1), _lib.ptr(sig_rgb),
                   _lib.ptr(b.offsets), _lib.ptr(b.ray_te), R, b.region_cnt, _lib.ptr(dpk),
                   _lib.ptr(dsig), s)
-        self.field_backward(rays, b, dsig)
+        # NeRF fields and proposals in one backward pipeline (the proposals' MLP backward
+        # overlaps the NeRF scatter on the side stream)
+        jobs = [(self.fields, dsig)]
+        if interlevel:
+            jobs.append((self.proposals, dsig_prop))
+        self.field_backward_jobs(rays, b, jobs)
         return loss, out, b
 
     def _sample_protocol_train(self, rays, tg, dt, lambda_dist, background):
