@@ -1,8 +1,10 @@
 // K4 (per-segment composite, fwd + analytic bwd) and K5 (global composite, fwd +
 // train fwd/bwd), plus the deterministic loss reduction and the Adam step.
 //
-// K4 — one warp per (region, ray) segment, 32 samples per step, warp-shuffle scans
-// with float64 carries.  Forward (composite_samples quadrature.py:141-165 and
+// K4 — grouped: one warp per 32 consecutive (region, ray) segments walks their contiguous
+// sample range 32 samples at a time with segmented float64 warp scans (segscan.cuh),
+// loading the next chunk while scanning the current one.  Forward (composite_samples
+// quadrature.py:141-165 and
 // aggregate_segment segrender.py:71-90):
 //   s_i = sigma_i * delta_i,  keep_i = exp(-s_i),  alpha_i = -expm1(-s_i)
 //   T_i = prod_{j<i} keep_j,  w_i = T_i alpha_i
@@ -29,50 +31,6 @@ namespace vr {
 constexpr int SEG_WARPS = 8;
 
 __device__ __forceinline__ float order_bits(int32_t first) { return __int_as_float(first); }
-
-struct SegTotals {
-  double T, C[3], A, D, L;
-};
-
-// Forward sweep over one segment; every lane returns the same totals.
-__device__ __forceinline__ SegTotals seg_forward(const double* __restrict__ t0,
-                                                 const double* __restrict__ t1,
-                                                 const float4* __restrict__ sr, int64_t b,
-                                                 int64_t e, double te, int lane) {
-  SegTotals tot = {1.0, {0.0, 0.0, 0.0}, 0.0, 0.0, 0.0};
-  for (int64_t i0 = b; i0 < e; i0 += 32) {
-    const int64_t i = i0 + lane;
-    double keep = 1.0, alpha = 0.0, m = 0.0;
-    float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
-    if (i < e) {
-      const double a = t0[i], bb = t1[i];
-      v = sr[i];
-      const double s = (double)v.x * (bb - a);
-      keep = exp(-s);
-      alpha = -expm1(-s);
-      m = sample_mid(a, bb) - te;
-    }
-    const double pincl = warp_incl_prod(keep, lane);
-    double pexcl = __shfl_up_sync(0xffffffffu, pincl, 1);
-    if (lane == 0) pexcl = 1.0;
-    const double Ti = tot.T * pexcl;
-    const double w = Ti * alpha;
-    const double wm = w * m;
-    const double aincl = warp_incl_sum(w, lane);
-    const double dincl = warp_incl_sum(wm, lane);
-    const double a_lt = tot.A + (aincl - w);
-    const double d_lt = tot.D + (dincl - wm);
-    const double lterm = w * (m * a_lt - d_lt);
-    tot.L += 2.0 * warp_sum(lterm);
-    tot.C[0] += warp_sum(w * (double)v.y);
-    tot.C[1] += warp_sum(w * (double)v.z);
-    tot.C[2] += warp_sum(w * (double)v.w);
-    tot.A += __shfl_sync(0xffffffffu, aincl, 31);
-    tot.D += __shfl_sync(0xffffffffu, dincl, 31);
-    tot.T *= __shfl_sync(0xffffffffu, pincl, 31);
-  }
-  return tot;
-}
 
 struct Carry {
   double T, A, D, L, C0, C1, C2, V;
@@ -306,92 +264,6 @@ __global__ void __launch_bounds__(SEG_WARPS * 32)
       cin.V = __shfl_sync(0xffffffffu, v_incl, 31);
     }
     __syncwarp();
-  }
-}
-
-__global__ void __launch_bounds__(SEG_WARPS * 32)
-    k_segment_fwd(const double* __restrict__ t0, const double* __restrict__ t1,
-                  const float4* __restrict__ sr, const int64_t* __restrict__ off,
-                  const int32_t* __restrict__ seg_first, const double* __restrict__ ray_te,
-                  int64_t n_rays, int64_t n_segs, float4* __restrict__ packets) {
-  const int lane = threadIdx.x & 31;
-  for (int64_t seg = (int64_t)blockIdx.x * SEG_WARPS + (threadIdx.x >> 5); seg < n_segs;
-       seg += (int64_t)gridDim.x * SEG_WARPS) {
-    const int64_t b = off[seg], e = off[seg + 1];
-    float4 p0, p1;
-    if (b == e) {
-      p0 = make_float4(1.f, 0.f, 0.f, 0.f);
-      p1 = make_float4(0.f, 0.f, 0.f, order_bits(INT32_MAX));
-    } else {
-      const double te = ray_te[seg % n_rays];
-      const SegTotals t = seg_forward(t0, t1, sr, b, e, te, lane);
-      p0 = make_float4((float)t.T, (float)t.C[0], (float)t.C[1], (float)t.C[2]);
-      p1 = make_float4((float)t.A, (float)t.D, (float)t.L, order_bits(seg_first[seg]));
-    }
-    if (lane == 0) {
-      packets[2 * seg] = p0;
-      packets[2 * seg + 1] = p1;
-    }
-  }
-}
-
-__global__ void __launch_bounds__(SEG_WARPS * 32)
-    k_segment_bwd(const double* __restrict__ t0, const double* __restrict__ t1,
-                  const float4* __restrict__ sr, const int64_t* __restrict__ off,
-                  const double* __restrict__ ray_te, int64_t n_rays, int64_t n_segs,
-                  const float4* __restrict__ dpk, float4* __restrict__ dsr) {
-  const int lane = threadIdx.x & 31;
-  for (int64_t seg = (int64_t)blockIdx.x * SEG_WARPS + (threadIdx.x >> 5); seg < n_segs;
-       seg += (int64_t)gridDim.x * SEG_WARPS) {
-    const int64_t b = off[seg], e = off[seg + 1];
-    if (b == e) continue;
-    const double te = ray_te[seg % n_rays];
-    const float4 g0 = dpk[2 * seg], g1 = dpk[2 * seg + 1];
-    const double bT = g0.x, bC0 = g0.y, bC1 = g0.z, bC2 = g0.w, bA = g1.x, bD = g1.y,
-                 bL = g1.z;
-    const SegTotals tot = seg_forward(t0, t1, sr, b, e, te, lane);
-    const double Vtot = bC0 * tot.C[0] + bC1 * tot.C[1] + bC2 * tot.C[2] + bA * tot.A +
-                        bD * tot.D + bL * 2.0 * tot.L;
-    // second sweep: per-sample gradients
-    double Tc = 1.0, Ac = 0.0, Dc = 0.0, Vc = 0.0;
-    for (int64_t i0 = b; i0 < e; i0 += 32) {
-      const int64_t i = i0 + lane;
-      double keep = 1.0, alpha = 0.0, m = 0.0, dlt = 0.0;
-      float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
-      if (i < e) {
-        const double a = t0[i], bb = t1[i];
-        v = sr[i];
-        dlt = bb - a;
-        const double s = (double)v.x * dlt;
-        keep = exp(-s);
-        alpha = -expm1(-s);
-        m = sample_mid(a, bb) - te;
-      }
-      const double pincl = warp_incl_prod(keep, lane);
-      double pexcl = __shfl_up_sync(0xffffffffu, pincl, 1);
-      if (lane == 0) pexcl = 1.0;
-      const double Ti = Tc * pexcl;
-      const double Tn = Tc * pincl;  // T_{j+1}
-      const double w = Ti * alpha;
-      const double wm = w * m;
-      const double aincl = warp_incl_sum(w, lane);
-      const double dincl = warp_incl_sum(wm, lane);
-      const double a_lt = Ac + (aincl - w), d_lt = Dc + (dincl - wm);
-      const double a_gt = tot.A - (Ac + aincl), d_gt = tot.D - (Dc + dincl);
-      const double g = 2.0 * (m * a_lt - d_lt + d_gt - m * a_gt);
-      const double vi = bC0 * v.y + bC1 * v.z + bC2 * v.w + bA + bD * m + bL * g;
-      const double wv = w * vi;
-      const double vincl = warp_incl_sum(wv, lane);
-      const double v_gt = Vtot - (Vc + vincl);
-      const double ds = -bT * tot.T + Tn * vi - v_gt;
-      if (i < e)
-        dsr[i] = make_float4((float)(ds * dlt), (float)(w * bC0), (float)(w * bC1),
-                             (float)(w * bC2));
-      Tc *= __shfl_sync(0xffffffffu, pincl, 31);
-      Ac += __shfl_sync(0xffffffffu, aincl, 31);
-      Dc += __shfl_sync(0xffffffffu, dincl, 31);
-      Vc += __shfl_sync(0xffffffffu, vincl, 31);
-    }
   }
 }
 
