@@ -95,8 +95,6 @@ def test_exchange_world2_matches_single_process(name):
     world = 2
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
-    procs = [ctx.Process(target=_worker, args=(r, world, _free_port() if False else None, name, q))
-             for r in range(0)]
     port = _free_port()
     procs = [ctx.Process(target=_worker, args=(r, world, port, name, q)) for r in range(world)]
     for p in procs:
@@ -120,3 +118,47 @@ def test_exchange_world2_matches_single_process(name):
     # the folded result equals the reference tile render of these rays
     np.testing.assert_allclose(ref_fold[:, 1], g["out"][:, 3], atol=1e-6)
     np.testing.assert_allclose(ref_fold[:, 3], g["out"][:, 5], atol=1e-6)
+
+
+def _sample_worker(rank, world, port, q):
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        from paper_2404_16221_b200 import comm
+
+        K = 4
+        bounds = [0, 5, 5, 17, 30]  # region-major sample offsets (region 1 empty)
+        full = torch.arange(30 * 4, dtype=torch.float32).reshape(30, 4) + 0.5
+        lo, cnt = comm.owned_regions(K, rank, world)
+        mine = torch.zeros_like(full)
+        mine[bounds[lo]:bounds[lo + cnt]] = full[bounds[lo]:bounds[lo + cnt]]
+        a = mine.clone()
+        got_all = comm.exchange_samples(a, bounds, K, dist.group.WORLD, world, rank, None)
+        g = mine.clone()
+        got_root = comm.exchange_samples(g, bounds, K, dist.group.WORLD, world, rank, 0)
+        q.put((rank, got_all, a.numpy(), got_root, g.numpy(), full.numpy()))
+    finally:
+        dist.destroy_process_group()
+
+
+def test_sample_exchange_world2():
+    """Sample-broadcast protocol exchange (comm.exchange_samples): every rank's region block
+    of the per-sample (sigma, rgb) array reaches every rank (training) or rank 0 (render)."""
+    world = 2
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_sample_worker, args=(r, world, port, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    results = [q.get(timeout=300) for _ in range(world)]
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    for rank, got_all, a, got_root, g, full in results:
+        assert got_all and np.array_equal(a, full)
+        if rank == 0:
+            assert got_root and np.array_equal(g, full)
+        else:
+            assert not got_root
