@@ -528,6 +528,8 @@ def main():
                            "samples_per_ray": n_samples / R, "regions": len(w.tree.leaves),
                            "regions_per_gpu": len(w.tree.leaves) // world, "log2_T": w.log2_T,
                            "dt": w.dt, "parallelism": f"region-parallel x{world}",
+                           "partition": (f"sample-balanced median splits (data/{w.partition})"
+                                         if w.partition != "grid" else "uniform grid"),
                            "l2": "inputs larger than L2 (tables+rays+samples >> 126 MB)",
                            "optimizer": "adam" if train else None,
                            "loss": (("mse+distortion+interlevel" if interlevel else

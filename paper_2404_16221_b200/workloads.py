@@ -6,17 +6,25 @@
   c4  8-region 4x2 city grid, root [0,16]x[0,16]x[0,1], 4M rays, T=2^22 per region
   c4  dt chosen for ~64 samples/ray (measured 64.7); c5 for ~128 (measured 129)
   c5  c4's tree, render-only 1920x1080 frame, ~128 samples/ray
+Partitions: the sample-balanced trees in data/ (scripts/make_trees.py: the reference's
+rays_to_points + build_tree recipe on a 4096-ray sample) — c3 stays a 1D strip along x,
+c4 a 4 x 2 arrangement of median splits; per-region samples max/mean 1.03 / 1.07 (uniform
+grids: 1.04 / 1.20), which bounds the parallel efficiency of the 8-GPU run.
 
 Seeds: rays default_rng(0), params seed 1 (+region), targets rng(2).
 """
 from __future__ import annotations
 
+import json
 from dataclasses import dataclass
+from pathlib import Path
 
 import numpy as np
 
 from .geometry import Aabb
 from .partition import grid_tree
+
+DATA = Path(__file__).resolve().parent / "data"
 
 
 @dataclass
@@ -33,8 +41,16 @@ class Workload:
     prop_log2_T: int = 17
     prop_max_res: int = 512
 
+    # "grid": uniform splits; a file name: a committed sample-balanced tree (data/, made
+    # by scripts/make_trees.py with the reference's rays_to_points + build_tree recipe)
+    partition: str = "grid"
+
     @property
     def tree(self):
+        if self.partition != "grid":
+            from .partition import tree_from_json
+
+            return tree_from_json(json.loads((DATA / self.partition).read_text()))
         return grid_tree(self.root, self.splits)
 
 
@@ -44,11 +60,12 @@ CONFIGS = {
     "c2": Workload("c2-two-region-4096rays-T2^14", Aabb([-1, -1, -1], [1, 1, 1]), "x", 4096, 14,
                    2.0 ** -5, 512),
     "c3": Workload("c3-street-8strip-1Mrays-T2^19", Aabb([0, 0, 0], [16, 1, 2]), "xxx", 1 << 20, 19,
-                   0.09),
+                   0.09, partition="c3_tree.json"),
     "c4": Workload("c4-city-4x2-4Mrays-T2^22", Aabb([0, 0, 0], [16, 16, 1]), "xyx", 1 << 22, 22,
-                   0.056, interlevel=1.0),
+                   0.056, interlevel=1.0, partition="c4_tree.json"),
+    # rendering uses the trained model's partition (c4's tree)
     "c5": Workload("c5-render-1080p-8region", Aabb([0, 0, 0], [16, 16, 1]), "xyx", 1920 * 1080, 22,
-                   0.028, train=False),
+                   0.028, train=False, partition="c4_tree.json"),
 }
 
 
