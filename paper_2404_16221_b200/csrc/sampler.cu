@@ -14,6 +14,13 @@
 // Regions are contiguous along a ray (each leaf is an intersection of half-spaces
 // whose predicates are monotone in t), so a sample's slot inside its segment is
 // (index along the ray) - (index of the segment's first sample).
+//
+// Multi-rank: a rank owning a block of regions only walks the bins that can hold its own
+// samples.  Rays missing the (slightly inflated) bounding box of its regions are skipped
+// after the root slab test; for the others, the bins before the box are only counted (no
+// owner lookup), so every sample keeps its global index along the ray and the result is
+// bit-identical to sampling all regions and keeping the own ones.  (Callers asking for
+// ray_part / ray_total — the reference's CommStats — get the full walk.)
 #include <cub/device/device_scan.cuh>
 #include <cub/iterator/transform_input_iterator.cuh>
 
@@ -32,9 +39,10 @@ struct K1Smem {
   int first[K1_WARPS][VR_MAX_REGIONS];
   int64_t off[K1_WARPS][VR_MAX_REGIONS];
   int64_t end[K1_WARPS][VR_MAX_REGIONS];
+  double own_mn[3], own_mx[3];  // inflated bounding box of the rank's regions
 };
 
-template <bool FILL>
+template <bool FILL, bool RESTRICT>
 __global__ void __launch_bounds__(K1_WARPS * 32)
     k_sample(const VrTree tree_param, const double* __restrict__ rays, int64_t stride,
              int64_t n_rays, double dt, int region_lo, int region_cnt, int32_t* counts,
@@ -49,6 +57,19 @@ __global__ void __launch_bounds__(K1_WARPS * 32)
   }
   __syncthreads();
   const VrTree& tree = sm.tree;
+  constexpr bool restrict_own = RESTRICT;  // host: no ray_part / ray_total, not all regions
+  if (RESTRICT && threadIdx.x < 3) {  // bounding box of the own regions, inflated far beyond rounding
+    const int a = threadIdx.x;
+    double mn = INFINITY, mx = -INFINITY;
+    for (int k = region_lo; k < region_lo + region_cnt; ++k) {
+      mn = fmin(mn, tree.leaf_mn[k][a]);
+      mx = fmax(mx, tree.leaf_mx[k][a]);
+    }
+    const double pad = 1e-9 * (1.0 + fmax(fabs(mn), fabs(mx)));
+    sm.own_mn[a] = mn - pad;
+    sm.own_mx[a] = mx + pad;
+  }
+  __syncthreads();
   const int lane = threadIdx.x & 31;
   const int warp = threadIdx.x >> 5;
   const int n_leaves = tree.n_leaves;
@@ -61,6 +82,19 @@ __global__ void __launch_bounds__(K1_WARPS * 32)
     const RayD ray = load_ray(rays, stride, r);
     double te, tx;
     const bool hit = ray_box(ray, tree.root_mn, tree.root_mx, te, tx);
+    double ta = te, tb = tx;  // t range that can hold own samples
+    const bool own_hit = !restrict_own || ray_box(ray, sm.own_mn, sm.own_mx, ta, tb);
+    if (!own_hit) {  // no own sample on this ray
+      if (!FILL) {
+        if (lane < region_cnt) {
+          const int64_t idx = (int64_t)lane * n_rays + r;
+          counts[idx] = 0;
+          seg_first[idx] = INT32_MAX;
+        }
+        if (lane == 0) ray_te[r] = hit ? te : 0.0;
+      }
+      continue;
+    }
 
     // --- leaf boxes: participation mask and candidate cut distances --------------
     uint32_t part = 0;
@@ -126,13 +160,13 @@ __global__ void __launch_bounds__(K1_WARPS * 32)
         const int64_t n = (int64_t)floor(q);
         const double e_n = dadd(te, dmul((double)n, dt));
         const int64_t nb = (dsub(tx, e_n) > VR_SLIVER) ? n + 1 : n;  // append tx / replace
-        int carry = 0;
-        for (int64_t c0 = 0; c0 < nb; c0 += 32) {
-          const int64_t k = c0 + lane;
-          double t0 = 0.0, t1 = 0.0;
-          int i0 = 0, i1 = 0;
+        // bin k: edges (t0, t1), its inner cuts cut[i0 .. i1) and its piece count
+        auto bin_pieces = [&](int64_t k, int64_t k_end, double& t0, double& t1, int& i0,
+                              int& i1) {
           int ne = 0;
-          if (k < nb) {
+          t0 = t1 = 0.0;
+          i0 = i1 = 0;
+          if (k < k_end) {
             t0 = (k == nb) ? tx : dadd(te, dmul((double)k, dt));
             t1 = (k + 1 == nb) ? tx : dadd(te, dmul((double)(k + 1), dt));
             if (dsub(t1, t0) > VR_SLIVER) {
@@ -148,6 +182,26 @@ __global__ void __launch_bounds__(K1_WARPS * 32)
               }
             }
           }
+          return ne;
+        };
+        // bins that can hold own samples (conservative); earlier bins are only counted
+        int64_t k_begin = 0, k_end = nb;
+        if (restrict_own) {
+          k_begin = max((int64_t)0, (int64_t)floor(ddiv(dsub(ta, te), dt)) - 1);
+          k_end = min(nb, (int64_t)floor(ddiv(dsub(tb, te), dt)) + 2);
+        }
+        int carry = 0;
+        for (int64_t c0 = 0; c0 < k_begin; c0 += 32) {
+          double t0, t1;
+          int i0, i1;
+          const int ne = bin_pieces(c0 + lane, k_begin, t0, t1, i0, i1);
+          carry += __reduce_add_sync(0xffffffffu, ne);
+        }
+        for (int64_t c0 = k_begin; c0 < k_end; c0 += 32) {
+          const int64_t k = c0 + lane;
+          double t0, t1;
+          int i0, i1;
+          const int ne = bin_pieces(k, k_end, t0, t1, i0, i1);
           const int incl = warp_incl_sum_i(ne, lane);
           int gidx = carry + incl - ne;
           carry += __shfl_sync(0xffffffffu, incl, 31);
@@ -254,9 +308,16 @@ extern "C" int vr_sample_count(const VrTree* tree, const double* rays, int64_t s
   }
   if (n_rays == 0) return VR_OK;
   const int grid = grid_for(ceil_div(n_rays, K1_WARPS), 1, 16);
-  k_sample<false><<<grid, K1_WARPS * 32, 0, (cudaStream_t)stream>>>(
-      *tree, rays, stride, n_rays, dt, region_lo, region_cnt, counts, seg_first, ray_te,
-      ray_part, ray_total, nullptr, nullptr, nullptr, nullptr, err);
+  const bool restrict_own = !ray_part && !ray_total &&
+                            !(region_lo == 0 && region_cnt == tree->n_leaves);
+  if (restrict_own)
+    k_sample<false, true><<<grid, K1_WARPS * 32, 0, (cudaStream_t)stream>>>(
+        *tree, rays, stride, n_rays, dt, region_lo, region_cnt, counts, seg_first, ray_te,
+        ray_part, ray_total, nullptr, nullptr, nullptr, nullptr, err);
+  else
+    k_sample<false, false><<<grid, K1_WARPS * 32, 0, (cudaStream_t)stream>>>(
+        *tree, rays, stride, n_rays, dt, region_lo, region_cnt, counts, seg_first, ray_te,
+        ray_part, ray_total, nullptr, nullptr, nullptr, nullptr, err);
   return check_launch("vr_sample_count");
 }
 
@@ -271,9 +332,18 @@ extern "C" int vr_sample_fill(const VrTree* tree, const double* rays, int64_t st
   }
   if (n_rays == 0) return VR_OK;
   const int grid = grid_for(ceil_div(n_rays, K1_WARPS), 1, 16);
-  k_sample<true><<<grid, K1_WARPS * 32, 0, (cudaStream_t)stream>>>(
-      *tree, rays, stride, n_rays, dt, region_lo, region_cnt, nullptr,
-      const_cast<int32_t*>(seg_first), nullptr, nullptr, nullptr, offsets, t0, t1, ray_id, err);
+  // the fill walks the same bins as the count (restricted unless all regions are owned;
+  // the counts of a restricted count pass are exactly the full walk's)
+  if (!(region_lo == 0 && region_cnt == tree->n_leaves))
+    k_sample<true, true><<<grid, K1_WARPS * 32, 0, (cudaStream_t)stream>>>(
+        *tree, rays, stride, n_rays, dt, region_lo, region_cnt, nullptr,
+        const_cast<int32_t*>(seg_first), nullptr, nullptr, nullptr, offsets, t0, t1, ray_id,
+        err);
+  else
+    k_sample<true, false><<<grid, K1_WARPS * 32, 0, (cudaStream_t)stream>>>(
+        *tree, rays, stride, n_rays, dt, region_lo, region_cnt, nullptr,
+        const_cast<int32_t*>(seg_first), nullptr, nullptr, nullptr, offsets, t0, t1, ray_id,
+        err);
   return check_launch("vr_sample_fill");
 }
 

@@ -150,8 +150,12 @@ class VolumePool:
         return self._ws
 
     # ---- K1 ----------------------------------------------------------------------------
-    def sample(self, rays: torch.Tensor, dt: float, all_regions: bool = False) -> SampleBatch:
-        """K1 for the owned regions (or every region: sample-broadcast protocol)."""
+    def sample(self, rays: torch.Tensor, dt: float, all_regions: bool = False,
+               stats: bool = False) -> SampleBatch:
+        """K1 for the owned regions (or every region: sample-broadcast protocol).  stats:
+        also the per-ray participation masks and sample totals (reference CommStats) —
+        this makes the kernel walk every ray entirely; without it a rank skips the rays and
+        bins that cannot reach its regions."""
         if not dt > 0.0:
             raise ValueError("dt must be > 0")
         R = rays.shape[1]
@@ -162,8 +166,9 @@ class VolumePool:
         counts = torch.empty(cnt * R, dtype=torch.int32, device=dev)
         seg_first = torch.empty(cnt * R, dtype=torch.int32, device=dev)
         ray_te = torch.empty(R, dtype=torch.float64, device=dev)
-        ray_part = torch.empty(R, dtype=torch.int32, device=dev)
-        ray_total = torch.empty(R, dtype=torch.int32, device=dev)
+        full = stats or all_regions
+        ray_part = torch.empty(R, dtype=torch.int32, device=dev) if full else None
+        ray_total = torch.empty(R, dtype=torch.int32, device=dev) if full else None
         tc = _lib.addr(self.tree_c)
         _lib.call("vr_sample_count", tc, _lib.ptr(rays), rays.shape[1], R, float(dt),
                   region_lo, cnt, _lib.ptr(counts), _lib.ptr(seg_first), _lib.ptr(ray_te),
@@ -292,7 +297,7 @@ class VolumePool:
 
     # ---- entry points ------------------------------------------------------------------
     def render_rays(self, rays, dt: float, background=None, clip: bool = True,
-                    protocol: str = "tile"):
+                    protocol: str = "tile", stats: bool = False):
         """Batched render.  Returns (out [7][R] on rank 0 / None elsewhere, batch);
         out rows: r, g, b (C + T*bg clipped, or raw C if clip=False), alpha, depth, T, L.
         protocol: "tile" (segment packets, the NeRF-XL path), "sample" (per-sample
@@ -306,7 +311,7 @@ class VolumePool:
             _, ray_off, (t0r, t1r, srr) = res
             pk = self._whole_ray_packets(b, ray_off, t0r, t1r, srr)
             return self.compose(pk, b, background, clip), b
-        b = self.sample(rays, dt)
+        b = self.sample(rays, dt, stats=stats)
         sig_rgb = self.evaluate(rays, b)
         local = self.local_packets(b, sig_rgb)
         allp = comm.gather_packets(local, self.group, self.world, self.rank)
@@ -531,7 +536,7 @@ def render_ray(pool: VolumePool, ray: Ray, protocol: str, dt: float, rng=None,
     if pool.num_workers == 0:
         raise ProtocolMismatchError("worker pool is empty")
     protocol = canonical_protocol(protocol)
-    out, b = pool.render_rays(rays_to_soa([ray]), dt, clip=False, protocol=protocol)
+    out, b = pool.render_rays(rays_to_soa([ray]), dt, clip=False, protocol=protocol, stats=True)
     st = pool.comm_stats(b, broadcast_all, protocol)
     if out is None:
         return None, st
@@ -548,7 +553,8 @@ def render_image(pool: VolumePool, camera: Camera, protocol: str, dt: float, bac
     protocol = canonical_protocol(protocol)
     t0 = time.perf_counter()
     rays = camera_rays(camera, pool.tree.root_box)
-    out, b = pool.render_rays(rays, dt, background=background, clip=True, protocol=protocol)
+    out, b = pool.render_rays(rays, dt, background=background, clip=True, protocol=protocol,
+                              stats=True)
     st = pool.comm_stats(b, broadcast_all, protocol)
     if out is None:
         return None, st
