@@ -190,12 +190,28 @@ __global__ void __launch_bounds__(K1_WARPS * 32)
           k_begin = max((int64_t)0, (int64_t)floor(ddiv(dsub(ta, te), dt)) - 1);
           k_end = min(nb, (int64_t)floor(ddiv(dsub(tb, te), dt)) + 2);
         }
+        // pieces before bin k_begin: every bin is longer than a sliver, so it holds one
+        // piece plus (pieces - 1) extra where cuts fall strictly inside it — count those
+        // bins only (lane per cut, the bin's first inner cut does it), O(cuts) not O(bins)
         int carry = 0;
-        for (int64_t c0 = 0; c0 < k_begin; c0 += 32) {
-          double t0, t1;
-          int i0, i1;
-          const int ne = bin_pieces(c0 + lane, k_begin, t0, t1, i0, i1);
-          carry += __reduce_add_sync(0xffffffffu, ne);
+        if (k_begin > 0) {
+          const double e_begin = (k_begin >= nb) ? tx : dadd(te, dmul((double)k_begin, dt));
+          int extra = 0;
+          for (int s = lane; s < ncut; s += 32) {
+            const double c = cut[s];
+            if (!(c < e_begin)) continue;
+            auto edge = [&](int64_t k) { return (k >= nb) ? tx : dadd(te, dmul((double)k, dt)); };
+            int64_t k = (int64_t)floor(ddiv(dsub(c, te), dt));
+            k = max((int64_t)0, min(k, nb - 1));
+            while (k > 0 && edge(k) > c) --k;
+            while (k + 1 < nb && !(edge(k + 1) > c)) ++k;  // edge(k) <= c < edge(k + 1)
+            if (!(edge(k) < c)) continue;                    // on an edge: no split
+            if (s > 0 && cut[s - 1] > edge(k)) continue;     // not the bin's first inner cut
+            double t0, t1;
+            int i0, i1;
+            extra += bin_pieces(k, nb, t0, t1, i0, i1) - 1;
+          }
+          carry = (int)k_begin + __reduce_add_sync(0xffffffffu, extra);
         }
         for (int64_t c0 = k_begin; c0 < k_end; c0 += 32) {
           const int64_t k = c0 + lane;
