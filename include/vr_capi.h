@@ -149,10 +149,14 @@ int vr_scan_offsets(const int32_t* counts_dev, int64_t n, int64_t* offsets_dev,
                     void* workspace_dev, size_t workspace_bytes, void* stream);
 /* Fill pass: writes each owned sample's bin edges t0/t1 (float64, bit-exact with
  * the reference) and its ray index into the slots given by offsets. */
+/* capacity: entries of t0/t1/ray_id; samples at positions >= capacity are dropped and
+ * raise VR_FLAG_OVERFLOW (an asynchronous fill into a buffer sized before the count is
+ * known; the caller compares the total with the capacity). */
 int vr_sample_fill(const VrTree* tree, const double* rays_dev, int64_t ray_stride,
                    int64_t n_rays, double dt, int32_t region_lo, int32_t region_cnt,
                    const int64_t* offsets_dev, const int32_t* seg_first_dev, double* t0_dev,
-                   double* t1_dev, int32_t* ray_id_dev, int32_t* err_dev, void* stream);
+                   double* t1_dev, int32_t* ray_id_dev, int64_t capacity, int32_t* err_dev,
+                   void* stream);
 /* Owner lookup of arbitrary points (locate_many, partitioner.py:177-192). */
 int vr_locate(const VrTree* tree, const double* pts_dev /*[n][3]*/, int64_t n,
               int32_t* tile_dev, int32_t* err_dev, void* stream);

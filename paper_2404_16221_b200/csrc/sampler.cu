@@ -48,7 +48,7 @@ __global__ void __launch_bounds__(K1_WARPS * 32)
              int64_t n_rays, double dt, int region_lo, int region_cnt, int32_t* counts,
              int32_t* seg_first, double* ray_te, uint32_t* ray_part, int32_t* ray_total,
              const int64_t* __restrict__ offsets, double* t0o, double* t1o, int32_t* rido,
-             int32_t* err) {
+             int64_t capacity, int32_t* err) {
   __shared__ K1Smem sm;
   {
     const uint64_t* src = reinterpret_cast<const uint64_t*>(&tree_param);
@@ -239,7 +239,7 @@ __global__ void __launch_bounds__(K1_WARPS * 32)
                     atomicMin(&sm.first[warp][kk], gidx);
                   } else {
                     const int64_t pos = sm.off[warp][kk] + (int64_t)(gidx - sm.first[warp][kk]);
-                    if (pos >= sm.off[warp][kk] && pos < sm.end[warp][kk]) {
+                    if (pos >= sm.off[warp][kk] && pos < sm.end[warp][kk] && pos < capacity) {
                       t0o[pos] = a;
                       t1o[pos] = b;
                       rido[pos] = (int32_t)r;
@@ -329,18 +329,19 @@ extern "C" int vr_sample_count(const VrTree* tree, const double* rays, int64_t s
   if (restrict_own)
     k_sample<false, true><<<grid, K1_WARPS * 32, 0, (cudaStream_t)stream>>>(
         *tree, rays, stride, n_rays, dt, region_lo, region_cnt, counts, seg_first, ray_te,
-        ray_part, ray_total, nullptr, nullptr, nullptr, nullptr, err);
+        ray_part, ray_total, nullptr, nullptr, nullptr, nullptr, 0, err);
   else
     k_sample<false, false><<<grid, K1_WARPS * 32, 0, (cudaStream_t)stream>>>(
         *tree, rays, stride, n_rays, dt, region_lo, region_cnt, counts, seg_first, ray_te,
-        ray_part, ray_total, nullptr, nullptr, nullptr, nullptr, err);
+        ray_part, ray_total, nullptr, nullptr, nullptr, nullptr, 0, err);
   return check_launch("vr_sample_count");
 }
 
 extern "C" int vr_sample_fill(const VrTree* tree, const double* rays, int64_t stride,
                               int64_t n_rays, double dt, int32_t region_lo, int32_t region_cnt,
                               const int64_t* offsets, const int32_t* seg_first, double* t0,
-                              double* t1, int32_t* ray_id, int32_t* err, void* stream) {
+                              double* t1, int32_t* ray_id, int64_t capacity, int32_t* err,
+                              void* stream) {
   if (!valid_tree(tree) || !(dt > 0.0) || region_lo < 0 || region_cnt < 1 ||
       region_lo + region_cnt > tree->n_leaves || n_rays < 0 || !err) {
     set_error("vr_sample_fill: bad argument");
@@ -354,12 +355,12 @@ extern "C" int vr_sample_fill(const VrTree* tree, const double* rays, int64_t st
     k_sample<true, true><<<grid, K1_WARPS * 32, 0, (cudaStream_t)stream>>>(
         *tree, rays, stride, n_rays, dt, region_lo, region_cnt, nullptr,
         const_cast<int32_t*>(seg_first), nullptr, nullptr, nullptr, offsets, t0, t1, ray_id,
-        err);
+        capacity, err);
   else
     k_sample<true, false><<<grid, K1_WARPS * 32, 0, (cudaStream_t)stream>>>(
         *tree, rays, stride, n_rays, dt, region_lo, region_cnt, nullptr,
         const_cast<int32_t*>(seg_first), nullptr, nullptr, nullptr, offsets, t0, t1, ray_id,
-        err);
+        capacity, err);
   return check_launch("vr_sample_fill");
 }
 

@@ -187,9 +187,91 @@ class VolumePool:
         if N:
             _lib.call("vr_sample_fill", tc, _lib.ptr(rays), rays.shape[1], R, float(dt),
                       region_lo, cnt, _lib.ptr(offsets), _lib.ptr(seg_first), _lib.ptr(t0),
-                      _lib.ptr(t1), _lib.ptr(ray_id), _lib.ptr(self.err), s)
+                      _lib.ptr(t1), _lib.ptr(ray_id), N, _lib.ptr(self.err), s)
         return SampleBatch(R, region_lo, cnt, counts, seg_first, offsets, ray_te, ray_part,
                            ray_total, t0, t1, ray_id, [int(b) for b in bounds])
+
+    # ---- K1 one step ahead --------------------------------------------------------------
+    # Sampling depends only on the rays, not on the parameters, so the next batch's K1 can
+    # run on its own stream while this step's field kernels run (K1 is fp64/ALU-latency
+    # bound, the hash-grid kernels L2-bound).  The fill goes into buffers sized from the
+    # previous batch; a batch that does not fit is re-filled synchronously.
+    def _k1_stream(self):
+        if getattr(self, "_k1", None) is None:
+            self._k1 = torch.cuda.Stream(device=self.device)
+        return self._k1
+
+    def sample_async(self, rays: torch.Tensor, dt: float, capacity: int, ready=None):
+        """Enqueue K1 for the owned regions of ``rays`` on the sampling stream (after the
+        current stream's work and the optional event ``ready``, e.g. the rays' H2D copy);
+        returns a pending batch for :meth:`resolve_sample`."""
+        if not dt > 0.0:
+            raise ValueError("dt must be > 0")
+        R = rays.shape[1]
+        lo, cnt = self.region_lo, self.region_cnt
+        dev = self.device
+        main = torch.cuda.current_stream()
+        k1 = self._k1_stream()
+        k1.wait_stream(main)
+        if ready is not None:
+            k1.wait_event(ready)
+        rays.record_stream(k1)
+        tc = _lib.addr(self.tree_c)
+        with torch.cuda.stream(k1):
+            s = _lib.stream_ptr()
+            err = torch.zeros(1, dtype=torch.int32, device=dev)
+            counts = torch.empty(cnt * R, dtype=torch.int32, device=dev)
+            seg_first = torch.empty(cnt * R, dtype=torch.int32, device=dev)
+            ray_te = torch.empty(R, dtype=torch.float64, device=dev)
+            _lib.call("vr_sample_count", tc, _lib.ptr(rays), R, R, float(dt), lo, cnt,
+                      _lib.ptr(counts), _lib.ptr(seg_first), _lib.ptr(ray_te), None, None,
+                      _lib.ptr(err), s)
+            offsets = torch.empty(cnt * R + 1, dtype=torch.int64, device=dev)
+            ws = torch.empty(int(_lib.load().vr_scan_workspace_bytes(cnt * R)), dtype=torch.uint8,
+                             device=dev)
+            _lib.call("vr_scan_offsets", _lib.ptr(counts), cnt * R, _lib.ptr(offsets),
+                      _lib.ptr(ws), ws.numel(), s)
+            bounds_dev = offsets[torch.arange(cnt + 1, device=dev) * R]
+            bounds_host = torch.empty(cnt + 1, dtype=torch.int64, pin_memory=True)
+            bounds_host.copy_(bounds_dev, non_blocking=True)
+            cap = max(int(capacity), 1)
+            t0 = torch.empty(cap, dtype=torch.float64, device=dev)
+            t1 = torch.empty(cap, dtype=torch.float64, device=dev)
+            ray_id = torch.empty(cap, dtype=torch.int32, device=dev)
+            _lib.call("vr_sample_fill", tc, _lib.ptr(rays), R, R, float(dt), lo, cnt,
+                      _lib.ptr(offsets), _lib.ptr(seg_first), _lib.ptr(t0), _lib.ptr(t1),
+                      _lib.ptr(ray_id), cap, _lib.ptr(err), s)
+            done = torch.cuda.Event()
+            done.record(k1)
+        return dict(rays=rays, dt=dt, R=R, counts=counts, seg_first=seg_first, ray_te=ray_te,
+                    offsets=offsets, bounds=bounds_host, t0=t0, t1=t1, ray_id=ray_id, err=err,
+                    cap=cap, done=done, tensors=(err, counts, seg_first, ray_te, offsets, ws,
+                                                 t0, t1, ray_id))
+
+    def resolve_sample(self, p) -> SampleBatch:
+        """The SampleBatch of a :meth:`sample_async` (waits for its K1)."""
+        main = torch.cuda.current_stream()
+        main.wait_event(p["done"])
+        for t in p["tensors"]:
+            t.record_stream(main)
+        p["done"].synchronize()  # the host needs the per-region sample totals
+        bounds = [int(x) for x in p["bounds"].tolist()]
+        N = bounds[-1]
+        cnt, R = self.region_cnt, p["R"]
+        t0, t1, ray_id = p["t0"], p["t1"], p["ray_id"]
+        flags = int(p["err"].item())
+        if N > p["cap"]:  # did not fit: fill again on this stream
+            flags &= ~_lib.VR_FLAG_OVERFLOW
+            t0 = torch.empty(N, dtype=torch.float64, device=self.device)
+            t1 = torch.empty(N, dtype=torch.float64, device=self.device)
+            ray_id = torch.empty(N, dtype=torch.int32, device=self.device)
+            _lib.call("vr_sample_fill", _lib.addr(self.tree_c), _lib.ptr(p["rays"]), R, R,
+                      float(p["dt"]), self.region_lo, cnt, _lib.ptr(p["offsets"]),
+                      _lib.ptr(p["seg_first"]), _lib.ptr(t0), _lib.ptr(t1), _lib.ptr(ray_id), N,
+                      _lib.ptr(self.err), self._stream())
+        _lib.raise_flags(flags, "in sampling")
+        return SampleBatch(R, self.region_lo, cnt, p["counts"], p["seg_first"], p["offsets"],
+                           p["ray_te"], None, None, t0, t1, ray_id, bounds)
 
     # ---- fields -------------------------------------------------------------------------
     def evaluate(self, rays: torch.Tensor, b: SampleBatch, fields=None) -> torch.Tensor:
@@ -364,7 +446,7 @@ class VolumePool:
 
     def loss_and_grad(self, rays, targets, dt: float, lambda_dist: float = 1.0,
                       background=None, lambda_interlevel: float = 0.0, eps: float = 1e-7,
-                      protocol: str = "tile"):
+                      protocol: str = "tile", batch: SampleBatch | None = None):
         """Forward + backward of the NeRF-XL loss (segrender.py:198-207 definition:
         sum over rays of |C + T*bg - target|^2 + lambda * distortion), plus, with
         proposal fields and lambda_interlevel > 0, the interlevel loss of csrc/interlevel.cu
@@ -382,7 +464,7 @@ class VolumePool:
             if lambda_interlevel > 0.0:
                 raise ValueError("the interlevel loss is defined on the tile protocol")
             return self._sample_protocol_train(rays, tg, dt, lambda_dist, background)
-        b = self.sample(rays, dt)
+        b = batch if batch is not None else self.sample(rays, dt)  # batch: sample_async
         sig_rgb = self.evaluate(rays, b)
         local = self.local_packets(b, sig_rgb)
         allp = comm.all_gather_packets(local, self.group, self.world)
@@ -457,11 +539,13 @@ class VolumePool:
 
     def train_step(self, rays, targets, dt: float, lr: float = 1e-2, step: int = 1,
                    lambda_dist: float = 1.0, background=None, lambda_interlevel: float = 0.0,
-                   protocol: str = "tile"):
-        """One training iteration: zero grads, fwd+bwd, Adam.  Returns the device loss."""
+                   protocol: str = "tile", batch: SampleBatch | None = None):
+        """One training iteration: zero grads, fwd+bwd, Adam.  Returns the device loss.
+        batch: the rays' samples from :meth:`sample_async` / :meth:`resolve_sample` (K1
+        prefetched during the previous step)."""
         self.zero_grad()
         loss, _, _ = self.loss_and_grad(rays, targets, dt, lambda_dist, background,
-                                        lambda_interlevel, protocol=protocol)
+                                        lambda_interlevel, protocol=protocol, batch=batch)
         for f in self.fields + (self.proposals or []):
             if f.trainable:
                 f.step(lr, step)

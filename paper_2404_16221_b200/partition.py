@@ -246,7 +246,7 @@ def _k1_all_leaves(tree: PartitionTree, rays, dt: float, device=None):
     if n:
         _lib.call("vr_sample_fill", _lib.addr(tc), _lib.ptr(r), R, R, float(dt), 0, K,
                   _lib.ptr(off), _lib.ptr(first), _lib.ptr(t0), _lib.ptr(t1), _lib.ptr(rid),
-                  _lib.ptr(err), s)
+                  n, _lib.ptr(err), s)
     # an out-of-root midpoint (rounding at a grazing exit) only matters to owner lookup
     flags = int(err.item()) & ~_lib.VR_FLAG_OOB
     _lib.raise_flags(flags, "in sampling")

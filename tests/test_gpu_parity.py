@@ -90,6 +90,26 @@ def test_sampler_bit_exact(name, world, stats):
                 assert sf[kk, r] == want
 
 
+@pytest.mark.parametrize("capacity", [1, None])
+def test_sample_async_matches_sample(capacity):
+    """K1 one step ahead (sample_async / resolve_sample on the sampling stream) gives the
+    same batch as sample(); a capacity below the sample count is re-filled."""
+    g = load_npz("sampler_three_blobs_k8.npz")
+    tree = vr.tree_from_json(g["tree"])
+    for rank, world in ((0, 1), (1, 2)):
+        pool = _pool(tree, rank=rank, world=world)
+        rd = pool.rays_to_device(_soa(g["rays"]))
+        ref = pool.sample(rd, float(g["dt"]))
+        cap = ref.n_samples if capacity is None else capacity
+        b = pool.resolve_sample(pool.sample_async(rd, float(g["dt"]), cap))
+        torch.cuda.synchronize()
+        assert b.region_bounds == ref.region_bounds
+        n = ref.n_samples
+        for a, c in ((b.t0, ref.t0), (b.t1, ref.t1), (b.ray_id, ref.ray_id)):
+            assert torch.equal(a[:n], c[:n])
+        assert torch.equal(b.seg_first, ref.seg_first) and torch.equal(b.offsets, ref.offsets)
+
+
 def test_sampler_empty_and_bad_args(cuda_device):
     g = load_npz("sampler_random_d2.npz")
     tree = vr.tree_from_json(g["tree"])
