@@ -157,6 +157,27 @@ int vr_sample_fill(const VrTree* tree, const double* rays_dev, int64_t ray_strid
                    const int64_t* offsets_dev, const int32_t* seg_first_dev, double* t0_dev,
                    double* t1_dev, int32_t* ray_id_dev, int64_t capacity, int32_t* err_dev,
                    void* stream);
+/* One walk instead of count + fill: vr_sample_stage is vr_sample_count that also writes
+ * every own sample's t0/t1 into staging buffers st0/st1 (stage_capacity entries, split in
+ * vr_sample_stage_blocks(n_rays) equal slices, one per CTA; a ray reserves one slot per
+ * walked bin plus one per cut); sslot_dev[r] locates the ray's staged samples.
+ * stage_info_dev (2 x uint64, zeroed by the caller) receives [0] += slots reserved and
+ * [1] = max slots one CTA needed: if [1] > stage_capacity / vr_sample_stage_blocks(n_rays)
+ * the staging is incomplete and the caller runs vr_sample_fill (the counts are exact
+ * either way).  After vr_scan_offsets, vr_sample_compact moves the staged samples to their
+ * slots (the same t0/t1/ray_id vr_sample_fill writes, bit for bit). */
+int64_t vr_sample_stage_blocks(int64_t n_rays);
+int vr_sample_stage(const VrTree* tree, const double* rays_dev, int64_t ray_stride,
+                    int64_t n_rays, double dt, int32_t region_lo, int32_t region_cnt,
+                    int32_t* counts_dev, int32_t* seg_first_dev, double* ray_te_dev,
+                    uint32_t* ray_part_dev, int32_t* ray_total_dev, double* st0_dev,
+                    double* st1_dev, int64_t stage_capacity, int64_t* sslot_dev,
+                    uint64_t* stage_info_dev, int32_t* err_dev, void* stream);
+int vr_sample_compact(int64_t n_rays, int32_t region_cnt, const int32_t* counts_dev,
+                      const int32_t* seg_first_dev, const int64_t* offsets_dev,
+                      const int64_t* sslot_dev, const double* st0_dev, const double* st1_dev,
+                      double* t0_dev, double* t1_dev, int32_t* ray_id_dev, int64_t capacity,
+                      int32_t* err_dev, void* stream);
 /* Owner lookup of arbitrary points (locate_many, partitioner.py:177-192). */
 int vr_locate(const VrTree* tree, const double* pts_dev /*[n][3]*/, int64_t n,
               int32_t* tile_dev, int32_t* err_dev, void* stream);

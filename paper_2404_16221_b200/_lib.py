@@ -111,6 +111,9 @@ SIGNATURES = {
     "vr_scan_workspace_bytes": [I64],
     "vr_scan_offsets": [P, I64, P, P, C.c_size_t, P],
     "vr_sample_fill": [P, P, I64, I64, F64, I32, I32, P, P, P, P, P, I64, P, P],
+    "vr_sample_stage_blocks": [I64],
+    "vr_sample_stage": [P, P, I64, I64, F64, I32, I32, P, P, P, P, P, P, P, I64, P, P, P, P],
+    "vr_sample_compact": [I64, I32, P, P, P, P, P, P, P, P, P, I64, P, P],
     "vr_locate": [P, P, I64, P, P, P],
     "vr_field_analytic_fwd": [P, P, I64, P, P, P, I64, P, P],
     "vr_voxel_fwd": [P, P, P, P, I64, P, P, P, I64, P, P],
@@ -143,6 +146,7 @@ SIGNATURES = {
     "vr_cast_f32_f16": [P, P, I64, P],
 }
 _RESTYPES = {"vr_last_error": C.c_char_p, "vr_scan_workspace_bytes": C.c_size_t,
+             "vr_sample_stage_blocks": C.c_int64,
              "vr_hash_bwd_workspace_bytes": C.c_size_t}
 
 _LIB = None

@@ -21,6 +21,14 @@
 // owner lookup), so every sample keeps its global index along the ray and the result is
 // bit-identical to sampling all regions and keeping the own ones.  (Callers asking for
 // ray_part / ray_total — the reference's CommStats — get the full walk.)
+//
+// One walk instead of two (vr_sample_stage + vr_sample_compact): the count pass also
+// writes every own piece into a staging buffer, in a slot range each ray reserves from
+// its block's slice before walking (at most one piece per walked bin plus one per cut);
+// after the scan of the counts a warp-per-ray copy moves the segments to their
+// region-major slots.  The staging traffic (16 B written + 16 B read per sample) is a
+// fraction of the second fp64 walk it replaces.  A block whose slice is too small reports
+// it and the caller runs the fill pass instead.
 #include <cub/device/device_scan.cuh>
 #include <cub/iterator/transform_input_iterator.cuh>
 
@@ -40,16 +48,23 @@ struct K1Smem {
   int64_t off[K1_WARPS][VR_MAX_REGIONS];
   int64_t end[K1_WARPS][VR_MAX_REGIONS];
   double own_mn[3], own_mx[3];  // inflated bounding box of the rank's regions
+  unsigned long long stage_top; // staging slots reserved by this block
 };
 
-template <bool FILL, bool RESTRICT>
+// STAGE (count pass only): also write the own pieces to st0/st1 — block b owns slots
+// [b * slice, (b + 1) * slice); sslot[r] + (index along the ray) is a piece's slot.
+// stage_info[0] += slots reserved, stage_info[1] = max over blocks (the slice needed).
+template <bool FILL, bool RESTRICT, bool STAGE>
 __global__ void __launch_bounds__(K1_WARPS * 32)
     k_sample(const VrTree tree_param, const double* __restrict__ rays, int64_t stride,
              int64_t n_rays, double dt, int region_lo, int region_cnt, int32_t* counts,
              int32_t* seg_first, double* ray_te, uint32_t* ray_part, int32_t* ray_total,
              const int64_t* __restrict__ offsets, double* t0o, double* t1o, int32_t* rido,
-             int64_t capacity, int32_t* err) {
+             int64_t capacity, int32_t* err, double* st0, double* st1, int64_t* sslot,
+             int64_t slice, unsigned long long* stage_info) {
+  static_assert(!(FILL && STAGE), "staging is part of the count pass");
   __shared__ K1Smem sm;
+  if (STAGE && threadIdx.x == 0) sm.stage_top = 0;
   {
     const uint64_t* src = reinterpret_cast<const uint64_t*>(&tree_param);
     uint64_t* dst = reinterpret_cast<uint64_t*>(&sm.tree);
@@ -194,6 +209,16 @@ __global__ void __launch_bounds__(K1_WARPS * 32)
         // piece plus (pieces - 1) extra where cuts fall strictly inside it — count those
         // bins only (lane per cut, the bin's first inner cut does it), O(cuts) not O(bins)
         int carry = 0;
+        // staging: reserve one slot per walked bin plus one per cut
+        int64_t stage_base = -1;
+        int64_t stage_n = 0;
+        if (STAGE) {
+          stage_n = (k_end > k_begin ? k_end - k_begin : 0) + ncut;
+          unsigned long long b = 0;
+          if (lane == 0) b = atomicAdd(&sm.stage_top, (unsigned long long)stage_n);
+          b = __shfl_sync(0xffffffffu, b, 0);
+          if ((int64_t)b + stage_n <= slice) stage_base = (int64_t)blockIdx.x * slice + (int64_t)b;
+        }
         if (k_begin > 0) {
           const double e_begin = (k_begin >= nb) ? tx : dadd(te, dmul((double)k_begin, dt));
           int extra = 0;
@@ -213,6 +238,8 @@ __global__ void __launch_bounds__(K1_WARPS * 32)
           }
           carry = (int)k_begin + __reduce_add_sync(0xffffffffu, extra);
         }
+        const int carry_begin = carry;
+        if (STAGE && lane == 0) sslot[r] = stage_base >= 0 ? stage_base - carry_begin : INT64_MIN / 2;
         for (int64_t c0 = k_begin; c0 < k_end; c0 += 32) {
           const int64_t k = c0 + lane;
           double t0, t1;
@@ -237,6 +264,15 @@ __global__ void __launch_bounds__(K1_WARPS * 32)
                   if (!FILL) {
                     atomicAdd(&sm.cnt[warp][kk], 1);
                     atomicMin(&sm.first[warp][kk], gidx);
+                    if (STAGE && stage_base >= 0) {
+                      const int64_t j = (int64_t)(gidx - carry_begin);
+                      if (j < stage_n) {
+                        st0[stage_base + j] = a;
+                        st1[stage_base + j] = b;
+                      } else {
+                        flags |= VR_FLAG_OVERFLOW;  // cannot happen: one piece per bin + cut
+                      }
+                    }
                   } else {
                     const int64_t pos = sm.off[warp][kk] + (int64_t)(gidx - sm.first[warp][kk]);
                     if (pos >= sm.off[warp][kk] && pos < sm.end[warp][kk] && pos < capacity) {
@@ -272,6 +308,74 @@ __global__ void __launch_bounds__(K1_WARPS * 32)
       }
     }
     __syncwarp();
+  }
+  flags = (int)__reduce_or_sync(0xffffffffu, (unsigned)flags);
+  if (flags && lane == 0) atomicOr(err, flags);
+  if (STAGE) {
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      atomicAdd(&stage_info[0], sm.stage_top);
+      atomicMax(&stage_info[1], sm.stage_top);
+    }
+  }
+}
+
+// Staged pieces -> region-major slots: warp per ray.  A ray's staged samples are ordered
+// along the ray and each own segment is a contiguous run of them, so the lanes walk the
+// staged range 32 samples at a time and look up each sample's segment among the ray's
+// non-empty ones (lane kk holds segment kk's first index, count and output offset).
+// Rays with more than 32 own regions take the region loop below.
+__global__ void __launch_bounds__(256)
+    k_sample_compact(int64_t n_rays, int region_cnt, const int32_t* __restrict__ counts,
+                     const int32_t* __restrict__ seg_first, const int64_t* __restrict__ offsets,
+                     const int64_t* __restrict__ sslot, const double* __restrict__ st0,
+                     const double* __restrict__ st1, double* t0o, double* t1o, int32_t* rido,
+                     int64_t capacity, int32_t* err) {
+  const int lane = threadIdx.x & 31;
+  const int64_t warps = (int64_t)gridDim.x * (blockDim.x >> 5);
+  int flags = 0;
+  for (int64_t r = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5; r < n_rays; r += warps) {
+    for (int k0 = 0; k0 < region_cnt; k0 += 32) {
+      const int kk = k0 + lane;
+      const int64_t idx = (int64_t)kk * n_rays + r;
+      const int c = kk < region_cnt ? counts[idx] : 0;
+      const unsigned live = __ballot_sync(0xffffffffu, c > 0);
+      if (!live) continue;
+      const int64_t base = sslot[r];
+      if (base <= INT64_MIN / 4) {  // the ray was not staged (base itself may be negative)
+        flags |= VR_FLAG_OVERFLOW;
+        break;
+      }
+      int first = INT32_MAX, last = 0;
+      int64_t dst = 0;
+      if (c > 0) {
+        first = seg_first[idx];
+        last = first + c;
+        dst = offsets[idx];
+      }
+      const int g_lo = __reduce_min_sync(0xffffffffu, (unsigned)first);
+      const int g_hi = (int)__reduce_max_sync(0xffffffffu, (unsigned)last);
+      for (int g0 = g_lo; g0 < g_hi; g0 += 32) {
+        const int g = g0 + lane;
+        int64_t d = -1;
+        for (unsigned m = live; m; m &= m - 1) {
+          const int l = __ffs(m) - 1;
+          const int f = __shfl_sync(0xffffffffu, first, l);
+          const int e = __shfl_sync(0xffffffffu, last, l);
+          const int64_t o = __shfl_sync(0xffffffffu, dst, l);
+          if (g >= f && g < e) d = o + (g - f);
+        }
+        if (d >= 0) {
+          if (d < capacity) {
+            t0o[d] = st0[base + g];
+            t1o[d] = st1[base + g];
+            rido[d] = (int32_t)r;
+          } else {
+            flags |= VR_FLAG_OVERFLOW;
+          }
+        }
+      }
+    }
   }
   flags = (int)__reduce_or_sync(0xffffffffu, (unsigned)flags);
   if (flags && lane == 0) atomicOr(err, flags);
@@ -327,14 +431,67 @@ extern "C" int vr_sample_count(const VrTree* tree, const double* rays, int64_t s
   const bool restrict_own = !ray_part && !ray_total &&
                             !(region_lo == 0 && region_cnt == tree->n_leaves);
   if (restrict_own)
-    k_sample<false, true><<<grid, K1_WARPS * 32, 0, (cudaStream_t)stream>>>(
+    k_sample<false, true, false><<<grid, K1_WARPS * 32, 0, (cudaStream_t)stream>>>(
         *tree, rays, stride, n_rays, dt, region_lo, region_cnt, counts, seg_first, ray_te,
-        ray_part, ray_total, nullptr, nullptr, nullptr, nullptr, 0, err);
+        ray_part, ray_total, nullptr, nullptr, nullptr, nullptr, 0, err, nullptr, nullptr,
+        nullptr, 0, nullptr);
   else
-    k_sample<false, false><<<grid, K1_WARPS * 32, 0, (cudaStream_t)stream>>>(
+    k_sample<false, false, false><<<grid, K1_WARPS * 32, 0, (cudaStream_t)stream>>>(
         *tree, rays, stride, n_rays, dt, region_lo, region_cnt, counts, seg_first, ray_te,
-        ray_part, ray_total, nullptr, nullptr, nullptr, nullptr, 0, err);
+        ray_part, ray_total, nullptr, nullptr, nullptr, nullptr, 0, err, nullptr, nullptr,
+        nullptr, 0, nullptr);
   return check_launch("vr_sample_count");
+}
+
+extern "C" int64_t vr_sample_stage_blocks(int64_t n_rays) {
+  return n_rays > 0 ? grid_for(ceil_div(n_rays, K1_WARPS), 1, 16) : 0;
+}
+
+extern "C" int vr_sample_stage(const VrTree* tree, const double* rays, int64_t stride,
+                               int64_t n_rays, double dt, int32_t region_lo, int32_t region_cnt,
+                               int32_t* counts, int32_t* seg_first, double* ray_te,
+                               uint32_t* ray_part, int32_t* ray_total, double* st0, double* st1,
+                               int64_t stage_capacity, int64_t* sslot, uint64_t* stage_info,
+                               int32_t* err, void* stream) {
+  if (!valid_tree(tree) || !(dt > 0.0) || region_lo < 0 || region_cnt < 1 ||
+      region_lo + region_cnt > tree->n_leaves || n_rays < 0 || !err || !stage_info ||
+      stage_capacity < 0 || (n_rays > 0 && (!st0 || !st1 || !sslot))) {
+    set_error("vr_sample_stage: bad argument");
+    return VR_ERR_BAD_ARG;
+  }
+  if (n_rays == 0) return VR_OK;
+  const int grid = (int)vr_sample_stage_blocks(n_rays);
+  const int64_t slice = stage_capacity / grid;
+  const bool restrict_own = !ray_part && !ray_total &&
+                            !(region_lo == 0 && region_cnt == tree->n_leaves);
+  auto* info = reinterpret_cast<unsigned long long*>(stage_info);
+  if (restrict_own)
+    k_sample<false, true, true><<<grid, K1_WARPS * 32, 0, (cudaStream_t)stream>>>(
+        *tree, rays, stride, n_rays, dt, region_lo, region_cnt, counts, seg_first, ray_te,
+        ray_part, ray_total, nullptr, nullptr, nullptr, nullptr, 0, err, st0, st1, sslot, slice,
+        info);
+  else
+    k_sample<false, false, true><<<grid, K1_WARPS * 32, 0, (cudaStream_t)stream>>>(
+        *tree, rays, stride, n_rays, dt, region_lo, region_cnt, counts, seg_first, ray_te,
+        ray_part, ray_total, nullptr, nullptr, nullptr, nullptr, 0, err, st0, st1, sslot, slice,
+        info);
+  return check_launch("vr_sample_stage");
+}
+
+extern "C" int vr_sample_compact(int64_t n_rays, int32_t region_cnt, const int32_t* counts,
+                                 const int32_t* seg_first, const int64_t* offsets,
+                                 const int64_t* sslot, const double* st0, const double* st1,
+                                 double* t0, double* t1, int32_t* ray_id, int64_t capacity,
+                                 int32_t* err, void* stream) {
+  if (n_rays < 0 || region_cnt < 1 || !err) {
+    set_error("vr_sample_compact: bad argument");
+    return VR_ERR_BAD_ARG;
+  }
+  if (n_rays == 0) return VR_OK;
+  k_sample_compact<<<grid_for(n_rays, 8), 256, 0, (cudaStream_t)stream>>>(
+      n_rays, region_cnt, counts, seg_first, offsets, sslot, st0, st1, t0, t1, ray_id, capacity,
+      err);
+  return check_launch("vr_sample_compact");
 }
 
 extern "C" int vr_sample_fill(const VrTree* tree, const double* rays, int64_t stride,
@@ -352,15 +509,15 @@ extern "C" int vr_sample_fill(const VrTree* tree, const double* rays, int64_t st
   // the fill walks the same bins as the count (restricted unless all regions are owned;
   // the counts of a restricted count pass are exactly the full walk's)
   if (!(region_lo == 0 && region_cnt == tree->n_leaves))
-    k_sample<true, true><<<grid, K1_WARPS * 32, 0, (cudaStream_t)stream>>>(
+    k_sample<true, true, false><<<grid, K1_WARPS * 32, 0, (cudaStream_t)stream>>>(
         *tree, rays, stride, n_rays, dt, region_lo, region_cnt, nullptr,
         const_cast<int32_t*>(seg_first), nullptr, nullptr, nullptr, offsets, t0, t1, ray_id,
-        capacity, err);
+        capacity, err, nullptr, nullptr, nullptr, 0, nullptr);
   else
-    k_sample<true, false><<<grid, K1_WARPS * 32, 0, (cudaStream_t)stream>>>(
+    k_sample<true, false, false><<<grid, K1_WARPS * 32, 0, (cudaStream_t)stream>>>(
         *tree, rays, stride, n_rays, dt, region_lo, region_cnt, nullptr,
         const_cast<int32_t*>(seg_first), nullptr, nullptr, nullptr, offsets, t0, t1, ray_id,
-        capacity, err);
+        capacity, err, nullptr, nullptr, nullptr, 0, nullptr);
   return check_launch("vr_sample_fill");
 }
 

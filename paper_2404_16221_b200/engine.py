@@ -111,6 +111,9 @@ class VolumePool:
         # traffic queues behind the scatter's atomics either way, and the fused kernel has no
         # d(enc) round trip).  On c4 the split pipeline saves ~15 ms of 550.
         self.overlap_backward = os.environ.get("VR_OVERLAP_BWD", "1") != "0"
+        # K1 in one walk (count + staging, then a compaction copy) instead of count + fill
+        self.stage_k1 = os.environ.get("VR_K1_STAGE", "1") != "0"
+        self.stage_slots_per_ray = 96  # initial staging size; grown after an overflow
         self._bg = (ctypes.c_float * 3)()
         _lib.load()
 
@@ -170,26 +173,60 @@ class VolumePool:
         ray_part = torch.empty(R, dtype=torch.int32, device=dev) if full else None
         ray_total = torch.empty(R, dtype=torch.int32, device=dev) if full else None
         tc = _lib.addr(self.tree_c)
-        _lib.call("vr_sample_count", tc, _lib.ptr(rays), rays.shape[1], R, float(dt),
-                  region_lo, cnt, _lib.ptr(counts), _lib.ptr(seg_first), _lib.ptr(ray_te),
-                  _lib.ptr(ray_part), _lib.ptr(ray_total), _lib.ptr(self.err), s)
+        stage = self.stage_k1 and R > 0
+        if stage:  # one walk: count + staging (vr_sample_stage), compaction after the scan
+            blocks = int(_lib.load().vr_sample_stage_blocks(R))
+            st0, st1 = self._staging(R)
+            info = torch.zeros(2, dtype=torch.int64, device=dev)
+            sslot = torch.empty(R, dtype=torch.int64, device=dev)
+            _lib.call("vr_sample_stage", tc, _lib.ptr(rays), rays.shape[1], R, float(dt),
+                      region_lo, cnt, _lib.ptr(counts), _lib.ptr(seg_first), _lib.ptr(ray_te),
+                      _lib.ptr(ray_part), _lib.ptr(ray_total), _lib.ptr(st0), _lib.ptr(st1),
+                      st0.numel(), _lib.ptr(sslot), _lib.ptr(info), _lib.ptr(self.err), s)
+        else:
+            _lib.call("vr_sample_count", tc, _lib.ptr(rays), rays.shape[1], R, float(dt),
+                      region_lo, cnt, _lib.ptr(counts), _lib.ptr(seg_first), _lib.ptr(ray_te),
+                      _lib.ptr(ray_part), _lib.ptr(ray_total), _lib.ptr(self.err), s)
         offsets = torch.empty(cnt * R + 1, dtype=torch.int64, device=dev)
         ws = self._workspace(cnt * R)
         _lib.call("vr_scan_offsets", _lib.ptr(counts), cnt * R, _lib.ptr(offsets), _lib.ptr(ws),
                   ws.numel(), s)
         # the single host sync of a step: sample totals per region (allocation sizes)
-        bounds = offsets[torch.arange(cnt + 1, device=dev) * R].cpu().tolist()
+        meta = offsets[torch.arange(cnt + 1, device=dev) * R]
+        if stage:
+            meta = torch.cat((meta, info))
+        meta = meta.cpu().tolist()
+        bounds = meta[:cnt + 1]
         self.check("in sampling")
         N = int(bounds[-1])
         t0 = torch.empty(max(N, 1), dtype=torch.float64, device=dev)
         t1 = torch.empty(max(N, 1), dtype=torch.float64, device=dev)
         ray_id = torch.empty(max(N, 1), dtype=torch.int32, device=dev)
-        if N:
+        staged = stage and meta[-1] <= st0.numel() // blocks
+        if stage and not staged:  # a slice was too small: grow the staging for next time
+            self._stage_cap = int(meta[-1] * blocks * 1.15) + blocks
+        self.last_k1 = "stage" if staged else "fill"
+        if N and staged:
+            _lib.call("vr_sample_compact", R, cnt, _lib.ptr(counts), _lib.ptr(seg_first),
+                      _lib.ptr(offsets), _lib.ptr(sslot), _lib.ptr(st0), _lib.ptr(st1),
+                      _lib.ptr(t0), _lib.ptr(t1), _lib.ptr(ray_id), N, _lib.ptr(self.err), s)
+        elif N:
             _lib.call("vr_sample_fill", tc, _lib.ptr(rays), rays.shape[1], R, float(dt),
                       region_lo, cnt, _lib.ptr(offsets), _lib.ptr(seg_first), _lib.ptr(t0),
                       _lib.ptr(t1), _lib.ptr(ray_id), N, _lib.ptr(self.err), s)
         return SampleBatch(R, region_lo, cnt, counts, seg_first, offsets, ray_te, ray_part,
                            ray_total, t0, t1, ray_id, [int(b) for b in bounds])
+
+    def _staging(self, R: int):
+        """Persistent staging buffers of the one-walk K1 (grown when a slice overflowed)."""
+        cap = max(getattr(self, "_stage_cap", 0), self.stage_slots_per_ray * R)
+        st = getattr(self, "_stage", None)
+        if st is None or st[0].numel() < cap:
+            self._stage = None
+            st = (torch.empty(cap, dtype=torch.float64, device=self.device),
+                  torch.empty(cap, dtype=torch.float64, device=self.device))
+            self._stage = st
+        return st
 
     # ---- K1 one step ahead --------------------------------------------------------------
     # Sampling depends only on the rays, not on the parameters, so the next batch's K1 can

@@ -20,12 +20,16 @@ for name in sys.argv[1:] or ["c3"]:
             pool = vr.VolumePool(tree, fields, (0, 0, 0), DEV, rank, world)
             pool.sample(rays, w.dt)
             torch.cuda.synchronize()
-            a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-            a.record()
+            from paper_2404_16221_b200 import _lib
+            import bench
+            timer = bench.EventTimer()
+            _lib.TIMER = timer
             for _ in range(3):
                 bb = pool.sample(rays, w.dt)
-            b.record()
             torch.cuda.synchronize()
-            times.append((a.elapsed_time(b) / 3, bb.n_samples))
-        print(name, "world", world, "K1 ms per rank:", [round(t, 2) for t, _ in times],
-              "samples:", [s for _, s in times], flush=True)
+            _lib.TIMER = None
+            tot = timer.totals()
+            ms = sum(t for t, _ in tot.values()) / 3
+            times.append((ms, bb.n_samples, {k: round(t / 3, 2) for k, (t, _) in tot.items()}))
+        print(name, "world", world, "K1 kernel ms per rank:", [round(t[0], 2) for t in times],
+              "rank 0:", times[0][2], flush=True)

@@ -90,6 +90,39 @@ def test_sampler_bit_exact(name, world, stats):
                 assert sf[kk, r] == want
 
 
+@pytest.mark.parametrize("stats", [True, False])
+@pytest.mark.parametrize("name", ["sampler_three_blobs_k8.npz", "sampler_random_d2.npz"])
+def test_sampler_one_walk_matches_fill(name, stats):
+    """One-walk K1 (vr_sample_stage + vr_sample_compact) == count + fill, bit for bit, also
+    through the overflow path (staging too small: fill pass, staging grown for next call)."""
+    g = load_npz(name)
+    tree = vr.tree_from_json(g["tree"])
+    rays = _soa(g["rays"])
+    for rank, world in ((0, 1), (0, 2), (1, 2)):
+        pool = _pool(tree, rank=rank, world=world)
+        rd = pool.rays_to_device(rays)
+        pool.stage_k1 = False
+        ref = pool.sample(rd, float(g["dt"]), stats=stats)
+        assert pool.last_k1 == "fill"
+        pool.stage_k1 = True
+        pool.stage_slots_per_ray = 1
+        runs = []
+        for _ in range(2):
+            runs.append((pool.sample(rd, float(g["dt"]), stats=stats), pool.last_k1))
+        assert [k for _, k in runs] == ["fill", "stage"]
+        torch.cuda.synchronize()
+        pool.check()
+        n = ref.n_samples
+        for b, _ in runs:
+            assert b.region_bounds == ref.region_bounds
+            for a, c in ((b.t0, ref.t0), (b.t1, ref.t1), (b.ray_id, ref.ray_id)):
+                assert torch.equal(a[:n], c[:n])
+            for a, c in ((b.counts, ref.counts), (b.seg_first, ref.seg_first),
+                         (b.offsets, ref.offsets), (b.ray_te, ref.ray_te),
+                         (b.ray_part, ref.ray_part), (b.ray_total, ref.ray_total)):
+                assert (a is None and c is None) or torch.equal(a, c)
+
+
 @pytest.mark.parametrize("capacity", [1, None])
 def test_sample_async_matches_sample(capacity):
     """K1 one step ahead (sample_async / resolve_sample on the sampling stream) gives the
