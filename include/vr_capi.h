@@ -309,6 +309,21 @@ int vr_segment_permute(const int64_t* offsets_dev, const int32_t* seg_first_dev,
                        const int64_t* ray_offsets_dev, int64_t n_rays, int32_t n_regions,
                        const void* src_dev, void* dst_dev, int32_t elem_bytes,
                        int32_t to_ray_major, void* stream);
+/* Sparse packet exchange (the transit of TilePayloads, distsim.py:333-344 / :435-446:
+ * only participating segments travel).  vr_packets_pack writes the packets of this
+ * rank's non-empty segments (counts > 0) as records {global slab index (int32 bits), 8
+ * packet floats[, extra]} into rows 1..n of out [capacity + 1][width] (width 9, or 10
+ * with extra = per-segment proposal transmittance [region_cnt][n_rays]); row 0 holds n
+ * (int32 bits); count_dev receives n; n > capacity raises VR_FLAG_OVERFLOW.
+ * vr_packets_unpack takes world such buffers back to back ([world][rows][width]), fills
+ * slab [n_regions][n_rays][8] with identity packets (and extra_slab with 1) and scatters
+ * every record: the same slab the dense all-gather of vr_segment_fwd outputs gives. */
+int vr_packets_pack(const float* packets_dev, const float* extra_dev, const int32_t* counts_dev,
+                    int64_t n_rays, int32_t region_lo, int32_t region_cnt, float* out_dev,
+                    int64_t capacity, int32_t* count_dev, int32_t* err_dev, void* stream);
+int vr_packets_unpack(const float* recv_dev, int32_t world, int64_t rows, int32_t width,
+                      int64_t n_rays, int32_t n_regions, float* slab_dev, float* extra_slab_dev,
+                      int32_t* err_dev, void* stream);
 /* analytic backward: dpackets [region_cnt][n_rays][8] = adjoints of {T,C,A,D',L};
  * writes dsig_rgb[i] = {dL/dsigma, dL/dr, dL/dg, dL/db}. */
 int vr_segment_bwd(const double* t0_dev, const double* t1_dev, const float* sig_rgb_dev,

@@ -137,6 +137,8 @@ SIGNATURES = {
     "vr_segment_fwd": [P, P, P, P, P, P, I64, I32, P, P, P],
     "vr_segment_bwd": [P, P, P, P, P, I64, I32, P, P, P],
     "vr_segment_permute": [P, P, P, I64, I32, P, P, I32, I32, P],
+    "vr_packets_pack": [P, P, P, I64, I32, I32, P, I64, P, P, P],
+    "vr_packets_unpack": [P, I32, I64, I32, I64, I32, P, P, P, P],
     "vr_global_fwd": [P, I32, I64, P, P, I32, P, P, P],
     "vr_global_train": [P, I32, I64, P, P, P, F32, I32, I32, P, P, P, P, P],
     "vr_prefix_train": [P, P, I32, I64, I32, I32, P, P],

@@ -28,7 +28,8 @@ def _host_staged(group, t: torch.Tensor) -> bool:
 
 
 def all_gather_packets(local: torch.Tensor, group=None, world: int = 1) -> torch.Tensor:
-    """[K_own, R, 8] on every rank -> [world*K_own, R, 8] on every rank (training)."""
+    """[K_own, R, 8] on every rank -> [world*K_own, R, 8] on every rank (training); any
+    tensor is concatenated along dim 0 (the sparse exchange's [rows][width] buffers)."""
     if world == 1:
         return local
     src = local.contiguous()
@@ -97,6 +98,19 @@ def gather_packets(local: torch.Tensor, group=None, world: int = 1, rank: int = 
         return torch.cat(parts, dim=0).to(local.device)
     dist.gather(src, gather_list=None, dst=dst, group=group)
     return None
+
+
+def all_reduce_max_(t: torch.Tensor, group=None, world: int = 1) -> torch.Tensor:
+    """In-place MAX over the ranks of a small tensor (the sparse exchange's record count)."""
+    if world == 1:
+        return t
+    if _host_staged(group, t):
+        c = t.cpu()
+        dist.all_reduce(c, op=dist.ReduceOp.MAX, group=group)
+        t.copy_(c)
+        return t
+    dist.all_reduce(t, op=dist.ReduceOp.MAX, group=group)
+    return t
 
 
 def all_reduce_scalar(x: torch.Tensor, group=None, world: int = 1) -> torch.Tensor:

@@ -578,6 +578,124 @@ extern "C" int vr_segment_permute(const int64_t* off, const int32_t* seg_first,
   return check_launch("vr_segment_permute");
 }
 
+// ---- sparse packet exchange ---------------------------------------------------------
+// Only the packets of non-empty segments travel (a ray crosses ~3 of c3's 8 regions and
+// ~1.6 of c4's): record = {global slab index (int32 bits), 8 packet floats[, proposal T]};
+// row 0 of a rank's buffer holds its record count.  The receiver fills the dense
+// [K][R][8] slab with identity packets (what K4 writes for an empty segment) and
+// scatters the records, so K5 reads bit-identical slabs on every rank.
+__global__ void k_packets_pack(const float4* __restrict__ pk, const float* __restrict__ extra,
+                               const int32_t* __restrict__ counts, int64_t n_segs,
+                               int64_t n_rays, int region_lo, int width, float* out, int64_t cap,
+                               int32_t* n_out, int32_t* err) {
+  const int lane = threadIdx.x & 31;
+  int flags = 0;
+  for (int64_t base = (int64_t)blockIdx.x * blockDim.x + (threadIdx.x & ~31); base < n_segs;
+       base += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t seg = base + lane;
+    const bool live = seg < n_segs && counts[seg] > 0;
+    const unsigned m = __ballot_sync(0xffffffffu, live);
+    if (!m) continue;
+    int32_t slot0 = 0;
+    if (lane == 0) slot0 = atomicAdd(n_out, __popc(m));
+    slot0 = __shfl_sync(0xffffffffu, slot0, 0);
+    if (live) {
+      const int64_t slot = 1 + slot0 + __popc(m & ((1u << lane) - 1u));
+      if (slot > cap) {
+        flags |= VR_FLAG_OVERFLOW;
+      } else {
+        float* rec = out + slot * width;
+        const int64_t gidx = (int64_t)region_lo * n_rays + seg;
+        const float4 a = pk[2 * seg], b = pk[2 * seg + 1];
+        rec[0] = __int_as_float((int32_t)gidx);
+        rec[1] = a.x; rec[2] = a.y; rec[3] = a.z; rec[4] = a.w;
+        rec[5] = b.x; rec[6] = b.y; rec[7] = b.z; rec[8] = b.w;
+        if (extra) rec[9] = extra[seg];
+      }
+    }
+  }
+  flags = (int)__reduce_or_sync(0xffffffffu, (unsigned)flags);
+  if (flags && lane == 0) atomicOr(err, flags);
+}
+
+__global__ void k_packets_header(const int32_t* n_out, float* out) {
+  out[0] = __int_as_float(*n_out);
+}
+
+__global__ void k_packets_identity(float4* __restrict__ slab, float* __restrict__ extra_slab,
+                                   int64_t n_segs) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n_segs;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    slab[2 * i] = make_float4(1.f, 0.f, 0.f, 0.f);
+    slab[2 * i + 1] = make_float4(0.f, 0.f, 0.f, order_bits(INT32_MAX));
+    if (extra_slab) extra_slab[i] = 1.f;
+  }
+}
+
+__global__ void k_packets_unpack(const float* __restrict__ recv, int world, int64_t rows,
+                                 int width, int64_t n_segs, float4* __restrict__ slab,
+                                 float* __restrict__ extra_slab, int32_t* err) {
+  int flags = 0;
+  for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < (int64_t)world * rows;
+       t += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t rk = t / rows, i = t - rk * rows;
+    const float* buf = recv + rk * rows * width;
+    const int32_t n = __float_as_int(buf[0]);
+    if (i == 0 || i > n) continue;
+    if (n >= rows) {
+      flags |= VR_FLAG_OVERFLOW;
+      continue;
+    }
+    const float* rec = buf + i * width;
+    const int64_t g = (int64_t)__float_as_int(rec[0]);
+    if (g < 0 || g >= n_segs) {
+      flags |= VR_FLAG_OVERFLOW;
+      continue;
+    }
+    slab[2 * g] = make_float4(rec[1], rec[2], rec[3], rec[4]);
+    slab[2 * g + 1] = make_float4(rec[5], rec[6], rec[7], rec[8]);
+    if (extra_slab) extra_slab[g] = rec[9];
+  }
+  if (flags) atomicOr(err, flags);
+}
+
+extern "C" int vr_packets_pack(const float* packets, const float* extra, const int32_t* counts,
+                               int64_t n_rays, int32_t region_lo, int32_t region_cnt, float* out,
+                               int64_t capacity, int32_t* count_dev, int32_t* err,
+                               void* stream) {
+  if (n_rays < 0 || region_lo < 0 || region_cnt < 1 || capacity < 0 || !out || !count_dev ||
+      !err || (int64_t)(region_lo + region_cnt) * n_rays > INT32_MAX) {
+    set_error("vr_packets_pack: bad argument");
+    return VR_ERR_BAD_ARG;
+  }
+  cudaStream_t s = (cudaStream_t)stream;
+  const int64_t n_segs = n_rays * region_cnt;
+  cudaMemsetAsync(count_dev, 0, sizeof(int32_t), s);
+  if (n_segs > 0)
+    k_packets_pack<<<grid_for(n_segs, 256), 256, 0, s>>>(
+        (const float4*)packets, extra, counts, n_segs, n_rays, region_lo, extra ? 10 : 9, out,
+        capacity, count_dev, err);
+  k_packets_header<<<1, 1, 0, s>>>(count_dev, out);
+  return check_launch("vr_packets_pack");
+}
+
+extern "C" int vr_packets_unpack(const float* recv, int32_t world, int64_t rows, int32_t width,
+                                 int64_t n_rays, int32_t n_regions, float* slab,
+                                 float* extra_slab, int32_t* err, void* stream) {
+  if (world < 1 || rows < 1 || (width != 9 && width != 10) || (width == 10) != !!extra_slab ||
+      n_rays < 0 || n_regions < 1 || n_regions > VR_MAX_REGIONS || !slab || !err) {
+    set_error("vr_packets_unpack: bad argument");
+    return VR_ERR_BAD_ARG;
+  }
+  cudaStream_t s = (cudaStream_t)stream;
+  const int64_t n_segs = n_rays * n_regions;
+  if (n_segs == 0) return VR_OK;
+  k_packets_identity<<<grid_for(n_segs, 256), 256, 0, s>>>((float4*)slab, extra_slab, n_segs);
+  k_packets_unpack<<<grid_for((int64_t)world * rows, 256), 256, 0, s>>>(
+      recv, world, rows, width, n_segs, (float4*)slab, extra_slab, err);
+  return check_launch("vr_packets_unpack");
+}
+
 extern "C" int vr_sum_f64(const double* x, int64_t n, double* out, void* stream) {
   if (n < 0 || !out) {
     set_error("vr_sum_f64: bad argument");

@@ -58,6 +58,8 @@ class SampleBatch:
     t1: torch.Tensor  # float64 [N]
     ray_id: torch.Tensor  # int32 [N]
     region_bounds: list  # host: sample offset of each owned region, len cnt+1
+    # sparse packet exchange: max over ranks of the non-empty segments (None: dense)
+    seg_max: int | None = None
 
     @property
     def n_samples(self) -> int:
@@ -114,6 +116,8 @@ class VolumePool:
         # K1 in one walk (count + staging, then a compaction copy) instead of count + fill
         self.stage_k1 = os.environ.get("VR_K1_STAGE", "1") != "0"
         self.stage_slots_per_ray = 96  # initial staging size; grown after an overflow
+        # packets of non-empty segments only cross the link (dense slab if "0")
+        self.sparse_exchange = os.environ.get("VR_SPARSE_EXCHANGE", "1") != "0"
         self._bg = (ctypes.c_float * 3)()
         _lib.load()
 
@@ -154,11 +158,13 @@ class VolumePool:
 
     # ---- K1 ----------------------------------------------------------------------------
     def sample(self, rays: torch.Tensor, dt: float, all_regions: bool = False,
-               stats: bool = False) -> SampleBatch:
+               stats: bool = False, exchange: bool = False) -> SampleBatch:
         """K1 for the owned regions (or every region: sample-broadcast protocol).  stats:
         also the per-ray participation masks and sample totals (reference CommStats) —
         this makes the kernel walk every ray entirely; without it a rank skips the rays and
-        bins that cannot reach its regions."""
+        bins that cannot reach its regions.  exchange: the batch's packets will be
+        exchanged (collective: every rank calls it) — size the sparse exchange here, in
+        the step's one host sync."""
         if not dt > 0.0:
             raise ValueError("dt must be > 0")
         R = rays.shape[1]
@@ -193,10 +199,15 @@ class VolumePool:
                   ws.numel(), s)
         # the single host sync of a step: sample totals per region (allocation sizes)
         meta = offsets[torch.arange(cnt + 1, device=dev) * R]
+        sparse = exchange and self.world > 1 and self.sparse_exchange and not all_regions
+        if sparse:  # records of the sparse exchange: non-empty segments, max over ranks
+            nz = (counts > 0).sum(dtype=torch.int64).reshape(1)
+            meta = torch.cat((meta, comm.all_reduce_max_(nz, self.group, self.world)))
         if stage:
             meta = torch.cat((meta, info))
         meta = meta.cpu().tolist()
         bounds = meta[:cnt + 1]
+        seg_max = int(meta[cnt + 1]) if sparse else None
         self.check("in sampling")
         N = int(bounds[-1])
         t0 = torch.empty(max(N, 1), dtype=torch.float64, device=dev)
@@ -215,7 +226,7 @@ class VolumePool:
                       region_lo, cnt, _lib.ptr(offsets), _lib.ptr(seg_first), _lib.ptr(t0),
                       _lib.ptr(t1), _lib.ptr(ray_id), N, _lib.ptr(self.err), s)
         return SampleBatch(R, region_lo, cnt, counts, seg_first, offsets, ray_te, ray_part,
-                           ray_total, t0, t1, ray_id, [int(b) for b in bounds])
+                           ray_total, t0, t1, ray_id, [int(b) for b in bounds], seg_max)
 
     def _staging(self, R: int):
         """Persistent staging buffers of the one-walk K1 (grown when a slice overflowed)."""
@@ -399,6 +410,48 @@ class VolumePool:
                   b.region_cnt, _lib.ptr(pk), _lib.ptr(self.err), self._stream())
         return pk
 
+    def exchange_packets(self, b: SampleBatch, local: torch.Tensor, extra=None,
+                         dst: int | None = None):
+        """The packet exchange: [K_own][R][8] (+ optional per-segment proposal T
+        [K_own][R]) of every rank -> the global [K][R][8] (and [K][R]) slabs on every rank
+        (dst None, training) or on rank dst only (render; None elsewhere).  Dense: one
+        all-gather / gather of the slabs.  Sparse (b.seg_max set): only the records of
+        non-empty segments travel (vr_packets_pack / vr_packets_unpack), which gives the
+        same slabs bit for bit."""
+        if self.world == 1:
+            return local, extra
+        if b.seg_max is None:
+            if dst is None:
+                allp = comm.all_gather_packets(local, self.group, self.world)
+                all_e = (comm.all_gather_packets(extra, self.group, self.world)
+                         if extra is not None else None)
+                return allp, all_e
+            allp = comm.gather_packets(local, self.group, self.world, self.rank, dst)
+            if extra is not None:
+                raise ValueError("extra slabs are exchanged in training only")
+            return allp, None
+        s = self._stream()
+        R = b.n_rays
+        width = 9 if extra is None else 10
+        cap = max(int(b.seg_max), 1)
+        send = torch.empty((cap + 1, width), dtype=torch.float32, device=self.device)
+        n_dev = torch.empty(1, dtype=torch.int32, device=self.device)
+        _lib.call("vr_packets_pack", _lib.ptr(local), _lib.ptr(extra), _lib.ptr(b.counts), R,
+                  b.region_lo, b.region_cnt, _lib.ptr(send), cap, _lib.ptr(n_dev),
+                  _lib.ptr(self.err), s)
+        if dst is None:
+            recv = comm.all_gather_packets(send, self.group, self.world)
+        else:
+            recv = comm.gather_packets(send, self.group, self.world, self.rank, dst)
+            if recv is None:
+                return None, None
+        allp = torch.empty((self.n_regions, R, 8), dtype=torch.float32, device=self.device)
+        all_e = (torch.empty((self.n_regions, R), dtype=torch.float32, device=self.device)
+                 if extra is not None else None)
+        _lib.call("vr_packets_unpack", _lib.ptr(recv), self.world, cap + 1, width, R,
+                  self.n_regions, _lib.ptr(allp), _lib.ptr(all_e), _lib.ptr(self.err), s)
+        return allp, all_e
+
     # ---- K5 ----------------------------------------------------------------------------
     def _set_bg(self, background):
         bg = self.background if background is None else vec3(background)
@@ -430,10 +483,10 @@ class VolumePool:
             _, ray_off, (t0r, t1r, srr) = res
             pk = self._whole_ray_packets(b, ray_off, t0r, t1r, srr)
             return self.compose(pk, b, background, clip), b
-        b = self.sample(rays, dt, stats=stats)
+        b = self.sample(rays, dt, stats=stats, exchange=True)
         sig_rgb = self.evaluate(rays, b)
         local = self.local_packets(b, sig_rgb)
-        allp = comm.gather_packets(local, self.group, self.world, self.rank)
+        allp, _ = self.exchange_packets(b, local, dst=0)
         if allp is None:
             return None, b
         return self.compose(allp, b, background, clip), b
@@ -501,16 +554,17 @@ class VolumePool:
             if lambda_interlevel > 0.0:
                 raise ValueError("the interlevel loss is defined on the tile protocol")
             return self._sample_protocol_train(rays, tg, dt, lambda_dist, background)
-        b = batch if batch is not None else self.sample(rays, dt)  # batch: sample_async
+        # batch: sample_async
+        b = batch if batch is not None else self.sample(rays, dt, exchange=True)
         sig_rgb = self.evaluate(rays, b)
         local = self.local_packets(b, sig_rgb)
-        allp = comm.all_gather_packets(local, self.group, self.world)
         interlevel = self.proposals is not None and lambda_interlevel > 0.0
+        prop_T = None
         if interlevel:
             sig_prop = self.evaluate(rays, b, self.proposals)
             # only the proposal transmittance of each segment crosses the link
             prop_T = self.local_packets(b, sig_prop)[:, :, 0].contiguous()
-            all_T = comm.all_gather_packets(prop_T, self.group, self.world)
+        allp, all_T = self.exchange_packets(b, local, prop_T)
         R = b.n_rays
         out = torch.empty((7, R), dtype=torch.float32, device=self.device)
         ray_loss = torch.empty(R, dtype=torch.float64, device=self.device)
@@ -632,7 +686,12 @@ class VolumePool:
                 sent = int((mine * (nparts - 1)).sum().item())
                 st._party(k).scalars_sent += SCALARS_PER_TILE_PACKET * sent
                 st._party(k).messages_sent += sent
-        st.link_bytes = (self.world - 1) * self.region_cnt * b.n_rays * 32 if self.world > 1 else 0
+        if self.world == 1:
+            st.link_bytes = 0
+        elif b.seg_max is not None:  # sparse exchange: padded 36-byte records
+            st.link_bytes = (self.world - 1) * (b.seg_max + 1) * 36
+        else:
+            st.link_bytes = (self.world - 1) * self.region_cnt * b.n_rays * 32
         return st
 
 

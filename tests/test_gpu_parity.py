@@ -253,6 +253,72 @@ def test_multi_rank_composite_is_bitwise_identical():
     assert torch.equal(out1, out2)
 
 
+@pytest.mark.parametrize("world", [2, 4])
+@pytest.mark.parametrize("with_extra", [False, True])
+def test_sparse_packet_exchange_kernels(world, with_extra):
+    """vr_packets_pack / vr_packets_unpack with simulated ranks: the records are the
+    non-empty segments' packets (the numpy restatement, as a set), and the unpacked slab is
+    the dense all-gather's slab bit for bit; a too-small capacity raises the overflow."""
+    import packets_ref as pr
+    from paper_2404_16221_b200 import _lib
+
+    g = load_npz("render_street_k8.npz")
+    rays = _soa(g["rays"])
+    dt = float(g["dt"])
+    bufs, dense, dense_e, ns = [], [], [], []
+    for rank in range(world):
+        p, _, _ = _scene_pool(g, world=world, rank=rank)
+        rd = p.rays_to_device(rays)
+        b = p.sample(rd, dt)
+        local = p.local_packets(b, p.evaluate(rd, b))
+        R = b.n_rays
+        extra = None
+        if with_extra:
+            extra = torch.where(b.counts.reshape(b.region_cnt, R) > 0, local[:, :, 0] * 0.25,
+                                torch.ones_like(local[:, :, 0])).contiguous()
+        cap = b.region_cnt * R
+        width = 10 if with_extra else 9
+        send = torch.zeros((cap + 1, width), dtype=torch.float32, device=DEV)
+        n_dev = torch.zeros(1, dtype=torch.int32, device=DEV)
+        _lib.call("vr_packets_pack", _lib.ptr(local), _lib.ptr(extra), _lib.ptr(b.counts), R,
+                  b.region_lo, b.region_cnt, _lib.ptr(send), cap, _lib.ptr(n_dev),
+                  _lib.ptr(p.err), _lib.stream_ptr())
+        torch.cuda.synchronize()
+        p.check()
+        n = int(n_dev.item())
+        rec, n_ref = pr.pack(local.cpu().numpy(), b.counts.cpu().numpy(), b.region_lo,
+                             None if extra is None else extra.cpu().numpy())
+        assert n == n_ref and int(send[0, 0].view(torch.int32).item()) == n
+        got = send[1:n + 1].cpu().numpy()
+        order = np.argsort(got[:, 0].copy().view(np.int32))
+        assert np.array_equal(got[order].view(np.uint32), rec.view(np.uint32))
+        bufs.append(send)
+        dense.append(local)
+        dense_e.append(extra)
+        ns.append(n)
+        # capacity below the record count: flagged
+        small = torch.zeros((max(n - 1, 0) + 1, width), dtype=torch.float32, device=DEV)
+        if n > 0:
+            _lib.call("vr_packets_pack", _lib.ptr(local), _lib.ptr(extra), _lib.ptr(b.counts),
+                      R, b.region_lo, b.region_cnt, _lib.ptr(small), n - 1, _lib.ptr(n_dev),
+                      _lib.ptr(p.err), _lib.stream_ptr())
+            with pytest.raises(vr.CapacityError):
+                p.check()
+    K = world * dense[0].shape[0]
+    R = dense[0].shape[1]
+    recv = torch.cat(bufs, 0)
+    slab = torch.empty((K, R, 8), dtype=torch.float32, device=DEV)
+    slab_e = torch.empty((K, R), dtype=torch.float32, device=DEV) if with_extra else None
+    _lib.call("vr_packets_unpack", _lib.ptr(recv), world, bufs[0].shape[0], recv.shape[1], R, K,
+              _lib.ptr(slab), _lib.ptr(slab_e), _lib.ptr(p.err), _lib.stream_ptr())
+    torch.cuda.synchronize()
+    p.check()
+    assert torch.equal(slab.view(torch.int32), torch.cat(dense, 0).view(torch.int32))
+    if with_extra:
+        assert torch.equal(slab_e, torch.cat(dense_e, 0))
+    assert sum(ns) < K * R
+
+
 @pytest.mark.parametrize("name", ["partition_street.npz", "partition_voxel_room.npz"])
 def test_rays_to_points_and_balance_report_match_reference(name):
     """rays_to_points (K1 on a one-leaf tree + the reference's numpy subsample) gives the

@@ -120,6 +120,71 @@ def test_exchange_world2_matches_single_process(name):
     np.testing.assert_allclose(ref_fold[:, 3], g["out"][:, 5], atol=1e-6)
 
 
+def _sparse_worker(rank, world, port, name, q):
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        import packets_ref as pr
+        from paper_2404_16221_b200 import comm
+
+        g = load_npz(name)
+        K = len(vo.Tree(g["tree"]).leaf_mn)
+        lo, cnt = comm.owned_regions(K, rank, world)
+        local = oracle_packets(g, lo, cnt)
+        counts = (local[:, :, 7].copy().view(np.int32) != INT_MAX).astype(np.int32)
+        # stands in for the proposal transmittance (1 on empty segments, as K4 writes)
+        extra = np.where(counts > 0, local[:, :, 0] * 0.5, 1.0).astype(np.float32)
+        rec, n = pr.pack(local, counts, lo, extra)
+        n_max = comm.all_reduce_max_(torch.tensor([n], dtype=torch.int64), dist.group.WORLD,
+                                     world)
+        buf = torch.from_numpy(pr.buffer(rec, int(n_max.item())))
+        allb = comm.all_gather_packets(buf, dist.group.WORLD, world)
+        slab, ex = pr.unpack(allb.numpy(), world, K, local.shape[1])
+        got = comm.gather_packets(buf, dist.group.WORLD, world, rank)
+        q.put((rank, int(n_max.item()), n, slab, ex, None if got is None else got.numpy()))
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("name", ["render_three_blobs_k4.npz", "render_street_k8.npz"])
+def test_sparse_exchange_world2_matches_dense(name):
+    """Sparse packet exchange (records of non-empty segments; VolumePool.exchange_packets):
+    the record-count MAX all-reduce, the padded all-gather and the gather, unpacked with the
+    numpy restatement of vr_packets_unpack, rebuild the dense single-process slab bit for
+    bit on every rank (and on rank 0 for the gather)."""
+    import packets_ref as pr
+
+    world = 2
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_sparse_worker, args=(r, world, port, name, q))
+             for r in range(world)]
+    for p in procs:
+        p.start()
+    results = [q.get(timeout=300) for _ in range(world)]
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    g = load_npz(name)
+    K = len(vo.Tree(g["tree"]).leaf_mn)
+    single = oracle_packets(g, 0, K)
+    R = single.shape[1]
+    counts = [n for _, _, n, _, _, _ in results]
+    for rank, n_max, n, slab, ex, got in sorted(results, key=lambda x: x[0]):
+        assert n_max == max(counts)
+        assert np.array_equal(slab.view(np.uint32), single.view(np.uint32))
+        live = single[:, :, 7].copy().view(np.int32) != INT_MAX
+        assert np.array_equal(ex, np.where(live, single[:, :, 0] * 0.5, 1.0).astype(np.float32))
+        if rank == 0:
+            s0, _ = pr.unpack(got, world, K, R)
+            assert np.array_equal(s0.view(np.uint32), single.view(np.uint32))
+        else:
+            assert got is None
+    assert sum(counts) < K * R  # fewer records than dense packets
+
+
 def _sample_worker(rank, world, port, q):
     os.environ["MASTER_ADDR"] = "127.0.0.1"
     os.environ["MASTER_PORT"] = str(port)
