@@ -447,6 +447,11 @@ def main():
     if world > 1:
         dist.all_reduce(n_samples)
     n_samples = int(n_samples.item())
+    # non-empty (ray, region) segments: the records of the sparse packet exchange
+    n_live = (b.counts > 0).sum(dtype=torch.int64).reshape(1).to(red_dev)
+    if world > 1:
+        dist.all_reduce(n_live)
+    n_live = int(n_live.item())
 
     # ---- roofline of the dominant kernel (events over the timed region) ------------
     totals = timer.totals()
@@ -562,13 +567,20 @@ def main():
                 "exchange": {
                     "protocol": args.protocol,
                     # data that crosses the link when every region is on its own GPU:
-                    # tile = one 32 B packet per (ray, region); sample = 16 B per sample
-                    "wire": "32 B/(ray, region) packet" if args.protocol == "tile"
-                            else "16 B/sample (sigma, rgb)",
-                    "bytes_per_step_1_region_per_gpu": (len(w.tree.leaves) * R * 32
+                    # tile = one record {slab index, 8-float packet[, proposal T]} per
+                    # non-empty (ray, region) segment (sparse exchange; the dense slab is
+                    # one 32 B packet per (ray, region)); sample = 16 B per sample
+                    "wire": ("36 B/non-empty segment" + (" (+4 B proposal T)" if interlevel
+                                                          else "")
+                             if args.protocol == "tile" else "16 B/sample (sigma, rgb)"),
+                    "nonempty_segments": n_live,
+                    "segments": len(w.tree.leaves) * R,
+                    "bytes_per_step_1_region_per_gpu": (n_live * (40 if interlevel else 36)
                                                         if args.protocol == "tile"
                                                         else n_samples * 16),
-                    "tile_vs_sample_bytes": (len(w.tree.leaves) * R * 32) / max(1, n_samples * 16)},
+                    "dense_slab_bytes": len(w.tree.leaves) * R * (36 if interlevel else 32),
+                    "tile_vs_sample_bytes": (n_live * (40 if interlevel else 36))
+                                            / max(1, n_samples * 16)},
                 "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e,
                 "gpu_launches": launches, "clocks": clk, "loss": final_loss,
                 "step_ms": [round(x, 3) for x in step_ms],
