@@ -488,6 +488,23 @@ def main():
                     "share_of_step": t_total / args.steps / ms_instrumented,
                     "ms_per_step_instrumented": ms_instrumented}
 
+    # every costed kernel against its roofline (the north_star names the hash encode's
+    # fraction of HBM peak and the MLP's tensor-pipe share; the headline roofline above is
+    # the dominant kernel's)
+    rooflines = {}
+    for k, (t_total, n_launch) in totals.items():
+        if k not in KERNEL_COST or t_total <= 0:
+            continue
+        bound, per_unit, _ = KERNEL_COST[k]
+        units = timer.samples.get(k, n_samples_rank * args.steps)
+        rate = per_unit * units / (t_total / 1e3)
+        achieved = rate / 1e9 if bound == "hbm" else rate / 1e12
+        peak = peaks["hbm"] if bound == "hbm" else peaks["tensor"]
+        rooflines[k] = {"bound": bound, "achieved": round(achieved, 1),
+                        "unit": "GB/s" if bound == "hbm" else "TFLOP/s",
+                        "frac": round(achieved / peak, 3),
+                        "ms_per_step": round(t_total / args.steps, 3)}
+
     # ---- end to end through the public API with host buffers ------------------------
     e2e = None
     if not args.no_e2e:
@@ -581,7 +598,7 @@ def main():
                     "dense_slab_bytes": len(w.tree.leaves) * R * (36 if interlevel else 32),
                     "tile_vs_sample_bytes": (n_live * (40 if interlevel else 36))
                                             / max(1, n_samples * 16)},
-                "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e,
+                "roofline": roofline, "rooflines": rooflines, "cpu_baseline": cpu, "e2e": e2e,
                 "gpu_launches": launches, "clocks": clk, "loss": final_loss,
                 "step_ms": [round(x, 3) for x in step_ms],
                 "kernels": per_kernel}
