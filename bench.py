@@ -43,6 +43,8 @@ KERNEL_COST = {
     "vr_hash_fwd_lm": ("hbm", 16 * (12 + 64 + 4.0), 3),
     # level-major: pos (12) + denc (8) + 8 float2 atomics (64), x 16 levels
     "vr_hash_bwd_lm": ("hbm", 16 * (12 + 8 + 64.0), 2),
+    # split backward's scatter: pos (12) + denc f32 (128) + 16 x 8 float2 atomics (1024)
+    "vr_hash_scatter": ("hbm", 1164.0, 2),
     # 2 * (32*64 + 64*16 + 32*64 + 64*64 + 64*3)
     "vr_mlp_fwd": ("tensor", 18816.0, 5),
     "vr_mlp_fwd_tc": ("tensor", 18816.0, 5),

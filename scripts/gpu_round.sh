@@ -15,7 +15,7 @@ $CMD > gpurun_out/r_plain.log 2>&1 && \
       --log-file gpurun_out/r_launches.csv $CMD > gpurun_out/r_ncu_launch.log 2>&1
 bash scripts/prof_one.sh k_mlp_bwd_tc 9 r_mlp_bwd_fused > /dev/null 2>&1
 bash scripts/prof_one.sh k_hash_fwd 9 r_hash_fwd > /dev/null 2>&1
-bash scripts/prof_one.sh "k_sample<" 1 r_sample_stage > /dev/null 2>&1
+bash scripts/prof_one.sh "^k_sample$" 1 r_sample_stage > /dev/null 2>&1
 bash scripts/prof_one.sh k_sample_compact 1 r_sample_compact > /dev/null 2>&1
 cat gpurun_out/r_tests.log gpurun_out/r_smoke.log
 for f in r_bench_c3 r_bench_c4 r_bench_c5 r_bench_ref; do echo "== $f"; tail -1 gpurun_out/$f.log | cut -c1-400; done
