@@ -338,25 +338,20 @@ __global__ void __launch_bounds__(256)
     for (int k0 = 0; k0 < region_cnt; k0 += 32) {
       const int kk = k0 + lane;
       const int64_t idx = (int64_t)kk * n_rays + r;
-      // all of the ray's metadata in one round of independent loads
-      int c = 0, f_raw = 0;
-      int64_t dst = 0;
-      if (kk < region_cnt) {
-        c = counts[idx];
-        f_raw = seg_first[idx];
-        dst = offsets[idx];
-      }
-      const int64_t base = sslot[r];
+      const int c = kk < region_cnt ? counts[idx] : 0;
       const unsigned live = __ballot_sync(0xffffffffu, c > 0);
       if (!live) continue;
+      const int64_t base = sslot[r];
       if (base <= INT64_MIN / 4) {  // the ray was not staged (base itself may be negative)
         flags |= VR_FLAG_OVERFLOW;
         break;
       }
       int first = INT32_MAX, last = 0;
+      int64_t dst = 0;
       if (c > 0) {
-        first = f_raw;
+        first = seg_first[idx];
         last = first + c;
+        dst = offsets[idx];
       }
       const int g_lo = __reduce_min_sync(0xffffffffu, (unsigned)first);
       const int g_hi = (int)__reduce_max_sync(0xffffffffu, (unsigned)last);
