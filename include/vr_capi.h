@@ -165,14 +165,18 @@ int vr_sample_fill(const VrTree* tree, const double* rays_dev, int64_t ray_strid
  * [1] = max slots one CTA needed: if [1] > stage_capacity / vr_sample_stage_blocks(n_rays)
  * the staging is incomplete and the caller runs vr_sample_fill (the counts are exact
  * either way).  After vr_scan_offsets, vr_sample_compact moves the staged samples to their
- * slots (the same t0/t1/ray_id vr_sample_fill writes, bit for bit). */
+ * slots (the same t0/t1/ray_id vr_sample_fill writes, bit for bit).  ray_list_dev
+ * (optional, n_rays + 1 int32 of scratch): with a region block smaller than the tree, a
+ * thread-per-ray prefilter first settles the rays that miss the block's box, and the
+ * warp-per-ray walk only visits the others. */
 int64_t vr_sample_stage_blocks(int64_t n_rays);
 int vr_sample_stage(const VrTree* tree, const double* rays_dev, int64_t ray_stride,
                     int64_t n_rays, double dt, int32_t region_lo, int32_t region_cnt,
                     int32_t* counts_dev, int32_t* seg_first_dev, double* ray_te_dev,
                     uint32_t* ray_part_dev, int32_t* ray_total_dev, double* st0_dev,
                     double* st1_dev, int64_t stage_capacity, int64_t* sslot_dev,
-                    uint64_t* stage_info_dev, int32_t* err_dev, void* stream);
+                    uint64_t* stage_info_dev, int32_t* ray_list_dev, int32_t* err_dev,
+                    void* stream);
 int vr_sample_compact(int64_t n_rays, int32_t region_cnt, const int32_t* counts_dev,
                       const int32_t* seg_first_dev, const int64_t* offsets_dev,
                       const int64_t* sslot_dev, const double* st0_dev, const double* st1_dev,

@@ -112,7 +112,7 @@ SIGNATURES = {
     "vr_scan_offsets": [P, I64, P, P, C.c_size_t, P],
     "vr_sample_fill": [P, P, I64, I64, F64, I32, I32, P, P, P, P, P, I64, P, P],
     "vr_sample_stage_blocks": [I64],
-    "vr_sample_stage": [P, P, I64, I64, F64, I32, I32, P, P, P, P, P, P, P, I64, P, P, P, P],
+    "vr_sample_stage": [P, P, I64, I64, F64, I32, I32, P, P, P, P, P, P, P, I64, P, P, P, P, P],
     "vr_sample_compact": [I64, I32, P, P, P, P, P, P, P, P, P, I64, P, P],
     "vr_locate": [P, P, I64, P, P, P],
     "vr_field_analytic_fwd": [P, P, I64, P, P, P, I64, P, P],

@@ -116,6 +116,8 @@ class VolumePool:
         # K1 in one walk (count + staging, then a compaction copy) instead of count + fill
         self.stage_k1 = os.environ.get("VR_K1_STAGE", "1") != "0"
         self.stage_slots_per_ray = 96  # initial staging size; grown after an overflow
+        # multi-rank K1: thread-per-ray prefilter of the rays that miss the own regions
+        self.k1_prefilter = os.environ.get("VR_K1_PREFILTER", "1") != "0"
         # packets of non-empty segments only cross the link (dense slab if "0")
         self.sparse_exchange = os.environ.get("VR_SPARSE_EXCHANGE", "1") != "0"
         self._bg = (ctypes.c_float * 3)()
@@ -185,10 +187,13 @@ class VolumePool:
             st0, st1 = self._staging(R)
             info = torch.zeros(2, dtype=torch.int64, device=dev)
             sslot = torch.empty(R, dtype=torch.int64, device=dev)
+            ray_list = (torch.empty(R + 1, dtype=torch.int32, device=dev)
+                        if self.k1_prefilter else None)
             _lib.call("vr_sample_stage", tc, _lib.ptr(rays), rays.shape[1], R, float(dt),
                       region_lo, cnt, _lib.ptr(counts), _lib.ptr(seg_first), _lib.ptr(ray_te),
                       _lib.ptr(ray_part), _lib.ptr(ray_total), _lib.ptr(st0), _lib.ptr(st1),
-                      st0.numel(), _lib.ptr(sslot), _lib.ptr(info), _lib.ptr(self.err), s)
+                      st0.numel(), _lib.ptr(sslot), _lib.ptr(info), _lib.ptr(ray_list),
+                      _lib.ptr(self.err), s)
         else:
             _lib.call("vr_sample_count", tc, _lib.ptr(rays), rays.shape[1], R, float(dt),
                       region_lo, cnt, _lib.ptr(counts), _lib.ptr(seg_first), _lib.ptr(ray_te),

@@ -90,16 +90,21 @@ def test_sampler_bit_exact(name, world, stats):
                 assert sf[kk, r] == want
 
 
+@pytest.mark.parametrize("prefilter", [True, False])
 @pytest.mark.parametrize("stats", [True, False])
 @pytest.mark.parametrize("name", ["sampler_three_blobs_k8.npz", "sampler_random_d2.npz"])
-def test_sampler_one_walk_matches_fill(name, stats):
-    """One-walk K1 (vr_sample_stage + vr_sample_compact) == count + fill, bit for bit, also
-    through the overflow path (staging too small: fill pass, staging grown for next call)."""
+def test_sampler_one_walk_matches_fill(name, stats, prefilter):
+    """One-walk K1 (vr_sample_stage + vr_sample_compact, with or without the multi-rank
+    ray prefilter) == count + fill, bit for bit, also through the overflow path (staging
+    too small: fill pass, staging grown for next call)."""
     g = load_npz(name)
     tree = vr.tree_from_json(g["tree"])
     rays = _soa(g["rays"])
-    for rank, world in ((0, 1), (0, 2), (1, 2)):
+    for rank, world in ((0, 1), (0, 2), (1, 2), (3, 4)):
+        if len(tree.leaves) % world:
+            continue
         pool = _pool(tree, rank=rank, world=world)
+        pool.k1_prefilter = prefilter
         rd = pool.rays_to_device(rays)
         pool.stage_k1 = False
         ref = pool.sample(rd, float(g["dt"]), stats=stats)
