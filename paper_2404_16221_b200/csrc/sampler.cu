@@ -37,6 +37,7 @@
 namespace vr {
 
 constexpr int K1_WARPS = 4;
+constexpr int K1_MIN_BLOCKS = 8;   // 64 registers: 32 resident warps per SM
 
 struct K1Smem {
   VrTree tree;
@@ -104,7 +105,7 @@ __global__ void __launch_bounds__(256)
 // [b * slice, (b + 1) * slice); sslot[r] + (index along the ray) is a piece's slot.
 // stage_info[0] += slots reserved, stage_info[1] = max over blocks (the slice needed).
 template <bool FILL, bool RESTRICT, bool STAGE>
-__global__ void __launch_bounds__(K1_WARPS * 32)
+__global__ void __launch_bounds__(K1_WARPS * 32, K1_MIN_BLOCKS)
     k_sample(const VrTree tree_param, const double* __restrict__ rays, int64_t stride,
              int64_t n_rays, double dt, int region_lo, int region_cnt, int32_t* counts,
              int32_t* seg_first, double* ray_te, uint32_t* ray_part, int32_t* ray_total,
