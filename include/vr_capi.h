@@ -365,8 +365,10 @@ int vr_interlevel(const double* t0_dev, const double* t1_dev, const float* sig_r
                   int64_t n_rays, int32_t region_cnt, float lambda_interlevel, float eps,
                   double* seg_loss_dev, float* dsig_prop_dev, void* stream);
 
-/* deterministic float64 sum (fixed reduction tree) */
-int vr_sum_f64(const double* x_dev, int64_t n, double* out_dev, void* stream);
+/* deterministic float64 sum (fixed reduction tree); ws_dev: VR_SUM_PARTIALS doubles of
+ * caller-owned scratch (stream-ordered like every buffer here) */
+#define VR_SUM_PARTIALS 296
+int vr_sum_f64(const double* x_dev, int64_t n, double* out_dev, double* ws_dev, void* stream);
 
 /* ---- optimiser ------------------------------------------------ */
 int vr_adam_step(float* param_dev, const float* grad_dev, float* m_dev, float* v_dev, int64_t n,

@@ -27,6 +27,7 @@ VR_MAX_CHILDREN = 8
 VR_MAX_LEVELS = 16
 VR_PACKET_FLOATS = 8
 VR_OUT_FIELDS = 7
+VR_SUM_PARTIALS = 296  # vr_sum_f64 scratch (doubles)
 
 VR_FLAG_NONFINITE = 1
 VR_FLAG_NEG_LOSS = 2
@@ -143,7 +144,7 @@ SIGNATURES = {
     "vr_global_train": [P, I32, I64, P, P, P, F32, I32, I32, P, P, P, P, P],
     "vr_prefix_train": [P, P, I32, I64, I32, I32, P, P],
     "vr_interlevel": [P, P, P, P, P, P, I64, I32, F32, F32, P, P, P],
-    "vr_sum_f64": [P, I64, P, P],
+    "vr_sum_f64": [P, I64, P, P, P],
     "vr_adam_step": [P, P, P, P, I64, F32, F32, F32, F32, I32, P],
     "vr_cast_f32_f16": [P, P, I64, P],
 }

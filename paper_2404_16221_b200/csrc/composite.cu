@@ -394,7 +394,7 @@ __global__ void k_global(const float4* __restrict__ pk, int n_regions, int64_t n
 }
 
 // ---- deterministic float64 sum ---------------------------------------------------------
-constexpr int SUM_BLOCKS = 296;
+constexpr int SUM_BLOCKS = VR_SUM_PARTIALS;
 constexpr int SUM_THREADS = 256;
 
 __global__ void k_sum_partial(const double* __restrict__ x, int64_t n, double* partial) {
@@ -696,18 +696,14 @@ extern "C" int vr_packets_unpack(const float* recv, int32_t world, int64_t rows,
   return check_launch("vr_packets_unpack");
 }
 
-extern "C" int vr_sum_f64(const double* x, int64_t n, double* out, void* stream) {
-  if (n < 0 || !out) {
+extern "C" int vr_sum_f64(const double* x, int64_t n, double* out, double* ws, void* stream) {
+  if (n < 0 || !out || !ws) {
     set_error("vr_sum_f64: bad argument");
     return VR_ERR_BAD_ARG;
   }
-  static double* partial = nullptr;
-  if (!partial && cudaMalloc(&partial, SUM_BLOCKS * sizeof(double)) != cudaSuccess) {
-    set_error("vr_sum_f64: cudaMalloc failed");
-    return VR_ERR_CUDA;
-  }
-  k_sum_partial<<<SUM_BLOCKS, SUM_THREADS, 0, (cudaStream_t)stream>>>(x, n, partial);
-  k_sum_final<<<1, 32, 0, (cudaStream_t)stream>>>(partial, out);
+  cudaStream_t s = (cudaStream_t)stream;
+  k_sum_partial<<<SUM_BLOCKS, SUM_THREADS, 0, s>>>(x, n, ws);
+  k_sum_final<<<1, 32, 0, s>>>(ws, out);
   return check_launch("vr_sum_f64");
 }
 

@@ -302,15 +302,11 @@ extern "C" int vr_mlp_bwd(const void* w, const void* enc, const double* rays, in
     return VR_ERR_BAD_ARG;
   }
   if (n == 0) return VR_OK;
-  static bool attr = false;
   const int smem = (int)sizeof(MlpBwdSmem);
-  if (!attr) {
-    if (cudaFuncSetAttribute(k_mlp_bwd, cudaFuncAttributeMaxDynamicSharedMemorySize, smem) !=
-        cudaSuccess) {
-      set_error("vr_mlp_bwd: cannot raise shared memory limit");
-      return VR_ERR_CUDA;
-    }
-    attr = true;
+  if (cudaFuncSetAttribute(k_mlp_bwd, cudaFuncAttributeMaxDynamicSharedMemorySize, smem) !=
+      cudaSuccess) {
+    set_error("vr_mlp_bwd: cannot raise shared memory limit");
+    return VR_ERR_CUDA;
   }
   k_mlp_bwd<<<grid_for(n, MLP_TILE, 1), MLP_TILE, smem, (cudaStream_t)stream>>>(
       (const __half*)w, (const __half2*)enc, rays, stride, rid, n,

@@ -896,15 +896,15 @@ using namespace vr;
 
 namespace {
 
+// set on every launch (a host call of ~1 us): no process-wide flag, so any device and any
+// host thread get the attribute on the context they launch in
 template <class K>
-int set_smem(K kernel, uint32_t bytes, bool& done, const char* who) {
-  if (done) return VR_OK;
+int set_smem(K kernel, uint32_t bytes, const char* who) {
   if (cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes) !=
       cudaSuccess) {
     set_error(who);
     return VR_ERR_CUDA;
   }
-  done = true;
   return VR_OK;
 }
 
@@ -913,8 +913,7 @@ int launch_fwd(const void* w, const void* enc, const double* rays, int64_t strid
                const int32_t* rid, int64_t n, float* out, const VrHashGridDesc* g,
                const float* table, const double* t0, const double* t1, void* enc_out,
                void* stream) {
-  static bool attr = false;
-  int rc = set_smem(mlp::k_mlp_fwd_tc<FUSED, DENS>, mlp::F_SMEM, attr, "mlp fwd: smem attribute");
+  int rc = set_smem(mlp::k_mlp_fwd_tc<FUSED, DENS>, mlp::F_SMEM, "mlp fwd: smem attribute");
   if (rc != VR_OK) return rc;
   VrHashGridDesc gd;
   if (g) gd = *g; else memset(&gd, 0, sizeof(gd));
@@ -932,8 +931,7 @@ int launch_bwd(const void* w, const void* enc, const double* rays, int64_t strid
                const int32_t* rid, int64_t n, const float* dsr, float* gW, float* denc,
                int32_t* err, const VrHashGridDesc* g, const double* t0, const double* t1,
                float* grad_table, void* ws, size_t ws_bytes, const float* pos, void* stream) {
-  static bool attr = false;
-  int rc = set_smem(mlp::k_mlp_bwd_tc<FUSED, DENS>, mlp::B_SMEM, attr, "mlp bwd: smem attribute");
+  int rc = set_smem(mlp::k_mlp_bwd_tc<FUSED, DENS>, mlp::B_SMEM, "mlp bwd: smem attribute");
   if (rc != VR_OK) return rc;
   VrHashGridDesc gd;
   RepPlan plan;

@@ -152,6 +152,12 @@ class VolumePool:
             raise ValueError("rays must be float64 SoA [8][R]")
         return t.to(self.device, non_blocking=True).contiguous()
 
+    def _sum_scratch(self) -> torch.Tensor:
+        if getattr(self, "_sum_ws", None) is None:
+            self._sum_ws = torch.empty(_lib.VR_SUM_PARTIALS, dtype=torch.float64,
+                                       device=self.device)
+        return self._sum_ws
+
     def _workspace(self, n: int) -> torch.Tensor:
         need = int(_lib.load().vr_scan_workspace_bytes(n))
         if self._ws is None or self._ws.numel() < need:
@@ -579,7 +585,8 @@ class VolumePool:
                   self.region_cnt, _lib.ptr(out), _lib.ptr(ray_loss), _lib.ptr(dpk),
                   _lib.ptr(self.err), s)
         loss = torch.empty(1, dtype=torch.float64, device=self.device)
-        _lib.call("vr_sum_f64", _lib.ptr(ray_loss), R, _lib.ptr(loss), s)
+        _lib.call("vr_sum_f64", _lib.ptr(ray_loss), R, _lib.ptr(loss),
+                  _lib.ptr(self._sum_scratch()), s)
         if interlevel:
             prefix = torch.empty((b.region_cnt, R, 2), dtype=torch.float32, device=self.device)
             _lib.call("vr_prefix_train", _lib.ptr(allp), _lib.ptr(all_T), allp.shape[0], R,
@@ -592,7 +599,8 @@ class VolumePool:
                       b.region_cnt, float(lambda_interlevel), float(eps), _lib.ptr(seg_loss),
                       _lib.ptr(dsig_prop), s)
             il = torch.empty(1, dtype=torch.float64, device=self.device)
-            _lib.call("vr_sum_f64", _lib.ptr(seg_loss), seg_loss.numel(), _lib.ptr(il), s)
+            _lib.call("vr_sum_f64", _lib.ptr(seg_loss), seg_loss.numel(), _lib.ptr(il),
+                      _lib.ptr(self._sum_scratch()), s)
             loss = loss + il
         dsig = torch.zeros((max(b.n_samples, 1), 4), dtype=torch.float32, device=self.device)
         _lib.call("vr_segment_bwd", _lib.ptr(b.t0), _lib.ptr(b.t1), _lib.ptr(sig_rgb),
@@ -621,7 +629,8 @@ class VolumePool:
                   _lib.addr(self._set_bg(background)), _lib.ptr(tg), float(lambda_dist), 0, 1,
                   _lib.ptr(out), _lib.ptr(ray_loss), _lib.ptr(dpk), _lib.ptr(self.err), s)
         loss = torch.empty(1, dtype=torch.float64, device=self.device)
-        _lib.call("vr_sum_f64", _lib.ptr(ray_loss), R, _lib.ptr(loss), s)
+        _lib.call("vr_sum_f64", _lib.ptr(ray_loss), R, _lib.ptr(loss),
+                  _lib.ptr(self._sum_scratch()), s)
         dsr = torch.zeros_like(srr)
         _lib.call("vr_segment_bwd", _lib.ptr(t0r), _lib.ptr(t1r), _lib.ptr(srr), _lib.ptr(ray_off),
                   _lib.ptr(b.ray_te), R, 1, _lib.ptr(dpk), _lib.ptr(dsr), s)

@@ -51,3 +51,13 @@ def test_bad_arguments_are_rejected_without_a_gpu():
     assert b"bad argument" in lib.vr_last_error()
     with pytest.raises(ValueError):
         _lib.call("vr_segment_fwd", None, None, None, None, None, None, 4, 0, None, None, None)
+
+
+def test_header_constants_match_ctypes_mirror():
+    """Every #define VR_* integer of the header has the same value in _lib."""
+    defs = dict(re.findall(r"#define\s+(VR_[A-Z0-9_]+)\s+(-?\d+)\b", HEADER.read_text()))
+    assert "VR_SUM_PARTIALS" in defs and "VR_MAX_REGIONS" in defs
+    mirrored = {k: v for k, v in defs.items() if hasattr(_lib, k)}
+    assert len(mirrored) >= 8
+    for k, v in mirrored.items():
+        assert getattr(_lib, k) == int(v), k
