@@ -439,7 +439,10 @@ def main():
         dist.all_reduce(t_ms, op=dist.ReduceOp.MAX)
     ms = float(t_ms.item())
     value = R / (ms / 1e3)
-    launches = sum(n * _lib.LAUNCHES.get(k, 1) for k, n in calls.items())
+    per_call = dict(_lib.LAUNCHES)
+    if world > 1:  # k_sample_prefilter + the walk
+        per_call["vr_sample_stage"] = 2
+    launches = sum(n * per_call.get(k, 1) for k, n in calls.items())
     final_loss = float(loss.item()) if train else None
 
     # samples per step (for per-sample kernel costs)

@@ -185,7 +185,12 @@ def load(path: str | os.PathLike | None = None) -> C.CDLL:
 # before(name, args) / after(name), both recording events on the current stream.
 TIMER = None
 # kernel launches per entry point (for bench.py's gpu_launches count)
-LAUNCHES = {"vr_scan_offsets": 3, "vr_sum_f64": 2, "vr_adam_step": 2}
+# kernels per call where it is not one (checked against the ncu launch list of a c3 step;
+# the hash-grid backward entry points add k_hash_rep_reduce for the replicated coarse
+# level, vr_sample_stage adds k_sample_prefilter on a rank owning part of the regions)
+LAUNCHES = {"vr_scan_offsets": 3, "vr_sum_f64": 2, "vr_field_bwd_tc": 2, "vr_hash_bwd": 2,
+            "vr_hash_scatter": 2, "vr_hash_bwd_lm": 2, "vr_packets_pack": 2,
+            "vr_packets_unpack": 2}
 CALLS = {}
 
 
