@@ -301,10 +301,13 @@ int vr_field_bwd_tc(const VrHashGridDesc* g, const void* weights_dev, const void
 
 /* ---- K4: per-segment front-to-back composite (composite_samples quadrature.py:141-165,
  * aggregate_segment segrender.py:71-90, process_inbox distsim.py:318-329) ------------- */
+/* seg_totals_dev (optional, [region_cnt * n_rays][7] float64): each non-empty segment's
+ * totals {T, C[3], A, D, L} before the float32 rounding of its packet, for
+ * vr_segment_bwd (which otherwise recomputes them in a first sweep). */
 int vr_segment_fwd(const double* t0_dev, const double* t1_dev, const float* sig_rgb_dev,
                    const int64_t* offsets_dev, const int32_t* seg_first_dev,
                    const double* ray_te_dev, int64_t n_rays, int32_t region_cnt,
-                   float* packets_dev, int32_t* err_dev, void* stream);
+                   float* packets_dev, double* seg_totals_dev, int32_t* err_dev, void* stream);
 /* Sample-broadcast protocol (distsim.py:311-316, _compose_samples distsim.py:385-392):
  * move per-sample elements (4, 8 or 16 bytes) between the region-major K1 layout and a
  * ray-major layout (ray_off = exclusive scan of per-ray totals, a ray's segments in t
@@ -332,8 +335,9 @@ int vr_packets_unpack(const float* recv_dev, int32_t world, int64_t rows, int32_
  * writes dsig_rgb[i] = {dL/dsigma, dL/dr, dL/dg, dL/db}. */
 int vr_segment_bwd(const double* t0_dev, const double* t1_dev, const float* sig_rgb_dev,
                    const int64_t* offsets_dev, const double* ray_te_dev, int64_t n_rays,
-                   int32_t region_cnt, const float* dpackets_dev, float* dsig_rgb_dev,
-                   void* stream);
+                   int32_t region_cnt, const float* dpackets_dev,
+                   const double* seg_totals_dev /* from vr_segment_fwd, or NULL */,
+                   float* dsig_rgb_dev, void* stream);
 
 /* ---- K5: global composite (compose_render segrender.py:93-110, compose_distortion
  * segrender.py:113-142, _compose_tile distsim.py:376-382) --------------------------

@@ -29,6 +29,7 @@
 namespace vr {
 
 constexpr int SEG_WARPS = 8;
+constexpr int SEG_TOT = 7;  // float64 segment totals kept for the backward: T, C[3], A, D, L
 
 __device__ __forceinline__ float order_bits(int32_t first) { return __int_as_float(first); }
 
@@ -145,7 +146,8 @@ __global__ void __launch_bounds__(SEG_WARPS * 32)
     k_segment_fwd_grp(const double* __restrict__ t0, const double* __restrict__ t1,
                       const float4* __restrict__ sr, const int64_t* __restrict__ off,
                       const int32_t* __restrict__ seg_first, const double* __restrict__ ray_te,
-                      int64_t n_rays, int64_t n_segs, float4* __restrict__ packets) {
+                      int64_t n_rays, int64_t n_segs, float4* __restrict__ packets,
+                      double* __restrict__ seg_tot) {
   const int lane = threadIdx.x & 31;
   const int64_t n_groups = ceil_div(n_segs, 32);
   for (int64_t grp = (int64_t)blockIdx.x * SEG_WARPS + (threadIdx.x >> 5); grp < n_groups;
@@ -176,6 +178,16 @@ __global__ void __launch_bounds__(SEG_WARPS * 32)
                                        (float)c.c_incl[2]);
         packets[2 * seg + 1] = make_float4((float)c.a_incl, (float)c.d_incl, (float)c.l_incl,
                                            order_bits(seg_first[seg]));
+        if (seg_tot) {  // float64 totals for the backward (its sweep 1)
+          double* st = seg_tot + SEG_TOT * seg;
+          st[0] = c.Tn;
+          st[1] = c.c_incl[0];
+          st[2] = c.c_incl[1];
+          st[3] = c.c_incl[2];
+          st[4] = c.a_incl;
+          st[5] = c.d_incl;
+          st[6] = c.l_incl;
+        }
       }
       cin = carry_out(c);
     }
@@ -188,7 +200,8 @@ __global__ void __launch_bounds__(SEG_WARPS * 32)
     k_segment_bwd_grp(const double* __restrict__ t0, const double* __restrict__ t1,
                       const float4* __restrict__ sr, const int64_t* __restrict__ off,
                       const double* __restrict__ ray_te, int64_t n_rays, int64_t n_segs,
-                      const float4* __restrict__ dpk, float4* __restrict__ dsr) {
+                      const float4* __restrict__ dpk, const double* __restrict__ seg_tot,
+                      float4* __restrict__ dsr) {
   __shared__ double s_tot[SEG_WARPS][32][6];  // T, A, D, L, Vtot, bT*T per segment
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
   double(*tot)[6] = s_tot[wid];
@@ -210,10 +223,25 @@ __global__ void __launch_bounds__(SEG_WARPS * 32)
       g0 = dpk[2 * my];
       g1 = dpk[2 * my + 1];
     }
-    // sweep 1: totals
+    // sweep 1: totals (from the forward's float64 totals when it kept them)
     Carry cin = {1.0, 0.0, 0.0, 0.0, 0.0, 0.0, 0.0, 0.0};
-    ChunkIn nxt = chunk_load(t0, t1, sr, s_beg + lane, s_end);
-    for (int64_t base = s_beg; base < s_end; base += 32) {
+    ChunkIn nxt = {0.0, 0.0, make_float4(0.f, 0.f, 0.f, 0.f)};
+    if (!seg_tot) nxt = chunk_load(t0, t1, sr, s_beg + lane, s_end);
+    if (seg_tot) {
+      if (lane < nseg && gs.lo < gs.hi) {
+        const double* st = seg_tot + SEG_TOT * my;
+        const double Tn = st[0], c0 = st[1], c1 = st[2], c2 = st[3], a = st[4], d = st[5],
+                     l = st[6];
+        tot[lane][0] = Tn;
+        tot[lane][1] = a;
+        tot[lane][2] = d;
+        tot[lane][3] = l;
+        tot[lane][4] = (double)g0.y * c0 + (double)g0.z * c1 + (double)g0.w * c2 +
+                       (double)g1.x * a + (double)g1.y * d + 2.0 * (double)g1.z * l;
+        tot[lane][5] = (double)g0.x * Tn;
+      }
+    }
+    for (int64_t base = s_beg; !seg_tot && base < s_end; base += 32) {
       const ChunkIn cur = nxt;
       nxt = chunk_load(t0, t1, sr, base + 32 + lane, s_end);
       const ChunkFwd c =
@@ -464,8 +492,8 @@ using namespace vr;
 
 extern "C" int vr_segment_fwd(const double* t0, const double* t1, const float* sr,
                               const int64_t* off, const int32_t* seg_first, const double* ray_te,
-                              int64_t n_rays, int32_t region_cnt, float* packets, int32_t* err,
-                              void* stream) {
+                              int64_t n_rays, int32_t region_cnt, float* packets,
+                              double* seg_totals, int32_t* err, void* stream) {
   (void)err;
   if (n_rays < 0 || region_cnt < 1 || region_cnt > VR_MAX_REGIONS) {
     set_error("vr_segment_fwd: bad argument");
@@ -476,13 +504,14 @@ extern "C" int vr_segment_fwd(const double* t0, const double* t1, const float* s
   k_segment_fwd_grp<<<grid_for(ceil_div(n_segs, 32 * SEG_WARPS), 1, 8), SEG_WARPS * 32, 0,
                       (cudaStream_t)stream>>>(t0, t1, reinterpret_cast<const float4*>(sr), off,
                                               seg_first, ray_te, n_rays, n_segs,
-                                              reinterpret_cast<float4*>(packets));
+                                              reinterpret_cast<float4*>(packets), seg_totals);
   return check_launch("vr_segment_fwd");
 }
 
 extern "C" int vr_segment_bwd(const double* t0, const double* t1, const float* sr,
                               const int64_t* off, const double* ray_te, int64_t n_rays,
-                              int32_t region_cnt, const float* dpk, float* dsr, void* stream) {
+                              int32_t region_cnt, const float* dpk, const double* seg_totals,
+                              float* dsr, void* stream) {
   if (n_rays < 0 || region_cnt < 1 || region_cnt > VR_MAX_REGIONS) {
     set_error("vr_segment_bwd: bad argument");
     return VR_ERR_BAD_ARG;
@@ -492,7 +521,7 @@ extern "C" int vr_segment_bwd(const double* t0, const double* t1, const float* s
   k_segment_bwd_grp<<<grid_for(ceil_div(n_segs, 32 * SEG_WARPS), 1, 8), SEG_WARPS * 32, 0,
                       (cudaStream_t)stream>>>(t0, t1, reinterpret_cast<const float4*>(sr), off,
                                               ray_te, n_rays, n_segs,
-                                              reinterpret_cast<const float4*>(dpk),
+                                              reinterpret_cast<const float4*>(dpk), seg_totals,
                                               reinterpret_cast<float4*>(dsr));
   return check_launch("vr_segment_bwd");
 }

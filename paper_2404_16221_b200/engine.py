@@ -414,12 +414,19 @@ class VolumePool:
                                dsig_rgb[lo:], s)
 
     # ---- K4 ----------------------------------------------------------------------------
-    def local_packets(self, b: SampleBatch, sig_rgb: torch.Tensor) -> torch.Tensor:
+    def local_packets(self, b: SampleBatch, sig_rgb: torch.Tensor,
+                      totals: torch.Tensor | None = None) -> torch.Tensor:
+        """K4 forward; totals (float64 [cnt*R*7], training): the segments' unrounded totals,
+        which spare vr_segment_bwd its first sweep."""
         pk = torch.empty((b.region_cnt, b.n_rays, 8), dtype=torch.float32, device=self.device)
         _lib.call("vr_segment_fwd", _lib.ptr(b.t0), _lib.ptr(b.t1), _lib.ptr(sig_rgb),
                   _lib.ptr(b.offsets), _lib.ptr(b.seg_first), _lib.ptr(b.ray_te), b.n_rays,
-                  b.region_cnt, _lib.ptr(pk), _lib.ptr(self.err), self._stream())
+                  b.region_cnt, _lib.ptr(pk), _lib.ptr(totals), _lib.ptr(self.err),
+                  self._stream())
         return pk
+
+    def _segment_totals(self, n_segs: int) -> torch.Tensor:
+        return torch.empty(max(n_segs, 1) * 7, dtype=torch.float64, device=self.device)
 
     def exchange_packets(self, b: SampleBatch, local: torch.Tensor, extra=None,
                          dst: int | None = None):
@@ -525,13 +532,13 @@ class VolumePool:
                   1 if to_ray_major else 0, self._stream())
         return dst
 
-    def _whole_ray_packets(self, b: SampleBatch, ray_off, t0r, t1r, srr):
+    def _whole_ray_packets(self, b: SampleBatch, ray_off, t0r, t1r, srr, totals=None):
         R = b.n_rays
         pk = torch.empty((1, R, 8), dtype=torch.float32, device=self.device)
         first = torch.zeros(R, dtype=torch.int32, device=self.device)  # one packet per ray
         _lib.call("vr_segment_fwd", _lib.ptr(t0r), _lib.ptr(t1r), _lib.ptr(srr),
                   _lib.ptr(ray_off), _lib.ptr(first), _lib.ptr(b.ray_te), R, 1, _lib.ptr(pk),
-                  _lib.ptr(self.err), self._stream())
+                  _lib.ptr(totals), _lib.ptr(self.err), self._stream())
         return pk
 
     def _sample_protocol_forward(self, rays, dt: float, train: bool):
@@ -568,7 +575,8 @@ class VolumePool:
         # batch: sample_async
         b = batch if batch is not None else self.sample(rays, dt, exchange=True)
         sig_rgb = self.evaluate(rays, b)
-        local = self.local_packets(b, sig_rgb)
+        totals = self._segment_totals(b.region_cnt * b.n_rays)
+        local = self.local_packets(b, sig_rgb, totals)
         interlevel = self.proposals is not None and lambda_interlevel > 0.0
         prop_T = None
         if interlevel:
@@ -605,7 +613,7 @@ class VolumePool:
         dsig = torch.zeros((max(b.n_samples, 1), 4), dtype=torch.float32, device=self.device)
         _lib.call("vr_segment_bwd", _lib.ptr(b.t0), _lib.ptr(b.t1), _lib.ptr(sig_rgb),
                   _lib.ptr(b.offsets), _lib.ptr(b.ray_te), R, b.region_cnt, _lib.ptr(dpk),
-                  _lib.ptr(dsig), s)
+                  _lib.ptr(totals), _lib.ptr(dsig), s)
         # NeRF fields and proposals in one backward pipeline (the proposals' MLP backward
         # overlaps the NeRF scatter on the side stream)
         jobs = [(self.fields, dsig)]
@@ -621,7 +629,8 @@ class VolumePool:
         s = self._stream()
         b, (sig_rgb, ray_off, (t0r, t1r, srr)) = self._sample_protocol_forward(rays, dt, True)
         R = b.n_rays
-        pk = self._whole_ray_packets(b, ray_off, t0r, t1r, srr)
+        totals = self._segment_totals(R)
+        pk = self._whole_ray_packets(b, ray_off, t0r, t1r, srr, totals)
         out = torch.empty((7, R), dtype=torch.float32, device=self.device)
         ray_loss = torch.empty(R, dtype=torch.float64, device=self.device)
         dpk = torch.empty((1, R, 8), dtype=torch.float32, device=self.device)
@@ -633,7 +642,7 @@ class VolumePool:
                   _lib.ptr(self._sum_scratch()), s)
         dsr = torch.zeros_like(srr)
         _lib.call("vr_segment_bwd", _lib.ptr(t0r), _lib.ptr(t1r), _lib.ptr(srr), _lib.ptr(ray_off),
-                  _lib.ptr(b.ray_te), R, 1, _lib.ptr(dpk), _lib.ptr(dsr), s)
+                  _lib.ptr(b.ray_te), R, 1, _lib.ptr(dpk), _lib.ptr(totals), _lib.ptr(dsr), s)
         dsig = self._permute(b, ray_off, dsr, False)
         self.field_backward(rays, b, dsig)
         return loss, out, b

@@ -50,7 +50,8 @@ def test_bad_arguments_are_rejected_without_a_gpu():
     assert rc == 1
     assert b"bad argument" in lib.vr_last_error()
     with pytest.raises(ValueError):
-        _lib.call("vr_segment_fwd", None, None, None, None, None, None, 4, 0, None, None, None)
+        _lib.call("vr_segment_fwd", None, None, None, None, None, None, 4, 0, None, None, None,
+                  None)
 
 
 def test_header_constants_match_ctypes_mirror():

@@ -258,6 +258,37 @@ def test_multi_rank_composite_is_bitwise_identical():
     assert torch.equal(out1, out2)
 
 
+@pytest.mark.parametrize("name", ["render_three_blobs_k8.npz", "render_street_k8.npz"])
+def test_segment_bwd_with_forward_totals(name):
+    """vr_segment_bwd from the forward's float64 segment totals (no first sweep) gives the
+    per-sample gradients of the recomputing path."""
+    from paper_2404_16221_b200 import _lib
+
+    g = load_npz(name)
+    rays = _soa(g["rays"])
+    dt = float(g["dt"])
+    p, _, _ = _scene_pool(g)
+    rd = p.rays_to_device(rays)
+    b = p.sample(rd, dt)
+    sr = p.evaluate(rd, b)
+    R = b.n_rays
+    totals = p._segment_totals(b.region_cnt * R)
+    pk = p.local_packets(b, sr, totals)
+    # keeping totals leaves the packets alone (bit compare: order keys of empty ones are NaNs)
+    assert torch.equal(pk.view(torch.int32), p.local_packets(b, sr).view(torch.int32))
+    gen = torch.Generator(device=DEV).manual_seed(5)
+    dpk = torch.randn((b.region_cnt, R, 8), device=DEV, generator=gen)
+    out = []
+    for t in (None, totals):
+        dsig = torch.zeros((max(b.n_samples, 1), 4), dtype=torch.float32, device=DEV)
+        _lib.call("vr_segment_bwd", _lib.ptr(b.t0), _lib.ptr(b.t1), _lib.ptr(sr),
+                  _lib.ptr(b.offsets), _lib.ptr(b.ray_te), R, b.region_cnt, _lib.ptr(dpk),
+                  _lib.ptr(t), _lib.ptr(dsig), _lib.stream_ptr())
+        out.append(dsig)
+    torch.cuda.synchronize()
+    torch.testing.assert_close(out[1], out[0], rtol=1e-6, atol=1e-9)
+
+
 @pytest.mark.parametrize("world", [2, 4])
 @pytest.mark.parametrize("with_extra", [False, True])
 def test_sparse_packet_exchange_kernels(world, with_extra):
@@ -397,7 +428,7 @@ def test_voxel_gradients_locality(world):
         losses.append(rl.sum().item())
         dsig = torch.zeros((max(b.n_samples, 1), 4), dtype=torch.float32, device=DEV)
         _lib.call("vr_segment_bwd", _lib.ptr(b.t0), _lib.ptr(b.t1), _lib.ptr(s), _lib.ptr(b.offsets),
-                  _lib.ptr(b.ray_te), R, b.region_cnt, _lib.ptr(dpk), _lib.ptr(dsig),
+                  _lib.ptr(b.ray_te), R, b.region_cnt, _lib.ptr(dpk), None, _lib.ptr(dsig),
                   _lib.stream_ptr())
         p.field_backward(rd, b, dsig)
     assert len(set(losses)) == 1  # bitwise identical loss on every rank
