@@ -192,7 +192,9 @@ def build_pool(w, rank, world, dev, group, seed_base=1):
     if w.interlevel > 0:  # config 4: proposal fields for the interlevel loss
         pcfg = vr.HashGridConfig(log2_T=w.prop_log2_T, max_res=w.prop_max_res)
         # the proposal's colour head is never read: density branch only
-        props = [vr.HashGridMLP(pcfg, tree.leaves[k].box, dev, seed=1000 + k, density_only=True)
+        porder = os.environ.get("VR_BENCH_PROP_HASH_ORDER", "auto")
+        props = [vr.HashGridMLP(pcfg, tree.leaves[k].box, dev, seed=1000 + k, density_only=True,
+                                hash_order=porder)
                  for k in range(lo, lo + cnt)]
     return vr.VolumePool(tree, fields, (0.05, 0.05, 0.08), dev, rank, world, group,
                          proposals=props)
