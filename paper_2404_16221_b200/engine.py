@@ -600,7 +600,8 @@ class VolumePool:
             _lib.call("vr_prefix_train", _lib.ptr(allp), _lib.ptr(all_T), allp.shape[0], R,
                       self.region_lo, self.region_cnt, _lib.ptr(prefix), s)
             seg_loss = torch.empty(b.region_cnt * R, dtype=torch.float64, device=self.device)
-            dsig_prop = torch.zeros((max(b.n_samples, 1), 4), dtype=torch.float32,
+            # every sample of a segment is written (no zero fill of the N x 16 B array)
+            dsig_prop = torch.empty((max(b.n_samples, 1), 4), dtype=torch.float32,
                                     device=self.device)
             _lib.call("vr_interlevel", _lib.ptr(b.t0), _lib.ptr(b.t1), _lib.ptr(sig_rgb),
                       _lib.ptr(sig_prop), _lib.ptr(b.offsets), _lib.ptr(prefix), R,
@@ -610,7 +611,8 @@ class VolumePool:
             _lib.call("vr_sum_f64", _lib.ptr(seg_loss), seg_loss.numel(), _lib.ptr(il),
                       _lib.ptr(self._sum_scratch()), s)
             loss = loss + il
-        dsig = torch.zeros((max(b.n_samples, 1), 4), dtype=torch.float32, device=self.device)
+        # vr_segment_bwd writes every sample (no zero fill of the N x 16 B array)
+        dsig = torch.empty((max(b.n_samples, 1), 4), dtype=torch.float32, device=self.device)
         _lib.call("vr_segment_bwd", _lib.ptr(b.t0), _lib.ptr(b.t1), _lib.ptr(sig_rgb),
                   _lib.ptr(b.offsets), _lib.ptr(b.ray_te), R, b.region_cnt, _lib.ptr(dpk),
                   _lib.ptr(totals), _lib.ptr(dsig), s)
