@@ -62,6 +62,8 @@ KERNEL_COST = {
     "vr_segment_fwd": ("hbm", 32.0, None),
     # t0,t1 (16) + sig_rgb (16) + dsig_rgb (16)
     "vr_segment_bwd": ("hbm", 48.0, None),
+    # t0,t1 (16) + sigma (4)
+    "vr_segment_transmittance": ("hbm", 20.0, None),
 }
 
 

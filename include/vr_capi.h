@@ -333,6 +333,11 @@ int vr_packets_unpack(const float* recv_dev, int32_t world, int64_t rows, int32_
                       int32_t* err_dev, void* stream);
 /* analytic backward: dpackets [region_cnt][n_rays][8] = adjoints of {T,C,A,D',L};
  * writes dsig_rgb[i] = {dL/dsigma, dL/dr, dL/dg, dL/db}. */
+/* transmittance only: T_dev[seg] = the T of vr_segment_fwd's packet (1 for an empty
+ * segment), [region_cnt][n_rays] float32 — the proposal fields' packets (interlevel) */
+int vr_segment_transmittance(const double* t0_dev, const double* t1_dev,
+                             const float* sig_rgb_dev, const int64_t* offsets_dev,
+                             int64_t n_rays, int32_t region_cnt, float* T_dev, void* stream);
 int vr_segment_bwd(const double* t0_dev, const double* t1_dev, const float* sig_rgb_dev,
                    const int64_t* offsets_dev, const double* ray_te_dev, int64_t n_rays,
                    int32_t region_cnt, const float* dpackets_dev,

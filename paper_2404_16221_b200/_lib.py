@@ -137,6 +137,7 @@ SIGNATURES = {
     "vr_field_bwd_tc": [P, P, P, P, I64, P, P, P, I64, P, P, P, P, C.c_size_t, P, P, P],
     "vr_segment_fwd": [P, P, P, P, P, P, I64, I32, P, P, P, P],
     "vr_segment_bwd": [P, P, P, P, P, I64, I32, P, P, P, P],
+    "vr_segment_transmittance": [P, P, P, P, I64, I32, P, P],
     "vr_segment_permute": [P, P, P, I64, I32, P, P, I32, I32, P],
     "vr_packets_pack": [P, P, P, I64, I32, I32, P, I64, P, P, P],
     "vr_packets_unpack": [P, I32, I64, I32, I64, I32, P, P, P, P],

@@ -194,6 +194,51 @@ __global__ void __launch_bounds__(SEG_WARPS * 32)
   }
 }
 
+// Segment transmittance only (the proposal fields' packets: the interlevel loss reads T
+// alone): the forward's product scan without the colour / depth / distortion scans, the
+// same float64 chain, so T[seg] == (float) of the full packet's T bit for bit.
+__global__ void __launch_bounds__(SEG_WARPS * 32)
+    k_segment_T_grp(const double* __restrict__ t0, const double* __restrict__ t1,
+                    const float4* __restrict__ sr, const int64_t* __restrict__ off,
+                    int64_t n_segs, float* __restrict__ T_out) {
+  const int lane = threadIdx.x & 31;
+  const int64_t n_groups = ceil_div(n_segs, 32);
+  const float* sigma = reinterpret_cast<const float*>(sr);
+  for (int64_t grp = (int64_t)blockIdx.x * SEG_WARPS + (threadIdx.x >> 5); grp < n_groups;
+       grp += (int64_t)gridDim.x * SEG_WARPS) {
+    const int64_t seg0 = grp * 32;
+    const int nseg = (int)min((int64_t)32, n_segs - seg0);
+    const int64_t my = seg0 + lane;
+    GroupSeg gs;
+    gs.lo = off[lane < nseg ? my : seg0 + nseg];
+    gs.hi = off[lane < nseg ? my + 1 : seg0 + nseg];
+    const int64_t s_beg = __shfl_sync(0xffffffffu, gs.lo, 0);
+    const int64_t s_end = __shfl_sync(0xffffffffu, gs.hi, nseg - 1);
+    if (lane < nseg && gs.lo == gs.hi) T_out[my] = 1.f;  // empty segment: identity
+    double carry = 1.0;
+    for (int64_t base = s_beg; base < s_end; base += 32) {
+      const int64_t s = base + lane;
+      const bool valid = s < s_end;
+      const int seg = find_seg(gs.lo, nseg, valid ? s : s_end - 1);
+      const int64_t seg_lo = __shfl_sync(0xffffffffu, gs.lo, seg);
+      const int64_t seg_hi = __shfl_sync(0xffffffffu, gs.hi, seg);
+      const bool head = (s == seg_lo) || lane == 0;
+      const int sg0 = __shfl_sync(0xffffffffu, seg, 0);
+      const bool cont = (__shfl_sync(0xffffffffu, (int)(s != seg_lo), 0) != 0) && seg == sg0;
+      double keep = 1.0;
+      if (valid) {
+        const double dlt = t1[s] - t0[s];
+        keep = exp(-((double)sigma[4 * s] * dlt));
+      }
+      double p[1] = {keep};
+      seg_scan<1>(p, head, lane, [](double a, double b) { return a * b; });
+      const double Tn = (cont ? carry : 1.0) * p[0];
+      if (valid && s + 1 == seg_hi) T_out[seg0 + seg] = (float)Tn;
+      carry = __shfl_sync(0xffffffffu, Tn, 31);
+    }
+  }
+}
+
 // Grouped K4 backward: sweep 1 = the forward (segment totals into shared memory),
 // sweep 2 = per-sample gradients with one more segmented scan for sum_{i>j} w_i v_i.
 __global__ void __launch_bounds__(SEG_WARPS * 32)
@@ -506,6 +551,21 @@ extern "C" int vr_segment_fwd(const double* t0, const double* t1, const float* s
                                               seg_first, ray_te, n_rays, n_segs,
                                               reinterpret_cast<float4*>(packets), seg_totals);
   return check_launch("vr_segment_fwd");
+}
+
+extern "C" int vr_segment_transmittance(const double* t0, const double* t1, const float* sr,
+                                        const int64_t* off, int64_t n_rays, int32_t region_cnt,
+                                        float* T_out, void* stream) {
+  if (n_rays < 0 || region_cnt < 1 || region_cnt > VR_MAX_REGIONS || !T_out) {
+    set_error("vr_segment_transmittance: bad argument");
+    return VR_ERR_BAD_ARG;
+  }
+  const int64_t n_segs = n_rays * region_cnt;
+  if (n_segs == 0) return VR_OK;
+  k_segment_T_grp<<<grid_for(ceil_div(n_segs, 32 * SEG_WARPS), 1, 8), SEG_WARPS * 32, 0,
+                    (cudaStream_t)stream>>>(t0, t1, reinterpret_cast<const float4*>(sr), off,
+                                            n_segs, T_out);
+  return check_launch("vr_segment_transmittance");
 }
 
 extern "C" int vr_segment_bwd(const double* t0, const double* t1, const float* sr,

@@ -582,7 +582,11 @@ class VolumePool:
         if interlevel:
             sig_prop = self.evaluate(rays, b, self.proposals)
             # only the proposal transmittance of each segment crosses the link
-            prop_T = self.local_packets(b, sig_prop)[:, :, 0].contiguous()
+            prop_T = torch.empty((b.region_cnt, b.n_rays), dtype=torch.float32,
+                                 device=self.device)
+            _lib.call("vr_segment_transmittance", _lib.ptr(b.t0), _lib.ptr(b.t1),
+                      _lib.ptr(sig_prop), _lib.ptr(b.offsets), b.n_rays, b.region_cnt,
+                      _lib.ptr(prop_T), s)
         allp, all_T = self.exchange_packets(b, local, prop_T)
         R = b.n_rays
         out = torch.empty((7, R), dtype=torch.float32, device=self.device)

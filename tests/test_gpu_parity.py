@@ -287,6 +287,12 @@ def test_segment_bwd_with_forward_totals(name):
         out.append(dsig)
     torch.cuda.synchronize()
     torch.testing.assert_close(out[1], out[0], rtol=1e-6, atol=1e-9)
+    # the transmittance-only kernel (proposal packets) gives the packets' T bit for bit
+    T = torch.empty((b.region_cnt, R), dtype=torch.float32, device=DEV)
+    _lib.call("vr_segment_transmittance", _lib.ptr(b.t0), _lib.ptr(b.t1), _lib.ptr(sr),
+              _lib.ptr(b.offsets), R, b.region_cnt, _lib.ptr(T), _lib.stream_ptr())
+    torch.cuda.synchronize()
+    assert torch.equal(T, pk[:, :, 0])
 
 
 @pytest.mark.parametrize("world", [2, 4])
