@@ -106,7 +106,7 @@ class VolumePool:
                 f.err = self.err  # kernels of the fields report into the pool's flag word
         self._ws = None
         self._side = None
-        self.overlap_regions = False
+        self.overlap_regions = os.environ.get("VR_OVERLAP_FWD", "0") == "1"
         # split backward (MLP here, hash-grid scatter on a side stream) for the fields that
         # prefer it (HashGridMLP.split_backward); the others use the fused tensor-core kernel
         # (vr_field_bwd_tc), measured faster on c3 (61.3 vs 64.8 ms: the MLP's shared-memory
@@ -340,8 +340,10 @@ class VolumePool:
         alloc = torch.zeros if base or len(fields) < b.region_cnt else torch.empty
         sig_rgb = alloc((max(b.n_samples, 1), 4), dtype=torch.float32, device=self.device)
         s = self._stream()
-        # Off by default: measured on c3 the concurrent MLP CTAs (52 KB smem each) shrink the
-        # L1 the gathers live on and the step got slower (76.7 vs 67.6 ms).
+        # Off by default (VR_OVERLAP_FWD=1): with the old 52 KB-smem MLP forward the step got
+        # slower (c3 76.7 vs 67.6 ms); with the 20 KB TS-mode forward it is a wash at c3
+        # (56.6 vs 56.7 ms) and slower at c5 (86.9 vs 84.2) — the gathers are L2-request
+        # bound and the MLP CTAs still take their issue slots.
         split = (self.overlap_regions and len(fields) > 1
                  and all(getattr(f, "splittable", False) for f in fields))
         if not split:
