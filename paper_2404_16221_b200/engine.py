@@ -2,10 +2,11 @@
 
 Reference call stack replaced (distsim._run_ray, distsim.py:395-454):
 
-    _prepare_samples + bin assignment   -> K1  vr_sample_count / vr_scan_offsets / vr_sample_fill
+    _prepare_samples + bin assignment   -> K1  vr_sample_stage / vr_scan_offsets / vr_sample_compact
     Worker.process_inbox: fill_samples  -> region field kernels (analytic / voxel / hash+MLP)
     Worker.process_inbox: composite     -> K4  vr_segment_fwd        (one packet per segment)
-    transit + stats.record              -> comm.all_gather_packets / gather_packets (NCCL)
+    transit + stats.record              -> vr_packets_pack, NCCL all-gather / gather,
+                                           vr_packets_unpack (records of non-empty segments)
     _compose_tile / _broadcast_compose  -> K5  vr_global_fwd / vr_global_train
     (no reference)                      -> K5 bwd, K4 bwd, field bwd, Adam
 
