@@ -527,10 +527,10 @@ def main():
         copy_stream = torch.cuda.Stream(device=dev)
         main_stream = torch.cuda.current_stream()
 
-        def fetch():
+        def fetch():  # render needs no targets
             with torch.cuda.stream(copy_stream):
                 r = rays_h.to(dev, non_blocking=True)
-                t = tg_h.to(dev, non_blocking=True)
+                t = tg_h.to(dev, non_blocking=True) if train else None
                 ev = torch.cuda.Event()
                 ev.record(copy_stream)
             return r, t, ev
@@ -538,25 +538,37 @@ def main():
         # the step's result lands in a pinned host buffer (a pageable D2H of the 25 MB c5
         # frame runs at a few GB/s and would time the host allocator, not the path)
         out_h = None if train else torch.empty((3, R), dtype=torch.float32, pin_memory=True)
+
+        def e2e_loop(steps):
+            nxt = fetch()
+            for k in range(steps):
+                r_d, t_d, ev = nxt
+                main_stream.wait_event(ev)
+                r_d.record_stream(main_stream)
+                if t_d is not None:
+                    t_d.record_stream(main_stream)
+                if k + 1 < steps:
+                    nxt = fetch()
+                    res = one_step(r_d, t_d, nxt[0], nxt[2])
+                else:
+                    res = one_step(r_d, t_d)
+                if train:
+                    _ = float(res.item())  # D2H read of the step's loss
+                elif res is not None:  # D2H read of the rendered colours
+                    out_h.copy_(res[0:3], non_blocking=True)
+                    torch.cuda.current_stream().synchronize()
+
+        # untimed warm-up of the pipeline itself (first-use allocations of the per-step
+        # device input buffers on the copy stream cost tens of ms on a fresh box)
+        e2e_loop(args.warmup)
+        torch.cuda.synchronize()
+        restore()
+        if world > 1:
+            dist.barrier()
         t0 = torch.cuda.Event(enable_timing=True)
         t1 = torch.cuda.Event(enable_timing=True)
         t0.record()
-        nxt = fetch()
-        for k in range(args.steps):
-            r_d, t_d, ev = nxt
-            main_stream.wait_event(ev)
-            r_d.record_stream(main_stream)
-            t_d.record_stream(main_stream)
-            if k + 1 < args.steps:
-                nxt = fetch()
-                res = one_step(r_d, t_d, nxt[0], nxt[2])
-            else:
-                res = one_step(r_d, t_d)
-            if train:
-                _ = float(res.item())  # D2H read of the step's loss
-            elif res is not None:  # D2H read of the rendered colours
-                out_h.copy_(res[0:3], non_blocking=True)
-                torch.cuda.current_stream().synchronize()
+        e2e_loop(args.steps)
         t1.record()
         torch.cuda.synchronize()
         e_ms = torch.tensor([t0.elapsed_time(t1) / args.steps], dtype=torch.float64,
@@ -565,7 +577,7 @@ def main():
             dist.all_reduce(e_ms, op=dist.ReduceOp.MAX)
         e2e = {"value": R / (float(e_ms.item()) / 1e3), "unit": UNIT,
                "input_pipeline": "pinned host batch, H2D on a copy stream one step ahead",
-               "h2d_bytes_per_step": rays_h.numel() * 8 + tg_h.numel() * 4,
+               "h2d_bytes_per_step": rays_h.numel() * 8 + (tg_h.numel() * 4 if train else 0),
                "d2h_bytes_per_step": 8 if train else 3 * 4 * R, "ms_per_step": float(e_ms.item())}
 
     cpu = None
