@@ -462,6 +462,36 @@ def main():
         dist.all_reduce(n_live)
     n_live = int(n_live.item())
 
+    # NVLink roofline of the exchange (N > 1): the step's all-gather of the sparse packet
+    # records, timed alone on the device, max over ranks, against the nominal NVLink 5
+    # bandwidth per direction (this run cannot measure the link: one GPU per box)
+    link = None
+    if world > 1 and args.protocol == "tile":
+        b_ex = pool.sample(rays, w.dt, exchange=True)
+        rows = (b_ex.seg_max or 0) + 1
+        width = 10 if interlevel else 9
+        buf = torch.zeros((rows, width), dtype=torch.float32, device=dev)
+        for _ in range(3):
+            vr.comm.all_gather_packets(buf, group, world)
+        torch.cuda.synchronize()
+        dist.barrier()
+        ea, eb = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        ea.record()
+        for _ in range(10):
+            vr.comm.all_gather_packets(buf, group, world)
+        eb.record()
+        torch.cuda.synchronize()
+        x_ms = torch.tensor([ea.elapsed_time(eb) / 10], dtype=torch.float64, device=red_dev)
+        dist.all_reduce(x_ms, op=dist.ReduceOp.MAX)
+        x_ms = float(x_ms.item())
+        recv = (world - 1) * rows * width * 4
+        link = {"collective": "all_gather_into_tensor of the sparse packet records",
+                "bytes_received_per_rank": recv, "ms": x_ms,
+                "achieved": recv / (x_ms / 1e3) / 1e9, "peak": 900.0, "unit": "GB/s",
+                "frac": recv / (x_ms / 1e3) / 1e9 / 900.0,
+                "peak_source": "nominal NVLink 5, per direction",
+                "backend": args.backend}
+
     # ---- roofline of the dominant kernel (events over the timed region) ------------
     totals = timer.totals()
     peaks = load_peaks()
@@ -623,7 +653,8 @@ def main():
                     "dense_slab_bytes": len(w.tree.leaves) * R * (36 if interlevel else 32),
                     "tile_vs_sample_bytes": (n_live * (40 if interlevel else 36))
                                             / max(1, n_samples * 16)},
-                "roofline": roofline, "rooflines": rooflines, "cpu_baseline": cpu, "e2e": e2e,
+                "roofline": roofline, "rooflines": rooflines, "nvlink": link,
+                "cpu_baseline": cpu, "e2e": e2e,
                 "gpu_launches": launches, "clocks": clk, "loss": final_loss,
                 "step_ms": [round(x, 3) for x in step_ms],
                 "kernels": per_kernel}
