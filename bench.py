@@ -612,11 +612,13 @@ def main():
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu and train:
-        n_cpu = 64
-        v, _ = cpu_baseline_port(w, n_cpu)
+        # 64 rays, repeated: ~10 s of single-thread CPU work at c3 (larger samples make the
+        # port's compact tables and autograd graph slower per ray, not more representative)
+        n_cpu, reps = 64, 12
+        v, _ = cpu_baseline_port(w, n_cpu, reps=reps)
         cpu = {"value": v, "unit": UNIT, "cores": 1, "kind": "port",
-               "sample": f"{n_cpu} rays of {w.name}: oracle hash+MLP fwd + torch fp64 autograd "
-                         "bwd, single thread"}
+               "sample": f"{n_cpu} rays of {w.name}, {reps} repetitions: oracle hash+MLP fwd "
+                         "+ torch fp64 autograd bwd, single thread"}
 
     if rank == 0:
         line = {"metric": metric, "value": value, "unit": UNIT, "n_gpus": world,
