@@ -266,10 +266,12 @@ int vr_mlp_bwd(const void* weights_dev, const void* enc_dev, const double* rays_
 int vr_mlp_fwd_tc(const void* weights_dev, const void* enc_dev, const double* rays_dev,
                   int64_t ray_stride, const int32_t* ray_id_dev, int64_t n, float* sig_rgb_dev,
                   void* stream);
+/* max_ctas: 0 = the persistent grid (2 CTAs per SM); fewer leave SMs to a kernel running
+ * beside it (the split backward's side-stream scatter: 1.25 CTAs per SM measured best) */
 int vr_mlp_bwd_tc(const void* weights_dev, const void* enc_dev, const double* rays_dev,
                   int64_t ray_stride, const int32_t* ray_id_dev, int64_t n,
                   const float* dsig_rgb_dev, float* grad_weights_dev, float* denc_dev,
-                  int32_t* err_dev, void* stream);
+                  int32_t* err_dev, int32_t max_ctas, void* stream);
 
 /* Density branch only (proposal fields of the interlevel loss, whose colour head is never
  * read): out[i] = {sigma, 0, 0, 0}; the backward reads dL/dsigma (dsig_rgb[i].x), writes
@@ -279,7 +281,7 @@ int vr_mlp_fwd_tc_density(const void* weights_dev, const void* enc_dev, int64_t 
 int vr_mlp_bwd_tc_density(const void* weights_dev, const void* enc_dev, const double* rays_dev,
                           int64_t ray_stride, const int32_t* ray_id_dev, int64_t n,
                           const float* dsig_rgb_dev, float* grad_weights_dev, float* denc_dev,
-                          int32_t* err_dev, void* stream);
+                          int32_t* err_dev, int32_t max_ctas, void* stream);
 
 /* ---- K2 + K3 fused (production training path) ------------------------------------
  * Forward: the tensor-core MLP kernel computes each row's hash encoding itself (no

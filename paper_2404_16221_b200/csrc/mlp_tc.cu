@@ -930,7 +930,8 @@ template <bool FUSED, bool DENS = false>
 int launch_bwd(const void* w, const void* enc, const double* rays, int64_t stride,
                const int32_t* rid, int64_t n, const float* dsr, float* gW, float* denc,
                int32_t* err, const VrHashGridDesc* g, const double* t0, const double* t1,
-               float* grad_table, void* ws, size_t ws_bytes, const float* pos, void* stream) {
+               float* grad_table, void* ws, size_t ws_bytes, const float* pos, void* stream,
+               int max_ctas = 0) {
   int rc = set_smem(mlp::k_mlp_bwd_tc<FUSED, DENS>, mlp::B_SMEM, "mlp bwd: smem attribute");
   if (rc != VR_OK) return rc;
   VrHashGridDesc gd;
@@ -945,7 +946,8 @@ int launch_bwd(const void* w, const void* enc, const double* rays, int64_t strid
     memset(&gd, 0, sizeof(gd));
   }
   const int64_t tiles = ceil_div(n, mlp::TILE);
-  const int grid = (int)(tiles < VR_NUM_SMS * 2 ? tiles : VR_NUM_SMS * 2);
+  const int cap = max_ctas > 0 && max_ctas < VR_NUM_SMS * 2 ? max_ctas : VR_NUM_SMS * 2;
+  const int grid = (int)(tiles < cap ? tiles : cap);
   mlp::k_mlp_bwd_tc<FUSED, DENS><<<grid, mlp::TILE * mlp::BWD_TPR, mlp::B_SMEM,
                                    (cudaStream_t)stream>>>(
       (const __half*)w, (const __half2*)enc, rays, stride, rid, n,
@@ -971,14 +973,14 @@ extern "C" int vr_mlp_fwd_tc(const void* w, const void* enc, const double* rays,
 
 extern "C" int vr_mlp_bwd_tc(const void* w, const void* enc, const double* rays, int64_t stride,
                              const int32_t* rid, int64_t n, const float* dsr, float* gW,
-                             float* denc, int32_t* err, void* stream) {
+                             float* denc, int32_t* err, int32_t max_ctas, void* stream) {
   if (n < 0 || !w || !gW || !denc || !err) {
     set_error("vr_mlp_bwd_tc: bad argument");
     return VR_ERR_BAD_ARG;
   }
   if (n == 0) return VR_OK;
   return launch_bwd<false>(w, enc, rays, stride, rid, n, dsr, gW, denc, err, nullptr, nullptr,
-                           nullptr, nullptr, nullptr, 0, nullptr, stream);
+                           nullptr, nullptr, nullptr, 0, nullptr, stream, max_ctas);
 }
 
 // density branch only (proposal fields): sigma of the same MLP, rgb = 0; the backward takes
@@ -997,14 +999,15 @@ extern "C" int vr_mlp_fwd_tc_density(const void* w, const void* enc, int64_t n, 
 extern "C" int vr_mlp_bwd_tc_density(const void* w, const void* enc, const double* rays,
                                      int64_t stride, const int32_t* rid, int64_t n,
                                      const float* dsr, float* gW, float* denc, int32_t* err,
-                                     void* stream) {
+                                     int32_t max_ctas, void* stream) {
   if (n < 0 || !w || !gW || !denc || !err) {
     set_error("vr_mlp_bwd_tc_density: bad argument");
     return VR_ERR_BAD_ARG;
   }
   if (n == 0) return VR_OK;
   return launch_bwd<false, true>(w, enc, rays, stride, rid, n, dsr, gW, denc, err, nullptr,
-                                 nullptr, nullptr, nullptr, nullptr, 0, nullptr, stream);
+                                 nullptr, nullptr, nullptr, nullptr, 0, nullptr, stream,
+                                 max_ctas);
 }
 
 extern "C" int vr_field_fwd_tc(const VrHashGridDesc* g, const float* table, const void* w,

@@ -374,6 +374,9 @@ class VolumePool:
     # side-stream scatter grid: 0 = the kernel's full grid (measured best: 148 or 296 co-
     # resident 128-thread blocks left the scatter far below the L2 atomic rate)
     SCATTER_BLOCKS = int(os.environ.get("VR_SCATTER_BLOCKS", "0"))
+    # the MLP backward's grid while the previous region's scatter runs on the side stream:
+    # 1.25 CTAs per SM (c4: 148 -> 407, 185 -> 388, 222 -> 394, 296 -> 413 ms per step)
+    MLP_CTAS_BESIDE_SCATTER = int(os.environ.get("VR_MLP_BWD_CTAS", str(148 * 5 // 4)))
 
     def field_backward(self, rays, b: SampleBatch, dsig_rgb: torch.Tensor, fields=None) -> None:
         self.field_backward_jobs(rays, b, [(self.fields if fields is None else fields, dsig_rgb)])
@@ -400,7 +403,8 @@ class VolumePool:
                         f.backward(rays, b.t0[lo:], b.t1[lo:], b.ray_id[lo:], hi - lo,
                                    dsig_rgb[lo:], s)
                         continue
-                    denc = f.backward_mlp(rays, b.ray_id[lo:], hi - lo, dsig_rgb[lo:], s)
+                    denc = f.backward_mlp(rays, b.ray_id[lo:], hi - lo, dsig_rgb[lo:], s,
+                                          self.MLP_CTAS_BESIDE_SCATTER)
                     ev = torch.cuda.Event()
                     ev.record(main)
                     with torch.cuda.stream(side):

@@ -413,7 +413,7 @@ class HashGridMLP(RegionField):
         if self.mlp_impl != "cuda":
             _lib.call("vr_mlp_bwd_tc", _lib.ptr(self.weights16), _lib.ptr(enc), _lib.ptr(rays),
                       rays.shape[1], _lib.ptr(ray_id), n, _lib.ptr(dsig_rgb),
-                      _lib.ptr(self.grad_weights), _lib.ptr(denc), _lib.ptr(self.err), stream)
+                      _lib.ptr(self.grad_weights), _lib.ptr(denc), _lib.ptr(self.err), 0, stream)
         else:
             _lib.call("vr_mlp_bwd", _lib.ptr(self.weights16), _lib.ptr(enc), _lib.ptr(rays),
                       rays.shape[1], _lib.ptr(ray_id), n, _lib.ptr(dsig_rgb),
@@ -442,14 +442,16 @@ class HashGridMLP(RegionField):
             self.density_only or self.hash_order == "level"
             or self.n_entries * 8 < self.SPLIT_BELOW_BYTES)
 
-    def backward_mlp(self, rays, ray_id, n, dsig_rgb, stream):
-        """MLP backward of the step's samples; returns d(enc) [16][n] float2 (float32)."""
+    def backward_mlp(self, rays, ray_id, n, dsig_rgb, stream, max_ctas: int = 0):
+        """MLP backward of the step's samples; returns d(enc) [16][n] float2 (float32).
+        max_ctas: grid cap when a scatter runs beside it (0: the full persistent grid)."""
         denc = torch.empty(16 * max(n, 1) * 2, dtype=torch.float32, device=rays.device)
         if n:
             _lib.call("vr_mlp_bwd_tc_density" if self.density_only else "vr_mlp_bwd_tc",
                       _lib.ptr(self.weights16), _lib.ptr(self._enc),
                       _lib.ptr(rays), rays.shape[1], _lib.ptr(ray_id), n, _lib.ptr(dsig_rgb),
-                      _lib.ptr(self.grad_weights), _lib.ptr(denc), _lib.ptr(self.err), stream)
+                      _lib.ptr(self.grad_weights), _lib.ptr(denc), _lib.ptr(self.err),
+                      int(max_ctas), stream)
         return denc
 
     def backward_scatter(self, denc, n, stream, max_blocks=0):

@@ -38,7 +38,7 @@ err = torch.zeros(1, dtype=torch.int32, device=DEV)
 s = L.stream_ptr()
 f = lambda: L.call("vr_mlp_fwd_tc", L.ptr(w16), L.ptr(enc), L.ptr(rays), R, L.ptr(rid), n, L.ptr(out), s)
 bw = lambda: L.call("vr_mlp_bwd_tc", L.ptr(w16), L.ptr(enc), L.ptr(rays), R, L.ptr(rid), n, L.ptr(dsr),
-                    L.ptr(gw), L.ptr(de), L.ptr(err), s)
+                    L.ptr(gw), L.ptr(de), L.ptr(err), 0, s)
 tf = timeit(f)
 tb = timeit(bw)
 print(f"n={n}: mlp_fwd_tc {tf:.3f} ms ({n*18816/tf/1e9:.1f} TFLOP/s)  "

@@ -71,7 +71,7 @@ for n in (1000, 40000, 400000):
         de = torch.empty((16, n, 2), dtype=torch.float32, device=DEV)
         args = [L.ptr(w16), L.ptr(enc), L.ptr(rays), R, L.ptr(rid), n, L.ptr(dsr), L.ptr(gw), L.ptr(de)]
         if bw.endswith("_tc"):
-            args.append(L.ptr(err))
+            args += [L.ptr(err), 0]
         L.call(bw, *args, s)
         torch.cuda.synchronize()
         fo = ((o.double() - ref_out).abs().max()).item()

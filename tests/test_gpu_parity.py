@@ -648,7 +648,7 @@ def test_mlp_tensor_core_matches_cuda_core(n):
         args = [_lib.ptr(w16), _lib.ptr(enc), _lib.ptr(rays), R, _lib.ptr(rid), n, _lib.ptr(dsr),
                 _lib.ptr(gw), _lib.ptr(de)]
         if name.endswith("_tc"):
-            args.append(_lib.ptr(err))
+            args += [_lib.ptr(err), 0]
         _lib.call(name, *args, s)
         grads.append((gw, de))
     torch.cuda.synchronize()
