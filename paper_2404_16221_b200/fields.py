@@ -15,6 +15,7 @@ from __future__ import annotations
 
 import ctypes
 import math
+import os
 from dataclasses import dataclass, field as dc_field
 
 import numpy as np
@@ -431,10 +432,12 @@ class HashGridMLP(RegionField):
     # ---- split backward: the MLP part and the hash-grid scatter as separate launches, so
     # VolumePool can run region k's scatter (L2-atomic bound) on a side stream while the
     # tensor-core MLP backward of region k+1 runs on the main stream
+    # (VR_SPLIT_BELOW_MB overrides the threshold; c3 re-measured with the capped MLP grid:
+    # fused 56.7 vs split 58.0 ms)
     # measured: split + side-stream scatter beats the fused kernel for level-major tables
     # (c4 NeRF) and for small tables (c4 proposals, 12 MB: 549 -> 535 ms per c4 step); the
     # fused kernel wins for mid-size L2-resident tables (c3, 49 MB: 61.3 vs 64.8 ms)
-    SPLIT_BELOW_BYTES = 16 << 20
+    SPLIT_BELOW_BYTES = int(os.environ.get("VR_SPLIT_BELOW_MB", "16")) << 20
 
     @property
     def split_backward(self):
