@@ -343,8 +343,9 @@ class VolumePool:
         s = self._stream()
         # Off by default (VR_OVERLAP_FWD=1): with the old 52 KB-smem MLP forward the step got
         # slower (c3 76.7 vs 67.6 ms); with the 20 KB TS-mode forward it is a wash at c3
-        # (56.6 vs 56.7 ms) and slower at c5 (86.9 vs 84.2) — the gathers are L2-request
-        # bound and the MLP CTAs still take their issue slots.
+        # (56.6 vs 56.7 ms) and slower at c5 (86.9 vs 84.2; with the MLP grid capped at 2 / 1
+        # / 0.5 CTAs per SM: 87.3 / 97.2 / 118.8) — the gathers are L2-request bound and the
+        # MLP CTAs still take their issue slots.
         split = (self.overlap_regions and len(fields) > 1
                  and all(getattr(f, "splittable", False) for f in fields))
         if not split:
