@@ -157,7 +157,10 @@ int vr_sample_fill(const VrTree* tree, const double* rays_dev, int64_t ray_strid
                    const int64_t* offsets_dev, const int32_t* seg_first_dev, double* t0_dev,
                    double* t1_dev, int32_t* ray_id_dev, int64_t capacity, int32_t* err_dev,
                    void* stream);
-/* One walk instead of count + fill: vr_sample_stage is vr_sample_count that also writes
+/* One walk instead of count + fill (the same generate_samples quadrature.py:66-88 /
+ * split_at_planes :91-114 / locate_many partitioner.py:177-192 replacement as the pair
+ * above, for _prepare_samples distsim.py:369-373 + the assignment :406-425):
+ * vr_sample_stage is vr_sample_count that also writes
  * every own sample's t0/t1 into staging buffers st0/st1 (stage_capacity entries, split in
  * vr_sample_stage_blocks(n_rays) equal slices, one per CTA; a ray reserves one slot per
  * walked bin plus one per cut); sslot_dev[r] locates the ray's staged samples.
@@ -335,8 +338,9 @@ int vr_packets_unpack(const float* recv_dev, int32_t world, int64_t rows, int32_
                       int32_t* err_dev, void* stream);
 /* analytic backward: dpackets [region_cnt][n_rays][8] = adjoints of {T,C,A,D',L};
  * writes dsig_rgb[i] = {dL/dsigma, dL/dr, dL/dg, dL/db}. */
-/* transmittance only: T_dev[seg] = the T of vr_segment_fwd's packet (1 for an empty
- * segment), [region_cnt][n_rays] float32 — the proposal fields' packets (interlevel) */
+/* transmittance only (the T of composite_samples quadrature.py:141-165 per run):
+ * T_dev[seg] = the T of vr_segment_fwd's packet (1 for an empty segment),
+ * [region_cnt][n_rays] float32 — the proposal fields' packets (interlevel) */
 int vr_segment_transmittance(const double* t0_dev, const double* t1_dev,
                              const float* sig_rgb_dev, const int64_t* offsets_dev,
                              int64_t n_rays, int32_t region_cnt, float* T_dev, void* stream);
@@ -376,7 +380,8 @@ int vr_interlevel(const double* t0_dev, const double* t1_dev, const float* sig_r
                   int64_t n_rays, int32_t region_cnt, float lambda_interlevel, float eps,
                   double* seg_loss_dev, float* dsig_prop_dev, void* stream);
 
-/* deterministic float64 sum (fixed reduction tree); ws_dev: VR_SUM_PARTIALS doubles of
+/* deterministic float64 sum (fixed reduction tree) — the probe's loss total
+ * (segrender.py:198-207 sums per-ray terms); ws_dev: VR_SUM_PARTIALS doubles of
  * caller-owned scratch (stream-ordered like every buffer here) */
 #define VR_SUM_PARTIALS 296
 int vr_sum_f64(const double* x_dev, int64_t n, double* out_dev, double* ws_dev, void* stream);
