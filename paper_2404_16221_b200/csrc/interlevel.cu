@@ -56,7 +56,8 @@ __global__ void k_prefix(const float4* __restrict__ pk, const float* __restrict_
 // Grouped like K4 (segscan.cuh): one warp per 32 consecutive (region, ray) segments walks
 // their contiguous sample range 32 samples at a time with segmented scans, so no lane
 // idles on short segments.  Sweep 1: local transmittances (NeRF, proposal), per-segment
-// loss L and S = sum_i wh_loc_i e_i; sweep 2: per-sample proposal gradients.
+// loss L and S = sum_i wh_loc_i e_i, and each sample's gradient up to the S term; sweep 2
+// (reads 16 B per sample, no re-evaluation): per-sample proposal gradients.
 struct IlChunk {
   bool valid, head, tail, cont;
   int seg;
@@ -143,8 +144,11 @@ __global__ void __launch_bounds__(IL_WARPS * 32)
     const int64_t s_beg = __shfl_sync(0xffffffffu, gs.lo, 0);
     const int64_t s_end = __shfl_sync(0xffffffffu, gs.hi, nseg - 1);
     if (s_beg == s_end) continue;
-    // sweep 1: L and S per segment
+    // sweep 1: L and S per segment, and per sample the two terms of its gradient that do
+    // not need the segment total S — parked in the sample's dsp slot as two doubles
+    //   ds_i dt_i = x_i - y_i S,  x_i = Ph dt_i (Th_{i+1} e_i + S_<=i),  y_i = Ph dt_i
     double cT = 1.0, cTh = 1.0, cL = 0.0, cS = 0.0;
+    double2* park = reinterpret_cast<double2*>(dsp);
     IlIn nxt = il_load(t0, t1, sr, sp, s_beg + lane, s_end);
     for (int64_t base = s_beg; base < s_end; base += 32) {
       const IlIn cur = nxt;
@@ -155,46 +159,35 @@ __global__ void __launch_bounds__(IL_WARPS * 32)
       const double w = P * c.T * c.alpha;
       const double whl = c.Th * c.alphah;
       const double d = fmax(w - Ph * whl, 0.0);
-      const double inv = 1.0 / (w + ep);
-      double q[2] = {c.valid ? lam * d * d * inv : 0.0, c.valid ? whl * (-2.0 * lam * d * inv) : 0.0};
+      const double ei = -2.0 * lam * d / (w + ep);
+      double q[2] = {c.valid ? lam * d * d / (w + ep) : 0.0, c.valid ? whl * ei : 0.0};
       seg_scan<2>(q, c.head, lane, [](double a, double b) { return a + b; });
       const double L = (c.cont ? cL : 0.0) + q[0];
       const double S = (c.cont ? cS : 0.0) + q[1];
+      const double Thn = c.Th * c.keeph;  // local proposal transmittance after sample i
+      if (c.valid) {
+        const double y = Ph * c.dlt;
+        park[base + lane] = make_double2(y * (Thn * ei + S), y);
+      }
       if (c.tail) {
         seg_loss[seg0 + c.seg] = L;
         Sseg[c.seg] = S;
       }
       cT = __shfl_sync(0xffffffffu, c.T * c.keep, 31);
-      cTh = __shfl_sync(0xffffffffu, c.Th * c.keeph, 31);
+      cTh = __shfl_sync(0xffffffffu, Thn, 31);
       cL = __shfl_sync(0xffffffffu, L, 31);
       cS = __shfl_sync(0xffffffffu, S, 31);
     }
     __syncwarp();
-    // sweep 2: dL/dsigma_prop per sample
-    cT = 1.0;
-    cTh = 1.0;
-    double cSc = 0.0;
-    nxt = il_load(t0, t1, sr, sp, s_beg + lane, s_end);
+    // sweep 2: dL/dsigma_prop = x_i - y_i S of the sample's segment (no re-evaluation)
     for (int64_t base = s_beg; base < s_end; base += 32) {
-      const IlIn cur = nxt;
-      nxt = il_load(t0, t1, sr, sp, base + 32 + lane, s_end);
-      const IlChunk c = il_chunk(cur, base + lane, s_end, gs, nseg, cT, cTh, lane);
-      const double P = __shfl_sync(0xffffffffu, (double)pre.x, c.seg);
-      const double Ph = __shfl_sync(0xffffffffu, (double)pre.y, c.seg);
-      const double w = P * c.T * c.alpha;
-      const double whl = c.Th * c.alphah;
-      const double d = fmax(w - Ph * whl, 0.0);
-      const double ei = -2.0 * lam * d / (w + ep);
-      double q[1] = {c.valid ? whl * ei : 0.0};
-      seg_scan<1>(q, c.head, lane, [](double a, double b) { return a + b; });
-      const double incl = (c.cont ? cSc : 0.0) + q[0];
-      const double s_gt = Sseg[c.seg] - incl;
-      const double Thn = c.Th * c.keeph;  // local proposal transmittance after sample i
-      const double ds = Ph * (Thn * ei - s_gt);
-      if (c.valid) dsp[base + lane] = make_float4((float)(ds * c.dlt), 0.f, 0.f, 0.f);
-      cT = __shfl_sync(0xffffffffu, c.T * c.keep, 31);
-      cTh = __shfl_sync(0xffffffffu, Thn, 31);
-      cSc = __shfl_sync(0xffffffffu, incl, 31);
+      const int64_t s = base + lane;
+      const bool valid = s < s_end;
+      const int seg = find_seg(gs.lo, nseg, valid ? s : s_end - 1);
+      if (valid) {
+        const double2 xy = park[s];
+        dsp[s] = make_float4((float)(xy.x - xy.y * Sseg[seg]), 0.f, 0.f, 0.f);
+      }
     }
     __syncwarp();
   }
