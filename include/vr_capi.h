@@ -270,11 +270,15 @@ int vr_mlp_fwd_tc(const void* weights_dev, const void* enc_dev, const double* ra
                   int64_t ray_stride, const int32_t* ray_id_dev, int64_t n, float* sig_rgb_dev,
                   void* stream);
 /* max_ctas: 0 = the persistent grid (2 CTAs per SM); fewer leave SMs to a kernel running
- * beside it (the split backward's side-stream scatter: 1.25 CTAs per SM measured best) */
+ * beside it (the split backward's side-stream scatter: 1.25 CTAs per SM measured best).
+ * sig_rgb_dev (may be NULL): the forward's output for these samples; with it each CTA
+ * scales its gradients by a power of two so that the fp16 hi + lo split of the upstream
+ * gradients keeps full precision (without it: 2^-24 absolute precision, ~4e-5 relative
+ * at the typical |dL/dsigma| ~ 1e-3), and unscales d(enc) and the weight gradients. */
 int vr_mlp_bwd_tc(const void* weights_dev, const void* enc_dev, const double* rays_dev,
                   int64_t ray_stride, const int32_t* ray_id_dev, int64_t n,
-                  const float* dsig_rgb_dev, float* grad_weights_dev, float* denc_dev,
-                  int32_t* err_dev, int32_t max_ctas, void* stream);
+                  const float* dsig_rgb_dev, const float* sig_rgb_dev, float* grad_weights_dev,
+                  float* denc_dev, int32_t* err_dev, int32_t max_ctas, void* stream);
 
 /* Density branch only (proposal fields of the interlevel loss, whose colour head is never
  * read): out[i] = {sigma, 0, 0, 0}; the backward reads dL/dsigma (dsig_rgb[i].x), writes
@@ -283,8 +287,9 @@ int vr_mlp_fwd_tc_density(const void* weights_dev, const void* enc_dev, int64_t 
                           float* sig_rgb_dev, void* stream);
 int vr_mlp_bwd_tc_density(const void* weights_dev, const void* enc_dev, const double* rays_dev,
                           int64_t ray_stride, const int32_t* ray_id_dev, int64_t n,
-                          const float* dsig_rgb_dev, float* grad_weights_dev, float* denc_dev,
-                          int32_t* err_dev, int32_t max_ctas, void* stream);
+                          const float* dsig_rgb_dev, const float* sig_rgb_dev,
+                          float* grad_weights_dev, float* denc_dev, int32_t* err_dev,
+                          int32_t max_ctas, void* stream);
 
 /* ---- K2 + K3 fused (production training path) ------------------------------------
  * Forward: the tensor-core MLP kernel computes each row's hash encoding itself (no
@@ -300,9 +305,9 @@ int vr_field_fwd_tc(const VrHashGridDesc* g, const float* table_dev, const void*
 int vr_field_bwd_tc(const VrHashGridDesc* g, const void* weights_dev, const void* enc_dev,
                     const double* rays_dev, int64_t ray_stride, const double* t0_dev,
                     const double* t1_dev, const int32_t* ray_id_dev, int64_t n,
-                    const float* dsig_rgb_dev, float* grad_weights_dev, float* grad_table_dev,
-                    void* workspace_dev, size_t workspace_bytes, int32_t* err_dev,
-                    const float* pos_dev, void* stream);
+                    const float* dsig_rgb_dev, const float* sig_rgb_dev, float* grad_weights_dev,
+                    float* grad_table_dev, void* workspace_dev, size_t workspace_bytes,
+                    int32_t* err_dev, const float* pos_dev, void* stream);
 
 /* ---- K4: per-segment front-to-back composite (composite_samples quadrature.py:141-165,
  * aggregate_segment segrender.py:71-90, process_inbox distsim.py:318-329) ------------- */

@@ -121,13 +121,18 @@ class HashMLPModel:
     """One region's model with float64 torch parameters (table, packed weights)."""
 
     def __init__(self, table: np.ndarray, weights: np.ndarray, log2_T: int, box_mn, box_mx,
-                 max_res: int = 2048):
+                 max_res: int = 2048, quantize: bool = True):
         self.table = torch.tensor(np.asarray(table, dtype=np.float64), requires_grad=True)
-        # the kernels consume fp16 copies of the float32 master weights
-        w16 = np.asarray(weights, dtype=np.float32).astype(np.float16).astype(np.float64)
-        self.weights = torch.tensor(w16, requires_grad=True)
+        # the kernels consume fp16 copies of the float32 master weights; quantize=False is
+        # the ideal float64 model (no fp16 weights/activations, float64 features): it bounds
+        # the quantisation error of the kernels' precision choice separately from parity
+        self.quantize = quantize
+        w = np.asarray(weights, dtype=np.float32)
+        w = w.astype(np.float16).astype(np.float64) if quantize else w.astype(np.float64)
+        self.weights = torch.tensor(w, requires_grad=True)
         self.log2_T = log2_T
         self.box_mn, self.box_mx = box_mn, box_mx
+        self.max_res = max_res
         self.levels, self.n_entries = levels(log2_T, max_res=max_res)
 
     def encode(self, pts) -> torch.Tensor:
@@ -140,22 +145,70 @@ class HashMLPModel:
             gidx = idx.astype(np.int64) + off
             rows = self.table[torch.from_numpy(gidx)]  # (n, 8, 2)
             f = (rows * torch.from_numpy(w.astype(np.float64))[:, :, None]).sum(1)
-            # forward value: the kernel's float32 sum (bit-exact, feature32 order);
-            # gradient: the exact linear map
-            f32 = feature32(w, tab32[gidx])
-            f = f + (torch.from_numpy(f32.astype(np.float64)) - f).detach()
+            if self.quantize:
+                # forward value: the kernel's float32 sum (bit-exact, feature32 order);
+                # gradient: the exact linear map
+                f32 = feature32(w, tab32[gidx])
+                f = f + (torch.from_numpy(f32.astype(np.float64)) - f).detach()
             feats.append(f)
-        return _q16(torch.cat(feats, dim=1))
+        return self._q(torch.cat(feats, dim=1))
+
+    def _q(self, x: torch.Tensor) -> torch.Tensor:
+        return _q16(x) if getattr(self, "quantize", True) else x
+
+    def _linear(self, a: torch.Tensor, Wm: torch.Tensor) -> torch.Tensor:
+        """a @ Wm^T, recorded (output with its gradient retained, input) so weight_contrib
+        can size each weight gradient's terms."""
+        x = a @ Wm.T
+        if x.requires_grad:
+            x.retain_grad()
+        self._layers.append((x, a))
+        return x
+
+    def weight_contrib(self) -> np.ndarray:
+        """Per packed weight: sum over samples of |dL/d(layer output)| * |layer input| —
+        the magnitude of the terms its gradient sums (of the last backward through the last
+        mlp() call; layers in the packed order W1d, W2d, W1c, W2c, W3c)."""
+        S = np.zeros(NPARAMS)
+        offs = [W1D, W2D, W1C, W2C, W3C]
+        for (x, a), off in zip(self._layers, offs):
+            if x.grad is None:
+                continue
+            m = (x.grad.abs().T @ a.detach().abs()).numpy()
+            S[off:off + m.size] = m.ravel()
+        return S
+
+    def clear_layer_grads(self):
+        for x, _ in getattr(self, "_layers", []):
+            x.grad = None
+
+    def _relu(self, a: torch.Tensor, Wm: torch.Tensor, margins: list) -> torch.Tensor:
+        """fp16(relu(a @ Wm^T)) with the kernels' derivative: 1 where the fp16 activation
+        is non-zero (csrc/mlp_tc.cu relu_mask8).  Records each row's relative kink margin
+        min_j |x_j| / sum_i |a_i W_ji|: where it is below the float32 accumulation error
+        (~K * 2^-24), float32 and float64 can take different sides of the ReLU kink."""
+        x = self._linear(a, Wm)
+        with torch.no_grad():
+            mag = a.detach().abs() @ Wm.detach().abs().T
+            margins.append((x.detach().abs() / mag.clamp_min(1e-300)).min(1).values)
+        if not getattr(self, "quantize", True):
+            return torch.relu(x)
+        hq = torch.relu(x).detach().to(torch.float16).to(torch.float64)
+        keep = (hq != 0).to(torch.float64)
+        return x * keep + (hq - x * keep).detach()
 
     def mlp(self, enc: torch.Tensor, dirs32: np.ndarray):
+        _q16 = self._q  # noqa: N806 - the quantisation points of the kernels
+        margins = []
+        self._layers = []
         W = self.weights
         W1d = W[W1D:W2D].reshape(64, 32)
         W2d = W[W2D:W1C].reshape(16, 64)
         W1c = W[W1C:W2C].reshape(64, 32)
         W2c = W[W2C:W3C].reshape(64, 64)
         W3c = W[W3C:W3C + 3 * 64].reshape(3, 64)
-        h = _q16(torch.relu(enc @ W1d.T))
-        od = h @ W2d.T
+        h = self._relu(enc, W1d, margins)
+        od = self._linear(h, W2d)
         x0 = od[:, 0]
         inside = ((x0 > -15.0) & (x0 < 15.0)).to(torch.float64)
         # exp(clamp(x)) with d/dx = sigma inside the clamp range, 0 outside
@@ -163,15 +216,27 @@ class HashMLPModel:
         sigma = torch.exp(x0 * inside + (xc * (1 - inside)).detach())
         sh = _q16(sh16_t(torch.from_numpy(np.asarray(dirs32, dtype=np.float32).astype(np.float64))))
         cin = torch.cat([_q16(od), sh], dim=1)
-        h1 = _q16(torch.relu(cin @ W1c.T))
-        h2 = _q16(torch.relu(h1 @ W2c.T))
-        rgb = torch.sigmoid(h2 @ W3c.T)
+        h1 = self._relu(cin, W1c, margins)
+        h2 = self._relu(h1, W2c, margins)
+        rgb = torch.sigmoid(self._linear(h2, W3c))
+        # per-sample relative ReLU kink margin of this call (see _relu)
+        self.last_margin = torch.stack(margins).min(0).values.numpy()
         return sigma, rgb
 
     def eval_t(self, pts, d):
         n = np.asarray(pts).shape[0]
         dirs = np.broadcast_to(np.asarray(d, dtype=np.float64).astype(np.float32), (n, 3))
         return self.mlp(self.encode(pts), dirs)
+
+    def eval_dirs(self, pts, dirs):
+        """Batched evaluation with one view direction per point (grad_oracle.RayRuns).
+        The encodings are kept (last_enc, gradient retained) so tests can compare the
+        per-sample d(enc) of the kernels."""
+        enc = self.encode(pts)
+        enc.retain_grad()
+        self.last_enc = enc
+        self.last_pts = np.asarray(pts, dtype=np.float64)
+        return self.mlp(enc, np.asarray(dirs, dtype=np.float64).astype(np.float32))
 
     def grads(self):
         return (self.table.grad.numpy().copy(), self.weights.grad.numpy().copy())
@@ -187,6 +252,7 @@ class CompactHashMLPModel(HashMLPModel):
     def __init__(self, entry_init, weights, log2_T: int, box_mn, box_mx, pts, max_res: int = 2048):
         self.log2_T = log2_T
         self.box_mn, self.box_mx = box_mn, box_mx
+        self.max_res = max_res
         self.levels, self.n_entries = levels(log2_T, max_res=max_res)
         u = normalize(pts, box_mn, box_mx)
         touched = [corners(u, s, r, dn, log2_T)[0].astype(np.int64).ravel() + off

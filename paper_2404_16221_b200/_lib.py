@@ -130,11 +130,11 @@ SIGNATURES = {
     "vr_mlp_fwd": [P, P, P, I64, P, I64, P, P],
     "vr_mlp_bwd": [P, P, P, I64, P, I64, P, P, P, P],
     "vr_mlp_fwd_tc": [P, P, P, I64, P, I64, P, P],
-    "vr_mlp_bwd_tc": [P, P, P, I64, P, I64, P, P, P, P, I32, P],
+    "vr_mlp_bwd_tc": [P, P, P, I64, P, I64, P, P, P, P, P, I32, P],
     "vr_mlp_fwd_tc_density": [P, P, I64, P, P],
-    "vr_mlp_bwd_tc_density": [P, P, P, I64, P, I64, P, P, P, P, I32, P],
+    "vr_mlp_bwd_tc_density": [P, P, P, I64, P, I64, P, P, P, P, P, I32, P],
     "vr_field_fwd_tc": [P, P, P, P, I64, P, P, P, I64, P, P, P],
-    "vr_field_bwd_tc": [P, P, P, P, I64, P, P, P, I64, P, P, P, P, C.c_size_t, P, P, P],
+    "vr_field_bwd_tc": [P, P, P, P, I64, P, P, P, I64, P, P, P, P, P, C.c_size_t, P, P, P],
     "vr_segment_fwd": [P, P, P, P, P, P, I64, I32, P, P, P, P],
     "vr_segment_bwd": [P, P, P, P, P, I64, I32, P, P, P, P],
     "vr_segment_transmittance": [P, P, P, P, I64, I32, P, P],

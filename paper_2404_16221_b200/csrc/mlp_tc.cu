@@ -520,7 +520,7 @@ constexpr int BWD_TPR = 2;
 constexpr uint32_t B_A = WBYTES, B_X1 = B_A + TILE * 32 * 2, B_X3 = B_X1 + TILE * 64 * 2,
                    B_X4 = B_X3 + TILE * 64 * 2, B_GH = B_X4 + TILE * 64 * 2,
                    B_GL = B_GH + TILE * 64 * 2, B_BAR = B_GL + TILE * 64 * 2,
-                   B_SMEM = B_BAR + 32;
+                   B_WMAX = B_BAR + 32, B_SMEM = B_WMAX + 32;
 // TMEM columns: weight-gradient accumulators, then scratch.  W1d, W1c, W2c: M = 128
 // (rows 0..63 hi, 64..127 lo products); W2d^T, W3c^T: M = 64, columns [hi 16 | lo 16].
 // The forward's second scratch slice aliases the first (its results are consumed before
@@ -541,8 +541,9 @@ template <bool FUSED>
 __device__ __forceinline__ void fetch_row(RowIn& x, const __half2* __restrict__ enc,
                                           const double* __restrict__ rays, int64_t stride,
                                           const int32_t* __restrict__ rid,
-                                          const float4* __restrict__ dsr, int64_t n, int64_t i,
-                                          int part, const VrHashGridDesc& g,
+                                          const float4* __restrict__ dsr, float gscale,
+                                          int64_t n, int64_t i, int part,
+                                          const VrHashGridDesc& g,
                                           const double* __restrict__ t0,
                                           const double* __restrict__ t1,
                                           const float* __restrict__ pos) {
@@ -551,7 +552,12 @@ __device__ __forceinline__ void fetch_row(RowIn& x, const __half2* __restrict__ 
 #pragma unroll
   for (int l = 0; l < LV; ++l)
     x.enc[l] = valid ? enc[(int64_t)(part * LV + l) * n + i] : __floats2half2_rn(0.f, 0.f);
-  x.gin = (valid && part == 0) ? dsr[i] : make_float4(0.f, 0.f, 0.f, 0.f);
+  if (valid && part == 0) {
+    const float4 g4 = dsr[i];
+    x.gin = make_float4(g4.x * gscale, g4.y * gscale, g4.z * gscale, g4.w * gscale);
+  } else {
+    x.gin = make_float4(0.f, 0.f, 0.f, 0.f);
+  }
   x.dx = x.dy = x.dz = 0.f;
   x.u[0] = x.u[1] = x.u[2] = 0.f;
   if (valid) {
@@ -591,7 +597,8 @@ template <bool FUSED, bool DENS = false>
 __global__ void __launch_bounds__(TILE * BWD_TPR, 2)
     k_mlp_bwd_tc(const __half* __restrict__ W, const __half2* __restrict__ enc,
                  const double* __restrict__ rays, int64_t stride, const int32_t* __restrict__ rid,
-                 int64_t n, const float4* __restrict__ dsr, float* __restrict__ gW,
+                 int64_t n, const float4* __restrict__ dsr, const float4* __restrict__ sig,
+                 float* __restrict__ gW,
                  float2* __restrict__ denc, int32_t* err, const VrHashGridDesc hg,
                  const RepPlan plan, const double* __restrict__ t0,
                  const double* __restrict__ t1, float2* __restrict__ grad_table,
@@ -617,6 +624,47 @@ __global__ void __launch_bounds__(TILE * BWD_TPR, 2)
     mbar_init(barB, 1);
     fence_barrier_init();
   }
+  const int64_t n_tiles = ceil_div(n, TILE);
+  // Gradient scale of this CTA (a power of two, so exact both ways): the fp16 hi + lo
+  // split of G keeps 22 significant bits only while lo = G - fp16(G) is an fp16 normal,
+  // i.e. |G| >= 2^-3; below that lo's absolute precision is 2^-24 (measured: d(enc) at
+  // 4e-5 relative for the typical |G| ~ 1e-3 of a sum-of-squares loss).  The upstream
+  // magnitudes of the row's first two stages (|drgb| * rgb (1 - rgb) <= |drgb| / 4 and
+  // |dsigma| * sigma, sigma = the forward's output) over the CTA's rows set S so that
+  // their maximum lands at 2^4 — 2^12 of headroom below fp16's 65504 for the growth
+  // through the four weight matrices (overflow is still flagged, VR_FLAG_OVERFLOW).  The
+  // weight-gradient accumulators are per CTA, so one scale per CTA is exact: d(enc) and
+  // the flushed weight gradients are multiplied by 1/S.
+  float gscale = 1.f, ginv = 1.f;
+  if (sig) {
+    uint32_t* wmax = reinterpret_cast<uint32_t*>(smem + B_WMAX);
+    float m = 0.f;
+    for (int64_t tile = blockIdx.x + (int64_t)part * gridDim.x; tile < n_tiles;
+         tile += 2 * (int64_t)gridDim.x) {
+      const int64_t i = tile * TILE + r;
+      if (i < n) {
+        const float4 g4 = __ldg(dsr + i);
+        const float a = fabsf(g4.x * __ldg(&sig[i].x));
+        m = fmaxf(m, DENS ? a : fmaxf(a, 0.25f * fmaxf(fabsf(g4.y), fmaxf(fabsf(g4.z),
+                                                                          fabsf(g4.w)))));
+      }
+    }
+    // non-negative floats order like their bit patterns (NaN above inf)
+    const uint32_t wm = __reduce_max_sync(0xffffffffu, __float_as_uint(m));
+    if (lane == 0) wmax[threadIdx.x >> 5] = wm;
+    __syncthreads();
+    uint32_t mb = 0;
+#pragma unroll
+    for (int k = 0; k < TILE * BWD_TPR / 32; ++k) mb = max(mb, wmax[k]);
+    const float mx = __uint_as_float(mb);
+    if (mx > 0.f && isfinite(mx)) {
+      int k;
+      frexpf(mx, &k);  // 2^(k-1) <= mx < 2^k
+      const int e = min(64, max(-64, 4 - k));
+      gscale = ldexpf(1.f, e);
+      ginv = ldexpf(1.f, -e);
+    }
+  }
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
@@ -631,7 +679,6 @@ __global__ void __launch_bounds__(TILE * BWD_TPR, 2)
   bool acc = false;  // weight-gradient accumulators hold data
   constexpr int C64 = 64 / BWD_TPR, C16 = 16 / BWD_TPR;
   const int c64 = part * C64, c16 = part * C16;
-  const int64_t n_tiles = ceil_div(n, TILE);
 
   // one backward stage: wait until the previous wgrad released G, write G = hi + lo,
   // issue dX = G.W (commit -> barA) then dW += G^T X (commit -> barB), wait for dX only;
@@ -695,15 +742,15 @@ __global__ void __launch_bounds__(TILE * BWD_TPR, 2)
 
   RowIn nxt;
   if ((int64_t)blockIdx.x < n_tiles)
-    fetch_row<FUSED>(nxt, enc, rays, stride, rid, dsr, n, (int64_t)blockIdx.x * TILE + r, part,
-                     hg, t0, t1, pos);
+    fetch_row<FUSED>(nxt, enc, rays, stride, rid, dsr, gscale, n, (int64_t)blockIdx.x * TILE + r,
+                     part, hg, t0, t1, pos);
   for (int64_t tile = blockIdx.x; tile < n_tiles; tile += gridDim.x) {
     const int64_t i = tile * TILE + r;
     const bool valid = i < n;
     const RowIn cur = nxt;
     if (tile + gridDim.x < n_tiles)  // prefetch the next tile's inputs
-      fetch_row<FUSED>(nxt, enc, rays, stride, rid, dsr, n, (tile + gridDim.x) * TILE + r, part,
-                       hg, t0, t1, pos);
+      fetch_row<FUSED>(nxt, enc, rays, stride, rid, dsr, gscale, n, (tile + gridDim.x) * TILE + r,
+                       part, hg, t0, t1, pos);
     if (wgrad_pending) {  // the previous tile's last wgrad reads X4/Gh/Gl
       mbar_wait(barB, phB);
       phB ^= 1u;
@@ -743,7 +790,7 @@ __global__ void __launch_bounds__(TILE * BWD_TPR, 2)
       if (valid) {
 #pragma unroll
         for (int j = 0; j < 16; j += 2)
-          denc[(int64_t)(8 * part + j / 2) * n + i] = make_float2(v[j], v[j + 1]);
+          denc[(int64_t)(8 * part + j / 2) * n + i] = make_float2(v[j] * ginv, v[j + 1] * ginv);
       }
       acc = true;
       continue;
@@ -825,7 +872,7 @@ __global__ void __launch_bounds__(TILE * BWD_TPR, 2)
     tmem_ld16(tm_row + T_D0 + 16 * part, v);
     if (FUSED) {
 #pragma unroll
-      for (int j = 0; j < 16; ++j) pk[j] = valid ? v[j] : 0.f;
+      for (int j = 0; j < 16; ++j) pk[j] = valid ? v[j] * ginv : 0.f;
       pu[0] = cur.u[0];
       pu[1] = cur.u[1];
       pu[2] = cur.u[2];
@@ -833,7 +880,7 @@ __global__ void __launch_bounds__(TILE * BWD_TPR, 2)
     } else if (valid) {
 #pragma unroll
       for (int j = 0; j < 16; j += 2)
-        denc[(int64_t)(8 * part + j / 2) * n + i] = make_float2(v[j], v[j + 1]);
+        denc[(int64_t)(8 * part + j / 2) * n + i] = make_float2(v[j] * ginv, v[j + 1] * ginv);
     }
     acc = true;
   }
@@ -857,25 +904,28 @@ __global__ void __launch_bounds__(TILE * BWD_TPR, 2)
     float v[16], w[16];
     // this warp's column half of each accumulator
     tmem_ld16(tm_row + T_W1D + 16 * part, v);
-    for (int j = 0; j < 16; ++j) atomicAdd(gW + VR_MLP_W1D + m2 * 32 + 16 * part + j, v[j]);
+    for (int j = 0; j < 16; ++j) atomicAdd(gW + VR_MLP_W1D + m2 * 32 + 16 * part + j, v[j] * ginv);
     tmem_ld8(tm_row + T_W2DT + 8 * part, v);
     tmem_ld8(tm_row + T_W2DT + 16 + 8 * part, w);
     if (lane < 16)
-      for (int j = 0; j < 8; ++j) atomicAdd(gW + VR_MLP_W2D + (8 * part + j) * 64 + m, v[j] + w[j]);
+      for (int j = 0; j < 8; ++j)
+        atomicAdd(gW + VR_MLP_W2D + (8 * part + j) * 64 + m, (v[j] + w[j]) * ginv);
     if (!DENS) {  // the colour accumulators (never written in a density-only kernel)
       tmem_ld16(tm_row + T_W1C + 16 * part, v);
-      for (int j = 0; j < 16; ++j) atomicAdd(gW + VR_MLP_W1C + m2 * 32 + 16 * part + j, v[j]);
+      for (int j = 0; j < 16; ++j)
+        atomicAdd(gW + VR_MLP_W1C + m2 * 32 + 16 * part + j, v[j] * ginv);
 #pragma unroll
       for (int c = 0; c < 32; c += 16) {
         tmem_ld16(tm_row + T_W2C + 32 * part + c, v);
         for (int j = 0; j < 16; ++j)
-          atomicAdd(gW + VR_MLP_W2C + m2 * 64 + 32 * part + c + j, v[j]);
+          atomicAdd(gW + VR_MLP_W2C + m2 * 64 + 32 * part + c + j, v[j] * ginv);
       }
       if (part == 0) {
         tmem_ld8(tm_row + T_W3CT, v);
         tmem_ld8(tm_row + T_W3CT + 16, w);
         if (lane < 16)
-          for (int j = 0; j < 3; ++j) atomicAdd(gW + VR_MLP_W3C + j * 64 + m, v[j] + w[j]);
+          for (int j = 0; j < 3; ++j)
+            atomicAdd(gW + VR_MLP_W3C + j * 64 + m, (v[j] + w[j]) * ginv);
       }
     }
   }
@@ -928,8 +978,8 @@ int launch_fwd(const void* w, const void* enc, const double* rays, int64_t strid
 
 template <bool FUSED, bool DENS = false>
 int launch_bwd(const void* w, const void* enc, const double* rays, int64_t stride,
-               const int32_t* rid, int64_t n, const float* dsr, float* gW, float* denc,
-               int32_t* err, const VrHashGridDesc* g, const double* t0, const double* t1,
+               const int32_t* rid, int64_t n, const float* dsr, const float* sig, float* gW,
+               float* denc, int32_t* err, const VrHashGridDesc* g, const double* t0, const double* t1,
                float* grad_table, void* ws, size_t ws_bytes, const float* pos, void* stream,
                int max_ctas = 0) {
   int rc = set_smem(mlp::k_mlp_bwd_tc<FUSED, DENS>, mlp::B_SMEM, "mlp bwd: smem attribute");
@@ -951,7 +1001,9 @@ int launch_bwd(const void* w, const void* enc, const double* rays, int64_t strid
   mlp::k_mlp_bwd_tc<FUSED, DENS><<<grid, mlp::TILE * mlp::BWD_TPR, mlp::B_SMEM,
                                    (cudaStream_t)stream>>>(
       (const __half*)w, (const __half2*)enc, rays, stride, rid, n,
-      reinterpret_cast<const float4*>(dsr), gW, reinterpret_cast<float2*>(denc), err, gd, plan, t0, t1, reinterpret_cast<float2*>(grad_table),
+      reinterpret_cast<const float4*>(dsr), reinterpret_cast<const float4*>(sig), gW,
+      reinterpret_cast<float2*>(denc), err, gd, plan, t0, t1,
+      reinterpret_cast<float2*>(grad_table),
       reinterpret_cast<float2*>(ws), pos);
   rc = check_launch("vr_mlp_bwd_tc");
   if (rc != VR_OK || !FUSED) return rc;
@@ -972,15 +1024,16 @@ extern "C" int vr_mlp_fwd_tc(const void* w, const void* enc, const double* rays,
 }
 
 extern "C" int vr_mlp_bwd_tc(const void* w, const void* enc, const double* rays, int64_t stride,
-                             const int32_t* rid, int64_t n, const float* dsr, float* gW,
-                             float* denc, int32_t* err, int32_t max_ctas, void* stream) {
+                             const int32_t* rid, int64_t n, const float* dsr, const float* sig,
+                             float* gW, float* denc, int32_t* err, int32_t max_ctas,
+                             void* stream) {
   if (n < 0 || !w || !gW || !denc || !err) {
     set_error("vr_mlp_bwd_tc: bad argument");
     return VR_ERR_BAD_ARG;
   }
   if (n == 0) return VR_OK;
-  return launch_bwd<false>(w, enc, rays, stride, rid, n, dsr, gW, denc, err, nullptr, nullptr,
-                           nullptr, nullptr, nullptr, 0, nullptr, stream, max_ctas);
+  return launch_bwd<false>(w, enc, rays, stride, rid, n, dsr, sig, gW, denc, err, nullptr,
+                           nullptr, nullptr, nullptr, nullptr, 0, nullptr, stream, max_ctas);
 }
 
 // density branch only (proposal fields): sigma of the same MLP, rgb = 0; the backward takes
@@ -998,14 +1051,14 @@ extern "C" int vr_mlp_fwd_tc_density(const void* w, const void* enc, int64_t n, 
 
 extern "C" int vr_mlp_bwd_tc_density(const void* w, const void* enc, const double* rays,
                                      int64_t stride, const int32_t* rid, int64_t n,
-                                     const float* dsr, float* gW, float* denc, int32_t* err,
-                                     int32_t max_ctas, void* stream) {
+                                     const float* dsr, const float* sig, float* gW, float* denc,
+                                     int32_t* err, int32_t max_ctas, void* stream) {
   if (n < 0 || !w || !gW || !denc || !err) {
     set_error("vr_mlp_bwd_tc_density: bad argument");
     return VR_ERR_BAD_ARG;
   }
   if (n == 0) return VR_OK;
-  return launch_bwd<false, true>(w, enc, rays, stride, rid, n, dsr, gW, denc, err, nullptr,
+  return launch_bwd<false, true>(w, enc, rays, stride, rid, n, dsr, sig, gW, denc, err, nullptr,
                                  nullptr, nullptr, nullptr, nullptr, 0, nullptr, stream,
                                  max_ctas);
 }
@@ -1026,13 +1079,13 @@ extern "C" int vr_field_fwd_tc(const VrHashGridDesc* g, const float* table, cons
 extern "C" int vr_field_bwd_tc(const VrHashGridDesc* g, const void* w, const void* enc,
                                const double* rays, int64_t stride, const double* t0,
                                const double* t1, const int32_t* rid, int64_t n, const float* dsr,
-                               float* gW, float* grad_table, void* ws, size_t ws_bytes,
-                               int32_t* err, const float* pos, void* stream) {
+                               const float* sig, float* gW, float* grad_table, void* ws,
+                               size_t ws_bytes, int32_t* err, const float* pos, void* stream) {
   if (!valid_grid(g) || g->n_levels != 16 || n < 0 || !w || !enc || !gW || !grad_table || !err) {
     set_error("vr_field_bwd_tc: bad argument");
     return VR_ERR_BAD_ARG;
   }
   if (n == 0) return VR_OK;
-  return launch_bwd<true>(w, enc, rays, stride, rid, n, dsr, gW, nullptr, err, g, t0, t1,
+  return launch_bwd<true>(w, enc, rays, stride, rid, n, dsr, sig, gW, nullptr, err, g, t0, t1,
                           grad_table, ws, ws_bytes, pos, stream);
 }

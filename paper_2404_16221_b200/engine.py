@@ -379,33 +379,37 @@ class VolumePool:
     # 1.25 CTAs per SM (c4: 148 -> 407, 185 -> 388, 222 -> 394, 296 -> 413 ms per step)
     MLP_CTAS_BESIDE_SCATTER = int(os.environ.get("VR_MLP_BWD_CTAS", str(148 * 5 // 4)))
 
-    def field_backward(self, rays, b: SampleBatch, dsig_rgb: torch.Tensor, fields=None) -> None:
-        self.field_backward_jobs(rays, b, [(self.fields if fields is None else fields, dsig_rgb)])
+    def field_backward(self, rays, b: SampleBatch, dsig_rgb: torch.Tensor, fields=None,
+                       sig_rgb: torch.Tensor | None = None) -> None:
+        self.field_backward_jobs(rays, b, [(self.fields if fields is None else fields, dsig_rgb,
+                                            sig_rgb)])
 
     def field_backward_jobs(self, rays, b: SampleBatch, jobs) -> None:
-        """Backward of several field sets of the same batch ([(fields, dsig_rgb), ...]: the
-        NeRF fields and the proposals) as one pipeline."""
+        """Backward of several field sets of the same batch ([(fields, dsig_rgb, sig_rgb),
+        ...]: the NeRF fields and the proposals) as one pipeline; sig_rgb is the fields'
+        forward output (may be None)."""
         s = self._stream()
         base = self.region_lo - b.region_lo  # an all-region batch: skip the peers' regions
         split = [all(getattr(f, "split_backward", False) for f in fields if f.trainable)
-                 for fields, _ in jobs]
+                 for fields, _, _ in jobs]
         if self.overlap_backward and any(split):
             # region k's hash-grid scatter (L2-atomic bound) runs on the side stream while
             # the tensor-core MLP backward of the next region (of any field set) runs here
             main = torch.cuda.current_stream()
             side = self._side_stream()
             side.wait_stream(main)
-            for (fields, dsig_rgb), sp in zip(jobs, split):
+            for (fields, dsig_rgb, sig_rgb), sp in zip(jobs, split):
                 for kk, f in enumerate(fields):
                     lo, hi = b.region_slice(base + kk)
                     if hi <= lo or not f.trainable:
                         continue
+                    sig = sig_rgb[lo:] if sig_rgb is not None else None
                     if not sp:
                         f.backward(rays, b.t0[lo:], b.t1[lo:], b.ray_id[lo:], hi - lo,
-                                   dsig_rgb[lo:], s)
+                                   dsig_rgb[lo:], s, sig_rgb=sig)
                         continue
                     denc = f.backward_mlp(rays, b.ray_id[lo:], hi - lo, dsig_rgb[lo:], s,
-                                          self.MLP_CTAS_BESIDE_SCATTER)
+                                          self.MLP_CTAS_BESIDE_SCATTER, sig_rgb=sig)
                     ev = torch.cuda.Event()
                     ev.record(main)
                     with torch.cuda.stream(side):
@@ -414,12 +418,13 @@ class VolumePool:
                         f.backward_scatter(denc, hi - lo, _lib.stream_ptr(), self.SCATTER_BLOCKS)
             main.wait_stream(side)
             return
-        for fields, dsig_rgb in jobs:
+        for fields, dsig_rgb, sig_rgb in jobs:
             for kk, f in enumerate(fields):
                 lo, hi = b.region_slice(base + kk)
                 if hi > lo and f.trainable:
                     f.backward(rays, b.t0[lo:], b.t1[lo:], b.ray_id[lo:], hi - lo,
-                               dsig_rgb[lo:], s)
+                               dsig_rgb[lo:], s,
+                               sig_rgb=sig_rgb[lo:] if sig_rgb is not None else None)
 
     # ---- K4 ----------------------------------------------------------------------------
     def local_packets(self, b: SampleBatch, sig_rgb: torch.Tensor,
@@ -630,9 +635,9 @@ class VolumePool:
                   _lib.ptr(totals), _lib.ptr(dsig), s)
         # NeRF fields and proposals in one backward pipeline (the proposals' MLP backward
         # overlaps the NeRF scatter on the side stream)
-        jobs = [(self.fields, dsig)]
+        jobs = [(self.fields, dsig, sig_rgb)]
         if interlevel:
-            jobs.append((self.proposals, dsig_prop))
+            jobs.append((self.proposals, dsig_prop, sig_prop))
         self.field_backward_jobs(rays, b, jobs)
         return loss, out, b
 
@@ -658,7 +663,7 @@ class VolumePool:
         _lib.call("vr_segment_bwd", _lib.ptr(t0r), _lib.ptr(t1r), _lib.ptr(srr), _lib.ptr(ray_off),
                   _lib.ptr(b.ray_te), R, 1, _lib.ptr(dpk), _lib.ptr(totals), _lib.ptr(dsr), s)
         dsig = self._permute(b, ray_off, dsr, False)
-        self.field_backward(rays, b, dsig)
+        self.field_backward(rays, b, dsig, sig_rgb=sig_rgb)
         return loss, out, b
 
     def zero_grad(self):

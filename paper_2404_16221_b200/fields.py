@@ -130,7 +130,9 @@ class RegionField:
     def forward(self, rays, t0, t1, ray_id, n, sig_rgb, stream):
         raise NotImplementedError
 
-    def backward(self, rays, t0, t1, ray_id, n, dsig_rgb, stream):
+    def backward(self, rays, t0, t1, ray_id, n, dsig_rgb, stream, sig_rgb=None):
+        """sig_rgb: the forward's output for the same samples (optional; the hash-grid
+        MLP backward uses it to scale its fp16 gradient operands)."""
         raise NotImplementedError(f"{type(self).__name__} has no parameters")
 
     def zero_grad(self):
@@ -211,7 +213,7 @@ class VoxelRegion(RegionField):
                   _lib.ptr(self.colors), _lib.ptr(rays), rays.shape[1], _lib.ptr(t0),
                   _lib.ptr(t1), _lib.ptr(ray_id), n, _lib.ptr(sig_rgb), stream)
 
-    def backward(self, rays, t0, t1, ray_id, n, dsig_rgb, stream):
+    def backward(self, rays, t0, t1, ray_id, n, dsig_rgb, stream, sig_rgb=None):
         _lib.call("vr_voxel_bwd", _lib.addr(self.desc), _lib.ptr(rays), rays.shape[1],
                   _lib.ptr(t0), _lib.ptr(t1), _lib.ptr(ray_id), n, _lib.ptr(dsig_rgb),
                   _lib.ptr(self.grad), stream)
@@ -394,26 +396,27 @@ class HashGridMLP(RegionField):
                   _lib.ptr(self.weights16), _lib.ptr(self._enc), _lib.ptr(rays), rays.shape[1],
                   _lib.ptr(ray_id), n, _lib.ptr(sig_rgb), stream)
 
-    def backward(self, rays, t0, t1, ray_id, n, dsig_rgb, stream):
+    def backward(self, rays, t0, t1, ray_id, n, dsig_rgb, stream, sig_rgb=None):
         if n == 0:
             return
         enc = self._enc  # written by the forward of the same step
         if self.density_only:
-            self.backward_scatter(self.backward_mlp(rays, ray_id, n, dsig_rgb, stream), n,
-                                  stream)
+            self.backward_scatter(self.backward_mlp(rays, ray_id, n, dsig_rgb, stream,
+                                                    sig_rgb=sig_rgb), n, stream)
             return
         if self.mlp_impl in ("fused", "fused_fwd") and self.hash_order == "sample":
             ws = self._workspace(rays.device)
             _lib.call("vr_field_bwd_tc", _lib.addr(self.desc), _lib.ptr(self.weights16),
                       _lib.ptr(enc), _lib.ptr(rays), rays.shape[1], _lib.ptr(t0), _lib.ptr(t1),
-                      _lib.ptr(ray_id), n, _lib.ptr(dsig_rgb), _lib.ptr(self.grad_weights),
-                      _lib.ptr(self.grad_table), _lib.ptr(ws), ws.numel(), _lib.ptr(self.err),
+                      _lib.ptr(ray_id), n, _lib.ptr(dsig_rgb), _lib.ptr(sig_rgb),
+                      _lib.ptr(self.grad_weights), _lib.ptr(self.grad_table), _lib.ptr(ws),
+                      ws.numel(), _lib.ptr(self.err),
                       _lib.ptr(self._pos) if self.mlp_impl == "fused" else None, stream)
             return
         denc = torch.empty(16 * n * 2, dtype=torch.float32, device=rays.device)
         if self.mlp_impl != "cuda":
             _lib.call("vr_mlp_bwd_tc", _lib.ptr(self.weights16), _lib.ptr(enc), _lib.ptr(rays),
-                      rays.shape[1], _lib.ptr(ray_id), n, _lib.ptr(dsig_rgb),
+                      rays.shape[1], _lib.ptr(ray_id), n, _lib.ptr(dsig_rgb), _lib.ptr(sig_rgb),
                       _lib.ptr(self.grad_weights), _lib.ptr(denc), _lib.ptr(self.err), 0, stream)
         else:
             _lib.call("vr_mlp_bwd", _lib.ptr(self.weights16), _lib.ptr(enc), _lib.ptr(rays),
@@ -445,16 +448,17 @@ class HashGridMLP(RegionField):
             self.density_only or self.hash_order == "level"
             or self.n_entries * 8 < self.SPLIT_BELOW_BYTES)
 
-    def backward_mlp(self, rays, ray_id, n, dsig_rgb, stream, max_ctas: int = 0):
+    def backward_mlp(self, rays, ray_id, n, dsig_rgb, stream, max_ctas: int = 0, sig_rgb=None):
         """MLP backward of the step's samples; returns d(enc) [16][n] float2 (float32).
-        max_ctas: grid cap when a scatter runs beside it (0: the full persistent grid)."""
+        max_ctas: grid cap when a scatter runs beside it (0: the full persistent grid);
+        sig_rgb: the forward's output (gradient scaling, vr_capi.h vr_mlp_bwd_tc)."""
         denc = torch.empty(16 * max(n, 1) * 2, dtype=torch.float32, device=rays.device)
         if n:
             _lib.call("vr_mlp_bwd_tc_density" if self.density_only else "vr_mlp_bwd_tc",
                       _lib.ptr(self.weights16), _lib.ptr(self._enc),
                       _lib.ptr(rays), rays.shape[1], _lib.ptr(ray_id), n, _lib.ptr(dsig_rgb),
-                      _lib.ptr(self.grad_weights), _lib.ptr(denc), _lib.ptr(self.err),
-                      int(max_ctas), stream)
+                      _lib.ptr(sig_rgb), _lib.ptr(self.grad_weights), _lib.ptr(denc),
+                      _lib.ptr(self.err), int(max_ctas), stream)
         return denc
 
     def backward_scatter(self, denc, n, stream, max_blocks=0):

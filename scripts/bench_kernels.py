@@ -37,7 +37,7 @@ de = torch.empty((16, n, 2), device=DEV)
 err = torch.zeros(1, dtype=torch.int32, device=DEV)
 s = L.stream_ptr()
 f = lambda: L.call("vr_mlp_fwd_tc", L.ptr(w16), L.ptr(enc), L.ptr(rays), R, L.ptr(rid), n, L.ptr(out), s)
-bw = lambda: L.call("vr_mlp_bwd_tc", L.ptr(w16), L.ptr(enc), L.ptr(rays), R, L.ptr(rid), n, L.ptr(dsr),
+bw = lambda: L.call("vr_mlp_bwd_tc", L.ptr(w16), L.ptr(enc), L.ptr(rays), R, L.ptr(rid), n, L.ptr(dsr), None,
                     L.ptr(gw), L.ptr(de), L.ptr(err), 0, s)
 tf = timeit(f)
 tb = timeit(bw)

@@ -645,8 +645,10 @@ def test_mlp_tensor_core_matches_cuda_core(n):
     for name in ("vr_mlp_bwd", "vr_mlp_bwd_tc"):
         gw = torch.zeros(_lib.VR_MLP_NPARAMS, dtype=torch.float32, device=DEV)
         de = torch.empty((16, n, 2), dtype=torch.float32, device=DEV)
-        args = [_lib.ptr(w16), _lib.ptr(enc), _lib.ptr(rays), R, _lib.ptr(rid), n, _lib.ptr(dsr),
-                _lib.ptr(gw), _lib.ptr(de)]
+        args = [_lib.ptr(w16), _lib.ptr(enc), _lib.ptr(rays), R, _lib.ptr(rid), n, _lib.ptr(dsr)]
+        if name.endswith("_tc"):  # with the forward's output: per-CTA gradient scaling
+            args += [_lib.ptr(b)]
+        args += [_lib.ptr(gw), _lib.ptr(de)]
         if name.endswith("_tc"):
             args += [_lib.ptr(err), 0]
         _lib.call(name, *args, s)
