@@ -59,6 +59,7 @@ extern "C" {
 #define VR_FLAG_OOB 4            /* partitioner.OutOfBoundsError, partitioner.py:179-180  */
 #define VR_FLAG_OVERFLOW 8       /* capacity / bin-count overflow (no reference analogue) */
 #define VR_FLAG_TOO_MANY_SEGS 16 /* > VR_MAX_REGIONS non-empty segments on one ray        */
+#define VR_FLAG_GRAD_OVERFLOW 32 /* a scaled MLP gradient not representable in fp16      */
 
 /* Partition tree (reference PartitionTree/SplitNode/LeafNode, partitioner.py:51-80).
  * Internal nodes are indexed 0..n_nodes-1 with node 0 the root; a child index
@@ -265,7 +266,7 @@ int vr_mlp_bwd(const void* weights_dev, const void* enc_dev, const double* rays_
 /* Same MLP on the 5th-gen tensor cores (tcgen05.mma kind::f16, TMEM accumulators,
  * persistent 128-sample tiles).  The production path; vr_mlp_fwd / vr_mlp_bwd are the
  * CUDA-core reference kernels it is tested against.  The backward raises
- * VR_FLAG_OVERFLOW in err_dev if a gradient is not representable in fp16. */
+ * VR_FLAG_GRAD_OVERFLOW in err_dev if a gradient is not representable in fp16. */
 int vr_mlp_fwd_tc(const void* weights_dev, const void* enc_dev, const double* rays_dev,
                   int64_t ray_stride, const int32_t* ray_id_dev, int64_t n, float* sig_rgb_dev,
                   void* stream);
@@ -376,7 +377,10 @@ int vr_global_train(const float* packets_dev, int32_t n_regions, int64_t n_rays,
  * transmittance in front of each owned segment, prefix [own_cnt][n_rays][2] float32,
  * from the exchanged packets and the exchanged proposal transmittances prop_T
  * [n_regions][n_rays].  vr_interlevel: per-segment loss (float64 [region_cnt][n_rays])
- * and d(loss)/d(proposal sigma) into dsig_prop[i].x (float4, other lanes zero). */
+ * and d(loss)/d(proposal sigma) into dsig_prop[i].x (float4, other lanes zero).
+ * dsig_prop_dev is also the kernel's scratch (its first sweep parks a double2 in each
+ * sample's 16-byte slot, the second overwrites it with the float4 result): it must be
+ * 16-byte aligned and must not alias sig_rgb_dev or sig_prop_dev (VR_ERR_BAD_ARG). */
 int vr_prefix_train(const float* packets_dev, const float* prop_T_dev, int32_t n_regions,
                     int64_t n_rays, int32_t own_lo, int32_t own_cnt, float* prefix_dev,
                     void* stream);
@@ -392,8 +396,14 @@ int vr_interlevel(const double* t0_dev, const double* t1_dev, const float* sig_r
 int vr_sum_f64(const double* x_dev, int64_t n, double* out_dev, double* ws_dev, void* stream);
 
 /* ---- optimiser ------------------------------------------------ */
+/* Adam (torch.optim.Adam semantics, no weight decay).  err_dev (may be NULL): the step's
+ * device error word; when it is non-zero at the time the kernel runs (an earlier kernel
+ * of the step flagged a non-finite packet, a negative distortion or an overflow) the
+ * update is skipped, so a poisoned gradient never reaches the parameters or the moments
+ * (segrender.py:124-141 raises before the value is used). */
 int vr_adam_step(float* param_dev, const float* grad_dev, float* m_dev, float* v_dev, int64_t n,
-                 float lr, float beta1, float beta2, float eps, int32_t step, void* stream);
+                 float lr, float beta1, float beta2, float eps, int32_t step,
+                 const int32_t* err_dev, void* stream);
 /* fp32 master -> fp16 copy (MLP weights) */
 int vr_cast_f32_f16(const float* src_dev, void* dst_dev, int64_t n, void* stream);
 

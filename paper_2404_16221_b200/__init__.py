@@ -20,6 +20,7 @@ from .engine import (
 from .errors import (
     CapacityError,
     DegenerateSplitError,
+    GradientOverflowError,
     InsufficientPointsError,
     NegativeLossError,
     NoPointsError,

@@ -13,6 +13,7 @@ from pathlib import Path
 
 from .errors import (
     CapacityError,
+    GradientOverflowError,
     NegativeLossError,
     NonFiniteInputError,
     OutOfBoundsError,
@@ -34,6 +35,7 @@ VR_FLAG_NEG_LOSS = 2
 VR_FLAG_OOB = 4
 VR_FLAG_OVERFLOW = 8
 VR_FLAG_TOO_MANY_SEGS = 16
+VR_FLAG_GRAD_OVERFLOW = 32
 
 VR_MLP_W1D = 0
 VR_MLP_W2D = VR_MLP_W1D + 64 * 32
@@ -146,7 +148,7 @@ SIGNATURES = {
     "vr_prefix_train": [P, P, I32, I64, I32, I32, P, P],
     "vr_interlevel": [P, P, P, P, P, P, I64, I32, F32, F32, P, P, P],
     "vr_sum_f64": [P, I64, P, P, P],
-    "vr_adam_step": [P, P, P, P, I64, F32, F32, F32, F32, I32, P],
+    "vr_adam_step": [P, P, P, P, I64, F32, F32, F32, F32, I32, P, P],
     "vr_cast_f32_f16": [P, P, I64, P],
 }
 _RESTYPES = {"vr_last_error": C.c_char_p, "vr_scan_workspace_bytes": C.c_size_t,
@@ -223,6 +225,8 @@ def raise_flags(flags: int, where: str = "") -> None:
         raise OutOfBoundsError(f"sample point outside the root box {where}")
     if flags & (VR_FLAG_OVERFLOW | VR_FLAG_TOO_MANY_SEGS):
         raise CapacityError(f"capacity overflow (flags={flags}) {where}")
+    if flags & VR_FLAG_GRAD_OVERFLOW:
+        raise GradientOverflowError(f"MLP gradient beyond the fp16 range {where}")
     raise VrError(f"device error flags {flags} {where}")
 
 

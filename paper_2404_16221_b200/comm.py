@@ -114,7 +114,14 @@ def all_reduce_max_(t: torch.Tensor, group=None, world: int = 1) -> torch.Tensor
 
 
 def all_reduce_scalar(x: torch.Tensor, group=None, world: int = 1) -> torch.Tensor:
-    """Logging only: sum a per-rank scalar (the loss is already identical everywhere)."""
-    if world > 1:
-        dist.all_reduce(x, group=group)
+    """In-place SUM over the ranks of a per-rank scalar (the interlevel loss: each rank sums
+    its own segments' terms; the main loss term is already identical everywhere)."""
+    if world == 1:
+        return x
+    if _host_staged(group, x):
+        c = x.cpu()
+        dist.all_reduce(c, group=group)
+        x.copy_(c)
+        return x
+    dist.all_reduce(x, group=group)
     return x

@@ -496,7 +496,8 @@ __global__ void k_sum_final(const double* partial, double* out) {
 // ---- Adam ------------------------------------------------------------------------------
 __global__ void k_adam(float4* __restrict__ p, const float4* __restrict__ g, float4* __restrict__ m,
                        float4* __restrict__ v, int64_t n4, float lr, float b1, float b2, float eps,
-                       float bc1, float bc2) {
+                       float bc1, float bc2, const int32_t* __restrict__ err) {
+  if (err && *err) return;  // the step flagged an error: no update (vr_capi.h)
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n4;
        i += (int64_t)gridDim.x * blockDim.x) {
     float4 pp = p[i], gg = g[i], mm = m[i], vv = v[i];
@@ -517,7 +518,9 @@ __global__ void k_adam(float4* __restrict__ p, const float4* __restrict__ g, flo
 }
 
 __global__ void k_adam_tail(float* p, const float* g, float* m, float* v, int64_t lo, int64_t n,
-                            float lr, float b1, float b2, float eps, float bc1, float bc2) {
+                            float lr, float b1, float b2, float eps, float bc1, float bc2,
+                            const int32_t* __restrict__ err) {
+  if (err && *err) return;
   for (int64_t i = lo + threadIdx.x; i < n; i += blockDim.x) {
     m[i] = b1 * m[i] + (1.f - b1) * g[i];
     v[i] = b2 * v[i] + (1.f - b2) * g[i] * g[i];
@@ -797,7 +800,8 @@ extern "C" int vr_sum_f64(const double* x, int64_t n, double* out, double* ws, v
 }
 
 extern "C" int vr_adam_step(float* p, const float* g, float* m, float* v, int64_t n, float lr,
-                            float b1, float b2, float eps, int32_t step, void* stream) {
+                            float b1, float b2, float eps, int32_t step, const int32_t* err,
+                            void* stream) {
   if (n < 0 || step < 1) {
     set_error("vr_adam_step: bad argument");
     return VR_ERR_BAD_ARG;
@@ -809,8 +813,9 @@ extern "C" int vr_adam_step(float* p, const float* g, float* m, float* v, int64_
   cudaStream_t s = (cudaStream_t)stream;
   if (n4)
     k_adam<<<grid_for(n4, 256), 256, 0, s>>>((float4*)p, (const float4*)g, (float4*)m,
-                                             (float4*)v, n4, lr, b1, b2, eps, bc1, bc2);
-  if (4 * n4 < n) k_adam_tail<<<1, 256, 0, s>>>(p, g, m, v, 4 * n4, n, lr, b1, b2, eps, bc1, bc2);
+                                             (float4*)v, n4, lr, b1, b2, eps, bc1, bc2, err);
+  if (4 * n4 < n)
+    k_adam_tail<<<1, 256, 0, s>>>(p, g, m, v, 4 * n4, n, lr, b1, b2, eps, bc1, bc2, err);
   return check_launch("vr_adam_step");
 }
 

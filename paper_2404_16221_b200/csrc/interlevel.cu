@@ -221,6 +221,14 @@ extern "C" int vr_interlevel(const double* t0, const double* t1, const float* si
     set_error("vr_interlevel: bad argument");
     return VR_ERR_BAD_ARG;
   }
+  // dsig_prop doubles as the first sweep's scratch (a double2 parked in each sample's
+  // 16-byte slot): it must be 16-byte aligned and must not alias the read-only inputs
+  if (reinterpret_cast<uintptr_t>(dsig_prop) % 16 != 0 ||
+      (const void*)dsig_prop == (const void*)sig_prop ||
+      (const void*)dsig_prop == (const void*)sig_rgb) {
+    set_error("vr_interlevel: dsig_prop must be 16-byte aligned and distinct from the inputs");
+    return VR_ERR_BAD_ARG;
+  }
   const int64_t n_segs = n_rays * region_cnt;
   if (n_segs == 0) return VR_OK;
   k_interlevel<<<grid_for(ceil_div(n_segs, 32 * IL_WARPS), 1, 8), IL_WARPS * 32, 0,

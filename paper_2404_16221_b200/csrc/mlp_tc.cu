@@ -632,7 +632,7 @@ __global__ void __launch_bounds__(TILE * BWD_TPR, 2)
   // magnitudes of the row's first two stages (|drgb| * rgb (1 - rgb) <= |drgb| / 4 and
   // |dsigma| * sigma, sigma = the forward's output) over the CTA's rows set S so that
   // their maximum lands at 2^4 — 2^12 of headroom below fp16's 65504 for the growth
-  // through the four weight matrices (overflow is still flagged, VR_FLAG_OVERFLOW).  The
+  // through the four weight matrices (overflow is flagged, VR_FLAG_GRAD_OVERFLOW).  The
   // weight-gradient accumulators are per CTA, so one scale per CTA is exact: d(enc) and
   // the flushed weight gradients are multiplied by 1/S.
   float gscale = 1.f, ginv = 1.f;
@@ -929,8 +929,7 @@ __global__ void __launch_bounds__(TILE * BWD_TPR, 2)
       }
     }
   }
-  const int flags = inf_bits ? VR_FLAG_OVERFLOW : 0;
-  if (__any_sync(0xffffffffu, flags != 0) && lane == 0) atomicOr(err, VR_FLAG_OVERFLOW);
+  if (__any_sync(0xffffffffu, inf_bits != 0) && lane == 0) atomicOr(err, VR_FLAG_GRAD_OVERFLOW);
   tc_fence_before();
   __syncthreads();
   if (threadIdx.x < 32) {

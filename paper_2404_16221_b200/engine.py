@@ -99,6 +99,12 @@ class VolumePool:
         self.proposals = list(proposals) if proposals is not None else None
         if self.proposals is not None and len(self.proposals) != self.region_cnt:
             raise ValueError("one proposal field per owned region")
+        # a trainable field keeps per-step state (encodings, positions, gradients, scatter
+        # workspace): one instance may serve only one region
+        trainable = [f for f in self.fields + (self.proposals or []) if f.trainable]
+        if len({id(f) for f in trainable}) != len(trainable):
+            raise ValueError("each region needs its own trainable field instance (a shared "
+                             "instance would mix the regions' encodings and gradients)")
         self.background = np.asarray(background, dtype=np.float64)
         self.device = torch.device(device) if device is not None else torch.device("cuda")
         self.err = torch.zeros(1, dtype=torch.int32, device=self.device)
@@ -143,6 +149,17 @@ class VolumePool:
         if flags:
             self.err.zero_()
             _lib.raise_flags(flags, where)
+
+    @staticmethod
+    def _flag_stage(flags: int) -> str:
+        """Which kernels of a training step set these flags."""
+        if flags & (_lib.VR_FLAG_NONFINITE | _lib.VR_FLAG_NEG_LOSS):
+            return "in the global composite (K5)"
+        if flags & _lib.VR_FLAG_GRAD_OVERFLOW:
+            return "in the field backward (tensor-core MLP)"
+        if flags & (_lib.VR_FLAG_OVERFLOW | _lib.VR_FLAG_TOO_MANY_SEGS):
+            return "in the packet exchange"
+        return "in the training step"
 
     def rays_to_device(self, rays) -> torch.Tensor:
         if isinstance(rays, torch.Tensor):
@@ -319,7 +336,8 @@ class VolumePool:
         N = bounds[-1]
         cnt, R = self.region_cnt, p["R"]
         t0, t1, ray_id = p["t0"], p["t1"], p["ray_id"]
-        flags = int(p["err"].item())
+        flags = int(p["err"].item()) | int(self.err.item())
+        self.err.zero_()
         if N > p["cap"]:  # did not fit: fill again on this stream
             flags &= ~_lib.VR_FLAG_OVERFLOW
             t0 = torch.empty(N, dtype=torch.float64, device=self.device)
@@ -567,13 +585,16 @@ class VolumePool:
 
     def loss_and_grad(self, rays, targets, dt: float, lambda_dist: float = 1.0,
                       background=None, lambda_interlevel: float = 0.0, eps: float = 1e-7,
-                      protocol: str = "tile", batch: SampleBatch | None = None):
+                      protocol: str = "tile", batch: SampleBatch | None = None,
+                      check_errors: bool = True):
         """Forward + backward of the NeRF-XL loss (segrender.py:198-207 definition:
         sum over rays of |C + T*bg - target|^2 + lambda * distortion), plus, with
         proposal fields and lambda_interlevel > 0, the interlevel loss of csrc/interlevel.cu
-        (this rank's segments; multi-rank totals need one scalar all-reduce for logging).
+        (summed over the ranks: identical on every rank, like the main term).
         Gradients accumulate into the owned region fields; returns (loss [1] float64
-        device tensor, out [7][R], batch)."""
+        device tensor, out [7][R], batch).  check_errors: read the device error word at
+        the end (one host sync) and raise the reference exception of a flagged non-finite
+        packet / negative distortion / overflow (segrender.py:124-141)."""
         rays = self.rays_to_device(rays)
         tg = torch.as_tensor(targets, dtype=torch.float32).to(self.device, non_blocking=True)
         tg = tg.reshape(-1, 3).contiguous()
@@ -584,7 +605,10 @@ class VolumePool:
         if protocol != "tile_aggregate":
             if lambda_interlevel > 0.0:
                 raise ValueError("the interlevel loss is defined on the tile protocol")
-            return self._sample_protocol_train(rays, tg, dt, lambda_dist, background)
+            res = self._sample_protocol_train(rays, tg, dt, lambda_dist, background)
+            if check_errors:
+                self.check_step()
+            return res
         # batch: sample_async
         b = batch if batch is not None else self.sample(rays, dt, exchange=True)
         sig_rgb = self.evaluate(rays, b)
@@ -627,7 +651,9 @@ class VolumePool:
             il = torch.empty(1, dtype=torch.float64, device=self.device)
             _lib.call("vr_sum_f64", _lib.ptr(seg_loss), seg_loss.numel(), _lib.ptr(il),
                       _lib.ptr(self._sum_scratch()), s)
-            loss = loss + il
+            # each rank sums its own segments' terms: the all-reduce makes the reported loss
+            # the whole batch's on every rank (the main term already is)
+            loss = loss + comm.all_reduce_scalar(il, self.group, self.world)
         # vr_segment_bwd writes every sample (no zero fill of the N x 16 B array)
         dsig = torch.empty((max(b.n_samples, 1), 4), dtype=torch.float32, device=self.device)
         _lib.call("vr_segment_bwd", _lib.ptr(b.t0), _lib.ptr(b.t1), _lib.ptr(sig_rgb),
@@ -639,7 +665,19 @@ class VolumePool:
         if interlevel:
             jobs.append((self.proposals, dsig_prop, sig_prop))
         self.field_backward_jobs(rays, b, jobs)
+        if check_errors:
+            self.check_step()
         return loss, out, b
+
+    def check_step(self, updated: bool = False) -> None:
+        """Read the step's device error word (one host sync) and raise the reference
+        exception with the stage that set it; the word is cleared.  A flagged step never
+        reaches the parameters: vr_adam_step is gated on the same word."""
+        flags = int(self.err.item())
+        if flags:
+            self.err.zero_()
+            _lib.raise_flags(flags, self._flag_stage(flags) + (" (parameters not updated)"
+                                                          if updated else ""))
 
     def _sample_protocol_train(self, rays, tg, dt, lambda_dist, background):
         """Training through the sample-broadcast protocol: every rank composites whole rays
@@ -678,10 +716,12 @@ class VolumePool:
         prefetched during the previous step)."""
         self.zero_grad()
         loss, _, _ = self.loss_and_grad(rays, targets, dt, lambda_dist, background,
-                                        lambda_interlevel, protocol=protocol, batch=batch)
+                                        lambda_interlevel, protocol=protocol, batch=batch,
+                                        check_errors=False)
         for f in self.fields + (self.proposals or []):
             if f.trainable:
-                f.step(lr, step)
+                f.step(lr, step)  # skipped on the device if the step flagged an error
+        self.check_step(updated=True)
         return loss
 
     # ---- accounting ----------------------------------------------------------------------
@@ -742,6 +782,9 @@ def spawn(tree: PartitionTree, scene: Scene, device=None, rank: int = 0, world: 
     """One region field per owned leaf (spawn, distsim.py:358-364)."""
     lo, cnt = comm.owned_regions(len(tree.leaves), rank, world)
     dev = torch.device(device) if device is not None else torch.device("cuda")
+    if isinstance(scene.field, RegionField) and scene.field.trainable and cnt > 1:
+        raise ValueError("a trainable RegionField cannot be spawned over several regions: "
+                         "build one field per region and pass them to VolumePool")
     fields = [region_field_for(scene.field, tree.leaves[k], tree, dev) for k in range(lo, lo + cnt)]
     return VolumePool(tree, fields, scene.background, dev, rank, world, group)
 

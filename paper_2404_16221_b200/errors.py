@@ -12,6 +12,11 @@ class CapacityError(VrError):
     """A kernel-side capacity bound was exceeded (bins per ray, segments per ray)."""
 
 
+class GradientOverflowError(VrError):
+    """A (scaled) MLP gradient is not representable in the tensor-core kernels' fp16
+    operands (no reference analogue: the reference has no backward)."""
+
+
 class NonFiniteInputError(ValueError):
     """A segment aggregate carries NaN or infinity (segrender.py:39-40)."""
 

@@ -481,11 +481,14 @@ class HashGridMLP(RegionField):
             self.adam = [torch.zeros_like(self.table), torch.zeros_like(self.table),
                          torch.zeros_like(self.weights), torch.zeros_like(self.weights)]
         mt, vt, mw, vw = self.adam
+        # gated on the pool's device error word: a step that flagged an error leaves the
+        # parameters and moments untouched (vr_capi.h vr_adam_step)
         _lib.call("vr_adam_step", _lib.ptr(self.table), _lib.ptr(self.grad_table), _lib.ptr(mt),
-                  _lib.ptr(vt), self.table.numel(), lr, betas[0], betas[1], eps, step, s)
+                  _lib.ptr(vt), self.table.numel(), lr, betas[0], betas[1], eps, step,
+                  _lib.ptr(self.err), s)
         _lib.call("vr_adam_step", _lib.ptr(self.weights), _lib.ptr(self.grad_weights),
                   _lib.ptr(mw), _lib.ptr(vw), self.weights.numel(), lr, betas[0], betas[1], eps,
-                  step, s)
+                  step, _lib.ptr(self.err), s)
         self.refresh_weights(s)
 
 

@@ -704,3 +704,104 @@ def test_interlevel_loss_and_proposal_grads_match_oracle(density_only):
             rel_t = np.linalg.norm(f.grad_table.cpu().numpy() - gt) / max(np.linalg.norm(gt), 1e-30)
             rel_w = np.linalg.norm(f.grad_weights.cpu().numpy() - gw) / max(np.linalg.norm(gw), 1e-30)
             assert rel_t <= 1e-3 and rel_w <= 1e-3, (kk, rel_t, rel_w)
+
+
+# ---- optimiser and error gating ---------------------------------------------------------
+
+@pytest.mark.parametrize("n", [1, 7, 4096, 100003])
+def test_adam_matches_torch(n):
+    """vr_adam_step == torch.optim.Adam (no weight decay) over several steps of the same
+    gradient sequence, betas (0.9, 0.99), eps 1e-15 (the training defaults)."""
+    from paper_2404_16221_b200 import _lib
+    g = torch.Generator(device="cpu").manual_seed(n)
+    p0 = torch.randn(n, generator=g)
+    grads = [torch.randn(n, generator=g) * 10.0 ** (-k) for k in range(6)]
+    mine = p0.clone().to(DEV)
+    m = torch.zeros_like(mine)
+    v = torch.zeros_like(mine)
+    ref = p0.clone().to(DEV).requires_grad_(True)
+    opt = torch.optim.Adam([ref], lr=1e-2, betas=(0.9, 0.99), eps=1e-15)
+    s = _lib.stream_ptr()
+    for step, gr in enumerate(grads, start=1):
+        gd = gr.to(DEV)
+        _lib.call("vr_adam_step", _lib.ptr(mine), _lib.ptr(gd), _lib.ptr(m), _lib.ptr(v), n, 1e-2,
+                  0.9, 0.99, 1e-15, step, None, s)
+        ref.grad = gd.clone()
+        opt.step()
+    torch.cuda.synchronize()
+    st = opt.state[ref]
+    torch.testing.assert_close(mine, ref.detach(), rtol=1e-5, atol=1e-7)
+    # the moments to a few float32 ulps of their scale (m cancels where the gradient
+    # sequence changes sign: relative error there is meaningless)
+    torch.testing.assert_close(m, st["exp_avg"], rtol=4e-6, atol=4e-7 * m.abs().max().item())
+    torch.testing.assert_close(v, st["exp_avg_sq"], rtol=4e-6, atol=0)
+
+
+def test_adam_is_skipped_when_the_error_word_is_set():
+    from paper_2404_16221_b200 import _lib
+    p = torch.randn(1000, device=DEV)
+    p0 = p.clone()
+    gr = torch.randn(1000, device=DEV)
+    m = torch.zeros_like(p)
+    v = torch.zeros_like(p)
+    err = torch.full((1,), _lib.VR_FLAG_NONFINITE, dtype=torch.int32, device=DEV)
+    _lib.call("vr_adam_step", _lib.ptr(p), _lib.ptr(gr), _lib.ptr(m), _lib.ptr(v), 1000, 1e-2,
+              0.9, 0.99, 1e-15, 1, _lib.ptr(err), _lib.stream_ptr())
+    torch.cuda.synchronize()
+    assert torch.equal(p, p0) and not m.any() and not v.any()
+    err.zero_()
+    _lib.call("vr_adam_step", _lib.ptr(p), _lib.ptr(gr), _lib.ptr(m), _lib.ptr(v), 1000, 1e-2,
+              0.9, 0.99, 1e-15, 1, _lib.ptr(err), _lib.stream_ptr())
+    torch.cuda.synchronize()
+    assert not torch.equal(p, p0)
+
+
+def _poisoned_pool(field, value):
+    """A hash+MLP pool whose exchanged packets get one non-empty packet's field set to
+    value (mid train_step: after K4, before K5)."""
+    pool, tree, models, rays, targets = _hash_setup(log2_T=12, K=2, n_rays=64)
+    orig = pool.exchange_packets
+
+    def poisoned(b, local, extra=None, dst=None):
+        allp, all_e = orig(b, local, extra, dst)
+        live = (allp[:, :, 7].view(torch.int32) != np.iinfo(np.int32).max).nonzero()
+        k, r = live[0].tolist()
+        allp[k, r, field] = value
+        return allp, all_e
+
+    pool.exchange_packets = poisoned
+    return pool, rays, targets
+
+
+@pytest.mark.parametrize("field,value,exc", [
+    (0, float("nan"), vr.NonFiniteInputError),   # T
+    (1, float("inf"), vr.NonFiniteInputError),   # C.r
+    (6, -1.0, vr.NegativeLossError),             # L: composed distortion below -1e-12
+])
+def test_train_step_raises_and_leaves_parameters_unchanged(field, value, exc):
+    """A non-finite packet / negative distortion in the middle of train_step raises the
+    reference exception from THAT step (segrender.py:124-141) and Adam does not run."""
+    pool, rays, targets = _poisoned_pool(field, value)
+    f = pool.fields[0]
+    before = [t.clone() for t in (f.table, f.weights)]
+    with pytest.raises(exc):
+        pool.train_step(rays, targets, 0.04, lr=1e-2, step=1)
+    for fl in pool.fields:
+        assert fl.adam is None or not any(t.any() for t in fl.adam)  # moments untouched
+    assert torch.equal(f.table, before[0]) and torch.equal(f.weights, before[1])
+    assert int(pool.err.item()) == 0  # cleared by the raise
+    # the next clean step trains normally
+    pool.exchange_packets = type(pool).exchange_packets.__get__(pool)
+    loss = pool.train_step(rays, targets, 0.04, lr=1e-2, step=1)
+    assert np.isfinite(loss.item()) and not torch.equal(f.table, before[0])
+
+
+
+
+def test_a_trainable_field_instance_serves_one_region_only():
+    pool, tree, models, rays, targets = _hash_setup(log2_T=12, K=2, n_rays=8)
+    with pytest.raises(ValueError):
+        vr.VolumePool(tree, [pool.fields[0], pool.fields[0]], (0, 0, 0), DEV)
+    scene = vr.Scene(tree.root_box, pool.fields[0], (0, 0, 0))
+    with pytest.raises(ValueError):
+        vr.spawn(tree, scene, DEV)
