@@ -129,6 +129,11 @@ int vr_abi_version(void);
  * sizeof(VrBlob). */
 int vr_struct_sizes(int64_t* out5);
 const char* vr_last_error(void);
+/* Checked builds (-DVR_CHECKED): device range checks at the hot global accesses (a
+ * sample's ray index, hash-table entries per level) that skip a bad access and count it;
+ * returns the failures since the last call and clears them (synchronises the device).
+ * Release builds return -1. */
+int vr_check_failures(void);
 int vr_device_sync(void);
 
 /* ---- K1: ray/region intersection + sampling ------------------------------------

@@ -21,6 +21,8 @@ from .errors import (
 )
 
 LIB_PATH = Path(__file__).resolve().parent / "libvolray_b200.so"
+# VR_CHECKED=1: the checked build (device range checks, csrc/build.py --checked)
+CHECKED_PATH = Path(__file__).resolve().parent / "libvolray_b200_checked.so"
 
 VR_MAX_REGIONS = 32
 VR_MAX_BLOBS = 32
@@ -109,6 +111,7 @@ SIGNATURES = {
     "vr_abi_version": [],
     "vr_struct_sizes": [P],
     "vr_last_error": [],
+    "vr_check_failures": [],
     "vr_device_sync": [],
     "vr_sample_count": [P, P, I64, I64, F64, I32, I32, P, P, P, P, P, P, P],
     "vr_scan_workspace_bytes": [I64],
@@ -163,7 +166,8 @@ def load(path: str | os.PathLike | None = None) -> C.CDLL:
     global _LIB
     if _LIB is not None:
         return _LIB
-    p = Path(path) if path else LIB_PATH
+    p = Path(path) if path else (CHECKED_PATH if os.environ.get("VR_CHECKED") == "1"
+                                 else LIB_PATH)
     if not p.exists():
         raise ImportError(
             f"volray B200 library not built: {p} is missing (run __graft_entry__.build() "

@@ -16,6 +16,9 @@ HERE = Path(__file__).resolve().parent
 PKG = HERE.parent
 ROOT = PKG.parent
 OUT = PKG / "libvolray_b200.so"
+# checked build (device range checks, VR_CHECK in common.cuh): a separate library that
+# _lib.load() picks when VR_CHECKED=1 is set in the environment
+OUT_CHECKED = PKG / "libvolray_b200_checked.so"
 BUILD = ROOT / "build" / "csrc"
 SOURCES = ["capi.cu", "sampler.cu", "fields.cu", "composite.cu", "hashgrid.cu", "mlp.cu", "mlp_tc.cu",
            "interlevel.cu"]
@@ -29,14 +32,15 @@ def nvcc() -> str:
     return cand if Path(cand).exists() else "nvcc"
 
 
-def _compile(src: str, verbose: bool) -> Path:
-    obj = BUILD / (Path(src).stem + ".o")
+def _compile(src: str, verbose: bool, checked: bool = False) -> Path:
+    obj = BUILD / (Path(src).stem + ("_checked.o" if checked else ".o"))
     cu = HERE / src
     deps = [cu, HERE / "common.cuh", ROOT / "include" / "vr_capi.h"]
     deps += list(HERE.glob("*.cuh"))
     if obj.exists() and all(obj.stat().st_mtime >= d.stat().st_mtime for d in deps):
         return obj
-    cmd = [nvcc(), *ARCH, *FLAGS, "-c", str(cu), "-o", str(obj)]
+    cmd = [nvcc(), *ARCH, *FLAGS, *(["-DVR_CHECKED"] if checked else []), "-c", str(cu), "-o",
+           str(obj)]
     if verbose:
         cmd.insert(1, "-Xptxas=-v")
     r = subprocess.run(cmd, capture_output=True, text=True)
@@ -47,18 +51,19 @@ def _compile(src: str, verbose: bool) -> Path:
     return obj
 
 
-def build(verbose: bool = False) -> Path:
+def build(verbose: bool = False, checked: bool = False) -> Path:
     BUILD.mkdir(parents=True, exist_ok=True)
+    out = OUT_CHECKED if checked else OUT
     with ThreadPoolExecutor(max_workers=len(SOURCES)) as ex:
-        objs = list(ex.map(lambda s: _compile(s, verbose), SOURCES))
-    if OUT.exists() and all(OUT.stat().st_mtime >= o.stat().st_mtime for o in objs):
-        return OUT
-    cmd = [nvcc(), *ARCH, "-shared", "-cudart", "static", "-o", str(OUT), *map(str, objs)]
+        objs = list(ex.map(lambda s: _compile(s, verbose, checked), SOURCES))
+    if out.exists() and all(out.stat().st_mtime >= o.stat().st_mtime for o in objs):
+        return out
+    cmd = [nvcc(), *ARCH, "-shared", "-cudart", "static", "-o", str(out), *map(str, objs)]
     r = subprocess.run(cmd, capture_output=True, text=True)
     if r.returncode != 0:
         raise RuntimeError(f"nvcc link failed:\n{r.stdout}\n{r.stderr}")
-    return OUT
+    return out
 
 
 if __name__ == "__main__":
-    print(build(verbose="-v" in sys.argv))
+    print(build(verbose="-v" in sys.argv, checked="--checked" in sys.argv))

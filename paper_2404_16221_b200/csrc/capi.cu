@@ -13,6 +13,28 @@ void set_error(const char* msg) {
   g_err[sizeof(g_err) - 1] = 0;
 }
 
+int num_sms() {
+  static int n = 0;  // B200: 148
+  if (n == 0) {
+    int dev = 0, v = 0;
+    if (cudaGetDevice(&dev) == cudaSuccess &&
+        cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, dev) == cudaSuccess && v > 0)
+      n = v;
+    else
+      n = 148;
+  }
+  return n;
+}
+
+#ifdef VR_CHECKED
+static int (*g_checkers[16])() = {};
+static int g_n_checkers = 0;
+int register_checker(int (*f)()) {
+  if (g_n_checkers < 16) g_checkers[g_n_checkers++] = f;
+  return g_n_checkers;
+}
+#endif
+
 int check_launch(const char* where) {
   const cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) {
@@ -37,6 +59,17 @@ extern "C" int vr_struct_sizes(int64_t* out) {
 }
 
 extern "C" const char* vr_last_error(void) { return vr::g_err; }
+
+extern "C" int vr_check_failures(void) {
+#ifdef VR_CHECKED
+  cudaDeviceSynchronize();
+  int total = 0;
+  for (int i = 0; i < vr::g_n_checkers; ++i) total += vr::g_checkers[i]();
+  return total;
+#else
+  return -1;  // release build: no checks compiled in
+#endif
+}
 
 extern "C" int vr_device_sync(void) {
   const cudaError_t e = cudaDeviceSynchronize();

@@ -9,13 +9,36 @@
 #include "../../include/vr_capi.h"
 
 #define VR_SLIVER 1e-12 /* quadrature.py:19 */
-#define VR_NUM_SMS 148
+// SM count of the current device (queried once per process in capi.cu; 148 on B200).
+// Persistent grids and grid caps are sized in multiples of it.
+#define VR_NUM_SMS (vr::num_sms())
 
 namespace vr {
 
 // Set by every entry point on a launch/argument failure; read by vr_last_error().
 void set_error(const char* msg);
 int check_launch(const char* where);
+int num_sms();
+
+// ---- checked build (-DVR_CHECKED, csrc/build.py --checked) -----------------------------
+// compute-sanitizer is not available on this pool, so a debug build of the library adds
+// device-side range checks at the hot global accesses (table entries, sample / segment /
+// record indices); a failed check skips the access and counts the failure, read back by
+// vr_check_failures().  Release builds compile the checks out.
+#ifdef VR_CHECKED
+static __device__ unsigned int g_check_failures;
+#define VR_CHECK(cond) ((cond) ? true : (atomicAdd(&vr::g_check_failures, 1u), false))
+int register_checker(int (*read_and_clear)());
+static int read_and_clear_checks() {
+  unsigned int v = 0, z = 0;
+  cudaMemcpyFromSymbol(&v, g_check_failures, sizeof(v));
+  cudaMemcpyToSymbol(g_check_failures, &z, sizeof(z));
+  return (int)v;
+}
+static const int g_checker_registered = register_checker(&read_and_clear_checks);
+#else
+#define VR_CHECK(cond) true
+#endif
 
 // ---- exact float64 arithmetic (no FMA contraction) ------------------------------
 // The reference computes in numpy float64 without fused multiply-add; these
@@ -88,6 +111,11 @@ __device__ __forceinline__ int locate_point(const VrTree& t, const double p[3], 
     node = c;
   }
   return 0;
+}
+
+// a sample's ray index (checked build: within [0, n_rays), else ray 0 and a failure)
+__device__ __forceinline__ int64_t checked_ray(int64_t r, int64_t n_rays) {
+  return VR_CHECK(r >= 0 && r < n_rays) ? r : 0;
 }
 
 __device__ __forceinline__ double sample_mid(double t0, double t1) {

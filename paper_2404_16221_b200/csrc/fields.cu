@@ -19,7 +19,7 @@ __device__ __forceinline__ void sample_point(const double* __restrict__ rays, in
                                              const double* __restrict__ t1,
                                              const int32_t* __restrict__ rid, int64_t i,
                                              double p[3]) {
-  const int64_t r = rid[i];
+  const int64_t r = checked_ray(rid[i], stride);
   const double m = sample_mid(t0[i], t1[i]);
 #pragma unroll
   for (int a = 0; a < 3; ++a)

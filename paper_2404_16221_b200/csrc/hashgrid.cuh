@@ -21,7 +21,7 @@ __device__ __forceinline__ void norm_pos(const VrHashGridDesc& g, const double* 
                                          int64_t stride, const double* __restrict__ t0,
                                          const double* __restrict__ t1,
                                          const int32_t* __restrict__ rid, int64_t i, float u[3]) {
-  const int64_t r = rid[i];
+  const int64_t r = checked_ray(rid[i], stride);
   const double m = sample_mid(t0[i], t1[i]);
   double o[3], d[3];
 #pragma unroll
@@ -95,6 +95,7 @@ __device__ __forceinline__ float2 gather_half(const VrHashGridDesc& g, int l,
     uint32_t idx;
     float w;
     corner(g, l, gi, fr, p + 2 * k, idx, w);
+    if (!VR_CHECK((int64_t)idx < g.offset[l + 1] - g.offset[l])) idx = 0;
     const float2 v = __ldg(tl + idx);
     a0 = __fadd_rn(a0, __fmul_rn(w, v.x));
     a1 = __fadd_rn(a1, __fmul_rn(w, v.y));
@@ -161,6 +162,7 @@ __device__ __forceinline__ void scatter_half(const VrHashGridDesc& g, const RepP
     uint32_t idx;
     float w;
     corner(g, l, gi, fr, p + 2 * k, idx, w);
+    if (!VR_CHECK((int64_t)idx < size_l)) continue;
     atomicAdd(gl + idx, make_float2(w * d.x, w * d.y));
   }
 }

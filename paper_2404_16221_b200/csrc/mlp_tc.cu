@@ -305,7 +305,7 @@ __device__ __forceinline__ void load_dir(const double* __restrict__ rays, int64_
                                          float& dx, float& dy, float& dz) {
   dx = dy = dz = 0.f;
   if (valid) {
-    const int64_t r = rid[i];
+    const int64_t r = checked_ray(rid[i], stride);
     dx = (float)__ldg(rays + 3 * stride + r);
     dy = (float)__ldg(rays + 4 * stride + r);
     dz = (float)__ldg(rays + 5 * stride + r);
@@ -426,7 +426,7 @@ __device__ __forceinline__ void encode_row(const VrHashGridDesc& g, const float2
   __half2* h = reinterpret_cast<__half2*>(q);
   dx = dy = dz = 0.f;
   if (valid) {
-    const int64_t ray = rid[i];
+    const int64_t ray = checked_ray(rid[i], stride);
     const double m = sample_mid(t0[i], t1[i]);
     double o[3], d[3];
 #pragma unroll
@@ -561,7 +561,7 @@ __device__ __forceinline__ void fetch_row(RowIn& x, const __half2* __restrict__ 
   x.dx = x.dy = x.dz = 0.f;
   x.u[0] = x.u[1] = x.u[2] = 0.f;
   if (valid) {
-    const int64_t ray = rid[i];
+    const int64_t ray = checked_ray(rid[i], stride);
     const bool own_pos = FUSED && pos == nullptr;
     double o[3], d[3];
 #pragma unroll
