@@ -209,6 +209,26 @@ int vr_voxel_fwd(const VrVoxelDesc* g, const double* densities_dev, const double
 int vr_voxel_bwd(const VrVoxelDesc* g, const double* rays_dev, int64_t ray_stride,
                  const double* t0_dev, const double* t1_dev, const int32_t* ray_id_dev, int64_t n,
                  const float* dsig_rgb_dev, double* grad_densities_dev, void* stream);
+/* The same lookup with float64 outputs sigma_dev[n], rgb_dev[n][3] (the finite-difference
+ * probe, DistributedLossProbe segrender.py:146-251, which needs float64 packets). */
+int vr_voxel_fwd_f64(const VrVoxelDesc* g, const double* densities_dev,
+                     const double* colors_dev, const double* rays_dev, int64_t ray_stride,
+                     const double* t0_dev, const double* t1_dev, const int32_t* ray_id_dev,
+                     int64_t n, double* sigma_dev, double* rgb_dev, void* stream);
+
+/* ---- float64 segment API (aggregate_segment / compose_render / compose_distortion,
+ * segrender.py:71-142) — for float64 callers (the reference's hand cases, the FD probe);
+ * the training path's float32 packets are K4 / K5 below.  Round-to-nearest, no FMA, the
+ * reference's operation order.  vr_segment_aggregate_f64: one segment per [seg_off[s],
+ * seg_off[s+1]) of the float64 bins (t0, t1, sigma, rgb[n][3]), out[s] = {T, C[3], A, D,
+ * L, order_t} (order_t = first bin's t0, +inf when empty).  vr_compose_f64: per ray its
+ * n_segs[r] packets seg[r][k] = {T, C[3], A, D, L} in (order_t, tile) order -> out[r] =
+ * {C[3], A, D, T, L}; VR_FLAG_NONFINITE / VR_FLAG_NEG_LOSS in err_dev (may be NULL). */
+int vr_segment_aggregate_f64(const double* t0_dev, const double* t1_dev, const double* sigma_dev,
+                             const double* rgb_dev, const int64_t* seg_off_dev, int64_t n_segs,
+                             double* out_dev, void* stream);
+int vr_compose_f64(const double* seg_dev, const int32_t* n_segs_dev, int32_t max_segs,
+                   int64_t n_rays, double* out_dev, int32_t* err_dev, void* stream);
 
 /* ---- K2: hash-grid encoding ---------------------------------------------------- */
 /* enc layout: [n_levels][n] half2 (level-major, coalesced on samples).  pos_dev (may be

@@ -64,6 +64,22 @@ from .partition import (
     tree_from_json,
     tree_to_json,
 )
+from .segments import (
+    DeviceFieldView,
+    DistributedLossProbe,
+    Field,
+    ParamRef,
+    SampleInterval,
+    SegmentAggregate,
+    aggregate_segment,
+    aggregate_segments,
+    compose_distortion,
+    compose_packets,
+    compose_render,
+    fill_samples,
+    identity_aggregate,
+    local_gradient_fd,
+)
 from .stats import CommStats, stats_json
 
 __version__ = "0.1.0"

@@ -124,6 +124,9 @@ SIGNATURES = {
     "vr_field_analytic_fwd": [P, P, I64, P, P, P, I64, P, P],
     "vr_voxel_fwd": [P, P, P, P, I64, P, P, P, I64, P, P],
     "vr_voxel_bwd": [P, P, I64, P, P, P, I64, P, P, P],
+    "vr_voxel_fwd_f64": [P, P, P, P, I64, P, P, P, I64, P, P, P],
+    "vr_segment_aggregate_f64": [P, P, P, P, P, I64, P, P],
+    "vr_compose_f64": [P, P, I32, I64, P, P, P],
     "vr_hash_fwd": [P, P, P, I64, P, P, P, I64, P, P, P],
     "vr_hash_bwd_workspace_bytes": [P],
     "vr_hash_bwd": [P, P, I64, P, P, P, I64, P, P, P, C.c_size_t, P],

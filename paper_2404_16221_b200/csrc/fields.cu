@@ -115,11 +115,15 @@ __device__ __forceinline__ bool voxel_stencil(const VrVoxelDesc& g, const double
   return in;
 }
 
+// F64: float64 outputs sig64[n], rgb64[n][3] (the finite-difference probe) instead of
+// the training path's float4 (sigma, rgb)
+template <bool F64>
 __global__ void k_voxel_fwd(const VrVoxelDesc g, const double* __restrict__ dens,
                             const double* __restrict__ cols, const double* __restrict__ rays,
                             int64_t stride, const double* __restrict__ t0,
                             const double* __restrict__ t1, const int32_t* __restrict__ rid,
-                            int64_t n, float4* __restrict__ out) {
+                            int64_t n, float4* __restrict__ out, double* __restrict__ sig64,
+                            double* __restrict__ rgb64) {
   const int ny = g.res[1], nz = g.res[2];
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
        i += (int64_t)gridDim.x * blockDim.x) {
@@ -128,7 +132,12 @@ __global__ void k_voxel_fwd(const VrVoxelDesc g, const double* __restrict__ dens
     VoxStencil st;
     int nidx[3];
     if (!voxel_stencil(g, p, st, nidx)) {
-      out[i] = make_float4(0.f, 0.f, 0.f, 0.f);
+      if (F64) {
+        sig64[i] = 0.0;
+        rgb64[3 * i] = rgb64[3 * i + 1] = rgb64[3 * i + 2] = 0.0;
+      } else {
+        out[i] = make_float4(0.f, 0.f, 0.f, 0.f);
+      }
       continue;
     }
     double sig = 0.0, rgb[3] = {0.0, 0.0, 0.0};
@@ -157,7 +166,13 @@ __global__ void k_voxel_fwd(const VrVoxelDesc g, const double* __restrict__ dens
     }
 #pragma unroll
     for (int k = 0; k < 3; ++k) rgb[k] = fmin(fmax(rgb[k], 0.0), 1.0);
-    out[i] = make_float4((float)sig, (float)rgb[0], (float)rgb[1], (float)rgb[2]);
+    if (F64) {
+      sig64[i] = sig;
+#pragma unroll
+      for (int k = 0; k < 3; ++k) rgb64[3 * i + k] = rgb[k];
+    } else {
+      out[i] = make_float4((float)sig, (float)rgb[0], (float)rgb[1], (float)rgb[2]);
+    }
   }
 }
 
@@ -221,9 +236,25 @@ extern "C" int vr_voxel_fwd(const VrVoxelDesc* g, const double* dens, const doub
     return VR_ERR_BAD_ARG;
   }
   if (n == 0) return VR_OK;
-  k_voxel_fwd<<<grid_for(n, 256), 256, 0, (cudaStream_t)stream>>>(
-      *g, dens, cols, rays, stride, t0, t1, rid, n, reinterpret_cast<float4*>(out));
+  k_voxel_fwd<false><<<grid_for(n, 256), 256, 0, (cudaStream_t)stream>>>(
+      *g, dens, cols, rays, stride, t0, t1, rid, n, reinterpret_cast<float4*>(out), nullptr,
+      nullptr);
   return check_launch("vr_voxel_fwd");
+}
+
+extern "C" int vr_voxel_fwd_f64(const VrVoxelDesc* g, const double* dens, const double* cols,
+                                const double* rays, int64_t stride, const double* t0,
+                                const double* t1, const int32_t* rid, int64_t n, double* sigma,
+                                double* rgb, void* stream) {
+  if (!g || g->res[0] < 1 || g->res[1] < 1 || g->res[2] < 1 || n < 0 ||
+      (n > 0 && (!sigma || !rgb))) {
+    set_error("vr_voxel_fwd_f64: bad argument");
+    return VR_ERR_BAD_ARG;
+  }
+  if (n == 0) return VR_OK;
+  k_voxel_fwd<true><<<grid_for(n, 256), 256, 0, (cudaStream_t)stream>>>(
+      *g, dens, cols, rays, stride, t0, t1, rid, n, nullptr, sigma, rgb);
+  return check_launch("vr_voxel_fwd_f64");
 }
 
 extern "C" int vr_voxel_bwd(const VrVoxelDesc* g, const double* rays, int64_t stride,

@@ -60,6 +60,22 @@ class CommStats:
     def messages_sent_total(self) -> int:
         return sum(w.messages_sent for w in self.workers.values()) + self.compositor.messages_sent
 
+    def merge(self, other: "CommStats") -> None:
+        """Accumulate another batch's counts (distsim.py:250-265): per-worker and compositor
+        scalars / messages, ray and sample totals, phase times, link bytes."""
+        self.rays += other.rays
+        self.participations += other.participations
+        self.samples_assigned += other.samples_assigned
+        for pid, ws in list(other.workers.items()) + [(COMPOSITOR, other.compositor)]:
+            mine = self._party(pid)
+            mine.scalars_sent += ws.scalars_sent
+            mine.scalars_received += ws.scalars_received
+            mine.messages_sent += ws.messages_sent
+            mine.messages_received += ws.messages_received
+        for phase, sec in other.phase_seconds.items():
+            self.add_time(phase, sec)
+        self.link_bytes += other.link_bytes
+
     def samples_per_ray_mean(self) -> float:
         return self.samples_assigned / self.rays if self.rays else 0.0
 

@@ -805,3 +805,46 @@ def test_a_trainable_field_instance_serves_one_region_only():
     scene = vr.Scene(tree.root_box, pool.fields[0], (0, 0, 0))
     with pytest.raises(ValueError):
         vr.spawn(tree, scene, DEV)
+
+
+@pytest.mark.parametrize("case_i", [0, 1, 2])
+def test_hash_kernels_match_hand_vectors(case_i):
+    """vr_hash_indices and vr_hash_fwd on the hand-worked points of tests/golden/hash_hand.json
+    (the published Instant-NGP hash, make_hash_hand.py): every corner index bit-exact; each
+    level's feature = sum of hand weight x table entry (fp16 output: within one fp16 ulp)."""
+    from paper_2404_16221_b200 import _lib
+    g = json.loads((GOLDEN / "hash_hand.json").read_text())
+    case = g["cases"][case_i]
+    pts = np.asarray(g["points"], dtype=np.float64)
+    n = len(pts)
+    cfg = vr.HashGridConfig(log2_T=case["log2_T"], max_res=case["max_res"])
+    rng = np.random.default_rng(case_i)
+    f = vr.HashGridMLP(cfg, vr.Aabb([0, 0, 0], [1, 1, 1]), DEV, seed=case_i, table_init=1.0)
+    table = f.table.cpu().numpy()
+    # rays from the points themselves (t0 = t1 = 0: the sample point is the origin)
+    rays = np.zeros((8, n))
+    rays[0:3] = pts.T
+    rays[3] = 1.0
+    rays[7] = 1.0
+    rd = torch.from_numpy(rays).to(DEV)
+    z = torch.zeros(n, dtype=torch.float64, device=DEV)
+    rid = torch.arange(n, dtype=torch.int32, device=DEV)
+    idx = torch.empty((16, n, 8), dtype=torch.int32, device=DEV)
+    s = _lib.stream_ptr()
+    _lib.call("vr_hash_indices", _lib.addr(f.desc), _lib.ptr(rd), n, _lib.ptr(z), _lib.ptr(z),
+              _lib.ptr(rid), n, _lib.ptr(idx), s)
+    enc = torch.empty((16, n), dtype=torch.float32, device=DEV)  # half2 per (level, sample)
+    pos = torch.empty((3, n), dtype=torch.float32, device=DEV)
+    _lib.call("vr_hash_fwd", _lib.addr(f.desc), _lib.ptr(f.table), _lib.ptr(rd), n, _lib.ptr(z),
+              _lib.ptr(z), _lib.ptr(rid), n, _lib.ptr(enc), _lib.ptr(pos), s)
+    torch.cuda.synchronize()
+    got = idx.cpu().numpy()
+    feats = enc.cpu().numpy().view(np.float16).reshape(16, n, 2).astype(np.float64)
+    offs = f.desc.offset
+    for l, hand in enumerate(case["levels"]):
+        want = np.asarray(hand["idx"], dtype=np.int64)
+        assert np.array_equal(got[l].astype(np.int64), want), f"level {l}"
+        w = np.asarray(hand["w"], dtype=np.float64)
+        ref = (w[:, :, None] * table[offs[l] + want]).sum(1)
+        ulp = np.maximum(np.spacing(np.abs(ref).astype(np.float16)).astype(np.float64), 2.0 ** -24)
+        assert (np.abs(feats[l] - ref) <= ulp * 1.01).all(), f"level {l}"

@@ -147,3 +147,28 @@ def test_build_tree_from_ray_points_matches_reference(name):
     assert vr.tree_to_json(tree) == g["tree"]
     box = vr.default_root_box(g["points"])
     assert np.all(box.mn <= g["points"].min(axis=0)) and np.all(box.mx >= g["points"].max(axis=0))
+
+
+def test_reference_value_type_methods():
+    """Ray.points_at / to_json / from_json, Aabb.contains_many (geometry.py:59-106) and
+    CommStats.merge (distsim.py:250-265): the reference surface on the host value types."""
+    import paper_2404_16221_b200 as vr
+
+    r = vr.Ray([0.0, 1.0, 2.0], [0.0, 0.6, 0.8], 0.5, 9.0)
+    pts = r.points_at([0.0, 1.0, 2.5])
+    np.testing.assert_array_equal(pts[2], [0.0, 1.0 + 2.5 * 0.6, 2.0 + 2.5 * 0.8])
+    r2 = vr.Ray.from_json(json.loads(json.dumps(r.to_json())))
+    assert np.array_equal(r2.origin, r.origin) and r2.t_far == r.t_far
+    box = vr.Aabb([0, 0, 0], [1, 1, 1])
+    assert box.contains_many(np.array([[0, 0, 0], [1, 1, 1], [1.0001, 0, 0]])).tolist() == \
+        [True, True, False]
+    a, b = vr.CommStats(), vr.CommStats()
+    a.rays, b.rays = 3, 4
+    a.record(0, -1, 9)
+    b.record(0, -1, 18, 2)
+    b.record(1, -1, 9)
+    b.add_time("compose", 0.5)
+    a.merge(b)
+    assert a.rays == 7 and a.workers[0].scalars_sent == 27 and a.workers[0].messages_sent == 3
+    assert a.workers[1].scalars_sent == 9 and a.compositor.scalars_received == 36
+    assert a.phase_seconds["compose"] == 0.5

@@ -130,3 +130,37 @@ def test_grid_edges_hand_cases():
     assert vo.grid_edges(1.0, 1.9, 0.25) == [(1.0, 1.25), (1.25, 1.5), (1.5, 1.75), (1.75, 1.9)]
     assert vo.split_bins([(1.0, 2.0)], [1.5]) == [(1.0, 1.5), (1.5, 2.0)]
     assert vo.split_bins([(1.0, 2.0)], [1.0 + 1e-14]) == [(1.0 + 1e-14, 2.0)]
+
+
+# ---- hash encoding: hand-worked vectors from the published algorithm ---------------------
+
+def test_hash_oracle_matches_hand_vectors():
+    """oracle/hashmlp_oracle.py against tests/golden/hash_hand.json (Instant-NGP's hash,
+    dense/hash switch and trilinear weights restated with Python ints and struct float32
+    rounding, tests/golden/make_hash_hand.py): indices bit-exact, weights bit-exact."""
+    from oracle import hashmlp_oracle as hmo
+
+    g = json.loads((GOLDEN / "hash_hand.json").read_text())
+    u = np.asarray(g["points"], dtype=np.float32)
+    for case in g["cases"]:
+        lv, _ = hmo.levels(case["log2_T"], max_res=case["max_res"])
+        assert len(lv) == len(case["levels"]) == 16
+        for (scale, res, dense, _), hand in zip(lv, case["levels"]):
+            assert float(scale) == hand["scale"] and res == hand["res"] and dense == hand["dense"]
+            idx, w = hmo.corners(u, scale, res, dense, case["log2_T"])
+            assert np.array_equal(idx.astype(np.int64), np.asarray(hand["idx"], dtype=np.int64))
+            assert np.array_equal(w, np.asarray(hand["w"], dtype=np.float32))
+
+
+def test_hash_config_levels_match_hand_vectors():
+    """The product's level derivation (HashGridConfig.level_params) gives the same scales,
+    resolutions and dense/hashed split as the hand vectors."""
+    import paper_2404_16221_b200 as vr
+
+    g = json.loads((GOLDEN / "hash_hand.json").read_text())
+    for case in g["cases"]:
+        scales, res, dense, _ = vr.HashGridConfig(log2_T=case["log2_T"],
+                                                  max_res=case["max_res"]).level_params()
+        for l, hand in enumerate(case["levels"]):
+            assert float(scales[l]) == hand["scale"]
+            assert res[l] == hand["res"] and dense[l] == hand["dense"]
