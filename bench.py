@@ -518,6 +518,8 @@ def run_workload(cfg_name, args, rank, world, local, dev, group, red_dev, headli
     totals = timer.totals()
     peaks = load_peaks()
     evidence = kernel_bounds(w.name)
+    ceilings = (json.loads(KERNEL_BOUNDS.read_text()).get("ceilings", {})
+                if KERNEL_BOUNDS.exists() else {})
     per_kernel = {k: {"ms_per_step": t / args.steps, "launches": n} for k, (t, n) in totals.items()}
 
     def roof(k):
@@ -540,8 +542,16 @@ def run_workload(cfg_name, args, rank, world, local, dev, group, red_dev, headli
                "ncu_bound": ev.get("bound"), "evidence": ev.get("source"),
                "ms_per_step": t_total / args.steps,
                "share_of_step": t_total / args.steps / ms_instrumented}
-        if ev.get("request_rate"):  # the L2 request roofline the capture names
-            out["request_roofline"] = ev["request_rate"]
+        reqs = ev.get("l2_read_requests_per_sample", 0.0) + ev.get("l2_red_requests_per_sample", 0.0)
+        if reqs > 1.0:  # gather / scatter kernels: the L2 request roofline they run against
+            ceil = ceilings.get("l2_red_requests_per_s" if ev.get("l2_red_requests_per_sample", 0)
+                                > ev.get("l2_read_requests_per_sample", 0)
+                                else "l2_gather_requests_per_s")
+            got = reqs * units / n_launch / avg_s
+            out["request_roofline"] = {"achieved": got / 1e9, "ceiling": ceil / 1e9,
+                                       "unit": "G L2 requests/s", "frac": got / ceil,
+                                       "requests_per_sample": reqs,
+                                       "ceiling_source": ceilings.get("source")}
         return out
 
     costed = [k for k in totals if k in KERNEL_COST and totals[k][0] > 0]
@@ -710,7 +720,7 @@ def main():
 
     res, w = run_workload(args.config, args, rank, world, local, dev, group, red_dev)
     subs = {}
-    for name in [c for c in args.sub.split(",") if c and c != args.config]:
+    for name in [c for c in args.sub.split(",") if c and c not in (args.config, "none")]:
         r, _ = run_workload(name, args, rank, world, local, dev, group, red_dev, headline=False)
         subs[name] = {k: r[k] for k in ("metric", "value", "unit", "ms_per_step",
                                         "ms_per_step_median", "step_ms_trend", "config", "e2e",

@@ -53,28 +53,41 @@ def _run(pool, rays, targets, dt):
             grads, b.seg_max)
 
 
-def _worker(rank, world, port, sparse, q):
+def _worker(rank, world, port, sparse, q, backend="gloo"):
     os.environ["MASTER_ADDR"] = "127.0.0.1"
     os.environ["MASTER_PORT"] = str(port)
-    dist.init_process_group("gloo", rank=rank, world_size=world)
+    dev = f"cuda:{rank}" if backend == "nccl" else "cuda:0"
+    if backend == "nccl":
+        torch.cuda.set_device(rank)
+        dist.init_process_group("nccl", rank=rank, world_size=world,
+                                device_id=torch.device(dev))
+    else:
+        dist.init_process_group("gloo", rank=rank, world_size=world)
     try:
         vr, doc, tree, scene, rays, targets = _setup()
-        pool = vr.spawn(tree, scene, "cuda:0", rank, world, dist.group.WORLD)
+        pool = vr.spawn(tree, scene, dev, rank, world, dist.group.WORLD)
         pool.sparse_exchange = sparse
         q.put((rank, _run(pool, rays, targets, doc["dt"])))
     finally:
         dist.destroy_process_group()
 
 
+@pytest.mark.parametrize("backend", ["gloo", "nccl"])
 @pytest.mark.parametrize("sparse", [True, False])
-def test_two_processes_match_single_process(sparse):
+def test_two_processes_match_single_process(sparse, backend):
+    """gloo: both ranks on cuda:0 (tensors staged through the host).  nccl: one GPU per rank,
+    the exchange is NCCL's all_gather_into_tensor / gather over the GPUs' link (skipped on a
+    single-GPU box)."""
+    if backend == "nccl" and torch.cuda.device_count() < 2:
+        pytest.skip("the NCCL path needs 2 GPUs")
     vr, doc, tree, scene, rays, targets = _setup()
     single = _run(vr.spawn(tree, scene, "cuda:0"), rays, targets, doc["dt"])
     world = 2
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
     port = _free_port()
-    procs = [ctx.Process(target=_worker, args=(r, world, port, sparse, q)) for r in range(world)]
+    procs = [ctx.Process(target=_worker, args=(r, world, port, sparse, q, backend))
+             for r in range(world)]
     for p in procs:
         p.start()
     results = dict(q.get(timeout=600) for _ in range(world))
