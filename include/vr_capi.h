@@ -77,6 +77,20 @@ typedef struct VrTree {
   int32_t n_nodes;
 } VrTree;
 
+/* Occupancy grid (the paper's per-region empty-space skipping,
+ * PAPER.md:296; the reference has none): one res^3 bitfield per leaf, over
+ * the leaf's own box.  bits[k * words + (c >> 5)] bit (c & 31), words = ceil(res^3 / 32),
+ * c = cx + res (cy + res cz), c_a = clamp(floor(((p_a - mn_a) / (mx_a - mn_a)) * res), 0,
+ * res - 1) in float64 without FMA (bit-exact in the oracle).  K1 keeps a sub-bin only
+ * when the bit of its midpoint in its owner's grid is set; kept samples are indexed
+ * consecutively along the ray (segments stay contiguous runs of kept samples).  bits ==
+ * NULL or res == 0: every sample is kept. */
+typedef struct VrOccupancy {
+  const uint32_t* bits;
+  int32_t res;
+  int32_t pad_;
+} VrOccupancy;
+
 /* Analytic test field: a SumField (field.py:212-240) of up to VR_MAX_CHILDREN
  * children, each GaussianBlobs (field.py:88-114) or ConstantBox (field.py:117-134).
  * A plain (non-sum) field is a one-child sum; both give identical results. */
@@ -147,8 +161,10 @@ int vr_device_sync(void);
 int vr_sample_count(const VrTree* tree, const double* rays_dev, int64_t ray_stride,
                     int64_t n_rays, double dt, int32_t region_lo, int32_t region_cnt,
                     int32_t* counts_dev, int32_t* seg_first_dev, double* ray_te_dev,
-                    uint32_t* ray_part_dev, int32_t* ray_total_dev, int32_t* err_dev,
-                    void* stream);
+                    uint32_t* ray_part_dev, int32_t* ray_total_dev, const VrOccupancy* occ,
+                    int32_t* err_dev, void* stream);
+/* occ (may be NULL) in every K1 entry point: the occupancy grid (VrOccupancy above) —
+ * with it, counts / indices / samples are those of the kept (occupied) sub-bins. */
 /* exclusive scan of n int32 counts into n+1 int64 offsets (offsets[n] = total) */
 size_t vr_scan_workspace_bytes(int64_t n);
 int vr_scan_offsets(const int32_t* counts_dev, int64_t n, int64_t* offsets_dev,
@@ -161,8 +177,8 @@ int vr_scan_offsets(const int32_t* counts_dev, int64_t n, int64_t* offsets_dev,
 int vr_sample_fill(const VrTree* tree, const double* rays_dev, int64_t ray_stride,
                    int64_t n_rays, double dt, int32_t region_lo, int32_t region_cnt,
                    const int64_t* offsets_dev, const int32_t* seg_first_dev, double* t0_dev,
-                   double* t1_dev, int32_t* ray_id_dev, int64_t capacity, int32_t* err_dev,
-                   void* stream);
+                   double* t1_dev, int32_t* ray_id_dev, int64_t capacity,
+                   const VrOccupancy* occ, int32_t* err_dev, void* stream);
 /* One walk instead of count + fill (the same generate_samples quadrature.py:66-88 /
  * split_at_planes :91-114 / locate_many partitioner.py:177-192 replacement as the pair
  * above, for _prepare_samples distsim.py:369-373 + the assignment :406-425):
@@ -184,8 +200,8 @@ int vr_sample_stage(const VrTree* tree, const double* rays_dev, int64_t ray_stri
                     int32_t* counts_dev, int32_t* seg_first_dev, double* ray_te_dev,
                     uint32_t* ray_part_dev, int32_t* ray_total_dev, double* st0_dev,
                     double* st1_dev, int64_t stage_capacity, int64_t* sslot_dev,
-                    uint64_t* stage_info_dev, int32_t* ray_list_dev, int32_t* err_dev,
-                    void* stream);
+                    uint64_t* stage_info_dev, int32_t* ray_list_dev, const VrOccupancy* occ,
+                    int32_t* err_dev, void* stream);
 int vr_sample_compact(int64_t n_rays, int32_t region_cnt, const int32_t* counts_dev,
                       const int32_t* seg_first_dev, const int64_t* offsets_dev,
                       const int64_t* sslot_dev, const double* st0_dev, const double* st1_dev,
@@ -215,6 +231,18 @@ int vr_voxel_fwd_f64(const VrVoxelDesc* g, const double* densities_dev,
                      const double* colors_dev, const double* rays_dev, int64_t ray_stride,
                      const double* t0_dev, const double* t1_dev, const int32_t* ray_id_dev,
                      int64_t n, double* sigma_dev, double* rgb_dev, void* stream);
+
+/* ---- occupancy grid maintenance (csrc/occupancy.cu; the grid itself: VrOccupancy) ----
+ * vr_occupancy_points: one jittered point per cell of the box's res^3 grid, written as
+ * zero-length rays (rays_dev [8][res^3] float64: origin = the point, dir = +x, t = [0, 1);
+ * evaluate with t0 = t1 = 0); jitter u_a = (lowbias32(seed * 0x9E3779B9 + 3 c + a) >> 8) *
+ * 2^-24, point = mn + ((cell + u) / res) (mx - mn).  vr_occupancy_update: per cell, density
+ * EMA d = max(decay d, sigma) from the field's output at those points (sig_rgb_dev [res^3]
+ * float4), bit = d > threshold into bits_dev (ceil(res^3 / 32) words of one leaf). */
+int vr_occupancy_points(const double* box_mn3, const double* box_mx3, int32_t res, uint32_t seed,
+                        double* rays_dev, void* stream);
+int vr_occupancy_update(const float* sig_rgb_dev, int32_t res, float decay, float threshold,
+                        float* density_dev, uint32_t* bits_dev, void* stream);
 
 /* ---- float64 segment API (aggregate_segment / compose_render / compose_distortion,
  * segrender.py:71-142) — for float64 callers (the reference's hand cases, the FD probe);

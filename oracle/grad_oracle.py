@@ -154,14 +154,14 @@ class RayRuns:
     global sample start, length); a segment's samples are [start, start+length) of the
     region-concatenated sample arrays t0 / t1 (regions in tile order)."""
 
-    def __init__(self, tree: vo.Tree, rays, dt):
+    def __init__(self, tree: vo.Tree, rays, dt, occ=None):
         rays = np.asarray(rays, dtype=np.float64)
         per = {k: ([], [], [], []) for k in range(tree.n_leaves)}  # pts, dirs, t0, t1
         raw = []  # (ray, order_t, tile, local start, length)
         fill = {k: 0 for k in range(tree.n_leaves)}
         for i, r in enumerate(rays):
             o, d = r[0:3], r[3:6]
-            t0, t1, tile = vo.sample_ray(tree, o, d, r[6], r[7], dt)
+            t0, t1, tile = vo.sample_ray(tree, o, d, r[6], r[7], dt, occ)
             for k in sorted(set(tile.tolist())):
                 sel = np.nonzero(tile == k)[0]
                 a, b = t0[sel], t1[sel]

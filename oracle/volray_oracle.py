@@ -21,6 +21,12 @@ Restated reference functions (file:line under /root/reference/pkg/src/volray):
   compose render/dist .. segrender.py:93-142      -> fold_packets
   tile protocol ray .... distsim.py:395-454       -> render_ray_tile
   loss ................. segrender.py:198-207     -> ray_loss
+
+Occupancy grid (SURVEY §8(f) 4 — the paper's empty-space skipping; the
+reference has none, so this part is the specification the CUDA path follows,
+parity unpinned): occupied / sample_ray(occ=...) drop the sub-bins whose midpoint falls
+in an empty cell of its owner's res^3 grid (include/vr_capi.h VrOccupancy);
+occupancy_points restates the grid update's jittered cell points.
 """
 from __future__ import annotations
 
@@ -146,8 +152,51 @@ def split_bins(bins, cuts):
     return out
 
 
-def sample_ray(tree: Tree, o, d, tn, tf, dt):
-    """All sub-bins of one ray in t order: arrays t0, t1, tile (distsim.py:369-373, :406-414)."""
+def occupancy_cell(tree: Tree, tile: int, p, res: int):
+    """Cell (cx, cy, cz) of p in leaf ``tile``'s res^3 grid: floor(((p - mn) / (mx - mn)) *
+    res) clamped to [0, res - 1], float64 (the kernel's op order, no FMA)."""
+    mn, mx = tree.leaf_mn[tile], tree.leaf_mx[tile]
+    u = (np.asarray(p, dtype=np.float64) - mn) / (mx - mn)
+    return np.clip(np.floor(u * float(res)), 0.0, float(res - 1)).astype(np.int64)
+
+
+def occupied(tree: Tree, occ, tile: int, p) -> bool:
+    """occ = (bits [n_leaves][words] uint32, res): the bit of p's cell in its owner's grid."""
+    bits, res = occ
+    c = occupancy_cell(tree, tile, p, res)
+    idx = int(c[0] + res * (c[1] + res * c[2]))
+    return bool((int(bits[tile][idx >> 5]) >> (idx & 31)) & 1)
+
+
+def _lowbias32(x):
+    x = np.asarray(x, dtype=np.uint64) & np.uint64(0xFFFFFFFF)
+    x ^= x >> np.uint64(16)
+    x = (x * np.uint64(0x7FEB352D)) & np.uint64(0xFFFFFFFF)
+    x ^= x >> np.uint64(15)
+    x = (x * np.uint64(0x846CA68B)) & np.uint64(0xFFFFFFFF)
+    x ^= x >> np.uint64(16)
+    return x
+
+
+def occupancy_points(mn, mx, res: int, seed: int) -> np.ndarray:
+    """(res^3, 3) jittered cell points of the grid update (csrc/occupancy.cu): cell c =
+    cx + res (cy + res cz), u_a = (lowbias32(seed * 0x9E3779B9 + 3 c + a) >> 8) * 2^-24,
+    point = mn + ((cell + u) / res) * (mx - mn)."""
+    n = res ** 3
+    c = np.arange(n, dtype=np.uint64)
+    cells = np.stack([c % res, (c // res) % res, c // (res * res)], axis=1).astype(np.float64)
+    out = np.empty((n, 3))
+    base = (np.uint64(seed) * np.uint64(0x9E3779B9)) & np.uint64(0xFFFFFFFF)
+    for a in range(3):
+        h = _lowbias32((base + c * np.uint64(3) + np.uint64(a)) & np.uint64(0xFFFFFFFF))
+        u = (h >> np.uint64(8)).astype(np.float64) * (1.0 / 16777216.0)
+        out[:, a] = mn[a] + ((cells[:, a] + u) / float(res)) * (mx[a] - mn[a])
+    return out
+
+
+def sample_ray(tree: Tree, o, d, tn, tf, dt, occ=None):
+    """All sub-bins of one ray in t order: arrays t0, t1, tile (distsim.py:369-373, :406-414);
+    with ``occ`` (occupancy grid) only the sub-bins whose midpoint cell is occupied."""
     if dt <= 0.0:
         raise ValueError("dt must be > 0")
     o = np.asarray(o, dtype=np.float64)
@@ -165,6 +214,9 @@ def sample_ray(tree: Tree, o, d, tn, tf, dt):
     mid = 0.5 * (t0 + t1)
     pts = o + mid[:, None] * d
     tile = np.array([tree.owner(p) for p in pts], dtype=np.int64)
+    if occ is not None:
+        keep = np.array([occupied(tree, occ, k, p) for k, p in zip(tile, pts)], dtype=bool)
+        return t0[keep], t1[keep], tile[keep]
     return t0, t1, tile
 
 

@@ -68,6 +68,10 @@ class VrBlob(C.Structure):
     _fields_ = [("center", D3), ("amplitude", C.c_double), ("scale", C.c_double), ("color", D3)]
 
 
+class VrOccupancy(C.Structure):
+    _fields_ = [("bits", C.c_void_p), ("res", C.c_int32), ("pad_", C.c_int32)]
+
+
 class VrAnalyticField(C.Structure):
     _fields_ = [
         ("n_children", C.c_int32),
@@ -113,18 +117,21 @@ SIGNATURES = {
     "vr_last_error": [],
     "vr_check_failures": [],
     "vr_device_sync": [],
-    "vr_sample_count": [P, P, I64, I64, F64, I32, I32, P, P, P, P, P, P, P],
+    "vr_sample_count": [P, P, I64, I64, F64, I32, I32, P, P, P, P, P, P, P, P],
     "vr_scan_workspace_bytes": [I64],
     "vr_scan_offsets": [P, I64, P, P, C.c_size_t, P],
-    "vr_sample_fill": [P, P, I64, I64, F64, I32, I32, P, P, P, P, P, I64, P, P],
+    "vr_sample_fill": [P, P, I64, I64, F64, I32, I32, P, P, P, P, P, I64, P, P, P],
     "vr_sample_stage_blocks": [I64],
-    "vr_sample_stage": [P, P, I64, I64, F64, I32, I32, P, P, P, P, P, P, P, I64, P, P, P, P, P],
+    "vr_sample_stage": [P, P, I64, I64, F64, I32, I32, P, P, P, P, P, P, P, I64, P, P, P, P, P,
+                        P],
     "vr_sample_compact": [I64, I32, P, P, P, P, P, P, P, P, P, I64, P, P],
     "vr_locate": [P, P, I64, P, P, P],
     "vr_field_analytic_fwd": [P, P, I64, P, P, P, I64, P, P],
     "vr_voxel_fwd": [P, P, P, P, I64, P, P, P, I64, P, P],
     "vr_voxel_bwd": [P, P, I64, P, P, P, I64, P, P, P],
     "vr_voxel_fwd_f64": [P, P, P, P, I64, P, P, P, I64, P, P, P],
+    "vr_occupancy_points": [P, P, I32, C.c_uint32, P, P],
+    "vr_occupancy_update": [P, I32, F32, F32, P, P, P],
     "vr_segment_aggregate_f64": [P, P, P, P, P, I64, P, P],
     "vr_compose_f64": [P, P, I32, I64, P, P, P],
     "vr_hash_fwd": [P, P, P, I64, P, P, P, I64, P, P, P],

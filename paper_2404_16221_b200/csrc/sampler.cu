@@ -106,9 +106,26 @@ __global__ void __launch_bounds__(256)
 // STAGE (count pass only): also write the own pieces to st0/st1 — block b owns slots
 // [b * slice, (b + 1) * slice); sslot[r] + (index along the ray) is a piece's slot.
 // stage_info[0] += slots reserved, stage_info[1] = max over blocks (the slice needed).
+// the occupancy bit of a point in leaf g's grid (VrOccupancy in vr_capi.h)
+__device__ __forceinline__ bool occupied(const VrOccupancy& occ, const VrTree& t, int g,
+                                         const double p[3]) {
+  const int G = occ.res;
+  int c[3];
+#pragma unroll
+  for (int a = 0; a < 3; ++a) {
+    const double u = ddiv(dsub(p[a], t.leaf_mn[g][a]), dsub(t.leaf_mx[g][a], t.leaf_mn[g][a]));
+    const double x = fmin(fmax(floor(dmul(u, (double)G)), 0.0), (double)(G - 1));
+    c[a] = (int)x;
+  }
+  const int64_t words = ((int64_t)G * G * G + 31) / 32;
+  const int64_t idx = c[0] + (int64_t)G * (c[1] + (int64_t)G * c[2]);
+  return (__ldg(occ.bits + (int64_t)g * words + (idx >> 5)) >> (idx & 31)) & 1u;
+}
+
 template <bool FILL, bool RESTRICT, bool STAGE>
 __global__ void __launch_bounds__(K1_WARPS * 32, K1_MIN_BLOCKS)
-    k_sample(const VrTree tree_param, const double* __restrict__ rays, int64_t stride,
+    k_sample(const VrTree tree_param, const VrOccupancy occ, const double* __restrict__ rays,
+             int64_t stride,
              int64_t n_rays, double dt, int region_lo, int region_cnt, int32_t* counts,
              int32_t* seg_first, double* ray_te, uint32_t* ray_part, int32_t* ray_total,
              const int64_t* __restrict__ offsets, double* t0o, double* t1o, int32_t* rido,
@@ -141,6 +158,9 @@ __global__ void __launch_bounds__(K1_WARPS * 32, K1_MIN_BLOCKS)
   const int lane = threadIdx.x & 31;
   const int warp = threadIdx.x >> 5;
   const int n_leaves = tree.n_leaves;
+  // occupancy: a sample's index along the ray counts kept samples only, so the bins
+  // before the own regions must be walked (their occupancy decides the indices)
+  const bool use_occ = occ.bits != nullptr && occ.res > 0;
   double* cand = sm.cand[warp];
   double* cut = sm.cut[warp];
   int flags = 0;
@@ -259,7 +279,7 @@ __global__ void __launch_bounds__(K1_WARPS * 32, K1_MIN_BLOCKS)
         // bins that can hold own samples (conservative); earlier bins are only counted
         int64_t k_begin = 0, k_end = nb;
         if (restrict_own) {
-          k_begin = max((int64_t)0, (int64_t)floor(ddiv(dsub(ta, te), dt)) - 1);
+          if (!use_occ) k_begin = max((int64_t)0, (int64_t)floor(ddiv(dsub(ta, te), dt)) - 1);
           k_end = min(nb, (int64_t)floor(ddiv(dsub(tb, te), dt)) + 2);
         }
         // pieces before bin k_begin: every bin is longer than a sliver, so it holds one
@@ -302,8 +322,24 @@ __global__ void __launch_bounds__(K1_WARPS * 32, K1_MIN_BLOCKS)
           double t0, t1;
           int i0, i1;
           const int ne = bin_pieces(k, k_end, t0, t1, i0, i1);
-          const int incl = warp_incl_sum_i(ne, lane);
-          int gidx = carry + incl - ne;
+          int nk = ne;  // kept pieces
+          if (use_occ && ne > 0) {
+            nk = 0;
+            double a = t0;
+            for (int s = i0; s <= i1; ++s) {
+              const double b = (s < i1) ? cut[s] : t1;
+              if (dsub(b, a) > VR_SLIVER) {
+                double p[3];
+                point_at(ray, sample_mid(a, b), p);
+                bool oob;
+                const int g = locate_point(tree, p, oob);
+                nk += occupied(occ, tree, g, p) ? 1 : 0;
+              }
+              a = b;
+            }
+          }
+          const int incl = warp_incl_sum_i(nk, lane);
+          int gidx = carry + incl - nk;
           carry += __shfl_sync(0xffffffffu, incl, 31);
           if (ne > 0) {
             double a = t0;
@@ -316,6 +352,10 @@ __global__ void __launch_bounds__(K1_WARPS * 32, K1_MIN_BLOCKS)
                 bool oob;
                 const int g = locate_point(tree, p, oob);
                 if (oob) flags |= VR_FLAG_OOB;
+                if (use_occ && !occupied(occ, tree, g, p)) {  // empty space: skipped
+                  a = b;
+                  continue;
+                }
                 const int kk = g - region_lo;
                 if (kk >= 0 && kk < region_cnt) {
                   if (!FILL) {
@@ -464,6 +504,18 @@ __global__ void k_scan_tail(const int32_t* counts, int64_t n, int64_t* offsets) 
   }
 }
 
+static bool valid_occ(const VrOccupancy* o) {
+  return !o || o->res == 0 || (o->res > 0 && o->res <= 1024 && o->bits);
+}
+
+static VrOccupancy occ_or_none(const VrOccupancy* o) {
+  VrOccupancy v;
+  v.bits = (o && o->res > 0) ? o->bits : nullptr;
+  v.res = (o && o->bits) ? o->res : 0;
+  v.pad_ = 0;
+  return v;
+}
+
 static bool valid_tree(const VrTree* t) {
   return t && t->n_leaves >= 1 && t->n_leaves <= VR_MAX_REGIONS && t->n_nodes >= 0 &&
          t->n_nodes < VR_MAX_REGIONS && (t->n_nodes == 0 ? t->n_leaves == 1 : true);
@@ -476,25 +528,26 @@ using namespace vr;
 extern "C" int vr_sample_count(const VrTree* tree, const double* rays, int64_t stride,
                                int64_t n_rays, double dt, int32_t region_lo, int32_t region_cnt,
                                int32_t* counts, int32_t* seg_first, double* ray_te,
-                               uint32_t* ray_part, int32_t* ray_total, int32_t* err,
-                               void* stream) {
+                               uint32_t* ray_part, int32_t* ray_total,
+                               const VrOccupancy* occ, int32_t* err, void* stream) {
   if (!valid_tree(tree) || !(dt > 0.0) || region_lo < 0 || region_cnt < 1 ||
-      region_lo + region_cnt > tree->n_leaves || n_rays < 0 || !err) {
+      region_lo + region_cnt > tree->n_leaves || n_rays < 0 || !err || !valid_occ(occ)) {
     set_error("vr_sample_count: bad argument");
     return VR_ERR_BAD_ARG;
   }
+  const VrOccupancy oc = occ_or_none(occ);
   if (n_rays == 0) return VR_OK;
   const int grid = grid_for(ceil_div(n_rays, K1_WARPS), 1, 16);
   const bool restrict_own = !ray_part && !ray_total &&
                             !(region_lo == 0 && region_cnt == tree->n_leaves);
   if (restrict_own)
     k_sample<false, true, false><<<grid, K1_WARPS * 32, 0, (cudaStream_t)stream>>>(
-        *tree, rays, stride, n_rays, dt, region_lo, region_cnt, counts, seg_first, ray_te,
+        *tree, oc, rays, stride, n_rays, dt, region_lo, region_cnt, counts, seg_first, ray_te,
         ray_part, ray_total, nullptr, nullptr, nullptr, nullptr, 0, err, nullptr, nullptr,
         nullptr, 0, nullptr, nullptr);
   else
     k_sample<false, false, false><<<grid, K1_WARPS * 32, 0, (cudaStream_t)stream>>>(
-        *tree, rays, stride, n_rays, dt, region_lo, region_cnt, counts, seg_first, ray_te,
+        *tree, oc, rays, stride, n_rays, dt, region_lo, region_cnt, counts, seg_first, ray_te,
         ray_part, ray_total, nullptr, nullptr, nullptr, nullptr, 0, err, nullptr, nullptr,
         nullptr, 0, nullptr, nullptr);
   return check_launch("vr_sample_count");
@@ -509,13 +562,15 @@ extern "C" int vr_sample_stage(const VrTree* tree, const double* rays, int64_t s
                                int32_t* counts, int32_t* seg_first, double* ray_te,
                                uint32_t* ray_part, int32_t* ray_total, double* st0, double* st1,
                                int64_t stage_capacity, int64_t* sslot, uint64_t* stage_info,
-                               int32_t* ray_list, int32_t* err, void* stream) {
+                               int32_t* ray_list, const VrOccupancy* occ, int32_t* err,
+                               void* stream) {
   if (!valid_tree(tree) || !(dt > 0.0) || region_lo < 0 || region_cnt < 1 ||
       region_lo + region_cnt > tree->n_leaves || n_rays < 0 || !err || !stage_info ||
-      stage_capacity < 0 || (n_rays > 0 && (!st0 || !st1 || !sslot))) {
+      stage_capacity < 0 || (n_rays > 0 && (!st0 || !st1 || !sslot)) || !valid_occ(occ)) {
     set_error("vr_sample_stage: bad argument");
     return VR_ERR_BAD_ARG;
   }
+  const VrOccupancy oc = occ_or_none(occ);
   if (n_rays == 0) return VR_OK;
   const int grid = (int)vr_sample_stage_blocks(n_rays);
   const int64_t slice = stage_capacity / grid;
@@ -532,12 +587,12 @@ extern "C" int vr_sample_stage(const VrTree* tree, const double* rays, int64_t s
   }
   if (restrict_own)
     k_sample<false, true, true><<<grid, K1_WARPS * 32, 0, s>>>(
-        *tree, rays, stride, n_rays, dt, region_lo, region_cnt, counts, seg_first, ray_te,
+        *tree, oc, rays, stride, n_rays, dt, region_lo, region_cnt, counts, seg_first, ray_te,
         ray_part, ray_total, nullptr, nullptr, nullptr, nullptr, 0, err, st0, st1, sslot, slice,
         info, list);
   else
     k_sample<false, false, true><<<grid, K1_WARPS * 32, 0, s>>>(
-        *tree, rays, stride, n_rays, dt, region_lo, region_cnt, counts, seg_first, ray_te,
+        *tree, oc, rays, stride, n_rays, dt, region_lo, region_cnt, counts, seg_first, ray_te,
         ray_part, ray_total, nullptr, nullptr, nullptr, nullptr, 0, err, st0, st1, sslot, slice,
         info, nullptr);
   return check_launch("vr_sample_stage");
@@ -562,25 +617,26 @@ extern "C" int vr_sample_compact(int64_t n_rays, int32_t region_cnt, const int32
 extern "C" int vr_sample_fill(const VrTree* tree, const double* rays, int64_t stride,
                               int64_t n_rays, double dt, int32_t region_lo, int32_t region_cnt,
                               const int64_t* offsets, const int32_t* seg_first, double* t0,
-                              double* t1, int32_t* ray_id, int64_t capacity, int32_t* err,
-                              void* stream) {
+                              double* t1, int32_t* ray_id, int64_t capacity,
+                              const VrOccupancy* occ, int32_t* err, void* stream) {
   if (!valid_tree(tree) || !(dt > 0.0) || region_lo < 0 || region_cnt < 1 ||
-      region_lo + region_cnt > tree->n_leaves || n_rays < 0 || !err) {
+      region_lo + region_cnt > tree->n_leaves || n_rays < 0 || !err || !valid_occ(occ)) {
     set_error("vr_sample_fill: bad argument");
     return VR_ERR_BAD_ARG;
   }
+  const VrOccupancy oc = occ_or_none(occ);
   if (n_rays == 0) return VR_OK;
   const int grid = grid_for(ceil_div(n_rays, K1_WARPS), 1, 16);
   // the fill walks the same bins as the count (restricted unless all regions are owned;
   // the counts of a restricted count pass are exactly the full walk's)
   if (!(region_lo == 0 && region_cnt == tree->n_leaves))
     k_sample<true, true, false><<<grid, K1_WARPS * 32, 0, (cudaStream_t)stream>>>(
-        *tree, rays, stride, n_rays, dt, region_lo, region_cnt, nullptr,
+        *tree, oc, rays, stride, n_rays, dt, region_lo, region_cnt, nullptr,
         const_cast<int32_t*>(seg_first), nullptr, nullptr, nullptr, offsets, t0, t1, ray_id,
         capacity, err, nullptr, nullptr, nullptr, 0, nullptr, nullptr);
   else
     k_sample<true, false, false><<<grid, K1_WARPS * 32, 0, (cudaStream_t)stream>>>(
-        *tree, rays, stride, n_rays, dt, region_lo, region_cnt, nullptr,
+        *tree, oc, rays, stride, n_rays, dt, region_lo, region_cnt, nullptr,
         const_cast<int32_t*>(seg_first), nullptr, nullptr, nullptr, offsets, t0, t1, ray_id,
         capacity, err, nullptr, nullptr, nullptr, 0, nullptr, nullptr);
   return check_launch("vr_sample_fill");

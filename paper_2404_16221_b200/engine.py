@@ -128,6 +128,12 @@ class VolumePool:
         # packets of non-empty segments only cross the link (dense slab if "0")
         self.sparse_exchange = os.environ.get("VR_SPARSE_EXCHANGE", "1") != "0"
         self._bg = (ctypes.c_float * 3)()
+        # occupancy grid: bits of EVERY region (K1 indexes samples along
+        # the whole ray, so each rank needs all regions' bits), density EMA of the own ones
+        self.occ_bits = None
+        self.occ_res = 0
+        self._occ_density = None
+        self._occ_desc = _lib.VrOccupancy()
         _lib.load()
 
     @property
@@ -182,6 +188,76 @@ class VolumePool:
             self._ws = torch.empty(need, dtype=torch.uint8, device=self.device)
         return self._ws
 
+    # ---- occupancy grid ------------------------------------------------------------------
+    def _occ_arg(self):
+        return _lib.addr(self._occ_desc) if self.occ_res else None
+
+    @staticmethod
+    def occupancy_words(res: int) -> int:
+        return (res ** 3 + 31) // 32
+
+    def set_occupancy(self, bits, res: int) -> None:
+        """Install an occupancy grid: bits [n_regions][occupancy_words(res)] (int32 / uint32
+        words, VrOccupancy layout in vr_capi.h) for every region, or None to sample
+        everything.  Samples in empty cells are skipped by K1 from the next sample()."""
+        if bits is None:
+            self.occ_bits, self.occ_res = None, 0
+            self._occ_desc.bits, self._occ_desc.res = None, 0
+            return
+        t = torch.as_tensor(bits)
+        if t.dtype not in (torch.int32, torch.uint32):
+            t = torch.as_tensor(np.ascontiguousarray(np.asarray(bits, dtype=np.uint32)).view(
+                np.int32))
+        t = t.view(torch.int32).to(self.device).contiguous()
+        if tuple(t.shape) != (self.n_regions, self.occupancy_words(res)):
+            raise ValueError(f"occupancy bits must be [{self.n_regions}][{self.occupancy_words(res)}]")
+        self.occ_bits, self.occ_res = t, int(res)
+        self._occ_desc.bits = t.data_ptr()
+        self._occ_desc.res = int(res)
+
+    @staticmethod
+    def pack_occupancy(mask) -> np.ndarray:
+        """bool [n_regions][res][res][res] (indexed [cz][cy][cx]) -> uint32 words."""
+        m = np.asarray(mask, dtype=bool)
+        k, res = m.shape[0], m.shape[1]
+        flat = m.reshape(k, -1)
+        pad = (-flat.shape[1]) % 32
+        flat = np.concatenate([flat, np.zeros((k, pad), dtype=bool)], axis=1)
+        return np.packbits(flat, axis=1, bitorder="little").view("<u4").reshape(k, -1)
+
+    def update_occupancy(self, res: int = 128, threshold: float = 0.01, decay: float = 0.95,
+                         seed: int = 0, fields=None) -> float:
+        """One Instant-NGP-style grid update: every owned region's field at one jittered
+        point per cell (vr_occupancy_points), density EMA and threshold
+        (vr_occupancy_update); the ranks' bits are all-gathered.  Returns the occupied
+        fraction of the owned cells."""
+        fields = self.fields if fields is None else fields
+        res = int(res)
+        words = self.occupancy_words(res)
+        n = res ** 3
+        if self._occ_density is None or self._occ_density.shape != (self.region_cnt, n):
+            self._occ_density = torch.zeros((self.region_cnt, n), dtype=torch.float32,
+                                            device=self.device)
+        own = torch.empty((self.region_cnt, words), dtype=torch.int32, device=self.device)
+        s = self._stream()
+        rays = torch.empty((8, n), dtype=torch.float64, device=self.device)
+        z = torch.zeros(n, dtype=torch.float64, device=self.device)
+        rid = torch.arange(n, dtype=torch.int32, device=self.device)
+        sig = torch.empty((n, 4), dtype=torch.float32, device=self.device)
+        for kk, f in enumerate(fields):
+            leaf = self.tree.leaves[self.region_lo + kk].box
+            mn = (ctypes.c_double * 3)(*leaf.mn)
+            mx = (ctypes.c_double * 3)(*leaf.mx)
+            _lib.call("vr_occupancy_points", _lib.addr(mn), _lib.addr(mx), res,
+                      (int(seed) * 1000003 + self.region_lo + kk) & 0xFFFFFFFF, _lib.ptr(rays), s)
+            f.forward(rays, z, z, rid, n, sig, s)
+            _lib.call("vr_occupancy_update", _lib.ptr(sig), res, float(decay), float(threshold),
+                      _lib.ptr(self._occ_density[kk]), _lib.ptr(own[kk]), s)
+        allb = comm.all_gather_packets(own, self.group, self.world)
+        self.set_occupancy(allb, res)
+        frac = (self._occ_density > threshold).float().mean()
+        return float(frac.item())
+
     # ---- K1 ----------------------------------------------------------------------------
     def sample(self, rays: torch.Tensor, dt: float, all_regions: bool = False,
                stats: bool = False, exchange: bool = False) -> SampleBatch:
@@ -217,11 +293,12 @@ class VolumePool:
                       region_lo, cnt, _lib.ptr(counts), _lib.ptr(seg_first), _lib.ptr(ray_te),
                       _lib.ptr(ray_part), _lib.ptr(ray_total), _lib.ptr(st0), _lib.ptr(st1),
                       st0.numel(), _lib.ptr(sslot), _lib.ptr(info), _lib.ptr(ray_list),
-                      _lib.ptr(self.err), s)
+                      self._occ_arg(), _lib.ptr(self.err), s)
         else:
             _lib.call("vr_sample_count", tc, _lib.ptr(rays), rays.shape[1], R, float(dt),
                       region_lo, cnt, _lib.ptr(counts), _lib.ptr(seg_first), _lib.ptr(ray_te),
-                      _lib.ptr(ray_part), _lib.ptr(ray_total), _lib.ptr(self.err), s)
+                      _lib.ptr(ray_part), _lib.ptr(ray_total), self._occ_arg(), _lib.ptr(self.err),
+                      s)
         offsets = torch.empty(cnt * R + 1, dtype=torch.int64, device=dev)
         ws = self._workspace(cnt * R)
         _lib.call("vr_scan_offsets", _lib.ptr(counts), cnt * R, _lib.ptr(offsets), _lib.ptr(ws),
@@ -253,7 +330,7 @@ class VolumePool:
         elif N:
             _lib.call("vr_sample_fill", tc, _lib.ptr(rays), rays.shape[1], R, float(dt),
                       region_lo, cnt, _lib.ptr(offsets), _lib.ptr(seg_first), _lib.ptr(t0),
-                      _lib.ptr(t1), _lib.ptr(ray_id), N, _lib.ptr(self.err), s)
+                      _lib.ptr(t1), _lib.ptr(ray_id), N, self._occ_arg(), _lib.ptr(self.err), s)
         return SampleBatch(R, region_lo, cnt, counts, seg_first, offsets, ray_te, ray_part,
                            ray_total, t0, t1, ray_id, [int(b) for b in bounds], seg_max)
 
@@ -302,7 +379,7 @@ class VolumePool:
             ray_te = torch.empty(R, dtype=torch.float64, device=dev)
             _lib.call("vr_sample_count", tc, _lib.ptr(rays), R, R, float(dt), lo, cnt,
                       _lib.ptr(counts), _lib.ptr(seg_first), _lib.ptr(ray_te), None, None,
-                      _lib.ptr(err), s)
+                      self._occ_arg(), _lib.ptr(err), s)
             offsets = torch.empty(cnt * R + 1, dtype=torch.int64, device=dev)
             ws = torch.empty(int(_lib.load().vr_scan_workspace_bytes(cnt * R)), dtype=torch.uint8,
                              device=dev)
@@ -317,7 +394,7 @@ class VolumePool:
             ray_id = torch.empty(cap, dtype=torch.int32, device=dev)
             _lib.call("vr_sample_fill", tc, _lib.ptr(rays), R, R, float(dt), lo, cnt,
                       _lib.ptr(offsets), _lib.ptr(seg_first), _lib.ptr(t0), _lib.ptr(t1),
-                      _lib.ptr(ray_id), cap, _lib.ptr(err), s)
+                      _lib.ptr(ray_id), cap, self._occ_arg(), _lib.ptr(err), s)
             done = torch.cuda.Event()
             done.record(k1)
         return dict(rays=rays, dt=dt, R=R, counts=counts, seg_first=seg_first, ray_te=ray_te,
@@ -346,7 +423,7 @@ class VolumePool:
             _lib.call("vr_sample_fill", _lib.addr(self.tree_c), _lib.ptr(p["rays"]), R, R,
                       float(p["dt"]), self.region_lo, cnt, _lib.ptr(p["offsets"]),
                       _lib.ptr(p["seg_first"]), _lib.ptr(t0), _lib.ptr(t1), _lib.ptr(ray_id), N,
-                      _lib.ptr(self.err), self._stream())
+                      self._occ_arg(), _lib.ptr(self.err), self._stream())
         _lib.raise_flags(flags, "in sampling")
         return SampleBatch(R, self.region_lo, cnt, p["counts"], p["seg_first"], p["offsets"],
                            p["ray_te"], None, None, t0, t1, ray_id, bounds)

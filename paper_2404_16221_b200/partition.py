@@ -233,7 +233,7 @@ def _k1_all_leaves(tree: PartitionTree, rays, dt: float, device=None):
     first = torch.empty(K * R, dtype=torch.int32, device=dev)
     te = torch.empty(R, dtype=torch.float64, device=dev)
     _lib.call("vr_sample_count", _lib.addr(tc), _lib.ptr(r), R, R, float(dt), 0, K,
-              _lib.ptr(counts), _lib.ptr(first), _lib.ptr(te), None, None, _lib.ptr(err), s)
+              _lib.ptr(counts), _lib.ptr(first), _lib.ptr(te), None, None, None, _lib.ptr(err), s)
     off = torch.empty(K * R + 1, dtype=torch.int64, device=dev)
     ws = torch.empty(int(_lib.load().vr_scan_workspace_bytes(K * R)), dtype=torch.uint8, device=dev)
     _lib.call("vr_scan_offsets", _lib.ptr(counts), K * R, _lib.ptr(off), _lib.ptr(ws), ws.numel(),
@@ -246,7 +246,7 @@ def _k1_all_leaves(tree: PartitionTree, rays, dt: float, device=None):
     if n:
         _lib.call("vr_sample_fill", _lib.addr(tc), _lib.ptr(r), R, R, float(dt), 0, K,
                   _lib.ptr(off), _lib.ptr(first), _lib.ptr(t0), _lib.ptr(t1), _lib.ptr(rid),
-                  n, _lib.ptr(err), s)
+                  n, None, _lib.ptr(err), s)
     # an out-of-root midpoint (rounding at a grazing exit) only matters to owner lookup
     flags = int(err.item()) & ~_lib.VR_FLAG_OOB
     _lib.raise_flags(flags, "in sampling")

@@ -46,7 +46,7 @@ def test_bad_arguments_are_rejected_without_a_gpu():
     t = _lib.VrTree()
     t.n_leaves = 0  # invalid
     rc = lib.vr_sample_count(ctypes.addressof(t), None, 0, 1, 0.1, 0, 1, None, None, None, None,
-                             None, None, None)
+                             None, None, None, None)
     assert rc == 1
     assert b"bad argument" in lib.vr_last_error()
     with pytest.raises(ValueError):
