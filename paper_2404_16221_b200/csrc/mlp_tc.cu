@@ -487,6 +487,31 @@ __global__ void __launch_bounds__(TILE * FWD_TPR, 4)
   const int r = G::row();
   uint32_t phase = 0;
   const int64_t n_tiles = ceil_div(n, TILE);
+  // !FUSED: the next tile's encodings and ray direction are loaded one tile ahead (raw,
+  // converted at use) and its ray index two tiles ahead, so no tile waits on a global
+  // load chain (rid -> rays) before its first MMA
+  uint32_t qn[16];
+  double dn[3] = {0.0, 0.0, 0.0};
+  int32_t rid_ahead = 0;
+  auto load_rid = [&](int64_t tile) -> int32_t {
+    const int64_t i = tile * TILE + r;
+    return (!DENS && tile < n_tiles && i < n) ? __ldg(rid + i) : 0;
+  };
+  auto prefetch = [&](int64_t tile, int32_t ray) {
+    const int64_t i = tile * TILE + r;
+    const bool ok = tile < n_tiles && i < n;
+#pragma unroll
+    for (int l = 0; l < 16; ++l) qn[l] = ok ? h2bits(enc[(int64_t)l * n + i]) : 0u;
+    if (!DENS && ok) {
+      const int64_t rr = checked_ray(ray, stride);
+#pragma unroll
+      for (int a = 0; a < 3; ++a) dn[a] = __ldg(rays + (3 + a) * stride + rr);
+    }
+  };
+  if (!FUSED && (int64_t)blockIdx.x < n_tiles) {
+    prefetch(blockIdx.x, load_rid(blockIdx.x));
+    rid_ahead = load_rid(blockIdx.x + (int64_t)gridDim.x);
+  }
   for (int64_t tile = blockIdx.x; tile < n_tiles; tile += gridDim.x) {
     const int64_t i = tile * TILE + r;
     const bool valid = i < n;
@@ -496,9 +521,14 @@ __global__ void __launch_bounds__(TILE * FWD_TPR, 4)
       encode_row(g, table, rays, stride, t0, t1, rid, n, i, valid, q, enc_out, dx, dy, dz);
     } else {
 #pragma unroll
-      for (int l = 0; l < 16; ++l)
-        q[l] = valid ? h2bits(enc[(int64_t)l * n + i]) : 0u;
-      if (!DENS) load_dir(rays, stride, rid, i, valid, dx, dy, dz);
+      for (int l = 0; l < 16; ++l) q[l] = qn[l];
+      if (!DENS && valid) {
+        dx = (float)dn[0];
+        dy = (float)dn[1];
+        dz = (float)dn[2];
+      }
+      prefetch(tile + gridDim.x, rid_ahead);
+      rid_ahead = load_rid(tile + 2 * (int64_t)gridDim.x);
     }
     tmem_st8(tm_row + TF_A2, q);  // enc -> A2 (the previous tile's last MMA is complete)
     tmem_st8(tm_row + TF_A2 + 8, q + 8);
@@ -529,21 +559,24 @@ constexpr uint32_t T_W1D = 0, T_W2DT = 32, T_W1C = 64, T_W2C = 96, T_W3CT = 160,
                    T_D1 = T_D0, T_COLS = 256;
 static_assert(B_GL == B_GH + TILE * 64 * 2, "stacked wgrad operand needs Gl right after Gh");
 
-// Inputs of one row for one tile, prefetched into registers one tile ahead.
+// Inputs of one row for one tile, prefetched into registers one tile ahead.  The loads are
+// only ISSUED here; every use of a loaded value (the direction's float conversion, the
+// gradient scale, the position) happens when the tile is processed, so the thread does not
+// wait on them inside the prefetch (measured: the conversions right after the loads were
+// the top long-scoreboard stalls of the c4 backward).  The sample's ray index, which the
+// direction loads depend on, is loaded one tile earlier still (rid_ahead).
 struct RowIn {
   __half2 enc[16 / BWD_TPR];
-  float dx, dy, dz;
-  float u[3];  // normalised hash-grid position (FUSED backward only)
-  float4 gin;
+  double d[3];   // ray direction (raw float64)
+  float u[3];    // normalised hash-grid position (FUSED backward only)
+  float4 gin;    // upstream gradient, unscaled
 };
 
 template <bool FUSED>
 __device__ __forceinline__ void fetch_row(RowIn& x, const __half2* __restrict__ enc,
                                           const double* __restrict__ rays, int64_t stride,
-                                          const int32_t* __restrict__ rid,
-                                          const float4* __restrict__ dsr, float gscale,
-                                          int64_t n, int64_t i, int part,
-                                          const VrHashGridDesc& g,
+                                          int32_t ray, const float4* __restrict__ dsr, int64_t n,
+                                          int64_t i, int part, const VrHashGridDesc& g,
                                           const double* __restrict__ t0,
                                           const double* __restrict__ t1,
                                           const float* __restrict__ pos) {
@@ -552,28 +585,18 @@ __device__ __forceinline__ void fetch_row(RowIn& x, const __half2* __restrict__ 
 #pragma unroll
   for (int l = 0; l < LV; ++l)
     x.enc[l] = valid ? enc[(int64_t)(part * LV + l) * n + i] : __floats2half2_rn(0.f, 0.f);
-  if (valid && part == 0) {
-    const float4 g4 = dsr[i];
-    x.gin = make_float4(g4.x * gscale, g4.y * gscale, g4.z * gscale, g4.w * gscale);
-  } else {
-    x.gin = make_float4(0.f, 0.f, 0.f, 0.f);
-  }
-  x.dx = x.dy = x.dz = 0.f;
+  x.gin = (valid && part == 0) ? dsr[i] : make_float4(0.f, 0.f, 0.f, 0.f);
+  x.d[0] = x.d[1] = x.d[2] = 0.0;
   x.u[0] = x.u[1] = x.u[2] = 0.f;
   if (valid) {
-    const int64_t ray = checked_ray(rid[i], stride);
-    const bool own_pos = FUSED && pos == nullptr;
-    double o[3], d[3];
+    const int64_t r = checked_ray(ray, stride);
 #pragma unroll
-    for (int a = 0; a < 3; ++a) {
-      d[a] = __ldg(rays + (3 + a) * stride + ray);
-      if (own_pos) o[a] = __ldg(rays + a * stride + ray);
-    }
-    x.dx = (float)d[0];
-    x.dy = (float)d[1];
-    x.dz = (float)d[2];
-    if (own_pos) {
-      norm_pos_od(g, o, d, sample_mid(t0[i], t1[i]), x.u);
+    for (int a = 0; a < 3; ++a) x.d[a] = __ldg(rays + (3 + a) * stride + r);
+    if (FUSED && pos == nullptr) {  // positions recomputed from the ray (no forward store)
+      double o[3];
+#pragma unroll
+      for (int a = 0; a < 3; ++a) o[a] = __ldg(rays + a * stride + r);
+      norm_pos_od(g, o, x.d, sample_mid(t0[i], t1[i]), x.u);
     } else if (FUSED) {  // positions written by the hash-grid forward
       x.u[0] = __ldcs(pos + i);
       x.u[1] = __ldcs(pos + n + i);
@@ -741,16 +764,27 @@ __global__ void __launch_bounds__(TILE * BWD_TPR, 2)
   auto scatter_ov = [&](int round) { scatter_one(round); };
 
   RowIn nxt;
-  if ((int64_t)blockIdx.x < n_tiles)
-    fetch_row<FUSED>(nxt, enc, rays, stride, rid, dsr, gscale, n, (int64_t)blockIdx.x * TILE + r,
-                     part, hg, t0, t1, pos);
+  // the ray index of this row in the tile after next (the direction loads of the next
+  // tile's prefetch depend on it)
+  auto load_rid = [&](int64_t tile) -> int32_t {
+    const int64_t i = tile * TILE + r;
+    return (tile < n_tiles && i < n) ? __ldg(rid + i) : 0;
+  };
+  int32_t rid_ahead = 0;
+  if ((int64_t)blockIdx.x < n_tiles) {
+    fetch_row<FUSED>(nxt, enc, rays, stride, load_rid(blockIdx.x), dsr, n,
+                     (int64_t)blockIdx.x * TILE + r, part, hg, t0, t1, pos);
+    rid_ahead = load_rid(blockIdx.x + (int64_t)gridDim.x);
+  }
   for (int64_t tile = blockIdx.x; tile < n_tiles; tile += gridDim.x) {
     const int64_t i = tile * TILE + r;
     const bool valid = i < n;
     const RowIn cur = nxt;
-    if (tile + gridDim.x < n_tiles)  // prefetch the next tile's inputs
-      fetch_row<FUSED>(nxt, enc, rays, stride, rid, dsr, gscale, n, (tile + gridDim.x) * TILE + r,
+    if (tile + gridDim.x < n_tiles) {  // prefetch the next tile's inputs (loads only)
+      fetch_row<FUSED>(nxt, enc, rays, stride, rid_ahead, dsr, n, (tile + gridDim.x) * TILE + r,
                        part, hg, t0, t1, pos);
+      rid_ahead = load_rid(tile + 2 * (int64_t)gridDim.x);
+    }
     if (wgrad_pending) {  // the previous tile's last wgrad reads X4/Gh/Gl
       mbar_wait(barB, phB);
       phB ^= 1u;
@@ -759,8 +793,10 @@ __global__ void __launch_bounds__(TILE * BWD_TPR, 2)
     put_enc(A, r, part, cur);
     // forward recompute: A(enc) -> X1(h1d) -> A(cin) -> X3(h1c) -> X4(h2c)
     const FwdRow f = forward_tile<BWD_TPR, DENS>(sw, A, X1, A, X3, X4, tm_row, tmem, T_D0, T_D1,
-                                                 barA, phA, cur.dx, cur.dy, cur.dz, scatter_ov);
-    const float4 gin = cur.gin;
+                                                 barA, phA, (float)cur.d[0], (float)cur.d[1],
+                                                 (float)cur.d[2], scatter_ov);
+    const float4 gin = make_float4(cur.gin.x * gscale, cur.gin.y * gscale, cur.gin.z * gscale,
+                                   cur.gin.w * gscale);
     float g[C64];
     float v[16];
     const bool a_w = acc;
