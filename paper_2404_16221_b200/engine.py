@@ -470,9 +470,12 @@ class VolumePool:
     # side-stream scatter grid: 0 = the kernel's full grid (measured best: 148 or 296 co-
     # resident 128-thread blocks left the scatter far below the L2 atomic rate)
     SCATTER_BLOCKS = int(os.environ.get("VR_SCATTER_BLOCKS", "0"))
-    # the MLP backward's grid while the previous region's scatter runs on the side stream:
-    # 1.25 CTAs per SM (c4: 148 -> 407, 185 -> 388, 222 -> 394, 296 -> 413 ms per step)
-    MLP_CTAS_BESIDE_SCATTER = int(os.environ.get("VR_MLP_BWD_CTAS", str(148 * 5 // 4)))
+    # the MLP backward's grid while the previous region's scatter runs on the side stream
+    # (0: the full persistent grid, 2 CTAs per SM).  Once the MLP backward's prefetch stopped
+    # stalling on its loads it became the longer of the two backward chains, and the full
+    # grid won (c4 ms per step, scripts/sweep_ctas.sh: 185 CTAs 327.3, 222 312.7, 259 310.8,
+    # 296 308.0; before that change 1.25 CTAs per SM was best: 185 388, 296 413)
+    MLP_CTAS_BESIDE_SCATTER = int(os.environ.get("VR_MLP_BWD_CTAS", "0"))
 
     def field_backward(self, rays, b: SampleBatch, dsig_rgb: torch.Tensor, fields=None,
                        sig_rgb: torch.Tensor | None = None) -> None:
