@@ -422,6 +422,7 @@ def run_workload(cfg_name, args, rank, world, local, dev, group, red_dev, headli
     restore()
     clocks = ClockSampler(local) if headline else None
     _lib.CALLS.clear()
+    _lib.LAUNCHED.clear()
     if clocks:
         clocks.start()
         time.sleep(0.3)
@@ -443,6 +444,7 @@ def run_workload(cfg_name, args, rank, world, local, dev, group, red_dev, headli
         dist.barrier()
     clk = clocks.stop() if clocks else None
     calls = dict(_lib.CALLS)
+    launched = dict(_lib.LAUNCHED)
 
     # ---- second pass, same steps, CUDA events around every C-ABI launch: per-kernel
     # durations for the rooflines (kept out of the headline number: the per-launch event
@@ -465,10 +467,9 @@ def run_workload(cfg_name, args, rank, world, local, dev, group, red_dev, headli
         dist.all_reduce(t_ms, op=dist.ReduceOp.MAX)
     ms = float(t_ms.item())
     value = R / (ms / 1e3)
-    per_call = dict(_lib.LAUNCHES)
+    launches = sum(launched.values())
     if world > 1:  # k_sample_prefilter + the walk
-        per_call["vr_sample_stage"] = 2
-    launches = sum(n * per_call.get(k, 1) for k, n in calls.items())
+        launches += calls.get("vr_sample_stage", 0)
     final_loss = float(loss.item()) if train else None
 
     # samples per step (for per-sample kernel costs), batch 0

@@ -282,6 +282,9 @@ int vr_hash_bwd(const VrHashGridDesc* g, const double* rays_dev, int64_t ray_str
 int vr_hash_positions(const VrHashGridDesc* g, const double* rays_dev, int64_t ray_stride,
                       const double* t0_dev, const double* t1_dev, const int32_t* ray_id_dev,
                       int64_t n, float* pos_dev, void* stream);
+/* number of level passes of the level-major kernels for g (one launch walks them in order
+ * through a work counter) */
+int vr_hash_lm_passes(const VrHashGridDesc* g);
 int vr_hash_fwd_lm(const VrHashGridDesc* g, const float* table_dev, const float* pos_dev,
                    int64_t n, void* enc_dev, void* stream);
 int vr_hash_bwd_lm(const VrHashGridDesc* g, const float* pos_dev, int64_t n,

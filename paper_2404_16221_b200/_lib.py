@@ -139,6 +139,7 @@ SIGNATURES = {
     "vr_hash_bwd": [P, P, I64, P, P, P, I64, P, P, P, C.c_size_t, P],
     "vr_hash_indices": [P, P, I64, P, P, P, I64, P, P],
     "vr_hash_positions": [P, P, I64, P, P, P, I64, P, P],
+    "vr_hash_lm_passes": [P],
     "vr_hash_fwd_lm": [P, P, P, I64, P, P],
     "vr_hash_bwd_lm": [P, P, I64, P, P, P, C.c_size_t, P],
     "vr_hash_scatter": [P, P, I64, P, P, P, C.c_size_t, I32, I32, P],
@@ -209,12 +210,19 @@ LAUNCHES = {"vr_scan_offsets": 3, "vr_sum_f64": 2, "vr_field_bwd_tc": 2, "vr_has
             "vr_hash_scatter": 2, "vr_hash_bwd_lm": 2, "vr_packets_pack": 2,
             "vr_packets_unpack": 2}
 CALLS = {}
+# kernels launched by the calls above
+LAUNCHED = {}
+
+
+def _launches(lib, name: str, args) -> int:
+    return LAUNCHES.get(name, 1)
 
 
 def call(name: str, *args) -> None:
     """Invoke an entry point and raise on a non-zero status."""
     lib = load()
     CALLS[name] = CALLS.get(name, 0) + 1
+    LAUNCHED[name] = LAUNCHED.get(name, 0) + _launches(lib, name, args)
     if TIMER is not None:
         TIMER.before(name, args)
     rc = getattr(lib, name)(*args)

@@ -19,6 +19,8 @@
 #include <stdlib.h>
 #include <string.h>
 
+#include <atomic>
+
 #include "hashgrid.cuh"
 
 namespace vr {
@@ -87,8 +89,12 @@ __global__ void __launch_bounds__(HASH_THREADS)
 // ---- level-major variants (tables larger than L2) ---------------------------------------
 // With T = 2^22 a region's table is ~0.5 GB: per-sample loops over all 16 levels turn every
 // corner access into a DRAM sector read-modify-write.  Level-major kernels walk the
-// samples once per level (grid.y = level, so the block scheduler finishes level l before
-// level l+1 starts): only one level's slice (<= 32 MB) is live, it stays in L2, and the
+// samples once per level pass: a persistent grid claims (pass, chunk) work items from a
+// counter in increasing order, so every block has claimed its last item of pass p before
+// any block starts pass p + 1 (ordered by construction — not by the block scheduler's
+// dispatch order — and without the drain between passes that one launch per pass costs:
+// c4 325.0 vs 311.7 ms measured for per-pass launches vs one launch): only one level's
+// slice (<= 32 MB) is live, it stays in L2, and the
 // DRAM traffic becomes the streaming of u / enc / d(enc) (16 B per sample and level).
 // The normalised positions are computed once (k_hash_pos) and reused by the backward;
 // the streamed pos / enc / d(enc) use evict-first accesses so they do not push the live
@@ -115,16 +121,31 @@ struct LmPasses {
   int32_t first[VR_MAX_LEVELS + 1];
 };
 
+constexpr int64_t LM_CHUNK = 4096;  // samples per work item
+
+// the block's next work item (block-uniform); item = pass * chunks + chunk
+__device__ __forceinline__ int64_t lm_claim(unsigned long long* ctr) {
+  __shared__ long long item;
+  __syncthreads();  // the previous item is consumed by every thread
+  if (threadIdx.x == 0) item = (long long)atomicAdd(ctr, 1ull);
+  __syncthreads();
+  return item;
+}
+
 __global__ void __launch_bounds__(HASH_THREADS, 6)  // 40 regs: c5 57.0 -> 55.2 ms
     k_hash_fwd_lm(const VrHashGridDesc g, const LmPasses passes, const float2* __restrict__ table,
-                  const float* __restrict__ pos, int64_t n, __half2* __restrict__ enc) {
-  const int l0 = passes.first[blockIdx.y], l1 = passes.first[blockIdx.y + 1];
+                  const float* __restrict__ pos, int64_t n, __half2* __restrict__ enc,
+                  unsigned long long* ctr) {
   const int lane = threadIdx.x & 31, p = lane & 1;  // lane pairs as in k_hash_fwd
-  const int64_t warp0 = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
-  const int64_t n_warps = ((int64_t)gridDim.x * blockDim.x) >> 5;
-  for (int64_t s0 = warp0 * 16; s0 < n; s0 += n_warps * 16) {
+  const int warp = threadIdx.x >> 5, n_warps = blockDim.x >> 5;
+  const int64_t chunks = ceil_div(n, LM_CHUNK);
+  for (int64_t item = lm_claim(ctr); item < passes.n * chunks; item = lm_claim(ctr)) {
+  const int pass = (int)(item / chunks);
+  const int l0 = passes.first[pass], l1 = passes.first[pass + 1];
+  const int64_t c0 = (item - pass * chunks) * LM_CHUNK, c1 = min(n, c0 + LM_CHUNK);
+  for (int64_t s0 = c0 + warp * 16; s0 < c1; s0 += n_warps * 16) {
     const int64_t i = s0 + (lane >> 1);
-    const bool valid = i < n;
+    const bool valid = i < c1;
     float u[3] = {0.f, 0.f, 0.f};
     if (valid) {
       u[0] = __ldcs(pos + i);
@@ -141,24 +162,29 @@ __global__ void __launch_bounds__(HASH_THREADS, 6)  // 40 regs: c5 57.0 -> 55.2 
                __floats2half2_rn(__fadd_rn(h.x, o.x), __fadd_rn(h.y, o.y)));
     }
   }
+  }
 }
 
 __global__ void __launch_bounds__(HASH_THREADS)
     k_hash_bwd_lm(const VrHashGridDesc g, const RepPlan plan, const LmPasses passes,
                   const float* __restrict__ pos, int64_t n, const float2* __restrict__ denc,
-                  float2* __restrict__ grad, float2* __restrict__ ws) {
-  const int l0 = passes.first[blockIdx.y], l1 = passes.first[blockIdx.y + 1];
+                  float2* __restrict__ grad, float2* __restrict__ ws, unsigned long long* ctr) {
   const int gwarp = blockIdx.x * (blockDim.x / 32) + (threadIdx.x >> 5);
   const int lane = threadIdx.x & 31, p = lane & 1;  // lane pairs (scatter_half)
-  const int64_t warp0 = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
-  const int64_t n_warps = ((int64_t)gridDim.x * blockDim.x) >> 5;
-  for (int64_t s0 = warp0 * 16; s0 < n; s0 += n_warps * 16) {
-    const int64_t i = s0 + (lane >> 1);
-    if (i >= n) continue;  // no shuffles below: lanes may leave independently
-    const float u[3] = {__ldcs(pos + i), __ldcs(pos + n + i), __ldcs(pos + 2 * n + i)};
-    for (int l = l0; l < l1; ++l) {
-      const float2 d = __ldcs(denc + (int64_t)l * n + i);
-      if (d.x != 0.f || d.y != 0.f) scatter_half(g, plan, l, u, d, p, gwarp, grad, ws);
+  const int warp = threadIdx.x >> 5, n_warps = blockDim.x >> 5;
+  const int64_t chunks = ceil_div(n, LM_CHUNK);
+  for (int64_t item = lm_claim(ctr); item < passes.n * chunks; item = lm_claim(ctr)) {
+    const int pass = (int)(item / chunks);
+    const int l0 = passes.first[pass], l1 = passes.first[pass + 1];
+    const int64_t c0 = (item - pass * chunks) * LM_CHUNK, c1 = min(n, c0 + LM_CHUNK);
+    for (int64_t s0 = c0 + warp * 16; s0 < c1; s0 += n_warps * 16) {
+      const int64_t i = s0 + (lane >> 1);
+      if (i >= c1) continue;  // no shuffles below: lanes may leave independently
+      const float u[3] = {__ldcs(pos + i), __ldcs(pos + n + i), __ldcs(pos + 2 * n + i)};
+      for (int l = l0; l < l1; ++l) {
+        const float2 d = __ldcs(denc + (int64_t)l * n + i);
+        if (d.x != 0.f || d.y != 0.f) scatter_half(g, plan, l, u, d, p, gwarp, grad, ws);
+      }
     }
   }
 }
@@ -334,9 +360,37 @@ extern "C" int vr_hash_positions(const VrHashGridDesc* g, const double* rays, in
   return check_launch("vr_hash_positions");
 }
 
-static dim3 lm_grid(const VrHashGridDesc* g, int64_t n) {
-  const int64_t blocks = ceil_div(2 * n, HASH_THREADS);  // lane pairs (forward) fit too
-  return dim3((unsigned)(blocks < VR_NUM_SMS * 8 ? blocks : VR_NUM_SMS * 8), (unsigned)g->n_levels);
+// persistent grid of the ordered level-major kernels: the SMs' resident blocks
+template <class K>
+static int lm_blocks(K kernel, int threads, int64_t items) {
+  int per_sm = 0;
+  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kernel, threads, 0) != cudaSuccess ||
+      per_sm < 1)
+    per_sm = 4;
+  const int64_t b = (int64_t)VR_NUM_SMS * per_sm;
+  return (int)(items < b ? (items > 0 ? items : 1) : b);
+}
+
+// a work counter zeroed on the stream: slot k of a ring allocated once per device (calls
+// in flight at the same time — on different streams — take different slots)
+static unsigned long long* lm_counter(cudaStream_t s) {
+  constexpr int SLOTS = 4096;
+  static unsigned long long* ring[64] = {};
+  static std::atomic<unsigned> next{0};
+  int dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= 64) return nullptr;
+  if (!ring[dev]) {
+    void* p = nullptr;
+    if (cudaMalloc(&p, SLOTS * sizeof(unsigned long long)) != cudaSuccess) return nullptr;
+    ring[dev] = reinterpret_cast<unsigned long long*>(p);
+  }
+  unsigned long long* c = ring[dev] + (next.fetch_add(1) % SLOTS);
+  cudaMemsetAsync(c, 0, sizeof(unsigned long long), s);
+  return c;
+}
+
+extern "C" int vr_hash_lm_passes(const VrHashGridDesc* g) {
+  return valid_grid(g) ? lm_passes(g).n : 0;
 }
 
 extern "C" int vr_hash_fwd_lm(const VrHashGridDesc* g, const float* table, const float* pos,
@@ -347,10 +401,15 @@ extern "C" int vr_hash_fwd_lm(const VrHashGridDesc* g, const float* table, const
   }
   if (n == 0) return VR_OK;
   const LmPasses passes = lm_passes(g);
-  dim3 grid = lm_grid(g, n);
-  grid.y = passes.n;
-  k_hash_fwd_lm<<<grid, HASH_THREADS, 0, (cudaStream_t)stream>>>(
-      *g, passes, reinterpret_cast<const float2*>(table), pos, n, reinterpret_cast<__half2*>(enc));
+  cudaStream_t s = (cudaStream_t)stream;
+  unsigned long long* ctr = lm_counter(s);
+  if (!ctr) {
+    set_error("vr_hash_fwd_lm: work counter allocation failed");
+    return VR_ERR_CUDA;
+  }
+  const int blocks = lm_blocks(k_hash_fwd_lm, HASH_THREADS, passes.n * ceil_div(n, LM_CHUNK));
+  k_hash_fwd_lm<<<blocks, HASH_THREADS, 0, s>>>(*g, passes, reinterpret_cast<const float2*>(table),
+                                               pos, n, reinterpret_cast<__half2*>(enc), ctr);
   return check_launch("vr_hash_fwd_lm");
 }
 
@@ -373,17 +432,22 @@ extern "C" int vr_hash_scatter(const VrHashGridDesc* g, const float* pos, int64_
     passes.n = 1;
     passes.first[1] = g->n_levels;
   }
-  dim3 grid = lm_grid(g, n);
-  grid.y = passes.n;
-  grid.x = (unsigned)grid_for(2 * n, HASH_THREADS, 8);  // lane pairs
+  cudaStream_t s = (cudaStream_t)stream;
   int threads = HASH_THREADS;
-  if (max_blocks > 0) {  // co-resident with another kernel: few small blocks per level pass
+  int blocks = lm_blocks(k_hash_bwd_lm, HASH_THREADS, passes.n * ceil_div(n, LM_CHUNK));
+  if (max_blocks > 0) {  // co-resident with another kernel: a few small blocks
     threads = 128;
-    grid.x = (unsigned)max_blocks;
+    blocks = max_blocks;
   }
-  k_hash_bwd_lm<<<grid, threads, 0, (cudaStream_t)stream>>>(
-      *g, plan, passes, pos, n, reinterpret_cast<const float2*>(denc),
-      reinterpret_cast<float2*>(grad), reinterpret_cast<float2*>(ws));
+  unsigned long long* ctr = lm_counter(s);
+  if (!ctr) {
+    set_error("vr_hash_scatter: work counter allocation failed");
+    return VR_ERR_CUDA;
+  }
+  k_hash_bwd_lm<<<blocks, threads, 0, s>>>(*g, plan, passes, pos, n,
+                                           reinterpret_cast<const float2*>(denc),
+                                           reinterpret_cast<float2*>(grad),
+                                           reinterpret_cast<float2*>(ws), ctr);
   const int rc = check_launch("vr_hash_scatter");
   if (rc != VR_OK) return rc;
   return hash_rep_reduce(g, plan, red, grad, ws, stream);
