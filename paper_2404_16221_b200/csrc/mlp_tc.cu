@@ -60,9 +60,11 @@ __device__ __forceinline__ void stage_one(const __half* __restrict__ Wg, uint8_t
   }
 }
 
+template <bool DENS = false>
 __device__ __forceinline__ void stage_weights(const __half* __restrict__ W, uint8_t* s) {
   stage_one(W + VR_MLP_W1D, s + OW1D, 64, 32);
   stage_one(W + VR_MLP_W2D, s + OW2D, 16, 64);
+  if (DENS) return;  // the density branch reads W1d, W2d only
   stage_one(W + VR_MLP_W1C, s + OW1C, 64, 32);
   stage_one(W + VR_MLP_W2C, s + OW2C, 64, 64);
   stage_one(W + VR_MLP_W3C, s + OW3C, 16, 64);
@@ -547,10 +549,24 @@ __global__ void __launch_bounds__(TILE * FWD_TPR, 4)
 // 256 threads (2 per tile row), 2 CTAs per SM.  Smem per CTA: weights 20 KB + A (enc,
 // then cin) 8 KB + X1 h1d 16 KB + X3 h1c 16 KB + X4 h2c 16 KB + Gh 16 KB + Gl 16 KB.
 constexpr int BWD_TPR = 2;
-constexpr uint32_t B_A = WBYTES, B_X1 = B_A + TILE * 32 * 2, B_X3 = B_X1 + TILE * 64 * 2,
-                   B_X4 = B_X3 + TILE * 64 * 2, B_GH = B_X4 + TILE * 64 * 2,
-                   B_GL = B_GH + TILE * 64 * 2, B_BAR = B_GL + TILE * 64 * 2,
-                   B_WMAX = B_BAR + 32, B_SMEM = B_WMAX + 32;
+// Density-only kernels (proposal fields) need W1d / W2d, enc, h1d and G only, and 128 TMEM
+// columns (W1d, W2d^T accumulators + scratch): 62 KB of smem, 3 CTAs per SM instead of 2.
+template <bool DENS>
+struct BwdLayout {
+  static constexpr uint32_t W = DENS ? OW1C : WBYTES;
+  static constexpr uint32_t A = W, X1 = A + TILE * 32 * 2;
+  static constexpr uint32_t X3 = DENS ? X1 : X1 + TILE * 64 * 2;  // unused when DENS
+  static constexpr uint32_t X4 = DENS ? X1 : X3 + TILE * 64 * 2;  // unused when DENS
+  static constexpr uint32_t GH = (DENS ? X1 : X4) + TILE * 64 * 2, GL = GH + TILE * 64 * 2;
+  static constexpr uint32_t BAR = GL + TILE * 64 * 2, WMAX = BAR + 32, SMEM = WMAX + 32;
+  static constexpr uint32_t D0 = DENS ? 64 : 192, COLS = DENS ? 128 : 256;
+  static constexpr int CTAS = DENS ? 3 : 2;
+};
+constexpr uint32_t B_A = BwdLayout<false>::A, B_X1 = BwdLayout<false>::X1,
+                   B_X3 = BwdLayout<false>::X3, B_X4 = BwdLayout<false>::X4,
+                   B_GH = BwdLayout<false>::GH, B_GL = BwdLayout<false>::GL,
+                   B_BAR = BwdLayout<false>::BAR, B_WMAX = BwdLayout<false>::WMAX,
+                   B_SMEM = BwdLayout<false>::SMEM;
 // TMEM columns: weight-gradient accumulators, then scratch.  W1d, W1c, W2c: M = 128
 // (rows 0..63 hi, 64..127 lo products); W2d^T, W3c^T: M = 64, columns [hi 16 | lo 16].
 // The forward's second scratch slice aliases the first (its results are consumed before
@@ -572,7 +588,7 @@ struct RowIn {
   float4 gin;    // upstream gradient, unscaled
 };
 
-template <bool FUSED>
+template <bool FUSED, bool DENS>
 __device__ __forceinline__ void fetch_row(RowIn& x, const __half2* __restrict__ enc,
                                           const double* __restrict__ rays, int64_t stride,
                                           int32_t ray, const float4* __restrict__ dsr, int64_t n,
@@ -588,7 +604,7 @@ __device__ __forceinline__ void fetch_row(RowIn& x, const __half2* __restrict__ 
   x.gin = (valid && part == 0) ? dsr[i] : make_float4(0.f, 0.f, 0.f, 0.f);
   x.d[0] = x.d[1] = x.d[2] = 0.0;
   x.u[0] = x.u[1] = x.u[2] = 0.f;
-  if (valid) {
+  if (valid && !DENS) {  // the density branch has no view direction
     const int64_t r = checked_ray(ray, stride);
 #pragma unroll
     for (int a = 0; a < 3; ++a) x.d[a] = __ldg(rays + (3 + a) * stride + r);
@@ -617,7 +633,7 @@ __device__ __forceinline__ void put_enc(uint8_t* tile, int r, int part, const Ro
 // row's hash-grid gradients (its 8 levels) straight from the last epilogue (K3 + K2
 // backward in one pass); the atomics overlap other tiles' tensor-core rounds.
 template <bool FUSED, bool DENS = false>
-__global__ void __launch_bounds__(TILE * BWD_TPR, 2)
+__global__ void __launch_bounds__(TILE * BWD_TPR, BwdLayout<DENS>::CTAS)
     k_mlp_bwd_tc(const __half* __restrict__ W, const __half2* __restrict__ enc,
                  const double* __restrict__ rays, int64_t stride, const int32_t* __restrict__ rid,
                  int64_t n, const float4* __restrict__ dsr, const float4* __restrict__ sig,
@@ -629,18 +645,20 @@ __global__ void __launch_bounds__(TILE * BWD_TPR, 2)
   using G = Geo<BWD_TPR>;
   extern __shared__ __align__(1024) uint8_t smem[];
   uint8_t* sw = smem;
-  uint8_t* A = smem + B_A;   // enc during L1d, cin afterwards
-  uint8_t* X1 = smem + B_X1;
-  uint8_t* X3 = smem + B_X3;
-  uint8_t* X4 = smem + B_X4;  // h2c, then enc (re-staged) for the last stage
-  uint8_t* Gh = smem + B_GH;
-  uint8_t* Gl = smem + B_GL;
-  uint64_t* barA = reinterpret_cast<uint64_t*>(smem + B_BAR);  // forward / dgrad MMAs
+  using LY = BwdLayout<DENS>;
+  constexpr uint32_t T_D0 = LY::D0, T_D1 = LY::D0, T_COLS = LY::COLS;
+  uint8_t* A = smem + LY::A;   // enc during L1d, cin afterwards
+  uint8_t* X1 = smem + LY::X1;
+  uint8_t* X3 = smem + LY::X3;
+  uint8_t* X4 = smem + LY::X4;  // h2c, then enc (re-staged) for the last stage
+  uint8_t* Gh = smem + LY::GH;
+  uint8_t* Gl = smem + LY::GL;
+  uint64_t* barA = reinterpret_cast<uint64_t*>(smem + LY::BAR);  // forward / dgrad MMAs
   uint64_t* barB = barA + 1;                                     // wgrad MMAs
-  uint32_t* slot = reinterpret_cast<uint32_t*>(smem + B_BAR + 16);
+  uint32_t* slot = reinterpret_cast<uint32_t*>(smem + LY::BAR + 16);
   const int r = G::row(), part = G::part();
   const int lane = threadIdx.x & 31, wq = (threadIdx.x >> 5) & 3;
-  stage_weights(W, sw);
+  stage_weights<DENS>(W, sw);
   if (threadIdx.x < 32) tmem_alloc(slot, T_COLS);
   if (threadIdx.x == 0) {
     mbar_init(barA, 1);
@@ -660,7 +678,7 @@ __global__ void __launch_bounds__(TILE * BWD_TPR, 2)
   // the flushed weight gradients are multiplied by 1/S.
   float gscale = 1.f, ginv = 1.f;
   if (sig) {
-    uint32_t* wmax = reinterpret_cast<uint32_t*>(smem + B_WMAX);
+    uint32_t* wmax = reinterpret_cast<uint32_t*>(smem + LY::WMAX);
     float m = 0.f;
     for (int64_t tile = blockIdx.x + (int64_t)part * gridDim.x; tile < n_tiles;
          tile += 2 * (int64_t)gridDim.x) {
@@ -768,11 +786,11 @@ __global__ void __launch_bounds__(TILE * BWD_TPR, 2)
   // tile's prefetch depend on it)
   auto load_rid = [&](int64_t tile) -> int32_t {
     const int64_t i = tile * TILE + r;
-    return (tile < n_tiles && i < n) ? __ldg(rid + i) : 0;
+    return (!DENS && tile < n_tiles && i < n) ? __ldg(rid + i) : 0;
   };
   int32_t rid_ahead = 0;
   if ((int64_t)blockIdx.x < n_tiles) {
-    fetch_row<FUSED>(nxt, enc, rays, stride, load_rid(blockIdx.x), dsr, n,
+    fetch_row<FUSED, DENS>(nxt, enc, rays, stride, load_rid(blockIdx.x), dsr, n,
                      (int64_t)blockIdx.x * TILE + r, part, hg, t0, t1, pos);
     rid_ahead = load_rid(blockIdx.x + (int64_t)gridDim.x);
   }
@@ -781,7 +799,7 @@ __global__ void __launch_bounds__(TILE * BWD_TPR, 2)
     const bool valid = i < n;
     const RowIn cur = nxt;
     if (tile + gridDim.x < n_tiles) {  // prefetch the next tile's inputs (loads only)
-      fetch_row<FUSED>(nxt, enc, rays, stride, rid_ahead, dsr, n, (tile + gridDim.x) * TILE + r,
+      fetch_row<FUSED, DENS>(nxt, enc, rays, stride, rid_ahead, dsr, n, (tile + gridDim.x) * TILE + r,
                        part, hg, t0, t1, pos);
       rid_ahead = load_rid(tile + 2 * (int64_t)gridDim.x);
     }
@@ -1017,7 +1035,8 @@ int launch_bwd(const void* w, const void* enc, const double* rays, int64_t strid
                float* denc, int32_t* err, const VrHashGridDesc* g, const double* t0, const double* t1,
                float* grad_table, void* ws, size_t ws_bytes, const float* pos, void* stream,
                int max_ctas = 0) {
-  int rc = set_smem(mlp::k_mlp_bwd_tc<FUSED, DENS>, mlp::B_SMEM, "mlp bwd: smem attribute");
+  using LY = mlp::BwdLayout<DENS>;
+  int rc = set_smem(mlp::k_mlp_bwd_tc<FUSED, DENS>, LY::SMEM, "mlp bwd: smem attribute");
   if (rc != VR_OK) return rc;
   VrHashGridDesc gd;
   RepPlan plan;
@@ -1031,9 +1050,10 @@ int launch_bwd(const void* w, const void* enc, const double* rays, int64_t strid
     memset(&gd, 0, sizeof(gd));
   }
   const int64_t tiles = ceil_div(n, mlp::TILE);
-  const int cap = max_ctas > 0 && max_ctas < VR_NUM_SMS * 2 ? max_ctas : VR_NUM_SMS * 2;
+  const int full = VR_NUM_SMS * LY::CTAS;
+  const int cap = max_ctas > 0 && max_ctas < full ? max_ctas : full;
   const int grid = (int)(tiles < cap ? tiles : cap);
-  mlp::k_mlp_bwd_tc<FUSED, DENS><<<grid, mlp::TILE * mlp::BWD_TPR, mlp::B_SMEM,
+  mlp::k_mlp_bwd_tc<FUSED, DENS><<<grid, mlp::TILE * mlp::BWD_TPR, LY::SMEM,
                                    (cudaStream_t)stream>>>(
       (const __half*)w, (const __half2*)enc, rays, stride, rid, n,
       reinterpret_cast<const float4*>(dsr), reinterpret_cast<const float4*>(sig), gW,
