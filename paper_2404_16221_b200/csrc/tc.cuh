@@ -64,15 +64,19 @@ __device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
   asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count));
 }
 
+// The suspend-time hint lets the hardware park a waiting warp until the phase completes
+// (or the hint expires) instead of returning at once: a spinning try_wait loop cost ~20 %
+// of the MLP kernels' issued instructions (SYNCS + BRA), slots the other CTA's epilogue
+// warps need.
 __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t phase) {
   const uint32_t a = smem_u32(bar);
   uint32_t ok = 0;
   do {
     asm volatile(
-        "{\n\t.reg .pred p;\n\tmbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"
+        "{\n\t.reg .pred p;\n\tmbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2, %3;\n\t"
         "selp.u32 %0, 1, 0, p;\n\t}\n"
         : "=r"(ok)
-        : "r"(a), "r"(phase)
+        : "r"(a), "r"(phase), "r"(1000000u)
         : "memory");
   } while (!ok);
 }
