@@ -322,7 +322,9 @@ int vr_mlp_bwd(const void* weights_dev, const void* enc_dev, const double* rays_
 /* Same MLP on the 5th-gen tensor cores (tcgen05.mma kind::f16, TMEM accumulators,
  * persistent 128-sample tiles).  The production path; vr_mlp_fwd / vr_mlp_bwd are the
  * CUDA-core reference kernels it is tested against.  The backward raises
- * VR_FLAG_GRAD_OVERFLOW in err_dev if a gradient is not representable in fp16. */
+ * VR_FLAG_GRAD_OVERFLOW in err_dev if a result is not finite (a scaled gradient operand
+ * overflowed fp16, or a non-finite upstream gradient): checked on d(enc) and the flushed
+ * weight gradients, not per operand. */
 int vr_mlp_fwd_tc(const void* weights_dev, const void* enc_dev, const double* rays_dev,
                   int64_t ray_stride, const int32_t* ray_id_dev, int64_t n, float* sig_rgb_dev,
                   void* stream);

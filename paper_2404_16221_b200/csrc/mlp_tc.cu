@@ -145,9 +145,16 @@ __device__ __forceinline__ void relu_mask8(const uint8_t* tile, int r, int cb, c
     g[2 * j + 1] = (u[j] & 0x7FFF0000u) ? v[2 * j + 1] : 0.f;
   }
 }
-// fp16 hi/lo split of 8 gradients into Gh / Gl (column block cb)
-__device__ __forceinline__ void put_grad8(uint8_t* Gh, uint8_t* Gl, int r, int cb, const float* g,
-                                          uint32_t& inf_bits) {
+// weight-gradient flush: global add, and the value joins the non-finite check
+__device__ __forceinline__ void flush_add(float* dst, float v, float& nonfinite) {
+  atomicAdd(dst, v);
+  nonfinite += v;
+}
+
+// fp16 hi/lo split of 8 gradients into Gh / Gl (column block cb).  An operand that
+// overflows fp16 (inf) is not tested here: it makes the stage's MMA results non-finite,
+// which the d(enc) and weight-gradient checks at the end of the tile / kernel catch.
+__device__ __forceinline__ void put_grad8(uint8_t* Gh, uint8_t* Gl, int r, int cb, const float* g) {
   uint4 qh, ql;
   __half2* hh = reinterpret_cast<__half2*>(&qh);
   __half2* hl = reinterpret_cast<__half2*>(&ql);
@@ -157,8 +164,6 @@ __device__ __forceinline__ void put_grad8(uint8_t* Gh, uint8_t* Gl, int r, int c
     const float2 f = __half22float2(h);
     hh[j] = h;
     hl[j] = __floats2half2_rn(g[2 * j] - f.x, g[2 * j + 1] - f.y);
-    const uint32_t u = *reinterpret_cast<const uint32_t*>(&h);
-    inf_bits |= ((u & 0x7C00u) == 0x7C00u) | ((u & 0x7C000000u) == 0x7C000000u);
   }
   *reinterpret_cast<uint4*>(Gh + tile_off(TILE, r, cb * 8)) = qh;
   *reinterpret_cast<uint4*>(Gl + tile_off(TILE, r, cb * 8)) = ql;
@@ -716,7 +721,7 @@ __global__ void __launch_bounds__(TILE * BWD_TPR, BwdLayout<DENS>::CTAS)
                  sGh = smem_u32(Gh), sGl = smem_u32(Gl), sGh16 = sGh + 2 * TILE * 16;
   uint32_t phA = 0, phB = 0;
   bool wgrad_pending = false;
-  uint32_t inf_bits = 0;
+  float nonfinite = 0.f;  // sum of this thread's d(enc) values: inf / NaN if any is
   bool acc = false;  // weight-gradient accumulators hold data
   constexpr int C64 = 64 / BWD_TPR, C16 = 16 / BWD_TPR;
   const int c64 = part * C64, c16 = part * C16;
@@ -731,7 +736,7 @@ __global__ void __launch_bounds__(TILE * BWD_TPR, BwdLayout<DENS>::CTAS)
       phB ^= 1u;
     }
     for (int c = 0; c < width_here; c += 8)  // 16-wide G: lo part -> Gh columns 16..31
-      put_grad8(Gh, total16 ? Gh + 2 * TILE * 16 : Gl, r, (col0 + c) / 8, g + c, inf_bits);
+      put_grad8(Gh, total16 ? Gh + 2 * TILE * 16 : Gl, r, (col0 + c) / 8, g + c);
     fence_async_smem();
     tc_fence_before();
     __syncthreads();
@@ -843,8 +848,10 @@ __global__ void __launch_bounds__(TILE * BWD_TPR, BwdLayout<DENS>::CTAS)
       tmem_ld16(tm_row + T_D0 + 16 * part, v);
       if (valid) {
 #pragma unroll
-        for (int j = 0; j < 16; j += 2)
+        for (int j = 0; j < 16; j += 2) {
           denc[(int64_t)(8 * part + j / 2) * n + i] = make_float2(v[j] * ginv, v[j + 1] * ginv);
+          nonfinite += v[j] + v[j + 1];
+        }
       }
       acc = true;
       continue;
@@ -924,6 +931,10 @@ __global__ void __launch_bounds__(TILE * BWD_TPR, BwdLayout<DENS>::CTAS)
           [] {});
     // d(enc) of this thread's levels part*8 .. part*8+7
     tmem_ld16(tm_row + T_D0 + 16 * part, v);
+    if (valid) {
+#pragma unroll
+      for (int j = 0; j < 16; ++j) nonfinite += v[j];
+    }
     if (FUSED) {
 #pragma unroll
       for (int j = 0; j < 16; ++j) pk[j] = valid ? v[j] * ginv : 0.f;
@@ -958,32 +969,35 @@ __global__ void __launch_bounds__(TILE * BWD_TPR, BwdLayout<DENS>::CTAS)
     float v[16], w[16];
     // this warp's column half of each accumulator
     tmem_ld16(tm_row + T_W1D + 16 * part, v);
-    for (int j = 0; j < 16; ++j) atomicAdd(gW + VR_MLP_W1D + m2 * 32 + 16 * part + j, v[j] * ginv);
+    for (int j = 0; j < 16; ++j) flush_add(gW + VR_MLP_W1D + m2 * 32 + 16 * part + j, v[j] * ginv, nonfinite);
     tmem_ld8(tm_row + T_W2DT + 8 * part, v);
     tmem_ld8(tm_row + T_W2DT + 16 + 8 * part, w);
     if (lane < 16)
       for (int j = 0; j < 8; ++j)
-        atomicAdd(gW + VR_MLP_W2D + (8 * part + j) * 64 + m, (v[j] + w[j]) * ginv);
+        flush_add(gW + VR_MLP_W2D + (8 * part + j) * 64 + m, (v[j] + w[j]) * ginv, nonfinite);
     if (!DENS) {  // the colour accumulators (never written in a density-only kernel)
       tmem_ld16(tm_row + T_W1C + 16 * part, v);
       for (int j = 0; j < 16; ++j)
-        atomicAdd(gW + VR_MLP_W1C + m2 * 32 + 16 * part + j, v[j] * ginv);
+        flush_add(gW + VR_MLP_W1C + m2 * 32 + 16 * part + j, v[j] * ginv, nonfinite);
 #pragma unroll
       for (int c = 0; c < 32; c += 16) {
         tmem_ld16(tm_row + T_W2C + 32 * part + c, v);
         for (int j = 0; j < 16; ++j)
-          atomicAdd(gW + VR_MLP_W2C + m2 * 64 + 32 * part + c + j, v[j] * ginv);
+          flush_add(gW + VR_MLP_W2C + m2 * 64 + 32 * part + c + j, v[j] * ginv, nonfinite);
       }
       if (part == 0) {
         tmem_ld8(tm_row + T_W3CT, v);
         tmem_ld8(tm_row + T_W3CT + 16, w);
         if (lane < 16)
           for (int j = 0; j < 3; ++j)
-            atomicAdd(gW + VR_MLP_W3C + j * 64 + m, (v[j] + w[j]) * ginv);
+            flush_add(gW + VR_MLP_W3C + j * 64 + m, (v[j] + w[j]) * ginv, nonfinite);
       }
     }
   }
-  if (__any_sync(0xffffffffu, inf_bits != 0) && lane == 0) atomicOr(err, VR_FLAG_GRAD_OVERFLOW);
+  // an fp16 gradient operand that overflowed (or a non-finite upstream) left inf / NaN in
+  // d(enc) or in a weight-gradient accumulator
+  if (__any_sync(0xffffffffu, !isfinite(nonfinite)) && lane == 0)
+    atomicOr(err, VR_FLAG_GRAD_OVERFLOW);
   tc_fence_before();
   __syncthreads();
   if (threadIdx.x < 32) {

@@ -848,3 +848,30 @@ def test_hash_kernels_match_hand_vectors(case_i):
         ref = (w[:, :, None] * table[offs[l] + want]).sum(1)
         ulp = np.maximum(np.spacing(np.abs(ref).astype(np.float16)).astype(np.float64), 2.0 ** -24)
         assert (np.abs(feats[l] - ref) <= ulp * 1.01).all(), f"level {l}"
+
+
+@pytest.mark.parametrize("name", ["vr_mlp_bwd_tc", "vr_mlp_bwd_tc_density"])
+def test_mlp_backward_flags_a_non_finite_gradient(name):
+    """A non-finite value in the MLP backward (an fp16 operand overflow, or a NaN upstream)
+    reaches d(enc) / the weight gradients and raises VR_FLAG_GRAD_OVERFLOW."""
+    from paper_2404_16221_b200 import _lib
+    g = torch.Generator(device="cpu").manual_seed(3)
+    n = 1000
+    w16 = vr.fields.init_mlp_weights(g).to(DEV).half()
+    enc = (torch.randn((16, n, 2), generator=g) * 0.5).half().to(DEV).contiguous()
+    rays = torch.zeros((8, n), dtype=torch.float64, device=DEV)
+    rays[3] = 1.0
+    rid = torch.arange(n, dtype=torch.int32, device=DEV)
+    sig = torch.ones((n, 4), device=DEV)
+    for poison, flagged in ((False, False), (True, True)):
+        dsr = (torch.randn((n, 4), generator=g) * 0.1).to(DEV)
+        if poison:
+            dsr[417, 0] = float("nan")
+        gw = torch.zeros(_lib.VR_MLP_NPARAMS, device=DEV)
+        de = torch.empty((16, n, 2), device=DEV)
+        err = torch.zeros(1, dtype=torch.int32, device=DEV)
+        _lib.call(name, _lib.ptr(w16), _lib.ptr(enc), _lib.ptr(rays), n, _lib.ptr(rid), n,
+                  _lib.ptr(dsr), _lib.ptr(sig), _lib.ptr(gw), _lib.ptr(de), _lib.ptr(err), 0,
+                  _lib.stream_ptr())
+        torch.cuda.synchronize()
+        assert bool(err.item() & _lib.VR_FLAG_GRAD_OVERFLOW) == flagged
