@@ -297,7 +297,7 @@ int vr_hash_bwd_lm(const VrHashGridDesc* g, const float* pos_dev, int64_t n,
 int vr_hash_scatter(const VrHashGridDesc* g, const float* pos_dev, int64_t n,
                     const float* denc_dev, float* grad_table_dev, void* workspace_dev,
                     size_t workspace_bytes, int32_t level_major, int32_t max_blocks,
-                    void* stream);
+                    const int32_t* rows_dev, const int32_t* n_rows_dev, void* stream);
 /* debug/parity: the 8 corner indices per (level, sample): idx[l][n][8] int32 */
 int vr_hash_indices(const VrHashGridDesc* g, const double* rays_dev, int64_t ray_stride,
                     const double* t0_dev, const double* t1_dev, const int32_t* ray_id_dev,
@@ -337,7 +337,8 @@ int vr_mlp_fwd_tc(const void* weights_dev, const void* enc_dev, const double* ra
 int vr_mlp_bwd_tc(const void* weights_dev, const void* enc_dev, const double* rays_dev,
                   int64_t ray_stride, const int32_t* ray_id_dev, int64_t n,
                   const float* dsig_rgb_dev, const float* sig_rgb_dev, float* grad_weights_dev,
-                  float* denc_dev, int32_t* err_dev, int32_t max_ctas, void* stream);
+                  float* denc_dev, int32_t* err_dev, int32_t max_ctas,
+                  const int32_t* rows_dev, const int32_t* n_rows_dev, void* stream);
 
 /* Density branch only (proposal fields of the interlevel loss, whose colour head is never
  * read): out[i] = {sigma, 0, 0, 0}; the backward reads dL/dsigma (dsig_rgb[i].x), writes
@@ -348,7 +349,8 @@ int vr_mlp_bwd_tc_density(const void* weights_dev, const void* enc_dev, const do
                           int64_t ray_stride, const int32_t* ray_id_dev, int64_t n,
                           const float* dsig_rgb_dev, const float* sig_rgb_dev,
                           float* grad_weights_dev, float* denc_dev, int32_t* err_dev,
-                          int32_t max_ctas, void* stream);
+                          int32_t max_ctas, const int32_t* rows_dev, const int32_t* n_rows_dev,
+                          void* stream);
 
 /* ---- K2 + K3 fused (production training path) ------------------------------------
  * Forward: the tensor-core MLP kernel computes each row's hash encoding itself (no
@@ -366,7 +368,23 @@ int vr_field_bwd_tc(const VrHashGridDesc* g, const void* weights_dev, const void
                     const double* t1_dev, const int32_t* ray_id_dev, int64_t n,
                     const float* dsig_rgb_dev, const float* sig_rgb_dev, float* grad_weights_dev,
                     float* grad_table_dev, void* workspace_dev, size_t workspace_bytes,
-                    int32_t* err_dev, const float* pos_dev, void* stream);
+                    int32_t* err_dev, const float* pos_dev, const int32_t* rows_dev,
+                    const int32_t* n_rows_dev, void* stream);
+
+/* ---- Active rows of a backward (sparse backward) ---------------------------------
+ * Samples whose upstream gradient dsig_rgb[i] (float4) is exactly zero contribute exactly
+ * zero to every parameter gradient (d(enc) = 0, no weight-gradient term), and behind an
+ * opaque surface most do (transmittance underflows to 0 in float32).  vr_active_rows
+ * writes the indices of the others, in increasing order, to rows_dev[0, m) and m to
+ * *n_rows_dev (device memory: no host sync).  NaN / inf upstream values count as active
+ * (the kernels downstream flag them).  Workspace: vr_active_rows_workspace_bytes(n).
+ * The backward kernels above take (rows_dev, n_rows_dev) — both NULL = every sample —
+ * and then cut their 128-row tiles from the list; vr_mlp_bwd_tc* write d(enc) at the
+ * compact position j of sample rows[j] (denc[l][j], row stride still n), and
+ * vr_hash_scatter reads it there with the position of sample rows[j]. */
+size_t vr_active_rows_workspace_bytes(int64_t n);
+int vr_active_rows(const float* dsig_rgb_dev, int64_t n, int32_t* rows_dev, int32_t* n_rows_dev,
+                   void* workspace_dev, size_t workspace_bytes, void* stream);
 
 /* ---- K4: per-segment front-to-back composite (composite_samples quadrature.py:141-165,
  * aggregate_segment segrender.py:71-90, process_inbox distsim.py:318-329) ------------- */

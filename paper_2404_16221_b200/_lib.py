@@ -142,15 +142,17 @@ SIGNATURES = {
     "vr_hash_lm_passes": [P],
     "vr_hash_fwd_lm": [P, P, P, I64, P, P],
     "vr_hash_bwd_lm": [P, P, I64, P, P, P, C.c_size_t, P],
-    "vr_hash_scatter": [P, P, I64, P, P, P, C.c_size_t, I32, I32, P],
+    "vr_hash_scatter": [P, P, I64, P, P, P, C.c_size_t, I32, I32, P, P, P],
     "vr_mlp_fwd": [P, P, P, I64, P, I64, P, P],
     "vr_mlp_bwd": [P, P, P, I64, P, I64, P, P, P, P],
     "vr_mlp_fwd_tc": [P, P, P, I64, P, I64, P, P],
-    "vr_mlp_bwd_tc": [P, P, P, I64, P, I64, P, P, P, P, P, I32, P],
+    "vr_mlp_bwd_tc": [P, P, P, I64, P, I64, P, P, P, P, P, I32, P, P, P],
     "vr_mlp_fwd_tc_density": [P, P, I64, P, P],
-    "vr_mlp_bwd_tc_density": [P, P, P, I64, P, I64, P, P, P, P, P, I32, P],
+    "vr_mlp_bwd_tc_density": [P, P, P, I64, P, I64, P, P, P, P, P, I32, P, P, P],
     "vr_field_fwd_tc": [P, P, P, P, I64, P, P, P, I64, P, P, P],
-    "vr_field_bwd_tc": [P, P, P, P, I64, P, P, P, I64, P, P, P, P, P, C.c_size_t, P, P, P],
+    "vr_field_bwd_tc": [P, P, P, P, I64, P, P, P, I64, P, P, P, P, P, C.c_size_t, P, P, P, P, P],
+    "vr_active_rows_workspace_bytes": [I64],
+    "vr_active_rows": [P, I64, P, P, P, C.c_size_t, P],
     "vr_segment_fwd": [P, P, P, P, P, P, I64, I32, P, P, P, P],
     "vr_segment_bwd": [P, P, P, P, P, I64, I32, P, P, P, P],
     "vr_segment_transmittance": [P, P, P, P, I64, I32, P, P],
@@ -167,7 +169,8 @@ SIGNATURES = {
 }
 _RESTYPES = {"vr_last_error": C.c_char_p, "vr_scan_workspace_bytes": C.c_size_t,
              "vr_sample_stage_blocks": C.c_int64,
-             "vr_hash_bwd_workspace_bytes": C.c_size_t}
+             "vr_hash_bwd_workspace_bytes": C.c_size_t,
+             "vr_active_rows_workspace_bytes": C.c_size_t}
 
 _LIB = None
 
@@ -208,7 +211,7 @@ TIMER = None
 # level, vr_sample_stage adds k_sample_prefilter on a rank owning part of the regions)
 LAUNCHES = {"vr_scan_offsets": 3, "vr_sum_f64": 2, "vr_field_bwd_tc": 2, "vr_hash_bwd": 2,
             "vr_hash_scatter": 2, "vr_hash_bwd_lm": 2, "vr_packets_pack": 2,
-            "vr_packets_unpack": 2}
+            "vr_packets_unpack": 2, "vr_active_rows": 3}
 CALLS = {}
 # kernels launched by the calls above
 LAUNCHED = {}

@@ -21,7 +21,7 @@ OUT = PKG / "libvolray_b200.so"
 OUT_CHECKED = PKG / "libvolray_b200_checked.so"
 BUILD = ROOT / "build" / "csrc"
 SOURCES = ["capi.cu", "sampler.cu", "fields.cu", "composite.cu", "hashgrid.cu", "mlp.cu", "mlp_tc.cu",
-           "interlevel.cu", "segapi.cu", "occupancy.cu"]
+           "interlevel.cu", "segapi.cu", "occupancy.cu", "rows.cu"]
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 FLAGS = ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC", "--expt-relaxed-constexpr",
          f"-I{ROOT / 'include'}"]

@@ -165,24 +165,30 @@ __global__ void __launch_bounds__(HASH_THREADS, 6)  // 40 regs: c5 57.0 -> 55.2 
   }
 }
 
+// rows (optional, vr_active_rows): scatter only the samples rows[0, m), m = *n_rows, whose
+// d(enc) the MLP backward wrote at compact positions (denc[l][j] belongs to sample rows[j]);
+// positions are read at the sample index.
 __global__ void __launch_bounds__(HASH_THREADS)
     k_hash_bwd_lm(const VrHashGridDesc g, const RepPlan plan, const LmPasses passes,
                   const float* __restrict__ pos, int64_t n, const float2* __restrict__ denc,
-                  float2* __restrict__ grad, float2* __restrict__ ws, unsigned long long* ctr) {
+                  float2* __restrict__ grad, float2* __restrict__ ws, unsigned long long* ctr,
+                  const int32_t* __restrict__ rows, const int32_t* __restrict__ n_rows) {
   const int gwarp = blockIdx.x * (blockDim.x / 32) + (threadIdx.x >> 5);
   const int lane = threadIdx.x & 31, p = lane & 1;  // lane pairs (scatter_half)
   const int warp = threadIdx.x >> 5, n_warps = blockDim.x >> 5;
-  const int64_t chunks = ceil_div(n, LM_CHUNK);
+  const int64_t m = rows ? (int64_t)__ldg(n_rows) : n;
+  const int64_t chunks = ceil_div(m, LM_CHUNK);
   for (int64_t item = lm_claim(ctr); item < passes.n * chunks; item = lm_claim(ctr)) {
     const int pass = (int)(item / chunks);
     const int l0 = passes.first[pass], l1 = passes.first[pass + 1];
-    const int64_t c0 = (item - pass * chunks) * LM_CHUNK, c1 = min(n, c0 + LM_CHUNK);
+    const int64_t c0 = (item - pass * chunks) * LM_CHUNK, c1 = min(m, c0 + LM_CHUNK);
     for (int64_t s0 = c0 + warp * 16; s0 < c1; s0 += n_warps * 16) {
-      const int64_t i = s0 + (lane >> 1);
-      if (i >= c1) continue;  // no shuffles below: lanes may leave independently
+      const int64_t j = s0 + (lane >> 1);
+      if (j >= c1) continue;  // no shuffles below: lanes may leave independently
+      const int64_t i = rows ? (int64_t)__ldg(rows + j) : j;
       const float u[3] = {__ldcs(pos + i), __ldcs(pos + n + i), __ldcs(pos + 2 * n + i)};
       for (int l = l0; l < l1; ++l) {
-        const float2 d = __ldcs(denc + (int64_t)l * n + i);
+        const float2 d = __ldcs(denc + (int64_t)l * n + j);
         if (d.x != 0.f || d.y != 0.f) scatter_half(g, plan, l, u, d, p, gwarp, grad, ws);
       }
     }
@@ -415,8 +421,10 @@ extern "C" int vr_hash_fwd_lm(const VrHashGridDesc* g, const float* table, const
 
 extern "C" int vr_hash_scatter(const VrHashGridDesc* g, const float* pos, int64_t n,
                                const float* denc, float* grad, void* ws, size_t ws_bytes,
-                               int32_t level_major, int32_t max_blocks, void* stream) {
-  if (!valid_grid(g) || n < 0 || max_blocks < 0 || (n > 0 && (!pos || !denc || !grad))) {
+                               int32_t level_major, int32_t max_blocks, const int32_t* rows,
+                               const int32_t* n_rows, void* stream) {
+  if (!valid_grid(g) || n < 0 || max_blocks < 0 || (n > 0 && (!pos || !denc || !grad)) ||
+      (!rows != !n_rows)) {
     set_error("vr_hash_scatter: bad argument");
     return VR_ERR_BAD_ARG;
   }
@@ -447,7 +455,7 @@ extern "C" int vr_hash_scatter(const VrHashGridDesc* g, const float* pos, int64_
   k_hash_bwd_lm<<<blocks, threads, 0, s>>>(*g, plan, passes, pos, n,
                                            reinterpret_cast<const float2*>(denc),
                                            reinterpret_cast<float2*>(grad),
-                                           reinterpret_cast<float2*>(ws), ctr);
+                                           reinterpret_cast<float2*>(ws), ctr, rows, n_rows);
   const int rc = check_launch("vr_hash_scatter");
   if (rc != VR_OK) return rc;
   return hash_rep_reduce(g, plan, red, grad, ws, stream);
@@ -456,5 +464,5 @@ extern "C" int vr_hash_scatter(const VrHashGridDesc* g, const float* pos, int64_
 extern "C" int vr_hash_bwd_lm(const VrHashGridDesc* g, const float* pos, int64_t n,
                               const float* denc, float* grad, void* ws, size_t ws_bytes,
                               void* stream) {
-  return vr_hash_scatter(g, pos, n, denc, grad, ws, ws_bytes, 1, 0, stream);
+  return vr_hash_scatter(g, pos, n, denc, grad, ws, ws_bytes, 1, 0, nullptr, nullptr, stream);
 }

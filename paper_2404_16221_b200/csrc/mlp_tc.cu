@@ -597,12 +597,12 @@ template <bool FUSED, bool DENS>
 __device__ __forceinline__ void fetch_row(RowIn& x, const __half2* __restrict__ enc,
                                           const double* __restrict__ rays, int64_t stride,
                                           int32_t ray, const float4* __restrict__ dsr, int64_t n,
-                                          int64_t i, int part, const VrHashGridDesc& g,
+                                          int64_t i, bool valid, int part,
+                                          const VrHashGridDesc& g,
                                           const double* __restrict__ t0,
                                           const double* __restrict__ t1,
                                           const float* __restrict__ pos) {
   constexpr int LV = 16 / BWD_TPR;
-  const bool valid = i < n;
 #pragma unroll
   for (int l = 0; l < LV; ++l)
     x.enc[l] = valid ? enc[(int64_t)(part * LV + l) * n + i] : __floats2half2_rn(0.f, 0.f);
@@ -646,7 +646,8 @@ __global__ void __launch_bounds__(TILE * BWD_TPR, BwdLayout<DENS>::CTAS)
                  float2* __restrict__ denc, int32_t* err, const VrHashGridDesc hg,
                  const RepPlan plan, const double* __restrict__ t0,
                  const double* __restrict__ t1, float2* __restrict__ grad_table,
-                 float2* __restrict__ rep_ws, const float* __restrict__ pos) {
+                 float2* __restrict__ rep_ws, const float* __restrict__ pos,
+                 const int32_t* __restrict__ rows, const int32_t* __restrict__ n_rows) {
   using G = Geo<BWD_TPR>;
   extern __shared__ __align__(1024) uint8_t smem[];
   uint8_t* sw = smem;
@@ -670,7 +671,12 @@ __global__ void __launch_bounds__(TILE * BWD_TPR, BwdLayout<DENS>::CTAS)
     mbar_init(barB, 1);
     fence_barrier_init();
   }
-  const int64_t n_tiles = ceil_div(n, TILE);
+  // Active rows: with a row list (vr_active_rows) the tiles are cut from rows[0, m) — the
+  // samples whose upstream gradient is non-zero — instead of [0, n); compact position j
+  // stands for sample rows[j], and d(enc) is written at compact position j.
+  const int64_t m = rows ? (int64_t)__ldg(n_rows) : n;
+  const int64_t n_tiles = ceil_div(m, TILE);
+  auto sample_of = [&](int64_t j) -> int64_t { return rows ? (int64_t)__ldg(rows + j) : j; };
   // Gradient scale of this CTA (a power of two, so exact both ways): the fp16 hi + lo
   // split of G keeps 22 significant bits only while lo = G - fp16(G) is an fp16 normal,
   // i.e. |G| >= 2^-3; below that lo's absolute precision is 2^-24 (measured: d(enc) at
@@ -687,8 +693,9 @@ __global__ void __launch_bounds__(TILE * BWD_TPR, BwdLayout<DENS>::CTAS)
     float m = 0.f;
     for (int64_t tile = blockIdx.x + (int64_t)part * gridDim.x; tile < n_tiles;
          tile += 2 * (int64_t)gridDim.x) {
-      const int64_t i = tile * TILE + r;
-      if (i < n) {
+      const int64_t j = tile * TILE + r;
+      if (j < m) {
+        const int64_t i = sample_of(j);
         const float4 g4 = __ldg(dsr + i);
         const float a = fabsf(g4.x * __ldg(&sig[i].x));
         m = fmaxf(m, DENS ? a : fmaxf(a, 0.25f * fmaxf(fabsf(g4.y), fmaxf(fabsf(g4.z),
@@ -787,26 +794,34 @@ __global__ void __launch_bounds__(TILE * BWD_TPR, BwdLayout<DENS>::CTAS)
   auto scatter_ov = [&](int round) { scatter_one(round); };
 
   RowIn nxt;
-  // the ray index of this row in the tile after next (the direction loads of the next
-  // tile's prefetch depend on it)
-  auto load_rid = [&](int64_t tile) -> int32_t {
-    const int64_t i = tile * TILE + r;
-    return (!DENS && tile < n_tiles && i < n) ? __ldg(rid + i) : 0;
+  // inputs are prefetched one tile ahead; the ray index they depend on one tile earlier
+  // (rid_a), and the sample index that depends on (a row list) one tile earlier still
+  auto index_of = [&](int64_t tile) -> int64_t {
+    const int64_t j = tile * TILE + r;
+    return (tile < n_tiles && j < m) ? sample_of(j) : -1;
   };
-  int32_t rid_ahead = 0;
+  auto load_rid = [&](int64_t i) -> int32_t { return (!DENS && i >= 0) ? __ldg(rid + i) : 0; };
+  const int64_t G1 = gridDim.x;
+  int64_t i_a = -1, i_b = -1;  // sample index of this row in the next tile / the one after
+  int32_t rid_a = 0;           // ray index of this row in the next tile
   if ((int64_t)blockIdx.x < n_tiles) {
-    fetch_row<FUSED, DENS>(nxt, enc, rays, stride, load_rid(blockIdx.x), dsr, n,
-                     (int64_t)blockIdx.x * TILE + r, part, hg, t0, t1, pos);
-    rid_ahead = load_rid(blockIdx.x + (int64_t)gridDim.x);
+    const int64_t i0 = index_of(blockIdx.x);
+    fetch_row<FUSED, DENS>(nxt, enc, rays, stride, load_rid(i0), dsr, n, i0, i0 >= 0, part, hg,
+                           t0, t1, pos);
+    i_a = index_of(blockIdx.x + G1);
+    rid_a = load_rid(i_a);
+    i_b = index_of(blockIdx.x + 2 * G1);
   }
-  for (int64_t tile = blockIdx.x; tile < n_tiles; tile += gridDim.x) {
-    const int64_t i = tile * TILE + r;
-    const bool valid = i < n;
+  for (int64_t tile = blockIdx.x; tile < n_tiles; tile += G1) {
+    const int64_t jrow = tile * TILE + r;  // compact position (== the sample without a list)
+    const bool valid = jrow < m;
     const RowIn cur = nxt;
-    if (tile + gridDim.x < n_tiles) {  // prefetch the next tile's inputs (loads only)
-      fetch_row<FUSED, DENS>(nxt, enc, rays, stride, rid_ahead, dsr, n, (tile + gridDim.x) * TILE + r,
-                       part, hg, t0, t1, pos);
-      rid_ahead = load_rid(tile + 2 * (int64_t)gridDim.x);
+    if (tile + G1 < n_tiles) {  // prefetch the next tile's inputs (loads only)
+      fetch_row<FUSED, DENS>(nxt, enc, rays, stride, rid_a, dsr, n, i_a, i_a >= 0, part, hg, t0,
+                             t1, pos);
+      rid_a = load_rid(i_b);
+      i_a = i_b;
+      i_b = index_of(tile + 3 * G1);
     }
     if (wgrad_pending) {  // the previous tile's last wgrad reads X4/Gh/Gl
       mbar_wait(barB, phB);
@@ -849,7 +864,7 @@ __global__ void __launch_bounds__(TILE * BWD_TPR, BwdLayout<DENS>::CTAS)
       if (valid) {
 #pragma unroll
         for (int j = 0; j < 16; j += 2) {
-          denc[(int64_t)(8 * part + j / 2) * n + i] = make_float2(v[j] * ginv, v[j + 1] * ginv);
+          denc[(int64_t)(8 * part + j / 2) * n + jrow] = make_float2(v[j] * ginv, v[j + 1] * ginv);
           nonfinite += v[j] + v[j + 1];
         }
       }
@@ -945,7 +960,7 @@ __global__ void __launch_bounds__(TILE * BWD_TPR, BwdLayout<DENS>::CTAS)
     } else if (valid) {
 #pragma unroll
       for (int j = 0; j < 16; j += 2)
-        denc[(int64_t)(8 * part + j / 2) * n + i] = make_float2(v[j] * ginv, v[j + 1] * ginv);
+        denc[(int64_t)(8 * part + j / 2) * n + jrow] = make_float2(v[j] * ginv, v[j + 1] * ginv);
     }
     acc = true;
   }
@@ -1047,8 +1062,8 @@ template <bool FUSED, bool DENS = false>
 int launch_bwd(const void* w, const void* enc, const double* rays, int64_t stride,
                const int32_t* rid, int64_t n, const float* dsr, const float* sig, float* gW,
                float* denc, int32_t* err, const VrHashGridDesc* g, const double* t0, const double* t1,
-               float* grad_table, void* ws, size_t ws_bytes, const float* pos, void* stream,
-               int max_ctas = 0) {
+               float* grad_table, void* ws, size_t ws_bytes, const float* pos,
+               const int32_t* rows, const int32_t* n_rows, void* stream, int max_ctas = 0) {
   using LY = mlp::BwdLayout<DENS>;
   int rc = set_smem(mlp::k_mlp_bwd_tc<FUSED, DENS>, LY::SMEM, "mlp bwd: smem attribute");
   if (rc != VR_OK) return rc;
@@ -1073,7 +1088,7 @@ int launch_bwd(const void* w, const void* enc, const double* rays, int64_t strid
       reinterpret_cast<const float4*>(dsr), reinterpret_cast<const float4*>(sig), gW,
       reinterpret_cast<float2*>(denc), err, gd, plan, t0, t1,
       reinterpret_cast<float2*>(grad_table),
-      reinterpret_cast<float2*>(ws), pos);
+      reinterpret_cast<float2*>(ws), pos, rows, n_rows);
   rc = check_launch("vr_mlp_bwd_tc");
   if (rc != VR_OK || !FUSED) return rc;
   return hash_rep_reduce(&gd, plan, red, grad_table, ws, stream);
@@ -1095,14 +1110,15 @@ extern "C" int vr_mlp_fwd_tc(const void* w, const void* enc, const double* rays,
 extern "C" int vr_mlp_bwd_tc(const void* w, const void* enc, const double* rays, int64_t stride,
                              const int32_t* rid, int64_t n, const float* dsr, const float* sig,
                              float* gW, float* denc, int32_t* err, int32_t max_ctas,
-                             void* stream) {
-  if (n < 0 || !w || !gW || !denc || !err) {
+                             const int32_t* rows, const int32_t* n_rows, void* stream) {
+  if (n < 0 || !w || !gW || !denc || !err || (!rows != !n_rows)) {
     set_error("vr_mlp_bwd_tc: bad argument");
     return VR_ERR_BAD_ARG;
   }
   if (n == 0) return VR_OK;
   return launch_bwd<false>(w, enc, rays, stride, rid, n, dsr, sig, gW, denc, err, nullptr,
-                           nullptr, nullptr, nullptr, nullptr, 0, nullptr, stream, max_ctas);
+                           nullptr, nullptr, nullptr, nullptr, 0, nullptr, rows, n_rows, stream,
+                           max_ctas);
 }
 
 // density branch only (proposal fields): sigma of the same MLP, rgb = 0; the backward takes
@@ -1121,15 +1137,16 @@ extern "C" int vr_mlp_fwd_tc_density(const void* w, const void* enc, int64_t n, 
 extern "C" int vr_mlp_bwd_tc_density(const void* w, const void* enc, const double* rays,
                                      int64_t stride, const int32_t* rid, int64_t n,
                                      const float* dsr, const float* sig, float* gW, float* denc,
-                                     int32_t* err, int32_t max_ctas, void* stream) {
-  if (n < 0 || !w || !gW || !denc || !err) {
+                                     int32_t* err, int32_t max_ctas, const int32_t* rows,
+                                     const int32_t* n_rows, void* stream) {
+  if (n < 0 || !w || !gW || !denc || !err || (!rows != !n_rows)) {
     set_error("vr_mlp_bwd_tc_density: bad argument");
     return VR_ERR_BAD_ARG;
   }
   if (n == 0) return VR_OK;
   return launch_bwd<false, true>(w, enc, rays, stride, rid, n, dsr, sig, gW, denc, err, nullptr,
-                                 nullptr, nullptr, nullptr, nullptr, 0, nullptr, stream,
-                                 max_ctas);
+                                 nullptr, nullptr, nullptr, nullptr, 0, nullptr, rows, n_rows,
+                                 stream, max_ctas);
 }
 
 extern "C" int vr_field_fwd_tc(const VrHashGridDesc* g, const float* table, const void* w,
@@ -1149,12 +1166,14 @@ extern "C" int vr_field_bwd_tc(const VrHashGridDesc* g, const void* w, const voi
                                const double* rays, int64_t stride, const double* t0,
                                const double* t1, const int32_t* rid, int64_t n, const float* dsr,
                                const float* sig, float* gW, float* grad_table, void* ws,
-                               size_t ws_bytes, int32_t* err, const float* pos, void* stream) {
-  if (!valid_grid(g) || g->n_levels != 16 || n < 0 || !w || !enc || !gW || !grad_table || !err) {
+                               size_t ws_bytes, int32_t* err, const float* pos,
+                               const int32_t* rows, const int32_t* n_rows, void* stream) {
+  if (!valid_grid(g) || g->n_levels != 16 || n < 0 || !w || !enc || !gW || !grad_table || !err ||
+      (!rows != !n_rows)) {
     set_error("vr_field_bwd_tc: bad argument");
     return VR_ERR_BAD_ARG;
   }
   if (n == 0) return VR_OK;
   return launch_bwd<true>(w, enc, rays, stride, rid, n, dsr, sig, gW, nullptr, err, g, t0, t1,
-                          grad_table, ws, ws_bytes, pos, stream);
+                          grad_table, ws, ws_bytes, pos, rows, n_rows, stream);
 }

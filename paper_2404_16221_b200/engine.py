@@ -108,6 +108,7 @@ class VolumePool:
         self.background = np.asarray(background, dtype=np.float64)
         self.device = torch.device(device) if device is not None else torch.device("cuda")
         self.err = torch.zeros(1, dtype=torch.int32, device=self.device)
+        self._rows_ws = None  # vr_active_rows workspace
         for f in self.fields + (self.proposals or []):
             if hasattr(f, "err"):
                 f.err = self.err  # kernels of the fields report into the pool's flag word
@@ -477,6 +478,22 @@ class VolumePool:
     # 296 308.0; before that change 1.25 CTAs per SM was best: 185 388, 296 413)
     MLP_CTAS_BESIDE_SCATTER = int(os.environ.get("VR_MLP_BWD_CTAS", "0"))
 
+    # sparse backward: only the samples with a non-zero upstream gradient go through the
+    # MLP backward and the hash-grid scatter (vr_active_rows; VR_ACTIVE_ROWS=0 disables)
+    ACTIVE_ROWS = os.environ.get("VR_ACTIVE_ROWS", "1") != "0"
+
+    def _active_rows(self, dsig_rgb: torch.Tensor, n: int):
+        """(rows, n_rows) device tensors: the ordered indices of the samples in
+        dsig_rgb[:n] (float4 rows) with a non-zero upstream gradient, and their count."""
+        need = int(_lib.load().vr_active_rows_workspace_bytes(n))
+        if self._rows_ws is None or self._rows_ws.numel() < need:
+            self._rows_ws = torch.empty(max(need, 256), dtype=torch.uint8, device=self.device)
+        rows = torch.empty(max(n, 1), dtype=torch.int32, device=self.device)
+        cnt = torch.empty(1, dtype=torch.int32, device=self.device)
+        _lib.call("vr_active_rows", _lib.ptr(dsig_rgb), n, _lib.ptr(rows), _lib.ptr(cnt),
+                  _lib.ptr(self._rows_ws), self._rows_ws.numel(), self._stream())
+        return rows, cnt
+
     def field_backward(self, rays, b: SampleBatch, dsig_rgb: torch.Tensor, fields=None,
                        sig_rgb: torch.Tensor | None = None) -> None:
         self.field_backward_jobs(rays, b, [(self.fields if fields is None else fields, dsig_rgb,
@@ -495,34 +512,51 @@ class VolumePool:
             # the tensor-core MLP backward of the next region (of any field set) runs here
             main = torch.cuda.current_stream()
             side = self._side_stream()
+            # every row list first: once the side stream's persistent scatter grids hold the
+            # SMs, a small kernel queued behind them waits for a whole scatter
+            row_lists = {}
+            for j, (fields, dsig_rgb, _) in enumerate(jobs):
+                for kk, f in enumerate(fields):
+                    lo, hi = b.region_slice(base + kk)
+                    if (hi > lo and f.trainable and self.ACTIVE_ROWS
+                            and getattr(f, "takes_rows", False)):
+                        row_lists[j, kk] = self._active_rows(dsig_rgb[lo:], hi - lo)
             side.wait_stream(main)
-            for (fields, dsig_rgb, sig_rgb), sp in zip(jobs, split):
+            for j, ((fields, dsig_rgb, sig_rgb), sp) in enumerate(zip(jobs, split)):
                 for kk, f in enumerate(fields):
                     lo, hi = b.region_slice(base + kk)
                     if hi <= lo or not f.trainable:
                         continue
                     sig = sig_rgb[lo:] if sig_rgb is not None else None
+                    rows = row_lists.get((j, kk))
                     if not sp:
                         f.backward(rays, b.t0[lo:], b.t1[lo:], b.ray_id[lo:], hi - lo,
-                                   dsig_rgb[lo:], s, sig_rgb=sig)
+                                   dsig_rgb[lo:], s, sig_rgb=sig,
+                                   **({"rows": rows} if rows is not None else {}))
                         continue
                     denc = f.backward_mlp(rays, b.ray_id[lo:], hi - lo, dsig_rgb[lo:], s,
-                                          self.MLP_CTAS_BESIDE_SCATTER, sig_rgb=sig)
+                                          self.MLP_CTAS_BESIDE_SCATTER, sig_rgb=sig, rows=rows)
                     ev = torch.cuda.Event()
                     ev.record(main)
                     with torch.cuda.stream(side):
                         side.wait_event(ev)
                         denc.record_stream(side)
-                        f.backward_scatter(denc, hi - lo, _lib.stream_ptr(), self.SCATTER_BLOCKS)
+                        if rows is not None:
+                            rows[0].record_stream(side)
+                            rows[1].record_stream(side)
+                        f.backward_scatter(denc, hi - lo, _lib.stream_ptr(), self.SCATTER_BLOCKS,
+                                           rows=rows)
             main.wait_stream(side)
             return
         for fields, dsig_rgb, sig_rgb in jobs:
             for kk, f in enumerate(fields):
                 lo, hi = b.region_slice(base + kk)
                 if hi > lo and f.trainable:
+                    extra = ({"rows": self._active_rows(dsig_rgb[lo:], hi - lo)}
+                             if self.ACTIVE_ROWS and getattr(f, "takes_rows", False) else {})
                     f.backward(rays, b.t0[lo:], b.t1[lo:], b.ray_id[lo:], hi - lo,
                                dsig_rgb[lo:], s,
-                               sig_rgb=sig_rgb[lo:] if sig_rgb is not None else None)
+                               sig_rgb=sig_rgb[lo:] if sig_rgb is not None else None, **extra)
 
     # ---- K4 ----------------------------------------------------------------------------
     def local_packets(self, b: SampleBatch, sig_rgb: torch.Tensor,

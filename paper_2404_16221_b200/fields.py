@@ -396,13 +396,17 @@ class HashGridMLP(RegionField):
                   _lib.ptr(self.weights16), _lib.ptr(self._enc), _lib.ptr(rays), rays.shape[1],
                   _lib.ptr(ray_id), n, _lib.ptr(sig_rgb), stream)
 
-    def backward(self, rays, t0, t1, ray_id, n, dsig_rgb, stream, sig_rgb=None):
+    def backward(self, rays, t0, t1, ray_id, n, dsig_rgb, stream, sig_rgb=None, rows=None):
+        """rows: optional (rows, n_rows) device tensors of vr_active_rows — only those
+        samples (the ones with a non-zero upstream gradient) are processed."""
         if n == 0:
             return
         enc = self._enc  # written by the forward of the same step
+        rp = (_lib.ptr(rows[0]), _lib.ptr(rows[1])) if rows is not None else (None, None)
         if self.density_only:
             self.backward_scatter(self.backward_mlp(rays, ray_id, n, dsig_rgb, stream,
-                                                    sig_rgb=sig_rgb), n, stream)
+                                                    sig_rgb=sig_rgb, rows=rows), n, stream,
+                                  rows=rows)
             return
         if self.mlp_impl in ("fused", "fused_fwd") and self.hash_order == "sample":
             ws = self._workspace(rays.device)
@@ -411,22 +415,30 @@ class HashGridMLP(RegionField):
                       _lib.ptr(ray_id), n, _lib.ptr(dsig_rgb), _lib.ptr(sig_rgb),
                       _lib.ptr(self.grad_weights), _lib.ptr(self.grad_table), _lib.ptr(ws),
                       ws.numel(), _lib.ptr(self.err),
-                      _lib.ptr(self._pos) if self.mlp_impl == "fused" else None, stream)
+                      _lib.ptr(self._pos) if self.mlp_impl == "fused" else None, *rp, stream)
             return
         denc = torch.empty(16 * n * 2, dtype=torch.float32, device=rays.device)
         if self.mlp_impl != "cuda":
             _lib.call("vr_mlp_bwd_tc", _lib.ptr(self.weights16), _lib.ptr(enc), _lib.ptr(rays),
                       rays.shape[1], _lib.ptr(ray_id), n, _lib.ptr(dsig_rgb), _lib.ptr(sig_rgb),
-                      _lib.ptr(self.grad_weights), _lib.ptr(denc), _lib.ptr(self.err), 0, stream)
+                      _lib.ptr(self.grad_weights), _lib.ptr(denc), _lib.ptr(self.err), 0, *rp,
+                      stream)
         else:
+            if rows is not None:
+                raise ValueError("the CUDA-core MLP backward takes no row list")
             _lib.call("vr_mlp_bwd", _lib.ptr(self.weights16), _lib.ptr(enc), _lib.ptr(rays),
                       rays.shape[1], _lib.ptr(ray_id), n, _lib.ptr(dsig_rgb),
                       _lib.ptr(self.grad_weights), _lib.ptr(denc), stream)
         ws = self._workspace(rays.device)
         if self.hash_order == "level":  # positions of the same step's forward
-            _lib.call("vr_hash_bwd_lm", _lib.addr(self.desc), _lib.ptr(self._pos), n,
-                      _lib.ptr(denc), _lib.ptr(self.grad_table), _lib.ptr(ws), ws.numel(),
-                      stream)
+            _lib.call("vr_hash_scatter", _lib.addr(self.desc), _lib.ptr(self._pos), n,
+                      _lib.ptr(denc), _lib.ptr(self.grad_table), _lib.ptr(ws), ws.numel(), 1, 0,
+                      *rp, stream)
+            return
+        if rows is not None:  # sample-order scatter of the compact d(enc) (stored positions)
+            _lib.call("vr_hash_scatter", _lib.addr(self.desc), _lib.ptr(self._pos), n,
+                      _lib.ptr(denc), _lib.ptr(self.grad_table), _lib.ptr(ws), ws.numel(), 0, 0,
+                      *rp, stream)
             return
         _lib.call("vr_hash_bwd", _lib.addr(self.desc), _lib.ptr(rays), rays.shape[1],
                   _lib.ptr(t0), _lib.ptr(t1), _lib.ptr(ray_id), n, _lib.ptr(denc),
@@ -448,27 +460,43 @@ class HashGridMLP(RegionField):
             self.density_only or self.hash_order == "level"
             or self.n_entries * 8 < self.SPLIT_BELOW_BYTES)
 
-    def backward_mlp(self, rays, ray_id, n, dsig_rgb, stream, max_ctas: int = 0, sig_rgb=None):
+    @property
+    def takes_rows(self):
+        """Whether backward / backward_mlp / backward_scatter accept a vr_active_rows list
+        (every tensor-core path; not the CUDA-core MLP nor the sample-order d(enc) scatter)."""
+        if self.mlp_impl == "cuda":
+            return False
+        return (self.split_backward or self.hash_order == "level"
+                or self.mlp_impl in ("fused", "fused_fwd"))
+
+    def backward_mlp(self, rays, ray_id, n, dsig_rgb, stream, max_ctas: int = 0, sig_rgb=None,
+                     rows=None):
         """MLP backward of the step's samples; returns d(enc) [16][n] float2 (float32).
         max_ctas: grid cap when a scatter runs beside it (0: the full persistent grid);
-        sig_rgb: the forward's output (gradient scaling, vr_capi.h vr_mlp_bwd_tc)."""
+        sig_rgb: the forward's output (gradient scaling, vr_capi.h vr_mlp_bwd_tc);
+        rows: (rows, n_rows) of vr_active_rows — d(enc) is then written at compact positions."""
         denc = torch.empty(16 * max(n, 1) * 2, dtype=torch.float32, device=rays.device)
         if n:
             _lib.call("vr_mlp_bwd_tc_density" if self.density_only else "vr_mlp_bwd_tc",
                       _lib.ptr(self.weights16), _lib.ptr(self._enc),
                       _lib.ptr(rays), rays.shape[1], _lib.ptr(ray_id), n, _lib.ptr(dsig_rgb),
                       _lib.ptr(sig_rgb), _lib.ptr(self.grad_weights), _lib.ptr(denc),
-                      _lib.ptr(self.err), int(max_ctas), stream)
+                      _lib.ptr(self.err), int(max_ctas),
+                      *((_lib.ptr(rows[0]), _lib.ptr(rows[1])) if rows is not None
+                        else (None, None)), stream)
         return denc
 
-    def backward_scatter(self, denc, n, stream, max_blocks=0):
-        """Hash-grid scatter of d(enc) at the positions stored by the forward."""
+    def backward_scatter(self, denc, n, stream, max_blocks=0, rows=None):
+        """Hash-grid scatter of d(enc) at the positions stored by the forward (rows: the
+        backward_mlp call's row list, d(enc) at compact positions)."""
         if n == 0:
             return
         ws = self._workspace(denc.device)
         _lib.call("vr_hash_scatter", _lib.addr(self.desc), _lib.ptr(self._pos), n,
                   _lib.ptr(denc), _lib.ptr(self.grad_table), _lib.ptr(ws), ws.numel(),
-                  1 if self.hash_order == "level" else 0, int(max_blocks), stream)
+                  1 if self.hash_order == "level" else 0, int(max_blocks),
+                  *((_lib.ptr(rows[0]), _lib.ptr(rows[1])) if rows is not None else (None, None)),
+                  stream)
 
     def zero_grad(self):
         self.grad_table.zero_()

@@ -588,7 +588,7 @@ def test_level_major_hash_kernels_match_sample_major():
               _lib.ptr(gb), _lib.ptr(ws), ws.numel(), s)
     gc = torch.zeros_like(f.table)  # sample order from stored positions, co-resident grid
     _lib.call("vr_hash_scatter", _lib.addr(f.desc), _lib.ptr(pos), n, _lib.ptr(denc),
-              _lib.ptr(gc), _lib.ptr(ws), ws.numel(), 0, 148, s)
+              _lib.ptr(gc), _lib.ptr(ws), ws.numel(), 0, 148, None, None, s)
     torch.cuda.synchronize()
     assert torch.count_nonzero(ga) > 1000
     for g in (gb, gc):
@@ -650,7 +650,7 @@ def test_mlp_tensor_core_matches_cuda_core(n):
             args += [_lib.ptr(b)]
         args += [_lib.ptr(gw), _lib.ptr(de)]
         if name.endswith("_tc"):
-            args += [_lib.ptr(err), 0]
+            args += [_lib.ptr(err), 0, None, None]
         _lib.call(name, *args, s)
         grads.append((gw, de))
     torch.cuda.synchronize()
@@ -872,6 +872,6 @@ def test_mlp_backward_flags_a_non_finite_gradient(name):
         err = torch.zeros(1, dtype=torch.int32, device=DEV)
         _lib.call(name, _lib.ptr(w16), _lib.ptr(enc), _lib.ptr(rays), n, _lib.ptr(rid), n,
                   _lib.ptr(dsr), _lib.ptr(sig), _lib.ptr(gw), _lib.ptr(de), _lib.ptr(err), 0,
-                  _lib.stream_ptr())
+                  None, None, _lib.stream_ptr())
         torch.cuda.synchronize()
         assert bool(err.item() & _lib.VR_FLAG_GRAD_OVERFLOW) == flagged
