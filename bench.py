@@ -88,6 +88,20 @@ def load_peaks():
             "sm_max_mhz": 1965.0}
 
 
+# entry points that take a vr_active_rows list: index of the device row-count argument (the
+# launch processes that many samples, not the sample-count argument's n)
+ROW_COUNT_ARG = {"vr_mlp_bwd_tc": 13, "vr_mlp_bwd_tc_density": 13, "vr_hash_scatter": 10,
+                 "vr_field_bwd_tc": 18}
+
+
+class _DevInt32:
+    """A device int32 at a raw address, viewable by torch (CUDA array interface)."""
+
+    def __init__(self, addr):
+        self.__cuda_array_interface__ = {"shape": (1,), "typestr": "<i4", "data": (addr, False),
+                                         "version": 3}
+
+
 class EventTimer:
     """CUDA events around every C-ABI call (current stream); per-entry-point totals."""
 
@@ -98,13 +112,20 @@ class EventTimer:
         self.pending = []
         self.open = {}
         self.samples = {}
+        self.row_counts = {}  # name -> device copies of the row counts of sparse launches
+        self.dense = {}  # name -> the samples those sparse launches were given
 
     def before(self, name, args=()):
         e = self.torch.cuda.Event(enable_timing=True)
         e.record()
         self.open[name] = e
         cost = KERNEL_COST.get(name)
-        if cost and cost[2] is not None:  # samples this launch processes
+        ri = ROW_COUNT_ARG.get(name)
+        if ri is not None and args[ri]:  # a row list: its device count, copied in stream order
+            v = self.torch.as_tensor(_DevInt32(args[ri]), device="cuda")
+            self.row_counts.setdefault(name, []).append(v.to(self.torch.int64, copy=True))
+            self.dense[name] = self.dense.get(name, 0) + int(args[cost[2]])
+        elif cost and cost[2] is not None:  # samples this launch processes
             self.samples[name] = self.samples.get(name, 0) + int(args[cost[2]])
 
     def after(self, name):
@@ -113,6 +134,9 @@ class EventTimer:
         self.pending.append((name, self.open.pop(name), e))
 
     def totals(self):
+        for name, vs in self.row_counts.items():
+            self.samples[name] = self.samples.get(name, 0) + int(sum(int(v) for v in vs))
+        self.row_counts = {}
         out = {}
         for name, a, b in self.pending:
             ms = a.elapsed_time(b)
@@ -670,7 +694,11 @@ def run_workload(cfg_name, args, rank, world, local, dev, group, red_dev, headli
                "tile_vs_sample_bytes": (n_live * (40 if interlevel else 36))
                / max(1, n_samples * 16)},
            "roofline": roofline, "rooflines": rooflines, "nvlink": link, "e2e": e2e,
-           "gpu_launches": launches, "clocks": clk, "loss": final_loss, "kernels": per_kernel}
+           "gpu_launches": launches, "clocks": clk, "loss": final_loss, "kernels": per_kernel,
+           # sparse backward: the fraction of each field backward's samples with a non-zero
+           # upstream gradient (the rest sit behind opaque surfaces: exactly zero gradients)
+           "active_rows": {k: round(timer.samples.get(k, 0) / v, 4)
+                           for k, v in timer.dense.items() if v}}
     del pool, batches
     torch.cuda.synchronize()
     torch.cuda.empty_cache()

@@ -23,8 +23,12 @@
 // (order_t, tile) sort, distsim.py:378), fold in float64 (compose_render
 // segrender.py:93-110, compose_distortion segrender.py:113-142), and for training
 // run the reverse sweep of that fold to get every owned packet's adjoint.
+#include <stdlib.h>
+#include <string.h>
+
 #include "common.cuh"
 #include "segscan.cuh"  // grouped-segment helpers (GroupSeg, find_seg, seg_scan)
+#include "segwalk.cuh"  // lane-serial segmented walks (LaneSpan, Comp, Pre, lane_seg_scan)
 
 namespace vr {
 
@@ -534,6 +538,402 @@ __global__ void k_cast_f16(const float* __restrict__ src, __half* __restrict__ d
     dst[i] = __float2half_rn(src[i]);
 }
 
+
+// ---- lane-serial K4 (segwalk.cuh): K consecutive samples per lane ------------------------
+// Per sample, the reference's own arithmetic (composite_samples quadrature.py:152-154):
+// alpha = 1 - exp(-sigma delta), keep = 1 - alpha — one exp per sample.
+constexpr int K4_LANE = 4;  // samples per lane (a chunk is 128 samples)
+
+struct K4In {
+  double a[K4_LANE], b[K4_LANE];
+  float4 v[K4_LANE];
+};
+
+__device__ __forceinline__ void k4_load(K4In& in, const double* __restrict__ t0,
+                                        const double* __restrict__ t1,
+                                        const float4* __restrict__ sr, int64_t s0, int cnt) {
+#pragma unroll
+  for (int k = 0; k < K4_LANE; ++k) {
+    if (k < cnt) {
+      in.a[k] = __ldcs(t0 + s0 + k);
+      in.b[k] = __ldcs(t1 + s0 + k);
+      in.v[k] = __ldcs(sr + s0 + k);
+    } else {
+      in.a[k] = in.b[k] = 0.0;
+      in.v[k] = make_float4(0.f, 0.f, 0.f, 0.f);
+    }
+  }
+}
+
+__device__ __forceinline__ void keep_alpha(double sigma, double dlt, double& keep,
+                                           double& alpha) {
+  alpha = 1.0 - exp(-(sigma * dlt));
+  keep = 1.0 - alpha;
+}
+
+__device__ __forceinline__ void k4_emit(float4* __restrict__ packets, double* __restrict__ seg_tot,
+                                        const int32_t* __restrict__ seg_first, int64_t seg,
+                                        const Comp& c) {
+  packets[2 * seg] = make_float4((float)c.T, (float)c.C0, (float)c.C1, (float)c.C2);
+  packets[2 * seg + 1] =
+      make_float4((float)c.A, (float)c.D, (float)c.L, order_bits(seg_first[seg]));
+  if (seg_tot) {  // float64 totals for the backward
+    double* st = seg_tot + SEG_TOT * seg;
+    st[0] = c.T;
+    st[1] = c.C0;
+    st[2] = c.C1;
+    st[3] = c.C2;
+    st[4] = c.A;
+    st[5] = c.D;
+    st[6] = c.L;
+  }
+}
+
+__global__ void __launch_bounds__(SEG_WARPS * 32, 2)
+    k_segment_fwd_ls(const double* __restrict__ t0, const double* __restrict__ t1,
+                     const float4* __restrict__ sr, const int64_t* __restrict__ off,
+                     const int32_t* __restrict__ seg_first, const double* __restrict__ ray_te,
+                     int64_t n_rays, int64_t n_segs, float4* __restrict__ packets,
+                     double* __restrict__ seg_tot) {
+  __shared__ int64_t s_off_all[SEG_WARPS][33];
+  __shared__ double s_te_all[SEG_WARPS][32];
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  int64_t* O = s_off_all[wid];
+  double* TE = s_te_all[wid];
+  const int64_t n_groups = ceil_div(n_segs, 32);
+  for (int64_t grp = (int64_t)blockIdx.x * SEG_WARPS + wid; grp < n_groups;
+       grp += (int64_t)gridDim.x * SEG_WARPS) {
+    const int64_t seg0 = grp * 32;
+    const int nseg = (int)min((int64_t)32, n_segs - seg0);
+    __syncwarp();  // the previous group's readers are done with O / TE
+    stage_offsets(off, seg0, nseg, lane, O);
+    TE[lane] = lane < nseg ? ray_te[(seg0 + lane) % n_rays] : 0.0;
+    __syncwarp();
+    const int64_t s_beg = O[0], s_end = O[nseg];
+    if (lane < nseg && O[lane] == O[lane + 1]) {  // empty segment: identity packet
+      packets[2 * (seg0 + lane)] = make_float4(1.f, 0.f, 0.f, 0.f);
+      packets[2 * (seg0 + lane) + 1] = make_float4(0.f, 0.f, 0.f, order_bits(INT32_MAX));
+    }
+    Comp carry = comp_id();
+    K4In nxt;
+    {
+      const LaneSpan sp = lane_span<K4_LANE>(O, nseg, s_beg, s_end, lane);
+      k4_load(nxt, t0, t1, sr, sp.s0, sp.cnt);
+    }
+    for (int64_t base = s_beg; base < s_end; base += 32 * K4_LANE) {
+      const LaneSpan sp = lane_span<K4_LANE>(O, nseg, base, s_end, lane);
+      const K4In in = nxt;
+      {  // next chunk's inputs (loads only; used one chunk later)
+        const LaneSpan sn = lane_span<K4_LANE>(O, nseg, base + 32 * K4_LANE, s_end, lane);
+        k4_load(nxt, t0, t1, sr, sn.s0, sn.cnt);
+      }
+      Comp head = comp_id(), cur = comp_id();
+      bool head_done = false;
+      int seg = sp.sf;
+#pragma unroll
+      for (int k = 0; k < K4_LANE; ++k) {
+        if (k < sp.cnt) {
+          const int64_t s = sp.s0 + k;
+          while (s >= O[seg + 1]) {  // the segment ended inside this lane
+            if (!head_done) {
+              head = cur;
+              head_done = true;
+            } else if (O[seg] < O[seg + 1]) {  // (empty segments have their identity)
+              k4_emit(packets, seg_tot, seg_first, seg0 + seg, cur);
+            }
+            ++seg;
+            cur = comp_id();
+          }
+          double keep, alpha;
+          keep_alpha((double)in.v[k].x, in.b[k] - in.a[k], keep, alpha);
+          comp_push(cur, keep, alpha, in.v[k], sample_mid(in.a[k], in.b[k]) - TE[seg]);
+        }
+      }
+      const bool closed = sp.cnt > 0 && O[seg + 1] == sp.s0 + sp.cnt;
+      const bool single = !head_done;  // one segment piece in this lane
+      if (single) head = cur;
+      else if (closed) k4_emit(packets, seg_tot, seg_first, seg0 + seg, cur);
+      // the piece open at the lane's end enters the cross-lane scan; a piece that started
+      // in an earlier lane (or chunk) continues its predecessors'
+      Comp e = cur;
+      bool f = !(single && sp.open_left);
+      if (sp.cnt == 0) {
+        e = comp_id();
+        f = false;
+      }
+      if (lane == 0 && sp.open_left && single) {
+        e = comp_cat(carry, e);
+        f = true;
+      }
+      const Comp S = lane_seg_scan(e, f, lane, comp_cat, comp_shfl_up);
+      Comp X = comp_shfl_up(S, 1);
+      if (lane == 0) X = carry;
+      // the head segment closes in this lane: prefix from the lanes (chunks) before
+      if (sp.cnt > 0 && (!single || closed))
+        k4_emit(packets, seg_tot, seg_first, seg0 + sp.sf, sp.open_left ? comp_cat(X, head) : head);
+      carry = comp_shfl(S, 31);
+    }
+  }
+}
+
+// T only (the proposal fields' segment transmittance): the same walk and fold order as
+// k_segment_fwd_ls, so T[seg] equals the full packet's T bit for bit.
+__global__ void __launch_bounds__(SEG_WARPS * 32)
+    k_segment_T_ls(const double* __restrict__ t0, const double* __restrict__ t1,
+                   const float4* __restrict__ sr, const int64_t* __restrict__ off,
+                   int64_t n_segs, float* __restrict__ T_out) {
+  __shared__ int64_t s_off_all[SEG_WARPS][33];
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  int64_t* O = s_off_all[wid];
+  const float* sigma = reinterpret_cast<const float*>(sr);
+  const int64_t n_groups = ceil_div(n_segs, 32);
+  auto mul = [](double a, double b) { return a * b; };
+  auto up = [](double a, int o) { return __shfl_up_sync(0xffffffffu, a, o); };
+  for (int64_t grp = (int64_t)blockIdx.x * SEG_WARPS + wid; grp < n_groups;
+       grp += (int64_t)gridDim.x * SEG_WARPS) {
+    const int64_t seg0 = grp * 32;
+    const int nseg = (int)min((int64_t)32, n_segs - seg0);
+    __syncwarp();
+    stage_offsets(off, seg0, nseg, lane, O);
+    const int64_t s_beg = O[0], s_end = O[nseg];
+    if (lane < nseg && O[lane] == O[lane + 1]) T_out[seg0 + lane] = 1.f;
+    double carry = 1.0;
+    for (int64_t base = s_beg; base < s_end; base += 32 * K4_LANE) {
+      const LaneSpan sp = lane_span<K4_LANE>(O, nseg, base, s_end, lane);
+      double a[K4_LANE], b[K4_LANE];
+      float sg[K4_LANE];
+#pragma unroll
+      for (int k = 0; k < K4_LANE; ++k) {
+        a[k] = k < sp.cnt ? __ldcs(t0 + sp.s0 + k) : 0.0;
+        b[k] = k < sp.cnt ? __ldcs(t1 + sp.s0 + k) : 0.0;
+        sg[k] = k < sp.cnt ? __ldcs(sigma + 4 * (sp.s0 + k)) : 0.f;
+      }
+      double head = 1.0, cur = 1.0;
+      bool head_done = false;
+      int seg = sp.sf;
+#pragma unroll
+      for (int k = 0; k < K4_LANE; ++k) {
+        if (k < sp.cnt) {
+          const int64_t s = sp.s0 + k;
+          while (s >= O[seg + 1]) {
+            if (!head_done) {
+              head = cur;
+              head_done = true;
+            } else if (O[seg] < O[seg + 1]) {
+              T_out[seg0 + seg] = (float)cur;
+            }
+            ++seg;
+            cur = 1.0;
+          }
+          double keep, alpha;
+          keep_alpha((double)sg[k], b[k] - a[k], keep, alpha);
+          cur *= keep;
+        }
+      }
+      const bool closed = sp.cnt > 0 && O[seg + 1] == sp.s0 + sp.cnt;
+      const bool single = !head_done;
+      if (single) head = cur;
+      else if (closed) T_out[seg0 + seg] = (float)cur;
+      double e = cur;
+      bool f = !(single && sp.open_left);
+      if (sp.cnt == 0) {
+        e = 1.0;
+        f = false;
+      }
+      if (lane == 0 && sp.open_left && single) {
+        e = carry * e;
+        f = true;
+      }
+      const double S = lane_seg_scan(e, f, lane, mul, up);
+      double X = __shfl_up_sync(0xffffffffu, S, 1);
+      if (lane == 0) X = carry;
+      if (sp.cnt > 0 && (!single || closed))
+        T_out[seg0 + sp.sf] = (float)(sp.open_left ? X * head : head);
+      carry = __shfl_sync(0xffffffffu, S, 31);
+    }
+  }
+}
+
+// Backward from the forward's float64 segment totals.  Per sample j of a segment with
+// packet adjoints (bT, bC, bA, bD, bL):
+//   v_j = bC.c_j + bA + bD m_j + bL g_j,  g_j = 2 (m_j a_<j - d_<j + d_>j - m_j a_>j)
+//   dL/ds_j = -bT T + T_{j+1} v_j - (V - sum_{i<=j} w_i v_i),  V = sum_i w_i v_i
+// Walk 1 folds the prefix state (T, A, D) per lane piece; a cross-lane scan gives each
+// lane's incoming prefix; walk 2 forms the per-sample terms and the lane pieces' sums of
+// w v; a second cross-lane scan gives their incoming sums; walk 3 writes the gradients.
+struct K4Seg {
+  float bC0, bC1, bC2, bA, bD, bL;
+  double te, A, Dt, V, bTT;
+};
+
+__global__ void __launch_bounds__(SEG_WARPS * 32, 2)
+    k_segment_bwd_ls(const double* __restrict__ t0, const double* __restrict__ t1,
+                     const float4* __restrict__ sr, const int64_t* __restrict__ off,
+                     const double* __restrict__ ray_te, int64_t n_rays, int64_t n_segs,
+                     const float4* __restrict__ dpk, const double* __restrict__ seg_tot,
+                     float4* __restrict__ dsr) {
+  __shared__ int64_t s_off_all[SEG_WARPS][33];
+  __shared__ K4Seg s_seg_all[SEG_WARPS][32];
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  int64_t* O = s_off_all[wid];
+  K4Seg* SG = s_seg_all[wid];
+  const int64_t n_groups = ceil_div(n_segs, 32);
+  auto add = [](double a, double b) { return a + b; };
+  auto up = [](double a, int o) { return __shfl_up_sync(0xffffffffu, a, o); };
+  for (int64_t grp = (int64_t)blockIdx.x * SEG_WARPS + wid; grp < n_groups;
+       grp += (int64_t)gridDim.x * SEG_WARPS) {
+    const int64_t seg0 = grp * 32;
+    const int nseg = (int)min((int64_t)32, n_segs - seg0);
+    __syncwarp();
+    stage_offsets(off, seg0, nseg, lane, O);
+    const int64_t s_beg = O[0], s_end = O[nseg];
+    if (s_beg == s_end) continue;
+    if (lane < nseg && O[lane] < O[lane + 1]) {
+      const int64_t my = seg0 + lane;
+      const float4 g0 = dpk[2 * my], g1 = dpk[2 * my + 1];
+      const double* st = seg_tot + SEG_TOT * my;
+      const double Tn = st[0], c0 = st[1], c1 = st[2], c2 = st[3], a = st[4], d = st[5],
+                   l = st[6];
+      K4Seg q;
+      q.bC0 = g0.y;
+      q.bC1 = g0.z;
+      q.bC2 = g0.w;
+      q.bA = g1.x;
+      q.bD = g1.y;
+      q.bL = g1.z;
+      q.te = ray_te[my % n_rays];
+      q.A = a;
+      q.Dt = d;
+      q.V = (double)g0.y * c0 + (double)g0.z * c1 + (double)g0.w * c2 + (double)g1.x * a +
+            (double)g1.y * d + 2.0 * (double)g1.z * l;
+      q.bTT = (double)g0.x * Tn;
+      SG[lane] = q;
+    }
+    __syncwarp();
+    Pre pcarry = pre_id();
+    double ucarry = 0.0;
+    K4In nxt;
+    {
+      const LaneSpan sp = lane_span<K4_LANE>(O, nseg, s_beg, s_end, lane);
+      k4_load(nxt, t0, t1, sr, sp.s0, sp.cnt);
+    }
+    for (int64_t base = s_beg; base < s_end; base += 32 * K4_LANE) {
+      const LaneSpan sp = lane_span<K4_LANE>(O, nseg, base, s_end, lane);
+      const K4In in = nxt;
+      {
+        const LaneSpan sn = lane_span<K4_LANE>(O, nseg, base + 32 * K4_LANE, s_end, lane);
+        k4_load(nxt, t0, t1, sr, sn.s0, sn.cnt);
+      }
+      double keep[K4_LANE], alpha[K4_LANE];
+      int sid[K4_LANE];
+      // walk 1: prefix state of the lane's pieces
+      Pre cur = pre_id();
+      int seg = sp.sf;
+#pragma unroll
+      for (int k = 0; k < K4_LANE; ++k) {
+        keep[k] = 1.0;
+        alpha[k] = 0.0;
+        sid[k] = seg;
+        if (k < sp.cnt) {
+          const int64_t s = sp.s0 + k;
+          while (s >= O[seg + 1]) {
+            ++seg;
+            cur = pre_id();
+          }
+          sid[k] = seg;
+          keep_alpha((double)in.v[k].x, in.b[k] - in.a[k], keep[k], alpha[k]);
+          const double m = sample_mid(in.a[k], in.b[k]) - SG[seg].te;
+          const double w = cur.T * alpha[k];
+          cur.A += w;
+          cur.D += w * m;
+          cur.T *= keep[k];
+        }
+      }
+      const bool single = seg == sp.sf;
+      Pre e = cur;
+      bool f = !(single && sp.open_left);
+      if (sp.cnt == 0) {
+        e = pre_id();
+        f = false;
+      }
+      if (lane == 0 && sp.open_left && single) {
+        e = pre_cat(pcarry, e);
+        f = true;
+      }
+      const Pre S = lane_seg_scan(e, f, lane, pre_cat, pre_shfl_up);
+      Pre X = pre_shfl_up(S, 1);
+      if (lane == 0) X = pcarry;
+      pcarry = pre_shfl(S, 31);
+      // walk 2: per-sample terms, lane-local running sums of w v per piece
+      double r[K4_LANE], ul[K4_LANE], wk[K4_LANE];
+      Pre q = sp.open_left ? X : pre_id();
+      double u = 0.0;
+#pragma unroll
+      for (int k = 0; k < K4_LANE; ++k) {
+        r[k] = ul[k] = wk[k] = 0.0;
+        if (k < sp.cnt) {
+          if (k > 0 && sid[k] != sid[k - 1]) {
+            q = pre_id();
+            u = 0.0;
+          }
+          const K4Seg& g = SG[sid[k]];
+          const double m = sample_mid(in.a[k], in.b[k]) - g.te;
+          const double w = q.T * alpha[k];
+          const double a_incl = q.A + w, d_incl = q.D + w * m;
+          const double gk = 2.0 * (m * q.A - q.D + (g.Dt - d_incl) - m * (g.A - a_incl));
+          const double v = (double)g.bC0 * in.v[k].y + (double)g.bC1 * in.v[k].z +
+                           (double)g.bC2 * in.v[k].w + (double)g.bA + (double)g.bD * m +
+                           (double)g.bL * gk;
+          const double Tn = q.T * keep[k];
+          u += w * v;
+          ul[k] = u;
+          r[k] = -g.bTT + Tn * v - g.V;
+          wk[k] = w;
+          q.T = Tn;
+          q.A = a_incl;
+          q.D = d_incl;
+        }
+      }
+      double eu = u;
+      bool fu = !(single && sp.open_left);
+      if (sp.cnt == 0) {
+        eu = 0.0;
+        fu = false;
+      }
+      if (lane == 0 && sp.open_left && single) {
+        eu = ucarry + eu;
+        fu = true;
+      }
+      const double SU = lane_seg_scan(eu, fu, lane, add, up);
+      double XU = __shfl_up_sync(0xffffffffu, SU, 1);
+      if (lane == 0) XU = ucarry;
+      ucarry = __shfl_sync(0xffffffffu, SU, 31);
+      // walk 3: dL/dsigma_j = delta_j dL/ds_j, dL/dc_j = w_j bC
+#pragma unroll
+      for (int k = 0; k < K4_LANE; ++k) {
+        if (k < sp.cnt) {
+          const bool in_head = sid[k] == sp.sf && sp.open_left;
+          const double ds = r[k] + (in_head ? XU : 0.0) + ul[k];
+          const K4Seg& g = SG[sid[k]];
+          const double dlt = in.b[k] - in.a[k];
+          __stcs(dsr + sp.s0 + k, make_float4((float)(ds * dlt), (float)(wk[k] * g.bC0),
+                                             (float)(wk[k] * g.bC1), (float)(wk[k] * g.bC2)));
+        }
+      }
+    }
+  }
+}
+
+// K4 kernels: lane-serial walks (default) or the per-sample grouped scans (VR_K4_WALK=grp,
+// kept for A/B measurement and as the backward without forward totals)
+static bool k4_lane_serial() {
+  static const bool ls = [] {
+    const char* e = getenv("VR_K4_WALK");
+    return !(e && strcmp(e, "grp") == 0);
+  }();
+  return ls;
+}
+
 }  // namespace vr
 
 using namespace vr;
@@ -549,10 +949,16 @@ extern "C" int vr_segment_fwd(const double* t0, const double* t1, const float* s
   }
   const int64_t n_segs = n_rays * region_cnt;
   if (n_segs == 0) return VR_OK;
-  k_segment_fwd_grp<<<grid_for(ceil_div(n_segs, 32 * SEG_WARPS), 1, 8), SEG_WARPS * 32, 0,
-                      (cudaStream_t)stream>>>(t0, t1, reinterpret_cast<const float4*>(sr), off,
-                                              seg_first, ray_te, n_rays, n_segs,
-                                              reinterpret_cast<float4*>(packets), seg_totals);
+  if (k4_lane_serial())
+    k_segment_fwd_ls<<<grid_for(ceil_div(n_segs, 32 * SEG_WARPS), 1, 8), SEG_WARPS * 32, 0,
+                       (cudaStream_t)stream>>>(t0, t1, reinterpret_cast<const float4*>(sr), off,
+                                               seg_first, ray_te, n_rays, n_segs,
+                                               reinterpret_cast<float4*>(packets), seg_totals);
+  else
+    k_segment_fwd_grp<<<grid_for(ceil_div(n_segs, 32 * SEG_WARPS), 1, 8), SEG_WARPS * 32, 0,
+                        (cudaStream_t)stream>>>(t0, t1, reinterpret_cast<const float4*>(sr), off,
+                                                seg_first, ray_te, n_rays, n_segs,
+                                                reinterpret_cast<float4*>(packets), seg_totals);
   return check_launch("vr_segment_fwd");
 }
 
@@ -565,9 +971,14 @@ extern "C" int vr_segment_transmittance(const double* t0, const double* t1, cons
   }
   const int64_t n_segs = n_rays * region_cnt;
   if (n_segs == 0) return VR_OK;
-  k_segment_T_grp<<<grid_for(ceil_div(n_segs, 32 * SEG_WARPS), 1, 8), SEG_WARPS * 32, 0,
-                    (cudaStream_t)stream>>>(t0, t1, reinterpret_cast<const float4*>(sr), off,
-                                            n_segs, T_out);
+  if (k4_lane_serial())
+    k_segment_T_ls<<<grid_for(ceil_div(n_segs, 32 * SEG_WARPS), 1, 8), SEG_WARPS * 32, 0,
+                     (cudaStream_t)stream>>>(t0, t1, reinterpret_cast<const float4*>(sr), off,
+                                             n_segs, T_out);
+  else
+    k_segment_T_grp<<<grid_for(ceil_div(n_segs, 32 * SEG_WARPS), 1, 8), SEG_WARPS * 32, 0,
+                      (cudaStream_t)stream>>>(t0, t1, reinterpret_cast<const float4*>(sr), off,
+                                              n_segs, T_out);
   return check_launch("vr_segment_transmittance");
 }
 
@@ -581,11 +992,18 @@ extern "C" int vr_segment_bwd(const double* t0, const double* t1, const float* s
   }
   const int64_t n_segs = n_rays * region_cnt;
   if (n_segs == 0) return VR_OK;
-  k_segment_bwd_grp<<<grid_for(ceil_div(n_segs, 32 * SEG_WARPS), 1, 8), SEG_WARPS * 32, 0,
-                      (cudaStream_t)stream>>>(t0, t1, reinterpret_cast<const float4*>(sr), off,
-                                              ray_te, n_rays, n_segs,
-                                              reinterpret_cast<const float4*>(dpk), seg_totals,
-                                              reinterpret_cast<float4*>(dsr));
+  if (k4_lane_serial() && seg_totals)
+    k_segment_bwd_ls<<<grid_for(ceil_div(n_segs, 32 * SEG_WARPS), 1, 8), SEG_WARPS * 32, 0,
+                       (cudaStream_t)stream>>>(t0, t1, reinterpret_cast<const float4*>(sr), off,
+                                               ray_te, n_rays, n_segs,
+                                               reinterpret_cast<const float4*>(dpk), seg_totals,
+                                               reinterpret_cast<float4*>(dsr));
+  else
+    k_segment_bwd_grp<<<grid_for(ceil_div(n_segs, 32 * SEG_WARPS), 1, 8), SEG_WARPS * 32, 0,
+                        (cudaStream_t)stream>>>(t0, t1, reinterpret_cast<const float4*>(sr), off,
+                                                ray_te, n_rays, n_segs,
+                                                reinterpret_cast<const float4*>(dpk), seg_totals,
+                                                reinterpret_cast<float4*>(dsr));
   return check_launch("vr_segment_bwd");
 }
 

@@ -1,0 +1,11 @@
+set -u
+mkdir -p gpurun_out
+timeout 900 python -m pytest tests/test_gpu_parity.py tests/test_gpu_hand_cases.py tests/test_gpu_fullsize.py tests/test_gpu_multirank.py tests/test_gpu_occupancy.py "tests/test_gpu_configs.py::test_c1_matches_oracle" -q -x -m gpu > gpurun_out/g5_tests.log 2>&1
+tail -15 gpurun_out/g5_tests.log
+for W in grp ls; do
+VR_K4_WALK=$W timeout 900 python bench.py --sub "" --no-cpu --no-e2e > gpurun_out/g5_bench_$W.log 2>&1
+tail -1 gpurun_out/g5_bench_$W.log | python -c "
+import json,sys; d=json.loads(sys.stdin.read()); print('$W', d['value'], d['ms_per_step'], d['loss'])
+for k,v in d['kernels'].items():
+  if 'segment' in k or 'interlevel' in k: print(k, round(v['ms_per_step'],2))"
+done
