@@ -127,11 +127,17 @@ __device__ __forceinline__ void put8(uint8_t* tile, int r, int cb, const float* 
   for (int j = 0; j < 4; ++j) h[j] = __floats2half2_rn(v[2 * j], v[2 * j + 1]);
   *reinterpret_cast<uint4*>(tile + tile_off(TILE, r, cb * 8)) = q;
 }
+// ReLU on the packed fp16 pair: fp16(max(x, 0)) == max(fp16(x), 0) (rounding is monotonic
+// and keeps the sign; a negative x may give -0, equal to +0 everywhere downstream — the
+// backward's ReLU mask tests the magnitude bits), one HMNMX2 per pair instead of two FMNMX
+__device__ __forceinline__ __half2 relu_h2(float a, float b) {
+  return __hmax2(__floats2half2_rn(a, b), __float2half2_rn(0.f));
+}
 __device__ __forceinline__ void put_relu8(uint8_t* tile, int r, int cb, const float* v) {
   uint4 q;
   __half2* h = reinterpret_cast<__half2*>(&q);
 #pragma unroll
-  for (int j = 0; j < 4; ++j) h[j] = __floats2half2_rn(fmaxf(v[2 * j], 0.f), fmaxf(v[2 * j + 1], 0.f));
+  for (int j = 0; j < 4; ++j) h[j] = relu_h2(v[2 * j], v[2 * j + 1]);
   *reinterpret_cast<uint4*>(tile + tile_off(TILE, r, cb * 8)) = q;
 }
 // g[j] = v[j] if the (post-relu, fp16) activation of column block cb is non-zero
@@ -380,7 +386,7 @@ __device__ __forceinline__ void epi_relu64(uint32_t tm_row, uint32_t dst) {
     tmem_ld16(tm_row + TF_D + c, v);
 #pragma unroll
     for (int j = 0; j < 8; ++j)
-      q[j] = h2bits(__floats2half2_rn(fmaxf(v[2 * j], 0.f), fmaxf(v[2 * j + 1], 0.f)));
+      q[j] = h2bits(relu_h2(v[2 * j], v[2 * j + 1]));
     tmem_st8(tm_row + dst + c / 2, q);
   }
 }
