@@ -555,9 +555,9 @@ __device__ __forceinline__ void k4_load(K4In& in, const double* __restrict__ t0,
 #pragma unroll
   for (int k = 0; k < K4_LANE; ++k) {
     if (k < cnt) {
-      in.a[k] = __ldcs(t0 + s0 + k);
-      in.b[k] = __ldcs(t1 + s0 + k);
-      in.v[k] = __ldcs(sr + s0 + k);
+      in.a[k] = __ldg(t0 + s0 + k);
+      in.b[k] = __ldg(t1 + s0 + k);
+      in.v[k] = __ldg(sr + s0 + k);
     } else {
       in.a[k] = in.b[k] = 0.0;
       in.v[k] = make_float4(0.f, 0.f, 0.f, 0.f);
@@ -704,9 +704,9 @@ __global__ void __launch_bounds__(SEG_WARPS * 32)
       float sg[K4_LANE];
 #pragma unroll
       for (int k = 0; k < K4_LANE; ++k) {
-        a[k] = k < sp.cnt ? __ldcs(t0 + sp.s0 + k) : 0.0;
-        b[k] = k < sp.cnt ? __ldcs(t1 + sp.s0 + k) : 0.0;
-        sg[k] = k < sp.cnt ? __ldcs(sigma + 4 * (sp.s0 + k)) : 0.f;
+        a[k] = k < sp.cnt ? __ldg(t0 + sp.s0 + k) : 0.0;
+        b[k] = k < sp.cnt ? __ldg(t1 + sp.s0 + k) : 0.0;
+        sg[k] = k < sp.cnt ? __ldg(sigma + 4 * (sp.s0 + k)) : 0.f;
       }
       double head = 1.0, cur = 1.0;
       bool head_done = false;

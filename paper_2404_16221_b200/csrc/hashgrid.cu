@@ -185,7 +185,8 @@ __global__ void __launch_bounds__(HASH_THREADS)
     for (int64_t s0 = c0 + warp * 16; s0 < c1; s0 += n_warps * 16) {
       const int64_t j = s0 + (lane >> 1);
       if (j >= c1) continue;  // no shuffles below: lanes may leave independently
-      const int64_t i = rows ? (int64_t)__ldg(rows + j) : j;
+      int64_t i = rows ? (int64_t)__ldg(rows + j) : j;
+      if (!VR_CHECK(i >= 0 && i < n)) i = 0;
       const float u[3] = {__ldcs(pos + i), __ldcs(pos + n + i), __ldcs(pos + 2 * n + i)};
       for (int l = l0; l < l1; ++l) {
         const float2 d = __ldcs(denc + (int64_t)l * n + j);

@@ -680,9 +680,13 @@ __global__ void __launch_bounds__(TILE * BWD_TPR, BwdLayout<DENS>::CTAS)
   // Active rows: with a row list (vr_active_rows) the tiles are cut from rows[0, m) — the
   // samples whose upstream gradient is non-zero — instead of [0, n); compact position j
   // stands for sample rows[j], and d(enc) is written at compact position j.
-  const int64_t m = rows ? (int64_t)__ldg(n_rows) : n;
-  const int64_t n_tiles = ceil_div(m, TILE);
-  auto sample_of = [&](int64_t j) -> int64_t { return rows ? (int64_t)__ldg(rows + j) : j; };
+  const int64_t n_act = rows ? (int64_t)__ldg(n_rows) : n;
+  const int64_t n_tiles = ceil_div(n_act, TILE);
+  auto sample_of = [&](int64_t j) -> int64_t {
+    if (!rows) return j;
+    const int64_t i = __ldg(rows + j);
+    return VR_CHECK(i >= 0 && i < n) ? i : 0;  // (checked build: a bad row list entry)
+  };
   // Gradient scale of this CTA (a power of two, so exact both ways): the fp16 hi + lo
   // split of G keeps 22 significant bits only while lo = G - fp16(G) is an fp16 normal,
   // i.e. |G| >= 2^-3; below that lo's absolute precision is 2^-24 (measured: d(enc) at
@@ -700,7 +704,7 @@ __global__ void __launch_bounds__(TILE * BWD_TPR, BwdLayout<DENS>::CTAS)
     for (int64_t tile = blockIdx.x + (int64_t)part * gridDim.x; tile < n_tiles;
          tile += 2 * (int64_t)gridDim.x) {
       const int64_t j = tile * TILE + r;
-      if (j < m) {
+      if (j < n_act) {
         const int64_t i = sample_of(j);
         const float4 g4 = __ldg(dsr + i);
         const float a = fabsf(g4.x * __ldg(&sig[i].x));
@@ -804,7 +808,7 @@ __global__ void __launch_bounds__(TILE * BWD_TPR, BwdLayout<DENS>::CTAS)
   // (rid_a), and the sample index that depends on (a row list) one tile earlier still
   auto index_of = [&](int64_t tile) -> int64_t {
     const int64_t j = tile * TILE + r;
-    return (tile < n_tiles && j < m) ? sample_of(j) : -1;
+    return (tile < n_tiles && j < n_act) ? sample_of(j) : -1;
   };
   auto load_rid = [&](int64_t i) -> int32_t { return (!DENS && i >= 0) ? __ldg(rid + i) : 0; };
   const int64_t G1 = gridDim.x;
@@ -820,7 +824,7 @@ __global__ void __launch_bounds__(TILE * BWD_TPR, BwdLayout<DENS>::CTAS)
   }
   for (int64_t tile = blockIdx.x; tile < n_tiles; tile += G1) {
     const int64_t jrow = tile * TILE + r;  // compact position (== the sample without a list)
-    const bool valid = jrow < m;
+    const bool valid = jrow < n_act;
     const RowIn cur = nxt;
     if (tile + G1 < n_tiles) {  // prefetch the next tile's inputs (loads only)
       fetch_row<FUSED, DENS>(nxt, enc, rays, stride, rid_a, dsr, n, i_a, i_a >= 0, part, hg, t0,

@@ -1,0 +1,10 @@
+set -u
+mkdir -p gpurun_out
+timeout 1500 python -m pytest tests -q -m gpu > gpurun_out/g12_tests.log 2>&1
+tail -3 gpurun_out/g12_tests.log
+timeout 300 python __graft_entry__.py --smoke 2>&1 | tail -1
+timeout 900 python bench.py > gpurun_out/g12_bench.log 2>&1
+tail -1 gpurun_out/g12_bench.log | python -c "
+import json,sys; d=json.loads(sys.stdin.read()); print(d['value'], d['ms_per_step'], d['step_ms_trend'], d['active_rows'], d['e2e']['value'], d['clocks'])
+print(json.dumps(d['roofline'])[:400])
+for k,v in d['sub_results'].items(): print(k, v['value'], v['ms_per_step'], v['e2e']['value'] if v.get('e2e') else None)"
