@@ -430,7 +430,11 @@ class VolumePool:
                            p["ray_te"], None, None, t0, t1, ray_id, bounds)
 
     # ---- fields -------------------------------------------------------------------------
-    def evaluate(self, rays: torch.Tensor, b: SampleBatch, fields=None) -> torch.Tensor:
+    def evaluate(self, rays: torch.Tensor, b: SampleBatch, fields=None,
+                 pos_from=None) -> torch.Tensor:
+        """Region fields' (sigma, rgb) of the batch's samples.  pos_from: fields evaluated
+        earlier in the step over the same samples (the NeRF fields, for the proposals): a
+        field whose normalisation box equals its partner's reads the partner's positions."""
         fields = self.fields if fields is None else fields
         base = self.region_lo - b.region_lo  # an all-region batch: skip the peers' regions
         # (an all-region batch leaves the peers' rows zero until the exchange fills them)
@@ -448,7 +452,9 @@ class VolumePool:
             for kk, f in enumerate(fields):
                 lo, hi = b.region_slice(base + kk)
                 if hi > lo:
-                    f.forward(rays, b.t0[lo:], b.t1[lo:], b.ray_id[lo:], hi - lo, sig_rgb[lo:], s)
+                    pos = self._shared_positions(f, pos_from[kk], hi - lo) if pos_from else None
+                    f.forward(rays, b.t0[lo:], b.t1[lo:], b.ray_id[lo:], hi - lo, sig_rgb[lo:], s,
+                              **({"pos": pos} if pos is not None else {}))
             return sig_rgb
         # two-stream pipeline over regions: gathers of region k+1 (L2-bound) run while the
         # tensor-core MLP of region k runs on the side stream
@@ -467,6 +473,16 @@ class VolumePool:
                 f.forward_mlp(rays, b.ray_id[lo:], hi - lo, sig_rgb[lo:], _lib.stream_ptr())
         main.wait_stream(side)
         return sig_rgb
+
+    @staticmethod
+    def _shared_positions(f, partner, n):
+        """partner's positions of this step's n samples if f normalises by the same box."""
+        if not (hasattr(f, "positions") and hasattr(partner, "positions")):
+            return None
+        if not (np.array_equal(f.box.mn, partner.box.mn)
+                and np.array_equal(f.box.mx, partner.box.mx)):
+            return None
+        return partner.positions(n)
 
     # side-stream scatter grid: 0 = the kernel's full grid (measured best: 148 or 296 co-
     # resident 128-thread blocks left the scatter far below the L2 atomic rate)
@@ -731,7 +747,9 @@ class VolumePool:
         interlevel = self.proposals is not None and lambda_interlevel > 0.0
         prop_T = None
         if interlevel:
-            sig_prop = self.evaluate(rays, b, self.proposals)
+            # the proposal of a region shares its NeRF field's box: its gathers read the
+            # positions the NeRF forward kept
+            sig_prop = self.evaluate(rays, b, self.proposals, pos_from=self.fields)
             # only the proposal transmittance of each segment crosses the link
             prop_T = torch.empty((b.region_cnt, b.n_rays), dtype=torch.float32,
                                  device=self.device)

@@ -339,9 +339,15 @@ class HashGridMLP(RegionField):
         return self._enc
 
     def _pos_buf(self, n, dev):
-        if self._pos is None or self._pos.numel() < 3 * n:
+        if (self._pos is None or self._pos.numel() < 3 * n
+                or getattr(self, "_pos_shared", False)):
             self._pos = torch.empty(3 * max(n, 1), dtype=torch.float32, device=dev)
+        self._pos_shared = False
         return self._pos
+
+    def positions(self, n):
+        """This step's normalised positions [3][n] (written by the forward), or None."""
+        return self._pos if getattr(self, "_pos_n", -1) == n and self._pos is not None else None
 
     def _workspace(self, dev):
         if self._hash_ws is None:
@@ -349,11 +355,19 @@ class HashGridMLP(RegionField):
             self._hash_ws = torch.zeros(max(nbytes, 16), dtype=torch.uint8, device=dev)
         return self._hash_ws
 
-    def forward(self, rays, t0, t1, ray_id, n, sig_rgb, stream):
+    def forward(self, rays, t0, t1, ray_id, n, sig_rgb, stream, pos=None):
+        """pos: the same samples' normalised positions [3][n] of a field with the same
+        normalisation box (the region's NeRF field for its proposal): the gathers read them
+        instead of recomputing them from the rays (no second position pass, no ray loads)."""
         if n == 0:
+            return
+        if pos is not None:
+            self.forward_hash(rays, t0, t1, ray_id, n, stream, pos=pos)
+            self.forward_mlp(rays, ray_id, n, sig_rgb, stream)
             return
         enc = self._enc_buf(n, rays.device)
         if self.mlp_impl == "fused_fwd":  # K2 + K3 in one tensor-core kernel
+            self._pos_n = -1  # (no positions kept: the backward recomputes them)
             _lib.call("vr_field_fwd_tc", _lib.addr(self.desc), _lib.ptr(self.table),
                       _lib.ptr(self.weights16), _lib.ptr(rays), rays.shape[1], _lib.ptr(t0),
                       _lib.ptr(t1), _lib.ptr(ray_id), n, _lib.ptr(enc), _lib.ptr(sig_rgb),
@@ -368,10 +382,16 @@ class HashGridMLP(RegionField):
     # region k+1's gathers on a second stream (L2-bound gathers || tensor-core MLP)
     splittable = property(lambda self: self.mlp_impl != "fused_fwd")
 
-    def forward_hash(self, rays, t0, t1, ray_id, n, stream):
+    def forward_hash(self, rays, t0, t1, ray_id, n, stream, pos=None):
         if n == 0:
             return
         enc = self._enc_buf(n, rays.device)
+        if pos is not None:  # shared positions: one pass of level-grouped gathers from them
+            self._pos, self._pos_shared, self._pos_n = pos, True, n
+            _lib.call("vr_hash_fwd_lm", _lib.addr(self.desc), _lib.ptr(self.table),
+                      _lib.ptr(pos), n, _lib.ptr(enc), stream)
+            return
+        self._pos_n = n
         if self.hash_order == "level":
             self._pos_buf(n, rays.device)
             _lib.call("vr_hash_positions", _lib.addr(self.desc), _lib.ptr(rays), rays.shape[1],
