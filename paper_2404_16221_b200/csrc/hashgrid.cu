@@ -122,6 +122,7 @@ struct LmPasses {
 };
 
 constexpr int64_t LM_CHUNK = 4096;  // samples per work item
+constexpr int SU = 4;               // scatter: warp steps (16 samples each) per iteration
 
 // the block's next work item (block-uniform); item = pass * chunks + chunk
 __device__ __forceinline__ int64_t lm_claim(unsigned long long* ctr) {
@@ -182,15 +183,43 @@ __global__ void __launch_bounds__(HASH_THREADS)
     const int pass = (int)(item / chunks);
     const int l0 = passes.first[pass], l1 = passes.first[pass + 1];
     const int64_t c0 = (item - pass * chunks) * LM_CHUNK, c1 = min(m, c0 + LM_CHUNK);
-    for (int64_t s0 = c0 + warp * 16; s0 < c1; s0 += n_warps * 16) {
-      const int64_t j = s0 + (lane >> 1);
-      if (j >= c1) continue;  // no shuffles below: lanes may leave independently
-      int64_t i = rows ? (int64_t)__ldg(rows + j) : j;
-      if (!VR_CHECK(i >= 0 && i < n)) i = 0;
-      const float u[3] = {__ldcs(pos + i), __ldcs(pos + n + i), __ldcs(pos + 2 * n + i)};
+    // SU warp steps of 16 samples per iteration, every load issued before the atomics that
+    // depend on it and the next level's d(enc) loaded while this level's atomics issue
+    // (ncu, c4 steady state: one step per iteration left 75 % of the warps' cycles waiting
+    // on the d(enc) / position loads — the scatter was latency-bound, not L2-atomic bound)
+    for (int64_t s0 = c0 + warp * 16 * SU; s0 < c1; s0 += n_warps * 16 * SU) {
+      int64_t jj[SU];
+      float u[SU][3];
+#pragma unroll
+      for (int k = 0; k < SU; ++k) {
+        jj[k] = s0 + 16 * k + (lane >> 1);
+        int64_t i = 0;
+        if (jj[k] < c1) {
+          i = rows ? (int64_t)__ldg(rows + jj[k]) : jj[k];
+          if (!VR_CHECK(i >= 0 && i < n)) i = 0;
+        }
+        u[k][0] = jj[k] < c1 ? __ldcs(pos + i) : 0.f;
+        u[k][1] = jj[k] < c1 ? __ldcs(pos + n + i) : 0.f;
+        u[k][2] = jj[k] < c1 ? __ldcs(pos + 2 * n + i) : 0.f;
+      }
+      float2 dc[SU];
+#pragma unroll
+      for (int k = 0; k < SU; ++k)
+        dc[k] = jj[k] < c1 ? __ldcs(denc + (int64_t)l0 * n + jj[k]) : make_float2(0.f, 0.f);
       for (int l = l0; l < l1; ++l) {
-        const float2 d = __ldcs(denc + (int64_t)l * n + j);
-        if (d.x != 0.f || d.y != 0.f) scatter_half(g, plan, l, u, d, p, gwarp, grad, ws);
+        float2 dn[SU];
+#pragma unroll
+        for (int k = 0; k < SU; ++k)
+          dn[k] = (l + 1 < l1 && jj[k] < c1) ? __ldcs(denc + (int64_t)(l + 1) * n + jj[k])
+                                             : make_float2(0.f, 0.f);
+#pragma unroll
+        for (int k = 0; k < SU; ++k)
+          if (dc[k].x != 0.f || dc[k].y != 0.f) {
+            const float uk[3] = {u[k][0], u[k][1], u[k][2]};
+            scatter_half(g, plan, l, uk, dc[k], p, gwarp, grad, ws);
+          }
+#pragma unroll
+        for (int k = 0; k < SU; ++k) dc[k] = dn[k];
       }
     }
   }
