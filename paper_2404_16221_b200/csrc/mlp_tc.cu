@@ -609,10 +609,16 @@ __device__ __forceinline__ void fetch_row(RowIn& x, const __half2* __restrict__ 
                                           const double* __restrict__ t1,
                                           const float* __restrict__ pos) {
   constexpr int LV = 16 / BWD_TPR;
+  // zero first, then predicated loads straight into the registers (a select between the
+  // loaded value and zero would wait for the load right here)
 #pragma unroll
-  for (int l = 0; l < LV; ++l)
-    x.enc[l] = valid ? enc[(int64_t)(part * LV + l) * n + i] : __floats2half2_rn(0.f, 0.f);
-  x.gin = (valid && part == 0) ? dsr[i] : make_float4(0.f, 0.f, 0.f, 0.f);
+  for (int l = 0; l < LV; ++l) x.enc[l] = __floats2half2_rn(0.f, 0.f);
+  x.gin = make_float4(0.f, 0.f, 0.f, 0.f);
+  if (valid) {
+#pragma unroll
+    for (int l = 0; l < LV; ++l) x.enc[l] = __ldg(enc + (int64_t)(part * LV + l) * n + i);
+    if (part == 0) x.gin = __ldg(dsr + i);
+  }
   x.d[0] = x.d[1] = x.d[2] = 0.0;
   x.u[0] = x.u[1] = x.u[2] = 0.f;
   if (valid && !DENS) {  // the density branch has no view direction
@@ -701,15 +707,29 @@ __global__ void __launch_bounds__(TILE * BWD_TPR, BwdLayout<DENS>::CTAS)
   if (sig) {
     uint32_t* wmax = reinterpret_cast<uint32_t*>(smem + LY::WMAX);
     float m = 0.f;
-    for (int64_t tile = blockIdx.x + (int64_t)part * gridDim.x; tile < n_tiles;
-         tile += 2 * (int64_t)gridDim.x) {
-      const int64_t j = tile * TILE + r;
-      if (j < n_act) {
-        const int64_t i = sample_of(j);
-        const float4 g4 = __ldg(dsr + i);
-        const float a = fabsf(g4.x * __ldg(&sig[i].x));
-        m = fmaxf(m, DENS ? a : fmaxf(a, 0.25f * fmaxf(fabsf(g4.y), fmaxf(fabsf(g4.z),
-                                                                          fabsf(g4.w)))));
+    // four of this thread's tiles per iteration, their loads independent (the row-list
+    // lookup and the two loads behind it were a serial latency chain per tile)
+    constexpr int PU = 4;
+    const int64_t tstep = 2 * (int64_t)gridDim.x;
+    for (int64_t t0_ = blockIdx.x + (int64_t)part * gridDim.x; t0_ < n_tiles; t0_ += PU * tstep) {
+      int64_t ii[PU];
+#pragma unroll
+      for (int k = 0; k < PU; ++k) {
+        const int64_t j = (t0_ + k * tstep) * TILE + r;
+        ii[k] = j < n_act ? sample_of(j) : -1;
+      }
+      float4 g4[PU];
+      float sg[PU];
+#pragma unroll
+      for (int k = 0; k < PU; ++k) {
+        g4[k] = ii[k] >= 0 ? __ldg(dsr + ii[k]) : make_float4(0.f, 0.f, 0.f, 0.f);
+        sg[k] = ii[k] >= 0 ? __ldg(&sig[ii[k]].x) : 0.f;
+      }
+#pragma unroll
+      for (int k = 0; k < PU; ++k) {
+        const float a = fabsf(g4[k].x * sg[k]);
+        m = fmaxf(m, DENS ? a : fmaxf(a, 0.25f * fmaxf(fabsf(g4[k].y),
+                                                       fmaxf(fabsf(g4[k].z), fabsf(g4[k].w)))));
       }
     }
     // non-negative floats order like their bit patterns (NaN above inf)
