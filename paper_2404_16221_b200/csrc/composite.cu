@@ -552,15 +552,19 @@ struct K4In {
 __device__ __forceinline__ void k4_load(K4In& in, const double* __restrict__ t0,
                                         const double* __restrict__ t1,
                                         const float4* __restrict__ sr, int64_t s0, int cnt) {
+  // zero, then predicated loads straight into the registers (no select that would wait
+  // for the loads here: they are consumed one chunk later)
+#pragma unroll
+  for (int k = 0; k < K4_LANE; ++k) {
+    in.a[k] = in.b[k] = 0.0;
+    in.v[k] = make_float4(0.f, 0.f, 0.f, 0.f);
+  }
 #pragma unroll
   for (int k = 0; k < K4_LANE; ++k) {
     if (k < cnt) {
       in.a[k] = __ldg(t0 + s0 + k);
       in.b[k] = __ldg(t1 + s0 + k);
       in.v[k] = __ldg(sr + s0 + k);
-    } else {
-      in.a[k] = in.b[k] = 0.0;
-      in.v[k] = make_float4(0.f, 0.f, 0.f, 0.f);
     }
   }
 }
@@ -601,13 +605,14 @@ __global__ void __launch_bounds__(SEG_WARPS * 32, 2)
   int64_t* O = s_off_all[wid];
   double* TE = s_te_all[wid];
   const int64_t n_groups = ceil_div(n_segs, 32);
+  const bool narrow = n_segs < INT32_MAX;
   for (int64_t grp = (int64_t)blockIdx.x * SEG_WARPS + wid; grp < n_groups;
        grp += (int64_t)gridDim.x * SEG_WARPS) {
     const int64_t seg0 = grp * 32;
     const int nseg = (int)min((int64_t)32, n_segs - seg0);
     __syncwarp();  // the previous group's readers are done with O / TE
     stage_offsets(off, seg0, nseg, lane, O);
-    TE[lane] = lane < nseg ? ray_te[(seg0 + lane) % n_rays] : 0.0;
+    TE[lane] = lane < nseg ? ray_te[seg_ray(seg0 + lane, n_rays, narrow)] : 0.0;
     __syncwarp();
     const int64_t s_beg = O[0], s_end = O[nseg];
     if (lane < nseg && O[lane] == O[lane + 1]) {  // empty segment: identity packet
@@ -689,12 +694,15 @@ __global__ void __launch_bounds__(SEG_WARPS * 32)
   const int64_t n_groups = ceil_div(n_segs, 32);
   auto mul = [](double a, double b) { return a * b; };
   auto up = [](double a, int o) { return __shfl_up_sync(0xffffffffu, a, o); };
-  for (int64_t grp = (int64_t)blockIdx.x * SEG_WARPS + wid; grp < n_groups;
-       grp += (int64_t)gridDim.x * SEG_WARPS) {
+  const int64_t gstep = (int64_t)gridDim.x * SEG_WARPS;
+  GroupPrefetch pf;
+  pf.load(off, (int64_t)blockIdx.x * SEG_WARPS + wid, n_groups, n_segs, lane);
+  for (int64_t grp = (int64_t)blockIdx.x * SEG_WARPS + wid; grp < n_groups; grp += gstep) {
     const int64_t seg0 = grp * 32;
     const int nseg = (int)min((int64_t)32, n_segs - seg0);
     __syncwarp();
-    stage_offsets(off, seg0, nseg, lane, O);
+    pf.stage(O, lane);
+    pf.load(off, grp + gstep, n_groups, n_segs, lane);
     const int64_t s_beg = O[0], s_end = O[nseg];
     if (lane < nseg && O[lane] == O[lane + 1]) T_out[seg0 + lane] = 1.f;
     double carry = 1.0;
@@ -704,9 +712,16 @@ __global__ void __launch_bounds__(SEG_WARPS * 32)
       float sg[K4_LANE];
 #pragma unroll
       for (int k = 0; k < K4_LANE; ++k) {
-        a[k] = k < sp.cnt ? __ldg(t0 + sp.s0 + k) : 0.0;
-        b[k] = k < sp.cnt ? __ldg(t1 + sp.s0 + k) : 0.0;
-        sg[k] = k < sp.cnt ? __ldg(sigma + 4 * (sp.s0 + k)) : 0.f;
+        a[k] = b[k] = 0.0;
+        sg[k] = 0.f;
+      }
+#pragma unroll
+      for (int k = 0; k < K4_LANE; ++k) {
+        if (k < sp.cnt) {
+          a[k] = __ldg(t0 + sp.s0 + k);
+          b[k] = __ldg(t1 + sp.s0 + k);
+          sg[k] = __ldg(sigma + 4 * (sp.s0 + k));
+        }
       }
       double head = 1.0, cur = 1.0;
       bool head_done = false;
@@ -780,6 +795,7 @@ __global__ void __launch_bounds__(SEG_WARPS * 32, 2)
   const int64_t n_groups = ceil_div(n_segs, 32);
   auto add = [](double a, double b) { return a + b; };
   auto up = [](double a, int o) { return __shfl_up_sync(0xffffffffu, a, o); };
+  const bool narrow = n_segs < INT32_MAX;
   for (int64_t grp = (int64_t)blockIdx.x * SEG_WARPS + wid; grp < n_groups;
        grp += (int64_t)gridDim.x * SEG_WARPS) {
     const int64_t seg0 = grp * 32;
@@ -801,7 +817,7 @@ __global__ void __launch_bounds__(SEG_WARPS * 32, 2)
       q.bA = g1.x;
       q.bD = g1.y;
       q.bL = g1.z;
-      q.te = ray_te[my % n_rays];
+      q.te = ray_te[seg_ray(my, n_rays, narrow)];
       q.A = a;
       q.Dt = d;
       q.V = (double)g0.y * c0 + (double)g0.z * c1 + (double)g0.w * c2 + (double)g1.x * a +

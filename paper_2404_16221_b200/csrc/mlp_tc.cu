@@ -506,15 +506,30 @@ __global__ void __launch_bounds__(TILE * FWD_TPR, 4)
   uint32_t qn[16];
   double dn[3] = {0.0, 0.0, 0.0};
   int32_t rid_ahead = 0;
-  auto load_rid = [&](int64_t tile) -> int32_t {
+  auto load_rid = [&](int64_t tile) -> int32_t {  // predicated load, no select (see bwd)
     const int64_t i = tile * TILE + r;
-    return (!DENS && tile < n_tiles && i < n) ? __ldg(rid + i) : 0;
+    int32_t v = 0;
+    if (!DENS && tile < n_tiles && i < n) v = __ldg(rid + i);
+    return v;
   };
   auto prefetch = [&](int64_t tile, int32_t ray) {
     const int64_t i = tile * TILE + r;
     const bool ok = tile < n_tiles && i < n;
+    // colour MLP: zero, then predicated loads into the registers (a select between the
+    // load and zero would wait for the load here instead of at the next tile: 10.7 -> 10.1
+    // ms at c4); the 2-round density MLP is faster with the select form (4.8 vs 5.9 ms)
+    if (DENS) {
 #pragma unroll
-    for (int l = 0; l < 16; ++l) qn[l] = ok ? h2bits(enc[(int64_t)l * n + i]) : 0u;
+      for (int l = 0; l < 16; ++l) qn[l] = ok ? h2bits(enc[(int64_t)l * n + i]) : 0u;
+    } else {
+#pragma unroll
+      for (int l = 0; l < 16; ++l) qn[l] = 0u;
+      if (ok) {
+        const uint32_t* e32 = reinterpret_cast<const uint32_t*>(enc);
+#pragma unroll
+        for (int l = 0; l < 16; ++l) qn[l] = __ldg(e32 + (int64_t)l * n + i);
+      }
+    }
     if (!DENS && ok) {
       const int64_t rr = checked_ray(ray, stride);
 #pragma unroll
@@ -688,7 +703,7 @@ __global__ void __launch_bounds__(TILE * BWD_TPR, BwdLayout<DENS>::CTAS)
   // stands for sample rows[j], and d(enc) is written at compact position j.
   const int64_t n_act = rows ? (int64_t)__ldg(n_rows) : n;
   const int64_t n_tiles = ceil_div(n_act, TILE);
-  auto sample_of = [&](int64_t j) -> int64_t {
+  auto sample_of = [&](int64_t j) -> int64_t {  // the gradient-scale pre-pass
     if (!rows) return j;
     const int64_t i = __ldg(rows + j);
     return VR_CHECK(i >= 0 && i < n) ? i : 0;  // (checked build: a bad row list entry)
@@ -826,16 +841,27 @@ __global__ void __launch_bounds__(TILE * BWD_TPR, BwdLayout<DENS>::CTAS)
   RowIn nxt;
   // inputs are prefetched one tile ahead; the ray index they depend on one tile earlier
   // (rid_a), and the sample index that depends on (a row list) one tile earlier still
-  auto index_of = [&](int64_t tile) -> int64_t {
+  // Both lookups are predicated loads into a pre-set int32 register (no select and no
+  // widening right after the load, which would wait for it at the issue point — ncu showed
+  // the row-list load as the top stall of the sparse backward before); the values are
+  // consumed a tile later.
+  auto index_of = [&](int64_t tile) -> int32_t {
     const int64_t j = tile * TILE + r;
-    return (tile < n_tiles && j < n_act) ? sample_of(j) : -1;
+    int32_t v = -1;
+    if (tile < n_tiles && j < n_act) v = rows ? __ldg(rows + j) : (int32_t)j;
+    if (rows && !VR_CHECK(v < n)) v = 0;  // (checked build only: a bad row-list entry)
+    return v;
   };
-  auto load_rid = [&](int64_t i) -> int32_t { return (!DENS && i >= 0) ? __ldg(rid + i) : 0; };
+  auto load_rid = [&](int32_t i) -> int32_t {
+    int32_t v = 0;
+    if (!DENS && i >= 0) v = __ldg(rid + i);
+    return v;
+  };
   const int64_t G1 = gridDim.x;
-  int64_t i_a = -1, i_b = -1;  // sample index of this row in the next tile / the one after
+  int32_t i_a = -1, i_b = -1;  // sample index of this row in the next tile / the one after
   int32_t rid_a = 0;           // ray index of this row in the next tile
   if ((int64_t)blockIdx.x < n_tiles) {
-    const int64_t i0 = index_of(blockIdx.x);
+    const int32_t i0 = index_of(blockIdx.x);
     fetch_row<FUSED, DENS>(nxt, enc, rays, stride, load_rid(i0), dsr, n, i0, i0 >= 0, part, hg,
                            t0, t1, pos);
     i_a = index_of(blockIdx.x + G1);

@@ -37,6 +37,38 @@ __device__ __forceinline__ void stage_offsets(const int64_t* __restrict__ off, i
   __syncwarp();
 }
 
+// The next group's offsets, loaded into registers while the current group is walked (a
+// group costs two dependent memory round trips — offsets, then its first chunk): used by
+// the T-only walk (2.32 -> 2.27 ms at c4); the forward / backward walks, at 128 registers,
+// spilled with it and got slower (5.7 -> 7.0 / 5.6 -> 5.8 ms).
+// GroupPrefetch::load(g) issues the loads, stage() stores them for the walk.
+struct GroupPrefetch {
+  int64_t o, o32;
+  int64_t seg0;
+  int nseg;
+  __device__ __forceinline__ void load(const int64_t* __restrict__ off, int64_t grp,
+                                       int64_t n_groups, int64_t n_segs, int lane) {
+    seg0 = grp * 32;
+    nseg = grp < n_groups ? (int)min((int64_t)32, n_segs - seg0) : 0;
+    o = o32 = 0;
+    if (grp < n_groups) {
+      o = __ldg(off + seg0 + min(lane, nseg));
+      if (lane == 0) o32 = __ldg(off + seg0 + nseg);
+    }
+  }
+  __device__ __forceinline__ void stage(int64_t* s_off, int lane) const {
+    s_off[lane] = o;
+    if (lane == 0) s_off[32] = o32;
+    __syncwarp();
+  }
+};
+
+// ray index of segment seg (segments are region-major, kk * n_rays + r); 32-bit when the
+// batch allows (a 64-bit modulo costs ~100 instructions)
+__device__ __forceinline__ int64_t seg_ray(int64_t seg, int64_t n_rays, bool narrow) {
+  return narrow ? (int64_t)((uint32_t)seg % (uint32_t)n_rays) : seg % n_rays;
+}
+
 // The lane's span of a chunk: samples [s0, s0 + cnt), the segment of s0 and whether that
 // segment started before s0 (its earlier part belongs to previous lanes / chunks).
 struct LaneSpan {

@@ -30,7 +30,7 @@ scale = {"ns": 1e-9, "us": 1e-6, "usecond": 1e-6, "ms": 1e-3, "msecond": 1e-3, "
 for arg in sys.argv[3:]:
     kern, rest = arg.split("=", 1)
     entry, bound = rest.split(":", 1)
-    rep = ROOT / "gpurun_out" / f"r2_{cfg}" / f"{kern}.ncu-rep"
+    rep = Path(kern) if kern.endswith(".ncu-rep") else ROOT / "gpurun_out" / f"r2_{cfg}" / f"{kern}.ncu-rep"
     raw = subprocess.run(["ncu", "-i", str(rep), "--page", "raw", "--csv"], capture_output=True,
                          text=True).stdout
     rows = list(csv.reader(io.StringIO(raw)))
