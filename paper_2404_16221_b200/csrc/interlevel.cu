@@ -12,6 +12,8 @@
 // proposal gradient is local and there is no gradient collective.
 //   dL/dsh_j = Ph_s (Th_{j+1} e_j - sum_{i>j} wh_loc_i e_i),  e_i = dL/dwh_i
 //            = -2 lambda max(0, w_i - wh_i) / (w_i + eps)
+#include <stdlib.h>
+
 #include "common.cuh"
 #include "segscan.cuh"
 
@@ -117,7 +119,8 @@ __device__ __forceinline__ IlChunk il_chunk(const IlIn& in, int64_t s, int64_t s
   return c;
 }
 
-__global__ void __launch_bounds__(IL_WARPS * 32)
+template <int MINB>
+__global__ void __launch_bounds__(IL_WARPS * 32, MINB)
     k_interlevel(const double* __restrict__ t0, const double* __restrict__ t1,
                  const float4* __restrict__ sr, const float4* __restrict__ sp,
                  const int64_t* __restrict__ off, const float2* __restrict__ prefix,
@@ -231,10 +234,14 @@ extern "C" int vr_interlevel(const double* t0, const double* t1, const float* si
   }
   const int64_t n_segs = n_rays * region_cnt;
   if (n_segs == 0) return VR_OK;
-  k_interlevel<<<grid_for(ceil_div(n_segs, 32 * IL_WARPS), 1, 8), IL_WARPS * 32, 0,
-                 (cudaStream_t)stream>>>(t0, t1, reinterpret_cast<const float4*>(sig_rgb),
-                                         reinterpret_cast<const float4*>(sig_prop), off,
-                                         reinterpret_cast<const float2*>(prefix), n_segs, lambda,
-                                         eps, seg_loss, reinterpret_cast<float4*>(dsig_prop));
+  static const int minb = [] {
+    const char* e = getenv("VR_IL_MINB");
+    return e ? atoi(e) : 1;
+  }();
+  auto k = minb >= 4 ? k_interlevel<4> : minb == 3 ? k_interlevel<3> : k_interlevel<1>;
+  k<<<grid_for(ceil_div(n_segs, 32 * IL_WARPS), 1, 8), IL_WARPS * 32, 0, (cudaStream_t)stream>>>(
+      t0, t1, reinterpret_cast<const float4*>(sig_rgb), reinterpret_cast<const float4*>(sig_prop),
+      off, reinterpret_cast<const float2*>(prefix), n_segs, lambda, eps, seg_loss,
+      reinterpret_cast<float4*>(dsig_prop));
   return check_launch("vr_interlevel");
 }

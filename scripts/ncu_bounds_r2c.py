@@ -84,7 +84,7 @@ for name, (cfg, entry, (what, field), _) in SPEC.items():
           "l2_red_requests_per_sample": m.get("rq_red", 0) / units,
           "l2_requests_per_s": (m.get("rq_rd", 0) + m.get("rq_red", 0) + m.get("rq_wr", 0)) / t,
           "samples": int(units),
-          "source": f"profiles/r2/{name}.txt (ncu --set full, one launch at the bench's steady "
+          "source": f"profiles/r2/steady/{name}.txt (ncu --set full, one launch at the bench's steady "
                     f"state, {int(units)} {'active rows' if what == 'rows' else 'samples'})"}
     doc.setdefault(cfg, {})[entry] = ev
     print(name, entry, json.dumps({k: (round(v, 3) if isinstance(v, float) else v)

@@ -37,6 +37,7 @@ if [ $PART = A ]; then
 else
   $C4 > $OUT/plain_c4b.json 2> $OUT/plain_c4b.err || { echo "plain run failed"; exit 1; }
   cap c4_k_mlp_fwd_tc '^k_mlp_fwd_tc' 400 $C4
+  cap c4_k_mlp_bwd_tc_nerf '^k_mlp_bwd_tc' 400 $C4
   cap c4_k_segment_fwd_ls '^k_segment_fwd_ls' 25 $C4
   cap c4_k_segment_bwd_ls '^k_segment_bwd_ls' 25 $C4
   cap c4_k_interlevel '^k_interlevel' 25 $C4
