@@ -593,8 +593,7 @@ __device__ __forceinline__ void k4_emit(float4* __restrict__ packets, double* __
   }
 }
 
-template <int MINB>
-__global__ void __launch_bounds__(SEG_WARPS * 32, MINB)
+__global__ void __launch_bounds__(SEG_WARPS * 32, 2)  // (3 blocks: spills, 5.9 -> 8.2 ms)
     k_segment_fwd_ls(const double* __restrict__ t0, const double* __restrict__ t1,
                      const float4* __restrict__ sr, const int64_t* __restrict__ off,
                      const int32_t* __restrict__ seg_first, const double* __restrict__ ray_te,
@@ -782,8 +781,7 @@ struct K4Seg {
   double te, A, Dt, V, bTT;
 };
 
-template <int MINB>
-__global__ void __launch_bounds__(SEG_WARPS * 32, MINB)
+__global__ void __launch_bounds__(SEG_WARPS * 32, 2)
     k_segment_bwd_ls(const double* __restrict__ t0, const double* __restrict__ t1,
                      const float4* __restrict__ sr, const int64_t* __restrict__ off,
                      const double* __restrict__ ray_te, int64_t n_rays, int64_t n_segs,
@@ -944,13 +942,6 @@ __global__ void __launch_bounds__(SEG_WARPS * 32, MINB)
 
 // K4 kernels: lane-serial walks (default) or the per-sample grouped scans (VR_K4_WALK=grp,
 // kept for A/B measurement and as the backward without forward totals)
-static int k4_minb() {  // experiments: resident blocks the lane-serial walks are built for
-  static const int m = [] {
-    const char* e = getenv("VR_K4_MINB");
-    return e ? atoi(e) : 2;
-  }();
-  return m;
-}
 static bool k4_lane_serial() {
   static const bool ls = [] {
     const char* e = getenv("VR_K4_WALK");
@@ -975,7 +966,7 @@ extern "C" int vr_segment_fwd(const double* t0, const double* t1, const float* s
   const int64_t n_segs = n_rays * region_cnt;
   if (n_segs == 0) return VR_OK;
   if (k4_lane_serial())
-    (k4_minb() >= 3 ? k_segment_fwd_ls<3> : k_segment_fwd_ls<2>)<<<grid_for(ceil_div(n_segs, 32 * SEG_WARPS), 1, 8), SEG_WARPS * 32, 0,
+    k_segment_fwd_ls<<<grid_for(ceil_div(n_segs, 32 * SEG_WARPS), 1, 8), SEG_WARPS * 32, 0,
                        (cudaStream_t)stream>>>(t0, t1, reinterpret_cast<const float4*>(sr), off,
                                                seg_first, ray_te, n_rays, n_segs,
                                                reinterpret_cast<float4*>(packets), seg_totals);
@@ -1018,7 +1009,7 @@ extern "C" int vr_segment_bwd(const double* t0, const double* t1, const float* s
   const int64_t n_segs = n_rays * region_cnt;
   if (n_segs == 0) return VR_OK;
   if (k4_lane_serial() && seg_totals)
-    (k4_minb() >= 3 ? k_segment_bwd_ls<3> : k_segment_bwd_ls<2>)<<<grid_for(ceil_div(n_segs, 32 * SEG_WARPS), 1, 8), SEG_WARPS * 32, 0,
+    k_segment_bwd_ls<<<grid_for(ceil_div(n_segs, 32 * SEG_WARPS), 1, 8), SEG_WARPS * 32, 0,
                        (cudaStream_t)stream>>>(t0, t1, reinterpret_cast<const float4*>(sr), off,
                                                ray_te, n_rays, n_segs,
                                                reinterpret_cast<const float4*>(dpk), seg_totals,
