@@ -138,6 +138,9 @@ typedef struct VrHashGridDesc {
 
 /* ---- meta ------------------------------------------------------------------ */
 int vr_abi_version(void);
+/* 1 when tensor maps can be encoded (the driver's cuTensorMapEncodeTiled is reachable):
+ * the K4 walks then stage their inputs by TMA. */
+int vr_tma_available(void);
 /* sizes of the descriptor structs, for host-side layout checks: out[0..4] =
  * sizeof(VrTree), sizeof(VrAnalyticField), sizeof(VrVoxelDesc), sizeof(VrHashGridDesc),
  * sizeof(VrBlob). */
@@ -388,13 +391,18 @@ int vr_active_rows(const float* dsig_rgb_dev, int64_t n, int32_t* rows_dev, int3
 
 /* ---- K4: per-segment front-to-back composite (composite_samples quadrature.py:141-165,
  * aggregate_segment segrender.py:71-90, process_inbox distsim.py:318-329) ------------- */
-/* seg_totals_dev (optional, [region_cnt * n_rays][7] float64): each non-empty segment's
+/* n_samples: the number of samples in t0 / t1 / sig_rgb, or 0: with it the walk stages each
+ * chunk's inputs into shared memory by TMA (cp.async.bulk.tensor) — t0 and t1 must then be
+ * allocated with an even number (>= n_samples) of elements, 16-byte aligned, since the
+ * copies read 16-byte pairs; with 0 every lane loads its own samples.
+ * seg_totals_dev (optional, [region_cnt * n_rays][7] float64): each non-empty segment's
  * totals {T, C[3], A, D, L} before the float32 rounding of its packet, for
  * vr_segment_bwd (which otherwise recomputes them in a first sweep). */
 int vr_segment_fwd(const double* t0_dev, const double* t1_dev, const float* sig_rgb_dev,
                    const int64_t* offsets_dev, const int32_t* seg_first_dev,
                    const double* ray_te_dev, int64_t n_rays, int32_t region_cnt,
-                   float* packets_dev, double* seg_totals_dev, int32_t* err_dev, void* stream);
+                   float* packets_dev, double* seg_totals_dev, int32_t* err_dev,
+                   int64_t n_samples, void* stream);
 /* Sample-broadcast protocol (distsim.py:311-316, _compose_samples distsim.py:385-392):
  * move per-sample elements (4, 8 or 16 bytes) between the region-major K1 layout and a
  * ray-major layout (ray_off = exclusive scan of per-ray totals, a ray's segments in t

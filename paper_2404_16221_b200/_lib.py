@@ -113,6 +113,7 @@ F64 = C.c_double
 # name -> argtypes (restype is int unless listed in _RESTYPES)
 SIGNATURES = {
     "vr_abi_version": [],
+    "vr_tma_available": [],
     "vr_struct_sizes": [P],
     "vr_last_error": [],
     "vr_check_failures": [],
@@ -153,7 +154,7 @@ SIGNATURES = {
     "vr_field_bwd_tc": [P, P, P, P, I64, P, P, P, I64, P, P, P, P, P, C.c_size_t, P, P, P, P, P],
     "vr_active_rows_workspace_bytes": [I64],
     "vr_active_rows": [P, I64, P, P, P, C.c_size_t, P],
-    "vr_segment_fwd": [P, P, P, P, P, P, I64, I32, P, P, P, P],
+    "vr_segment_fwd": [P, P, P, P, P, P, I64, I32, P, P, P, I64, P],
     "vr_segment_bwd": [P, P, P, P, P, I64, I32, P, P, P, P],
     "vr_segment_transmittance": [P, P, P, P, I64, I32, P, P],
     "vr_segment_permute": [P, P, P, I64, I32, P, P, I32, I32, P],

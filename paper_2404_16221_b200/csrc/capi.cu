@@ -2,7 +2,10 @@
 #include <stdio.h>
 #include <string.h>
 
+#include <cudaTypedefs.h>
+
 #include "common.cuh"
+#include "tma.cuh"
 
 namespace vr {
 
@@ -44,7 +47,65 @@ int check_launch(const char* where) {
   return VR_OK;
 }
 
+namespace tma {
+
+static PFN_cuTensorMapEncodeTiled_v12000 encoder() {
+  static PFN_cuTensorMapEncodeTiled_v12000 fn = [] {
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) !=
+            cudaSuccess ||
+        q != cudaDriverEntryPointSuccess)
+      p = nullptr;
+    return reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(p);
+  }();
+  return fn;
+}
+
+bool encode_pairs(CUtensorMap* map, const double* base, uint64_t n, uint32_t box_pairs) {
+  auto fn = encoder();
+  if (!fn || !base || n == 0 || reinterpret_cast<uintptr_t>(base) % 16 != 0 || box_pairs > 256)
+    return false;
+  // 16-byte rows of two float64 (as four 32-bit words): a tile's innermost start must be
+  // 16-byte aligned (an odd 8-byte start raised "illegal instruction",
+  // scripts/micro/tma_min2.cu), so chunks start at the even sample at or below theirs
+  const cuuint64_t dims[2] = {4, (n + 1) / 2};  // (the caller's array holds 2 * that)
+  const cuuint64_t strides[1] = {16};
+  const cuuint32_t boxd[2] = {4, box_pairs};
+  const cuuint32_t es[2] = {1, 1};
+  return fn(map, CU_TENSOR_MAP_DATA_TYPE_UINT32, 2, const_cast<double*>(base), dims, strides,
+            boxd, es, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+            CU_TENSOR_MAP_L2_PROMOTION_L2_128B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
+bool encode_rows(CUtensorMap* map, const float* base, uint64_t n, uint32_t row, uint32_t box) {
+  auto fn = encoder();
+  if (!fn || !base || n == 0 || reinterpret_cast<uintptr_t>(base) % 16 != 0 ||
+      (row * 4) % 16 != 0)
+    return false;
+  const cuuint64_t dims[2] = {row, n};
+  const cuuint64_t strides[1] = {(cuuint64_t)row * 4};
+  const cuuint32_t boxd[2] = {row, box};
+  const cuuint32_t es[2] = {1, 1};
+  return fn(map, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, const_cast<float*>(base), dims, strides,
+            boxd, es, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+            CU_TENSOR_MAP_L2_PROMOTION_L2_128B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
+}  // namespace tma
+
 }  // namespace vr
+
+extern "C" int vr_tma_available(void) {
+  CUtensorMap m;
+  static double probe[32];
+  double* d = nullptr;
+  if (cudaMalloc(&d, 256) != cudaSuccess) return 0;
+  const bool ok = vr::tma::encode_pairs(&m, d, 32, 8);
+  cudaFree(d);
+  (void)probe;
+  return ok ? 1 : 0;
+}
 
 extern "C" int vr_abi_version(void) { return VR_ABI_VERSION; }
 

@@ -29,6 +29,7 @@
 #include "common.cuh"
 #include "segscan.cuh"  // grouped-segment helpers (GroupSeg, find_seg, seg_scan)
 #include "segwalk.cuh"  // lane-serial segmented walks (LaneSpan, Comp, Pre, lane_seg_scan)
+#include "tma.cuh"      // TMA staging of the walks' per-sample inputs
 
 namespace vr {
 
@@ -593,27 +594,98 @@ __device__ __forceinline__ void k4_emit(float4* __restrict__ packets, double* __
   }
 }
 
+// TMA staging (tma.cuh): per warp two chunk buffers {t0, t1: 65 rows of two float64 from
+// the even sample at or below the chunk's first, sig_rgb [128] float4}, one mbarrier each
+constexpr int K4_CHUNK = 32 * K4_LANE;
+constexpr int K4_PAIRS = K4_CHUNK / 2 + 1;
+constexpr uint32_t K4_TB = (K4_PAIRS * 16 + 127) / 128 * 128;  // one t buffer, 128-aligned
+constexpr uint32_t K4_BUF = 2 * K4_TB + K4_CHUNK * 16;
+constexpr uint32_t K4_TMA_SMEM = SEG_WARPS * 2 * K4_BUF + 128;  // + alignment slack
+struct K4Maps {
+  CUtensorMap t0, t1, sr;
+};
+
+// lane 0: the chunk at sample `base` into buffer b of this warp
+__device__ __forceinline__ void k4_issue(uint8_t* wbuf, uint64_t* bars, int b, int64_t base,
+                                         const K4Maps& maps) {
+  uint8_t* dst = wbuf + b * K4_BUF;
+  tma::fence_proxy_async();
+  tma::expect_tx(&bars[b], 2 * K4_PAIRS * 16 + K4_CHUNK * 16);
+  tma::load_2d(dst, &maps.t0, 0, (int32_t)(base >> 1), &bars[b]);
+  tma::load_2d(dst + K4_TB, &maps.t1, 0, (int32_t)(base >> 1), &bars[b]);
+  tma::load_2d(dst + 2 * K4_TB, &maps.sr, 0, (int32_t)base, &bars[b]);
+}
+
+__device__ __forceinline__ void k4_from_smem(K4In& in, const uint8_t* buf, int lane, int cnt,
+                                             int64_t base) {
+  const double* a = reinterpret_cast<const double*>(buf) + (base & 1);
+  const double* b = reinterpret_cast<const double*>(buf + K4_TB) + (base & 1);
+  const float4* v = reinterpret_cast<const float4*>(buf + 2 * K4_TB);
+#pragma unroll
+  for (int k = 0; k < K4_LANE; ++k) {
+    const bool ok = k < cnt;
+    in.a[k] = ok ? a[K4_LANE * lane + k] : 0.0;
+    in.b[k] = ok ? b[K4_LANE * lane + k] : 0.0;
+    in.v[k] = ok ? v[K4_LANE * lane + k] : make_float4(0.f, 0.f, 0.f, 0.f);
+  }
+}
+
+template <bool TMA>
 __global__ void __launch_bounds__(SEG_WARPS * 32, 2)  // (3 blocks: spills, 5.9 -> 8.2 ms)
     k_segment_fwd_ls(const double* __restrict__ t0, const double* __restrict__ t1,
                      const float4* __restrict__ sr, const int64_t* __restrict__ off,
                      const int32_t* __restrict__ seg_first, const double* __restrict__ ray_te,
                      int64_t n_rays, int64_t n_segs, float4* __restrict__ packets,
-                     double* __restrict__ seg_tot) {
+                     double* __restrict__ seg_tot, const __grid_constant__ K4Maps maps) {
   __shared__ int64_t s_off_all[SEG_WARPS][33];
   __shared__ double s_te_all[SEG_WARPS][32];
+  __shared__ uint64_t s_bar[SEG_WARPS][2];
+  extern __shared__ __align__(128) uint8_t k4_dyn[];
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
   int64_t* O = s_off_all[wid];
   double* TE = s_te_all[wid];
+  // TMA destinations 128-byte aligned (the dynamic region follows the static arrays)
+  uint8_t* dyn = k4_dyn + ((128 - (tma::smem_addr(k4_dyn) & 127)) & 127);
+  uint8_t* wbuf = dyn + wid * 2 * K4_BUF;
+  uint64_t* bars = s_bar[wid];
+  uint32_t cc = 0;  // this warp's chunks so far: buffer cc & 1, its (cc >> 1)-th use
+  if (TMA) {
+    if (tma::elect_one()) {
+      tma::mbar_init(&bars[0], 1);
+      tma::mbar_init(&bars[1], 1);
+      tma::fence_init();
+    }
+    __syncwarp();
+  }
   const int64_t n_groups = ceil_div(n_segs, 32);
   const bool narrow = n_segs < INT32_MAX;
-  for (int64_t grp = (int64_t)blockIdx.x * SEG_WARPS + wid; grp < n_groups;
-       grp += (int64_t)gridDim.x * SEG_WARPS) {
+  const int64_t gstep = (int64_t)gridDim.x * SEG_WARPS;
+  // TMA: the next group's offsets and entry depths are loaded into registers while this
+  // group is walked, and its first chunk's copies are issued with this group's last chunk,
+  // so a group starts without a memory round trip
+  GroupPrefetch pf;
+  double te_n = 0.0;
+  bool first_issued = false;
+  if (TMA) {
+    const int64_t g0 = (int64_t)blockIdx.x * SEG_WARPS + wid;
+    pf.load(off, g0, n_groups, n_segs, lane);
+    te_n = lane < pf.nseg ? __ldg(ray_te + seg_ray(pf.seg0 + lane, n_rays, narrow)) : 0.0;
+  }
+  for (int64_t grp = (int64_t)blockIdx.x * SEG_WARPS + wid; grp < n_groups; grp += gstep) {
     const int64_t seg0 = grp * 32;
     const int nseg = (int)min((int64_t)32, n_segs - seg0);
     __syncwarp();  // the previous group's readers are done with O / TE
-    stage_offsets(off, seg0, nseg, lane, O);
-    TE[lane] = lane < nseg ? ray_te[seg_ray(seg0 + lane, n_rays, narrow)] : 0.0;
-    __syncwarp();
+    if (TMA) {
+      pf.stage(O, lane);
+      TE[lane] = te_n;
+      __syncwarp();
+      pf.load(off, grp + gstep, n_groups, n_segs, lane);
+      te_n = lane < pf.nseg ? __ldg(ray_te + seg_ray(pf.seg0 + lane, n_rays, narrow)) : 0.0;
+    } else {
+      stage_offsets(off, seg0, nseg, lane, O);
+      TE[lane] = lane < nseg ? ray_te[seg_ray(seg0 + lane, n_rays, narrow)] : 0.0;
+      __syncwarp();
+    }
     const int64_t s_beg = O[0], s_end = O[nseg];
     if (lane < nseg && O[lane] == O[lane + 1]) {  // empty segment: identity packet
       packets[2 * (seg0 + lane)] = make_float4(1.f, 0.f, 0.f, 0.f);
@@ -621,20 +693,47 @@ __global__ void __launch_bounds__(SEG_WARPS * 32, 2)  // (3 blocks: spills, 5.9 
     }
     Comp carry = comp_id();
     K4In nxt;
-    {
+    if (TMA) {
+      if (!first_issued && s_beg < s_end && tma::elect_one())
+        k4_issue(wbuf, bars, cc & 1, s_beg, maps);
+      first_issued = false;
+    } else {
       const LaneSpan sp = lane_span<K4_LANE>(O, nseg, s_beg, s_end, lane);
       k4_load(nxt, t0, t1, sr, sp.s0, sp.cnt);
     }
-    for (int64_t base = s_beg; base < s_end; base += 32 * K4_LANE) {
+    for (int64_t base = s_beg; base < s_end; base += K4_CHUNK) {
       const LaneSpan sp = lane_span<K4_LANE>(O, nseg, base, s_end, lane);
-      const K4In in = nxt;
-      {  // next chunk's inputs (loads only; used one chunk later)
-        const LaneSpan sn = lane_span<K4_LANE>(O, nseg, base + 32 * K4_LANE, s_end, lane);
+      K4In in;
+      if (TMA) {  // the next chunk's copies (or the next group's first), then this chunk's
+        if (base + K4_CHUNK < s_end) {
+          if (tma::elect_one()) k4_issue(wbuf, bars, (cc + 1) & 1, base + K4_CHUNK, maps);
+        } else if (pf.nseg > 0) {
+          const int64_t nb = __shfl_sync(0xffffffffu, pf.o, 0);
+          const int64_t ne = pf.nseg < 32 ? __shfl_sync(0xffffffffu, pf.o, pf.nseg)
+                                          : __shfl_sync(0xffffffffu, pf.o32, 0);
+          if (nb < ne) {
+            if (tma::elect_one()) k4_issue(wbuf, bars, (cc + 1) & 1, nb, maps);
+            first_issued = true;
+          }
+        }
+        tma::wait(&bars[cc & 1], (cc >> 1) & 1);
+        k4_from_smem(in, wbuf + (cc & 1) * K4_BUF, lane, sp.cnt, base);
+        __syncwarp();  // every lane has read the buffer before it is refilled
+        ++cc;
+      } else {
+        in = nxt;
+        // next chunk's inputs (loads only; used one chunk later)
+        const LaneSpan sn = lane_span<K4_LANE>(O, nseg, base + K4_CHUNK, s_end, lane);
         k4_load(nxt, t0, t1, sr, sn.s0, sn.cnt);
       }
       Comp head = comp_id(), cur = comp_id();
       bool head_done = false;
       int seg = sp.sf;
+      // the lane's exps first (independent: ILP), then the serial fold
+      double kp[K4_LANE], al[K4_LANE];
+#pragma unroll
+      for (int k = 0; k < K4_LANE; ++k)
+        keep_alpha((double)in.v[k].x, in.b[k] - in.a[k], kp[k], al[k]);
 #pragma unroll
       for (int k = 0; k < K4_LANE; ++k) {
         if (k < sp.cnt) {
@@ -649,9 +748,7 @@ __global__ void __launch_bounds__(SEG_WARPS * 32, 2)  // (3 blocks: spills, 5.9 
             ++seg;
             cur = comp_id();
           }
-          double keep, alpha;
-          keep_alpha((double)in.v[k].x, in.b[k] - in.a[k], keep, alpha);
-          comp_push(cur, keep, alpha, in.v[k], sample_mid(in.a[k], in.b[k]) - TE[seg]);
+          comp_push(cur, kp[k], al[k], in.v[k], sample_mid(in.a[k], in.b[k]) - TE[seg]);
         }
       }
       const bool closed = sp.cnt > 0 && O[seg + 1] == sp.s0 + sp.cnt;
@@ -726,6 +823,12 @@ __global__ void __launch_bounds__(SEG_WARPS * 32)
       double head = 1.0, cur = 1.0;
       bool head_done = false;
       int seg = sp.sf;
+      double kp[K4_LANE];
+#pragma unroll
+      for (int k = 0; k < K4_LANE; ++k) {
+        double al;
+        keep_alpha((double)sg[k], b[k] - a[k], kp[k], al);
+      }
 #pragma unroll
       for (int k = 0; k < K4_LANE; ++k) {
         if (k < sp.cnt) {
@@ -740,9 +843,7 @@ __global__ void __launch_bounds__(SEG_WARPS * 32)
             ++seg;
             cur = 1.0;
           }
-          double keep, alpha;
-          keep_alpha((double)sg[k], b[k] - a[k], keep, alpha);
-          cur *= keep;
+          cur *= kp[k];
         }
       }
       const bool closed = sp.cnt > 0 && O[seg + 1] == sp.s0 + sp.cnt;
@@ -846,9 +947,10 @@ __global__ void __launch_bounds__(SEG_WARPS * 32, 2)
       Pre cur = pre_id();
       int seg = sp.sf;
 #pragma unroll
+      for (int k = 0; k < K4_LANE; ++k)  // the exps first (independent), then the fold
+        keep_alpha((double)in.v[k].x, in.b[k] - in.a[k], keep[k], alpha[k]);
+#pragma unroll
       for (int k = 0; k < K4_LANE; ++k) {
-        keep[k] = 1.0;
-        alpha[k] = 0.0;
         sid[k] = seg;
         if (k < sp.cnt) {
           const int64_t s = sp.s0 + k;
@@ -857,7 +959,6 @@ __global__ void __launch_bounds__(SEG_WARPS * 32, 2)
             cur = pre_id();
           }
           sid[k] = seg;
-          keep_alpha((double)in.v[k].x, in.b[k] - in.a[k], keep[k], alpha[k]);
           const double m = sample_mid(in.a[k], in.b[k]) - SG[seg].te;
           const double w = cur.T * alpha[k];
           cur.A += w;
@@ -942,6 +1043,20 @@ __global__ void __launch_bounds__(SEG_WARPS * 32, 2)
 
 // K4 kernels: lane-serial walks (default) or the per-sample grouped scans (VR_K4_WALK=grp,
 // kept for A/B measurement and as the backward without forward totals)
+// tensor maps of the walks' inputs (n_samples: the arrays' length; 0 = unknown, no TMA);
+// VR_K4_TMA=0 keeps the per-lane loads
+static bool k4_maps(K4Maps& m, const double* t0, const double* t1, const float* sr,
+                    int64_t n_samples) {
+  static const bool on = [] {
+    const char* e = getenv("VR_K4_TMA");
+    return !(e && strcmp(e, "0") == 0);
+  }();
+  memset(&m, 0, sizeof(m));
+  if (!on || n_samples <= 0 || n_samples > INT32_MAX) return false;
+  return tma::encode_pairs(&m.t0, t0, (uint64_t)n_samples, K4_PAIRS) &&
+         tma::encode_pairs(&m.t1, t1, (uint64_t)n_samples, K4_PAIRS) &&
+         tma::encode_rows(&m.sr, sr, (uint64_t)n_samples, 4, K4_CHUNK);
+}
 static bool k4_lane_serial() {
   static const bool ls = [] {
     const char* e = getenv("VR_K4_WALK");
@@ -957,7 +1072,8 @@ using namespace vr;
 extern "C" int vr_segment_fwd(const double* t0, const double* t1, const float* sr,
                               const int64_t* off, const int32_t* seg_first, const double* ray_te,
                               int64_t n_rays, int32_t region_cnt, float* packets,
-                              double* seg_totals, int32_t* err, void* stream) {
+                              double* seg_totals, int32_t* err, int64_t n_samples,
+                              void* stream) {
   (void)err;
   if (n_rays < 0 || region_cnt < 1 || region_cnt > VR_MAX_REGIONS) {
     set_error("vr_segment_fwd: bad argument");
@@ -965,11 +1081,19 @@ extern "C" int vr_segment_fwd(const double* t0, const double* t1, const float* s
   }
   const int64_t n_segs = n_rays * region_cnt;
   if (n_segs == 0) return VR_OK;
-  if (k4_lane_serial())
-    k_segment_fwd_ls<<<grid_for(ceil_div(n_segs, 32 * SEG_WARPS), 1, 8), SEG_WARPS * 32, 0,
-                       (cudaStream_t)stream>>>(t0, t1, reinterpret_cast<const float4*>(sr), off,
-                                               seg_first, ray_te, n_rays, n_segs,
-                                               reinterpret_cast<float4*>(packets), seg_totals);
+  K4Maps maps;
+  const bool use_tma = k4_lane_serial() && k4_maps(maps, t0, t1, sr, n_samples);
+  const int grid = grid_for(ceil_div(n_segs, 32 * SEG_WARPS), 1, 8);
+  if (use_tma) {
+    cudaFuncSetAttribute(k_segment_fwd_ls<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         (int)K4_TMA_SMEM);
+    k_segment_fwd_ls<true><<<grid, SEG_WARPS * 32, K4_TMA_SMEM, (cudaStream_t)stream>>>(
+        t0, t1, reinterpret_cast<const float4*>(sr), off, seg_first, ray_te, n_rays, n_segs,
+        reinterpret_cast<float4*>(packets), seg_totals, maps);
+  } else if (k4_lane_serial())
+    k_segment_fwd_ls<false><<<grid, SEG_WARPS * 32, 0, (cudaStream_t)stream>>>(
+        t0, t1, reinterpret_cast<const float4*>(sr), off, seg_first, ray_te, n_rays, n_segs,
+        reinterpret_cast<float4*>(packets), seg_totals, maps);
   else
     k_segment_fwd_grp<<<grid_for(ceil_div(n_segs, 32 * SEG_WARPS), 1, 8), SEG_WARPS * 32, 0,
                         (cudaStream_t)stream>>>(t0, t1, reinterpret_cast<const float4*>(sr), off,

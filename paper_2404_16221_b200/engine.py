@@ -42,6 +42,12 @@ def canonical_protocol(name: str) -> str:
     return name
 
 
+def _even(n: int) -> int:
+    """Sample buffers hold an even number of float64: the K4 walks stage them by TMA in
+    16-byte pairs."""
+    return n + (n & 1)
+
+
 @dataclass
 class SampleBatch:
     """K1 output for one rank: region-major sample SoA plus per-segment metadata."""
@@ -317,8 +323,8 @@ class VolumePool:
         seg_max = int(meta[cnt + 1]) if sparse else None
         self.check("in sampling")
         N = int(bounds[-1])
-        t0 = torch.empty(max(N, 1), dtype=torch.float64, device=dev)
-        t1 = torch.empty(max(N, 1), dtype=torch.float64, device=dev)
+        t0 = torch.empty(_even(max(N, 1)), dtype=torch.float64, device=dev)
+        t1 = torch.empty(_even(max(N, 1)), dtype=torch.float64, device=dev)
         ray_id = torch.empty(max(N, 1), dtype=torch.int32, device=dev)
         staged = stage and meta[-1] <= st0.numel() // blocks
         if stage and not staged:  # a slice was too small: grow the staging for next time
@@ -390,8 +396,8 @@ class VolumePool:
             bounds_host = torch.empty(cnt + 1, dtype=torch.int64, pin_memory=True)
             bounds_host.copy_(bounds_dev, non_blocking=True)
             cap = max(int(capacity), 1)
-            t0 = torch.empty(cap, dtype=torch.float64, device=dev)
-            t1 = torch.empty(cap, dtype=torch.float64, device=dev)
+            t0 = torch.empty(_even(cap), dtype=torch.float64, device=dev)
+            t1 = torch.empty(_even(cap), dtype=torch.float64, device=dev)
             ray_id = torch.empty(cap, dtype=torch.int32, device=dev)
             _lib.call("vr_sample_fill", tc, _lib.ptr(rays), R, R, float(dt), lo, cnt,
                       _lib.ptr(offsets), _lib.ptr(seg_first), _lib.ptr(t0), _lib.ptr(t1),
@@ -418,8 +424,8 @@ class VolumePool:
         self.err.zero_()
         if N > p["cap"]:  # did not fit: fill again on this stream
             flags &= ~_lib.VR_FLAG_OVERFLOW
-            t0 = torch.empty(N, dtype=torch.float64, device=self.device)
-            t1 = torch.empty(N, dtype=torch.float64, device=self.device)
+            t0 = torch.empty(_even(N), dtype=torch.float64, device=self.device)
+            t1 = torch.empty(_even(N), dtype=torch.float64, device=self.device)
             ray_id = torch.empty(N, dtype=torch.int32, device=self.device)
             _lib.call("vr_sample_fill", _lib.addr(self.tree_c), _lib.ptr(p["rays"]), R, R,
                       float(p["dt"]), self.region_lo, cnt, _lib.ptr(p["offsets"]),
@@ -583,8 +589,17 @@ class VolumePool:
         _lib.call("vr_segment_fwd", _lib.ptr(b.t0), _lib.ptr(b.t1), _lib.ptr(sig_rgb),
                   _lib.ptr(b.offsets), _lib.ptr(b.seg_first), _lib.ptr(b.ray_te), b.n_rays,
                   b.region_cnt, _lib.ptr(pk), _lib.ptr(totals), _lib.ptr(self.err),
-                  self._stream())
+                  self._tma_n(b.n_samples, b.t0, b.t1, sig_rgb), self._stream())
         return pk
+
+    @staticmethod
+    def _tma_n(n: int, t0, t1, sr) -> int:
+        """n_samples for the K4 walks' TMA staging (vr_capi.h vr_segment_fwd): the sample
+        count when t0 / t1 hold an even number >= n of elements (the staging reads 16-byte
+        pairs) and sig_rgb >= n rows, else 0 (per-lane loads)."""
+        ok = (t0.numel() >= n and t1.numel() >= n and t0.numel() % 2 == 0
+              and t1.numel() % 2 == 0 and sr.shape[0] >= n)
+        return n if ok else 0
 
     def _segment_totals(self, n_segs: int) -> torch.Tensor:
         return torch.empty(max(n_segs, 1) * 7, dtype=torch.float64, device=self.device)
@@ -699,7 +714,8 @@ class VolumePool:
         first = torch.zeros(R, dtype=torch.int32, device=self.device)  # one packet per ray
         _lib.call("vr_segment_fwd", _lib.ptr(t0r), _lib.ptr(t1r), _lib.ptr(srr),
                   _lib.ptr(ray_off), _lib.ptr(first), _lib.ptr(b.ray_te), R, 1, _lib.ptr(pk),
-                  _lib.ptr(totals), _lib.ptr(self.err), self._stream())
+                  _lib.ptr(totals), _lib.ptr(self.err),
+                  self._tma_n(b.n_samples, t0r, t1r, srr), self._stream())
         return pk
 
     def _sample_protocol_forward(self, rays, dt: float, train: bool):

@@ -51,7 +51,7 @@ def test_bad_arguments_are_rejected_without_a_gpu():
     assert b"bad argument" in lib.vr_last_error()
     with pytest.raises(ValueError):
         _lib.call("vr_segment_fwd", None, None, None, None, None, None, 4, 0, None, None, None,
-                  None)
+                  0, None)
 
 
 def test_header_constants_match_ctypes_mirror():
