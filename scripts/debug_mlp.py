@@ -69,9 +69,11 @@ for n in (1000, 40000, 400000):
         L.call(fw, L.ptr(w16), L.ptr(enc), L.ptr(rays), R, L.ptr(rid), n, L.ptr(o), s)
         gw = torch.zeros(L.VR_MLP_NPARAMS, dtype=torch.float32, device=DEV)
         de = torch.empty((16, n, 2), dtype=torch.float32, device=DEV)
-        args = [L.ptr(w16), L.ptr(enc), L.ptr(rays), R, L.ptr(rid), n, L.ptr(dsr), L.ptr(gw), L.ptr(de)]
-        if bw.endswith("_tc"):
-            args += [L.ptr(err), 0]
+        args = [L.ptr(w16), L.ptr(enc), L.ptr(rays), R, L.ptr(rid), n, L.ptr(dsr)]
+        if bw.endswith("_tc"):  # (no forward output: no gradient scaling; no row list)
+            args += [None, L.ptr(gw), L.ptr(de), L.ptr(err), 0, None, None]
+        else:
+            args += [L.ptr(gw), L.ptr(de)]
         L.call(bw, *args, s)
         torch.cuda.synchronize()
         fo = ((o.double() - ref_out).abs().max()).item()

@@ -161,7 +161,7 @@ for sc in (1.0, 2.0 ** 6, 2.0 ** 10):
     rd = pool.rays_to_device(rays)
     _lib.call("vr_mlp_bwd_tc", _lib.ptr(f.weights16), _lib.ptr(f._enc), _lib.ptr(rd), rd.shape[1],
               _lib.ptr(b.ray_id), n, _lib.ptr(dsr), None, _lib.ptr(gwt), _lib.ptr(de), _lib.ptr(err_w), 0,
-              _lib.stream_ptr())
+              None, None, _lib.stream_ptr())
     torch.cuda.synchronize()
     d2 = (de.view(16, -1, 2)[:, :n].permute(1, 0, 2).reshape(n, 32).cpu().numpy() / sc)
     e2 = np.abs(d2 - enc16.grad.numpy()) / (np.abs(enc16.grad.numpy()).max(1, keepdims=True) + 1e-30)
