@@ -426,6 +426,13 @@ int vr_packets_pack(const float* packets_dev, const float* extra_dev, const int3
 int vr_packets_unpack(const float* recv_dev, int32_t world, int64_t rows, int32_t width,
                       int64_t n_rays, int32_t n_regions, float* slab_dev, float* extra_slab_dev,
                       int32_t* err_dev, void* stream);
+/* Instead of a dense slab: index_dev [n_regions][n_rays] int32 = the slot
+ * (rank * rows + i) of segment (k, r)'s record in recv_dev, -1 for an empty segment — 4 B
+ * per segment instead of the slab's 32 B write and read.  The *_records variants of K5 and
+ * the interlevel prefix read the packets through it (bit-identical results). */
+int vr_packets_index(const float* recv_dev, int32_t world, int64_t rows, int32_t width,
+                     int64_t n_rays, int32_t n_regions, int32_t* index_dev, int32_t* err_dev,
+                     void* stream);
 /* analytic backward: dpackets [region_cnt][n_rays][8] = adjoints of {T,C,A,D',L};
  * writes dsig_rgb[i] = {dL/dsigma, dL/dr, dL/dg, dL/db}. */
 /* transmittance only (the T of composite_samples quadrature.py:141-165 per run):
@@ -456,6 +463,17 @@ int vr_global_train(const float* packets_dev, int32_t n_regions, int64_t n_rays,
                     const float* targets_dev /*[n_rays][3]*/, float lambda_dist, int32_t own_lo,
                     int32_t own_cnt, float* out_dev, double* ray_loss_dev, float* dpackets_dev,
                     int32_t* err_dev, void* stream);
+/* the same two, reading the exchanged records through vr_packets_index's index */
+int vr_global_fwd_records(const float* recv_dev, int32_t width, const int32_t* index_dev,
+                          int32_t n_regions, int64_t n_rays, const double* ray_te_dev,
+                          const float* background3, int32_t clip_bg, float* out_dev,
+                          int32_t* err_dev, void* stream);
+int vr_global_train_records(const float* recv_dev, int32_t width, const int32_t* index_dev,
+                            int32_t n_regions, int64_t n_rays, const double* ray_te_dev,
+                            const float* background3, const float* targets_dev,
+                            float lambda_dist, int32_t own_lo, int32_t own_cnt, float* out_dev,
+                            double* ray_loss_dev, float* dpackets_dev, int32_t* err_dev,
+                            void* stream);
 /* ---- interlevel (proposal) loss — no reference code (spec in
  * csrc/interlevel.cu and oracle/grad_oracle.py).  vr_prefix_train: NeRF and proposal
  * transmittance in front of each owned segment, prefix [own_cnt][n_rays][2] float32,
@@ -468,6 +486,10 @@ int vr_global_train(const float* packets_dev, int32_t n_regions, int64_t n_rays,
 int vr_prefix_train(const float* packets_dev, const float* prop_T_dev, int32_t n_regions,
                     int64_t n_rays, int32_t own_lo, int32_t own_cnt, float* prefix_dev,
                     void* stream);
+/* the same from width-10 records (the proposal T in field 9) through vr_packets_index */
+int vr_prefix_train_records(const float* recv_dev, const int32_t* index_dev, int32_t n_regions,
+                            int64_t n_rays, int32_t own_lo, int32_t own_cnt, float* prefix_dev,
+                            void* stream);
 int vr_interlevel(const double* t0_dev, const double* t1_dev, const float* sig_rgb_dev,
                   const float* sig_prop_dev, const int64_t* offsets_dev, const float* prefix_dev,
                   int64_t n_rays, int32_t region_cnt, float lambda_interlevel, float eps,

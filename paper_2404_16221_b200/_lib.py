@@ -161,6 +161,10 @@ SIGNATURES = {
     "vr_packets_pack": [P, P, P, I64, I32, I32, P, I64, P, P, P],
     "vr_packets_unpack": [P, I32, I64, I32, I64, I32, P, P, P, P],
     "vr_global_fwd": [P, I32, I64, P, P, I32, P, P, P],
+    "vr_global_fwd_records": [P, I32, P, I32, I64, P, P, I32, P, P, P],
+    "vr_global_train_records": [P, I32, P, I32, I64, P, P, P, F32, I32, I32, P, P, P, P, P],
+    "vr_packets_index": [P, I32, I64, I32, I64, I32, P, P, P],
+    "vr_prefix_train_records": [P, P, I32, I64, I32, I32, P, P],
     "vr_global_train": [P, I32, I64, P, P, P, F32, I32, I32, P, P, P, P, P],
     "vr_prefix_train": [P, P, I32, I64, I32, I32, P, P],
     "vr_interlevel": [P, P, P, P, P, P, I64, I32, F32, F32, P, P, P],

@@ -30,6 +30,7 @@
 #include "segscan.cuh"  // grouped-segment helpers (GroupSeg, find_seg, seg_scan)
 #include "segwalk.cuh"  // lane-serial segmented walks (LaneSpan, Comp, Pre, lane_seg_scan)
 #include "tma.cuh"      // TMA staging of the walks' per-sample inputs
+#include "pksrc.cuh"    // K5's packet source: the dense slab or the exchanged records
 
 namespace vr {
 
@@ -350,8 +351,9 @@ struct Pk {
   double T, C[3], A, D, L;
 };
 
-__device__ __forceinline__ Pk load_pk(const float4* __restrict__ pk, int64_t idx) {
-  const float4 a = pk[2 * idx], b = pk[2 * idx + 1];
+__device__ __forceinline__ Pk load_pk(const PacketSrc& src, int64_t idx) {
+  float4 a, b;
+  pk_load(src, idx, a, b);
   Pk p;
   p.T = a.x;
   p.C[0] = a.y;
@@ -364,7 +366,7 @@ __device__ __forceinline__ Pk load_pk(const float4* __restrict__ pk, int64_t idx
 }
 
 template <bool TRAIN>
-__global__ void k_global(const float4* __restrict__ pk, int n_regions, int64_t n_rays,
+__global__ void k_global(const PacketSrc pk, int n_regions, int64_t n_rays,
                          const double* __restrict__ ray_te, float bg0, float bg1, float bg2,
                          int clip_bg, const float* __restrict__ targets, float lambda_dist,
                          int own_lo, int own_cnt, float* __restrict__ out,
@@ -377,7 +379,7 @@ __global__ void k_global(const float4* __restrict__ pk, int n_regions, int64_t n
     int key[VR_MAX_REGIONS];
     int n = 0;
     for (int k = 0; k < n_regions; ++k) {
-      const int kf = __float_as_int(pk[2 * ((int64_t)k * n_rays + r) + 1].w);
+      const int kf = pk_key(pk, (int64_t)k * n_rays + r);
       if (kf == INT32_MAX) continue;
       int j = n++;
       while (j > 0 && key[j - 1] > kf) {  // insertion sort, ties impossible
@@ -1057,6 +1059,16 @@ static bool k4_maps(K4Maps& m, const double* t0, const double* t1, const float* 
          tma::encode_pairs(&m.t1, t1, (uint64_t)n_samples, K4_PAIRS) &&
          tma::encode_rows(&m.sr, sr, (uint64_t)n_samples, 4, K4_CHUNK);
 }
+static PacketSrc pk_source(const float* pk, const float* extra, const float* rec,
+                           const int32_t* index, int width) {
+  PacketSrc s;
+  s.pk = reinterpret_cast<const float4*>(pk);
+  s.extra = extra;
+  s.rec = rec;
+  s.index = index;
+  s.width = width;
+  return s;
+}
 static bool k4_lane_serial() {
   static const bool ls = [] {
     const char* e = getenv("VR_K4_WALK");
@@ -1156,8 +1168,8 @@ extern "C" int vr_global_fwd(const float* pk, int32_t n_regions, int64_t n_rays,
   }
   if (n_rays == 0) return VR_OK;
   k_global<false><<<grid_for(n_rays, 128), 128, 0, (cudaStream_t)stream>>>(
-      reinterpret_cast<const float4*>(pk), n_regions, n_rays, ray_te, bg[0], bg[1], bg[2],
-      clip_bg, nullptr, 0.f, 0, 0, out, nullptr, nullptr, err);
+      pk_source(pk, nullptr, nullptr, nullptr, 0), n_regions, n_rays, ray_te, bg[0], bg[1],
+      bg[2], clip_bg, nullptr, 0.f, 0, 0, out, nullptr, nullptr, err);
   return check_launch("vr_global_fwd");
 }
 
@@ -1172,9 +1184,45 @@ extern "C" int vr_global_train(const float* pk, int32_t n_regions, int64_t n_ray
   }
   if (n_rays == 0) return VR_OK;
   k_global<true><<<grid_for(n_rays, 128), 128, 0, (cudaStream_t)stream>>>(
-      reinterpret_cast<const float4*>(pk), n_regions, n_rays, ray_te, bg[0], bg[1], bg[2], 0,
-      targets, lambda_dist, own_lo, own_cnt, out, ray_loss, reinterpret_cast<float4*>(dpk), err);
+      pk_source(pk, nullptr, nullptr, nullptr, 0), n_regions, n_rays, ray_te, bg[0], bg[1],
+      bg[2], 0, targets, lambda_dist, own_lo, own_cnt, out, ray_loss,
+      reinterpret_cast<float4*>(dpk), err);
   return check_launch("vr_global_train");
+}
+
+extern "C" int vr_global_fwd_records(const float* recv, int32_t width, const int32_t* index,
+                                     int32_t n_regions, int64_t n_rays, const double* ray_te,
+                                     const float* bg, int32_t clip_bg, float* out, int32_t* err,
+                                     void* stream) {
+  if (n_regions < 1 || n_regions > VR_MAX_REGIONS || n_rays < 0 || !bg || !err ||
+      (n_rays > 0 && (!recv || !index)) || (width != 9 && width != 10)) {
+    set_error("vr_global_fwd_records: bad argument");
+    return VR_ERR_BAD_ARG;
+  }
+  if (n_rays == 0) return VR_OK;
+  k_global<false><<<grid_for(n_rays, 128), 128, 0, (cudaStream_t)stream>>>(
+      pk_source(nullptr, nullptr, recv, index, width), n_regions, n_rays, ray_te, bg[0], bg[1],
+      bg[2], clip_bg, nullptr, 0.f, 0, 0, out, nullptr, nullptr, err);
+  return check_launch("vr_global_fwd_records");
+}
+
+extern "C" int vr_global_train_records(const float* recv, int32_t width, const int32_t* index,
+                                       int32_t n_regions, int64_t n_rays, const double* ray_te,
+                                       const float* bg, const float* targets, float lambda_dist,
+                                       int32_t own_lo, int32_t own_cnt, float* out,
+                                       double* ray_loss, float* dpk, int32_t* err, void* stream) {
+  if (n_regions < 1 || n_regions > VR_MAX_REGIONS || n_rays < 0 || !bg || !err || own_lo < 0 ||
+      own_cnt < 1 || own_lo + own_cnt > n_regions || (n_rays > 0 && (!recv || !index)) ||
+      (width != 9 && width != 10)) {
+    set_error("vr_global_train_records: bad argument");
+    return VR_ERR_BAD_ARG;
+  }
+  if (n_rays == 0) return VR_OK;
+  k_global<true><<<grid_for(n_rays, 128), 128, 0, (cudaStream_t)stream>>>(
+      pk_source(nullptr, nullptr, recv, index, width), n_regions, n_rays, ray_te, bg[0], bg[1],
+      bg[2], 0, targets, lambda_dist, own_lo, own_cnt, out, ray_loss,
+      reinterpret_cast<float4*>(dpk), err);
+  return check_launch("vr_global_train_records");
 }
 
 // ---- sample-broadcast protocol: region-major <-> ray-major sample order ---------------
@@ -1344,6 +1392,48 @@ extern "C" int vr_packets_unpack(const float* recv, int32_t world, int64_t rows,
   k_packets_unpack<<<grid_for((int64_t)world * rows, 256), 256, 0, s>>>(
       recv, world, rows, width, n_segs, (float4*)slab, extra_slab, err);
   return check_launch("vr_packets_unpack");
+}
+
+// index[g] = the record slot (rank * rows + i) of segment g; -1 (memset) for empty segments
+__global__ void k_packets_index(const float* __restrict__ recv, int world, int64_t rows,
+                                int width, int64_t n_segs, int32_t* __restrict__ index,
+                                int32_t* err) {
+  int flags = 0;
+  for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < (int64_t)world * rows;
+       t += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t rk = t / rows, i = t - rk * rows;
+    const float* buf = recv + rk * rows * width;
+    const int32_t n = __float_as_int(buf[0]);
+    if (i == 0 || i > n) continue;
+    if (n >= rows) {
+      flags |= VR_FLAG_OVERFLOW;
+      continue;
+    }
+    const int64_t g = (int64_t)__float_as_int(buf[i * width]);
+    if (g < 0 || g >= n_segs) {
+      flags |= VR_FLAG_OVERFLOW;
+      continue;
+    }
+    index[g] = (int32_t)t;
+  }
+  if (flags) atomicOr(err, flags);
+}
+
+extern "C" int vr_packets_index(const float* recv, int32_t world, int64_t rows, int32_t width,
+                                int64_t n_rays, int32_t n_regions, int32_t* index, int32_t* err,
+                                void* stream) {
+  if (world < 1 || rows < 1 || (width != 9 && width != 10) || n_rays < 0 || n_regions < 1 ||
+      n_regions > VR_MAX_REGIONS || !index || !err || (int64_t)world * rows > INT32_MAX) {
+    set_error("vr_packets_index: bad argument");
+    return VR_ERR_BAD_ARG;
+  }
+  cudaStream_t s = (cudaStream_t)stream;
+  const int64_t n_segs = n_rays * n_regions;
+  if (n_segs == 0) return VR_OK;
+  cudaMemsetAsync(index, 0xFF, (size_t)n_segs * sizeof(int32_t), s);
+  k_packets_index<<<grid_for((int64_t)world * rows, 256), 256, 0, s>>>(recv, world, rows, width,
+                                                                       n_segs, index, err);
+  return check_launch("vr_packets_index");
 }
 
 extern "C" int vr_sum_f64(const double* x, int64_t n, double* out, double* ws, void* stream) {

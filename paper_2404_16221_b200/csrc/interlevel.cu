@@ -15,6 +15,7 @@
 #include <stdlib.h>
 
 #include "common.cuh"
+#include "pksrc.cuh"
 #include "segscan.cuh"
 
 namespace vr {
@@ -23,15 +24,14 @@ constexpr int IL_WARPS = 8;
 
 // per ray: prefixes (P, Ph) of the NeRF and proposal transmittance before each owned
 // segment, folded in the same first-sample order as K5
-__global__ void k_prefix(const float4* __restrict__ pk, const float* __restrict__ propT,
-                         int n_regions, int64_t n_rays, int own_lo, int own_cnt,
-                         float2* __restrict__ prefix) {
+__global__ void k_prefix(const PacketSrc pk, int n_regions, int64_t n_rays, int own_lo,
+                         int own_cnt, float2* __restrict__ prefix) {
   for (int64_t r = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; r < n_rays;
        r += (int64_t)gridDim.x * blockDim.x) {
     int ord[VR_MAX_REGIONS], key[VR_MAX_REGIONS];
     int n = 0;
     for (int k = 0; k < n_regions; ++k) {
-      const int kf = __float_as_int(pk[2 * ((int64_t)k * n_rays + r) + 1].w);
+      const int kf = pk_key(pk, (int64_t)k * n_rays + r);
       if (kf == INT32_MAX) continue;
       int j = n++;
       while (j > 0 && key[j - 1] > kf) {
@@ -49,8 +49,10 @@ __global__ void k_prefix(const float4* __restrict__ pk, const float* __restrict_
       const int kk = ord[s] - own_lo;
       if (kk >= 0 && kk < own_cnt)
         prefix[(int64_t)kk * n_rays + r] = make_float2((float)P, (float)Ph);
-      P *= (double)pk[2 * idx].x;
-      Ph *= (double)propT[idx];
+      float4 a, b;
+      pk_load(pk, idx, a, b);
+      P *= (double)a.x;
+      Ph *= (double)pk_extra(pk, idx);
     }
   }
 }
@@ -210,10 +212,35 @@ extern "C" int vr_prefix_train(const float* pk, const float* prop_T, int32_t n_r
     return VR_ERR_BAD_ARG;
   }
   if (n_rays == 0) return VR_OK;
+  PacketSrc src;
+  src.pk = reinterpret_cast<const float4*>(pk);
+  src.extra = prop_T;
+  src.rec = nullptr;
+  src.index = nullptr;
+  src.width = 0;
   k_prefix<<<grid_for(n_rays, 128), 128, 0, (cudaStream_t)stream>>>(
-      reinterpret_cast<const float4*>(pk), prop_T, n_regions, n_rays, own_lo, own_cnt,
-      reinterpret_cast<float2*>(prefix));
+      src, n_regions, n_rays, own_lo, own_cnt, reinterpret_cast<float2*>(prefix));
   return check_launch("vr_prefix_train");
+}
+
+extern "C" int vr_prefix_train_records(const float* recv, const int32_t* index, int32_t n_regions,
+                                       int64_t n_rays, int32_t own_lo, int32_t own_cnt,
+                                       float* prefix, void* stream) {
+  if (n_regions < 1 || n_regions > VR_MAX_REGIONS || n_rays < 0 || own_lo < 0 || own_cnt < 1 ||
+      own_lo + own_cnt > n_regions || !prefix || (n_rays > 0 && (!recv || !index))) {
+    set_error("vr_prefix_train_records: bad argument");
+    return VR_ERR_BAD_ARG;
+  }
+  if (n_rays == 0) return VR_OK;
+  PacketSrc src;  // records of width 10: the proposal T rides in field 9
+  src.pk = nullptr;
+  src.extra = nullptr;
+  src.rec = recv;
+  src.index = index;
+  src.width = 10;
+  k_prefix<<<grid_for(n_rays, 128), 128, 0, (cudaStream_t)stream>>>(
+      src, n_regions, n_rays, own_lo, own_cnt, reinterpret_cast<float2*>(prefix));
+  return check_launch("vr_prefix_train_records");
 }
 
 extern "C" int vr_interlevel(const double* t0, const double* t1, const float* sig_rgb,

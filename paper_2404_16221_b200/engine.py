@@ -42,6 +42,18 @@ def canonical_protocol(name: str) -> str:
     return name
 
 
+@dataclass
+class PacketRecords:
+    """The sparse exchange's received records ([world * rows][width] float32: {global slab
+    index, packet (, proposal T)}) with the [K][R] int32 index of their slots
+    (vr_packets_index; -1 = empty segment): K5 and the interlevel prefix read the packets
+    through it instead of a dense [K][R][8] slab."""
+    recv: torch.Tensor
+    width: int
+    index: torch.Tensor
+    n_regions: int
+
+
 def _even(n: int) -> int:
     """Sample buffers hold an even number of float64: the K4 walks stage them by TMA in
     16-byte pairs."""
@@ -127,8 +139,9 @@ class VolumePool:
         # traffic queues behind the scatter's atomics either way, and the fused kernel has no
         # d(enc) round trip).  On c4 the split pipeline saves ~15 ms of 550.
         self.overlap_backward = os.environ.get("VR_OVERLAP_BWD", "1") != "0"
-        # the proposal forward beside K4's forward, the interlevel loss beside its backward
-        self.overlap_proposals = os.environ.get("VR_OVERLAP_PROP", "1") != "0"
+        # sparse exchange: K5 reads the received records through an index (VR_RECORDS_K5=0:
+        # rebuild the dense slab first, vr_packets_unpack)
+        self.records_k5 = os.environ.get("VR_RECORDS_K5", "1") != "0"
         # K1 in one walk (count + staging, then a compaction copy) instead of count + fill
         self.stage_k1 = os.environ.get("VR_K1_STAGE", "1") != "0"
         self.stage_slots_per_ray = 96  # initial staging size; grown after an overflow
@@ -641,6 +654,12 @@ class VolumePool:
             recv = comm.gather_packets(send, self.group, self.world, self.rank, dst)
             if recv is None:
                 return None, None
+        if self.records_k5:  # K5 reads the records through a 4-byte-per-segment index
+            index = torch.empty((self.n_regions, R), dtype=torch.int32, device=self.device)
+            _lib.call("vr_packets_index", _lib.ptr(recv), self.world, cap + 1, width, R,
+                      self.n_regions, _lib.ptr(index), _lib.ptr(self.err), s)
+            rec = PacketRecords(recv, width, index, self.n_regions)
+            return rec, (rec if extra is not None else None)
         allp = torch.empty((self.n_regions, R, 8), dtype=torch.float32, device=self.device)
         all_e = (torch.empty((self.n_regions, R), dtype=torch.float32, device=self.device)
                  if extra is not None else None)
@@ -655,9 +674,15 @@ class VolumePool:
             self._bg[c] = float(bg[c])
         return self._bg
 
-    def compose(self, packets: torch.Tensor, b: SampleBatch, background=None,
+    def compose(self, packets, b: SampleBatch, background=None,
                 clip: bool = True) -> torch.Tensor:
         out = torch.empty((7, b.n_rays), dtype=torch.float32, device=self.device)
+        if isinstance(packets, PacketRecords):
+            _lib.call("vr_global_fwd_records", _lib.ptr(packets.recv), packets.width,
+                      _lib.ptr(packets.index), packets.n_regions, b.n_rays, _lib.ptr(b.ray_te),
+                      _lib.addr(self._set_bg(background)), 1 if clip else 0, _lib.ptr(out),
+                      _lib.ptr(self.err), self._stream())
+            return out
         _lib.call("vr_global_fwd", _lib.ptr(packets), packets.shape[0], b.n_rays,
                   _lib.ptr(b.ray_te), _lib.addr(self._set_bg(background)), 1 if clip else 0, _lib.ptr(out),
                   _lib.ptr(self.err), self._stream())
@@ -761,77 +786,65 @@ class VolumePool:
         b = batch if batch is not None else self.sample(rays, dt, exchange=True)
         sig_rgb = self.evaluate(rays, b)
         totals = self._segment_totals(b.region_cnt * b.n_rays)
+        local = self.local_packets(b, sig_rgb, totals)
         interlevel = self.proposals is not None and lambda_interlevel > 0.0
         prop_T = None
-        # the proposal chain (L2-bound gathers) runs on the side stream beside the NeRF's K4
-        # forward (fp64 walk), and the interlevel loss beside K4's backward
-        par = interlevel and self.overlap_proposals
-        main = torch.cuda.current_stream()
         if interlevel:
-            side = self._side_stream()
-            if par:
-                side.wait_stream(main)
-            with torch.cuda.stream(side if par else main):
-                # the proposal of a region shares its NeRF field's box: its gathers read the
-                # positions the NeRF forward kept
-                sig_prop = self.evaluate(rays, b, self.proposals, pos_from=self.fields)
-                # only the proposal transmittance of each segment crosses the link
-                prop_T = torch.empty((b.region_cnt, b.n_rays), dtype=torch.float32,
-                                     device=self.device)
-                _lib.call("vr_segment_transmittance", _lib.ptr(b.t0), _lib.ptr(b.t1),
-                          _lib.ptr(sig_prop), _lib.ptr(b.offsets), b.n_rays, b.region_cnt,
-                          _lib.ptr(prop_T), self._stream())
-        local = self.local_packets(b, sig_rgb, totals)
-        if par:
-            main.wait_stream(side)
-            sig_prop.record_stream(main)
-            prop_T.record_stream(main)
+            # the proposal of a region shares its NeRF field's box: its gathers read the
+            # positions the NeRF forward kept
+            sig_prop = self.evaluate(rays, b, self.proposals, pos_from=self.fields)
+            # only the proposal transmittance of each segment crosses the link
+            prop_T = torch.empty((b.region_cnt, b.n_rays), dtype=torch.float32,
+                                 device=self.device)
+            _lib.call("vr_segment_transmittance", _lib.ptr(b.t0), _lib.ptr(b.t1),
+                      _lib.ptr(sig_prop), _lib.ptr(b.offsets), b.n_rays, b.region_cnt,
+                      _lib.ptr(prop_T), s)
         allp, all_T = self.exchange_packets(b, local, prop_T)
         R = b.n_rays
         out = torch.empty((7, R), dtype=torch.float32, device=self.device)
         ray_loss = torch.empty(R, dtype=torch.float64, device=self.device)
         dpk = torch.empty((b.region_cnt, R, 8), dtype=torch.float32, device=self.device)
-        _lib.call("vr_global_train", _lib.ptr(allp), allp.shape[0], R, _lib.ptr(b.ray_te),
-                  _lib.addr(self._set_bg(background)), _lib.ptr(tg), float(lambda_dist), self.region_lo,
-                  self.region_cnt, _lib.ptr(out), _lib.ptr(ray_loss), _lib.ptr(dpk),
-                  _lib.ptr(self.err), s)
+        if isinstance(allp, PacketRecords):
+            _lib.call("vr_global_train_records", _lib.ptr(allp.recv), allp.width,
+                      _lib.ptr(allp.index), allp.n_regions, R, _lib.ptr(b.ray_te),
+                      _lib.addr(self._set_bg(background)), _lib.ptr(tg), float(lambda_dist),
+                      self.region_lo, self.region_cnt, _lib.ptr(out), _lib.ptr(ray_loss),
+                      _lib.ptr(dpk), _lib.ptr(self.err), s)
+        else:
+            _lib.call("vr_global_train", _lib.ptr(allp), allp.shape[0], R, _lib.ptr(b.ray_te),
+                      _lib.addr(self._set_bg(background)), _lib.ptr(tg), float(lambda_dist),
+                      self.region_lo, self.region_cnt, _lib.ptr(out), _lib.ptr(ray_loss),
+                      _lib.ptr(dpk), _lib.ptr(self.err), s)
         loss = torch.empty(1, dtype=torch.float64, device=self.device)
         _lib.call("vr_sum_f64", _lib.ptr(ray_loss), R, _lib.ptr(loss),
                   _lib.ptr(self._sum_scratch()), s)
         if interlevel:
-            if par:
-                side.wait_stream(main)
-            with torch.cuda.stream(side if par else main):
-                ss = self._stream()
-                prefix = torch.empty((b.region_cnt, R, 2), dtype=torch.float32,
-                                     device=self.device)
+            prefix = torch.empty((b.region_cnt, R, 2), dtype=torch.float32, device=self.device)
+            if isinstance(allp, PacketRecords):
+                _lib.call("vr_prefix_train_records", _lib.ptr(allp.recv), _lib.ptr(allp.index),
+                          allp.n_regions, R, self.region_lo, self.region_cnt, _lib.ptr(prefix), s)
+            else:
                 _lib.call("vr_prefix_train", _lib.ptr(allp), _lib.ptr(all_T), allp.shape[0], R,
-                          self.region_lo, self.region_cnt, _lib.ptr(prefix), ss)
-                seg_loss = torch.empty(b.region_cnt * R, dtype=torch.float64, device=self.device)
-                # every sample of a segment is written (no zero fill of the N x 16 B array)
-                dsig_prop = torch.empty((max(b.n_samples, 1), 4), dtype=torch.float32,
-                                        device=self.device)
-                _lib.call("vr_interlevel", _lib.ptr(b.t0), _lib.ptr(b.t1), _lib.ptr(sig_rgb),
-                          _lib.ptr(sig_prop), _lib.ptr(b.offsets), _lib.ptr(prefix), R,
-                          b.region_cnt, float(lambda_interlevel), float(eps),
-                          _lib.ptr(seg_loss), _lib.ptr(dsig_prop), ss)
-                il = torch.empty(1, dtype=torch.float64, device=self.device)
-                # (the main stream's vr_sum_f64 above is complete: one scratch buffer)
-                _lib.call("vr_sum_f64", _lib.ptr(seg_loss), seg_loss.numel(), _lib.ptr(il),
-                          _lib.ptr(self._sum_scratch()), ss)
+                          self.region_lo, self.region_cnt, _lib.ptr(prefix), s)
+            seg_loss = torch.empty(b.region_cnt * R, dtype=torch.float64, device=self.device)
+            # every sample of a segment is written (no zero fill of the N x 16 B array)
+            dsig_prop = torch.empty((max(b.n_samples, 1), 4), dtype=torch.float32,
+                                    device=self.device)
+            _lib.call("vr_interlevel", _lib.ptr(b.t0), _lib.ptr(b.t1), _lib.ptr(sig_rgb),
+                      _lib.ptr(sig_prop), _lib.ptr(b.offsets), _lib.ptr(prefix), R,
+                      b.region_cnt, float(lambda_interlevel), float(eps), _lib.ptr(seg_loss),
+                      _lib.ptr(dsig_prop), s)
+            il = torch.empty(1, dtype=torch.float64, device=self.device)
+            _lib.call("vr_sum_f64", _lib.ptr(seg_loss), seg_loss.numel(), _lib.ptr(il),
+                      _lib.ptr(self._sum_scratch()), s)
+            # each rank sums its own segments' terms: the all-reduce makes the reported loss
+            # the whole batch's on every rank (the main term already is)
+            loss = loss + comm.all_reduce_scalar(il, self.group, self.world)
         # vr_segment_bwd writes every sample (no zero fill of the N x 16 B array)
         dsig = torch.empty((max(b.n_samples, 1), 4), dtype=torch.float32, device=self.device)
         _lib.call("vr_segment_bwd", _lib.ptr(b.t0), _lib.ptr(b.t1), _lib.ptr(sig_rgb),
                   _lib.ptr(b.offsets), _lib.ptr(b.ray_te), R, b.region_cnt, _lib.ptr(dpk),
                   _lib.ptr(totals), _lib.ptr(dsig), s)
-        if interlevel:
-            if par:
-                main.wait_stream(side)
-                dsig_prop.record_stream(main)
-                il.record_stream(main)
-            # each rank sums its own segments' terms: the all-reduce makes the reported loss
-            # the whole batch's on every rank (the main term already is)
-            loss = loss + comm.all_reduce_scalar(il, self.group, self.world)
         # NeRF fields and proposals in one backward pipeline (the proposals' MLP backward
         # overlaps the NeRF scatter on the side stream)
         jobs = [(self.fields, dsig, sig_rgb)]
