@@ -359,6 +359,49 @@ def test_sparse_packet_exchange_kernels(world, with_extra):
     if with_extra:
         assert torch.equal(slab_e, torch.cat(dense_e, 0))
     assert sum(ns) < K * R
+    # the record index (vr_packets_index): every non-empty segment points at its record,
+    # empty ones are -1, and K5 / the interlevel prefix through it equal the dense slab's
+    index = torch.empty((K, R), dtype=torch.int32, device=DEV)
+    _lib.call("vr_packets_index", _lib.ptr(recv), world, bufs[0].shape[0], recv.shape[1], R, K,
+              _lib.ptr(index), _lib.ptr(p.err), _lib.stream_ptr())
+    torch.cuda.synchronize()
+    p.check()
+    live = slab.view(torch.int32)[:, :, 7] != 2 ** 31 - 1
+    assert torch.equal(index >= 0, live)
+    got = recv[index[live].long()]
+    assert torch.equal(got[:, 1:9].view(torch.int32), slab[live].view(torch.int32))
+    te = torch.zeros(R, dtype=torch.float64, device=DEV)
+    tg = torch.rand((R, 3), device=DEV)
+    outs = []
+    for records in (False, True):
+        out = torch.empty((7, R), device=DEV)
+        loss = torch.empty(R, dtype=torch.float64, device=DEV)
+        dpk = torch.empty((K, R, 8), device=DEV)
+        bgv = p._set_bg((0.1, 0.2, 0.3))
+        if records:
+            _lib.call("vr_global_train_records", _lib.ptr(recv), recv.shape[1], _lib.ptr(index),
+                      K, R, _lib.ptr(te), _lib.addr(bgv), _lib.ptr(tg), 0.5, 0, K, _lib.ptr(out),
+                      _lib.ptr(loss), _lib.ptr(dpk), _lib.ptr(p.err), _lib.stream_ptr())
+        else:
+            _lib.call("vr_global_train", _lib.ptr(slab), K, R, _lib.ptr(te), _lib.addr(bgv),
+                      _lib.ptr(tg), 0.5, 0, K, _lib.ptr(out), _lib.ptr(loss), _lib.ptr(dpk),
+                      _lib.ptr(p.err), _lib.stream_ptr())
+        pre = None
+        if with_extra:
+            pre = torch.empty((K, R, 2), device=DEV)
+            if records:
+                _lib.call("vr_prefix_train_records", _lib.ptr(recv), _lib.ptr(index), K, R, 0, K,
+                          _lib.ptr(pre), _lib.stream_ptr())
+            else:
+                _lib.call("vr_prefix_train", _lib.ptr(slab), _lib.ptr(slab_e), K, R, 0, K,
+                          _lib.ptr(pre), _lib.stream_ptr())
+        torch.cuda.synchronize()
+        p.check()
+        outs.append((out, loss, dpk, pre))
+    (o0, l0, d0, p0), (o1, l1, d1, p1) = outs
+    assert torch.equal(o0, o1) and torch.equal(l0, l1) and torch.equal(d0, d1)
+    if with_extra:
+        assert torch.equal(p0, p1)
 
 
 @pytest.mark.parametrize("name", ["partition_street.npz", "partition_voxel_room.npz"])
