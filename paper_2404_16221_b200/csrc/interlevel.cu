@@ -107,10 +107,11 @@ __device__ __forceinline__ IlChunk il_chunk(const IlIn& in, int64_t s, int64_t s
   if (c.valid) {
     c.dlt = in.b - in.a;
     const double x = (double)in.sig * c.dlt, xh = (double)in.sigh * c.dlt;
-    c.keep = exp(-x);
-    c.alpha = -expm1(-x);
-    c.keeph = exp(-xh);
-    c.alphah = -expm1(-xh);
+    // composite_samples' arithmetic (quadrature.py:152-154) and the oracle's: one exp each
+    c.alpha = 1.0 - exp(-x);
+    c.keep = 1.0 - c.alpha;
+    c.alphah = 1.0 - exp(-xh);
+    c.keeph = 1.0 - c.alphah;
   }
   double p[2] = {c.keep, c.keeph};
   seg_scan<2>(p, c.head, lane, [](double a, double b) { return a * b; });
@@ -165,8 +166,9 @@ __global__ void __launch_bounds__(IL_WARPS * 32, 3)
       const double w = P * c.T * c.alpha;
       const double whl = c.Th * c.alphah;
       const double d = fmax(w - Ph * whl, 0.0);
-      const double ei = -2.0 * lam * d / (w + ep);
-      double q[2] = {c.valid ? lam * d * d / (w + ep) : 0.0, c.valid ? whl * ei : 0.0};
+      const double inv = 1.0 / (w + ep);
+      const double ei = -2.0 * lam * d * inv;
+      double q[2] = {c.valid ? lam * d * d * inv : 0.0, c.valid ? whl * ei : 0.0};
       seg_scan<2>(q, c.head, lane, [](double a, double b) { return a + b; });
       const double L = (c.cont ? cL : 0.0) + q[0];
       const double S = (c.cont ? cS : 0.0) + q[1];
