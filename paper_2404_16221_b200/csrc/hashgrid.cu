@@ -34,6 +34,7 @@ __global__ void __launch_bounds__(HASH_THREADS)
                const double* __restrict__ rays, int64_t stride, const double* __restrict__ t0,
                const double* __restrict__ t1, const int32_t* __restrict__ rid, int64_t n,
                __half2* __restrict__ enc, float* __restrict__ pos) {
+  const BoxInv bi = box_inv(g);
   const int lane = threadIdx.x & 31, p = lane & 1;
   const int64_t warp0 = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const int64_t n_warps = ((int64_t)gridDim.x * blockDim.x) >> 5;
@@ -41,7 +42,7 @@ __global__ void __launch_bounds__(HASH_THREADS)
     const int64_t i = s0 + (lane >> 1);
     const bool valid = i < n;
     float u[3] = {0.f, 0.f, 0.f};
-    if (valid && p == 0) norm_pos(g, rays, stride, t0, t1, rid, i, u);
+    if (valid && p == 0) norm_pos(g, bi, rays, stride, t0, t1, rid, i, u);
 #pragma unroll
     for (int a = 0; a < 3; ++a) u[a] = __shfl_sync(0xffffffffu, u[a], lane & ~1);
     if (pos && valid && p == 1) {
@@ -66,6 +67,7 @@ __global__ void __launch_bounds__(HASH_THREADS)
                int64_t stride, const double* __restrict__ t0, const double* __restrict__ t1,
                const int32_t* __restrict__ rid, int64_t n, const float2* __restrict__ denc,
                float2* __restrict__ grad, float2* __restrict__ ws) {
+  const BoxInv bi = box_inv(g);
   const int gwarp = blockIdx.x * (HASH_THREADS / 32) + (threadIdx.x >> 5);
   const int lane = threadIdx.x & 31, p = lane & 1;  // lane pairs (scatter_half)
   const int64_t warp0 = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
@@ -74,7 +76,7 @@ __global__ void __launch_bounds__(HASH_THREADS)
     const int64_t i = s0 + (lane >> 1);
     const bool valid = i < n;
     float u[3] = {0.f, 0.f, 0.f};
-    if (valid && p == 0) norm_pos(g, rays, stride, t0, t1, rid, i, u);
+    if (valid && p == 0) norm_pos(g, bi, rays, stride, t0, t1, rid, i, u);
 #pragma unroll
     for (int a = 0; a < 3; ++a) u[a] = __shfl_sync(0xffffffffu, u[a], lane & ~1);
     if (!valid) continue;
@@ -103,10 +105,11 @@ __global__ void __launch_bounds__(HASH_THREADS)
     k_hash_pos(const VrHashGridDesc g, const double* __restrict__ rays, int64_t stride,
                const double* __restrict__ t0, const double* __restrict__ t1,
                const int32_t* __restrict__ rid, int64_t n, float* __restrict__ pos) {
+  const BoxInv bi = box_inv(g);
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
        i += (int64_t)gridDim.x * blockDim.x) {
     float u[3];
-    norm_pos(g, rays, stride, t0, t1, rid, i, u);
+    norm_pos(g, bi, rays, stride, t0, t1, rid, i, u);
     pos[i] = u[0];
     pos[n + i] = u[1];
     pos[2 * n + i] = u[2];
@@ -306,10 +309,11 @@ int hash_rep_reduce(const VrHashGridDesc* g, const RepPlan& plan, int64_t red, f
 __global__ void k_hash_idx(const VrHashGridDesc g, const double* __restrict__ rays, int64_t stride,
                            const double* __restrict__ t0, const double* __restrict__ t1,
                            const int32_t* __restrict__ rid, int64_t n, int32_t* __restrict__ out) {
+  const BoxInv bi = box_inv(g);
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
        i += (int64_t)gridDim.x * blockDim.x) {
     float u[3];
-    norm_pos(g, rays, stride, t0, t1, rid, i, u);
+    norm_pos(g, bi, rays, stride, t0, t1, rid, i, u);
     for (int l = 0; l < g.n_levels; ++l) {
       Corners c;
       level_corners(g, l, u, c);

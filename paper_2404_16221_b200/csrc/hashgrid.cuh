@@ -7,17 +7,43 @@
 
 namespace vr {
 
-// u = float32((p - box_mn) / (box_mx - box_mn)) for p = o + m d (float64, no FMA)
-__device__ __forceinline__ void norm_pos_od(const VrHashGridDesc& g, const double o[3],
-                                            const double d[3], double m, float u[3]) {
+// u = float32((p - box_mn) / (box_mx - box_mn)) for p = o + m d (float64, no FMA in p).
+// The division is exact (correctly rounded) without a division instruction per sample:
+// with y = RN(1 / e) (one __drcp_rn per thread, BoxInv) and q0 = RN(a y), the remainder
+// r = a - e q0 is exact under an FMA and RN(q0 + r y) is the correctly rounded a / e
+// (Markstein's theorem: y within half an ulp of 1/e, q0 within one ulp of a/e; no overflow
+// or underflow for positions inside the box's range) — bit-identical to the division, at a
+// third of its instructions (the position pass was fp64-division bound).
+struct BoxInv {
+  double ext[3], inv[3];
+};
+__device__ __forceinline__ BoxInv box_inv(const VrHashGridDesc& g) {
+  BoxInv b;
+#pragma unroll
+  for (int a = 0; a < 3; ++a) {
+    b.ext[a] = dsub(g.box_mx[a], g.box_mn[a]);
+    b.inv[a] = __drcp_rn(b.ext[a]);
+  }
+  return b;
+}
+__device__ __forceinline__ double div_exact(double a, double e, double inv) {
+  const double q0 = __dmul_rn(a, inv);
+  const double r = __fma_rn(-q0, e, a);
+  return __fma_rn(r, inv, q0);
+}
+
+__device__ __forceinline__ void norm_pos_od(const VrHashGridDesc& g, const BoxInv& bi,
+                                            const double o[3], const double d[3], double m,
+                                            float u[3]) {
 #pragma unroll
   for (int a = 0; a < 3; ++a) {
     const double p = dadd(o[a], dmul(m, d[a]));
-    u[a] = (float)ddiv(dsub(p, g.box_mn[a]), dsub(g.box_mx[a], g.box_mn[a]));
+    u[a] = (float)div_exact(dsub(p, g.box_mn[a]), bi.ext[a], bi.inv[a]);
   }
 }
 
-__device__ __forceinline__ void norm_pos(const VrHashGridDesc& g, const double* __restrict__ rays,
+__device__ __forceinline__ void norm_pos(const VrHashGridDesc& g, const BoxInv& bi,
+                                         const double* __restrict__ rays,
                                          int64_t stride, const double* __restrict__ t0,
                                          const double* __restrict__ t1,
                                          const int32_t* __restrict__ rid, int64_t i, float u[3]) {
@@ -29,7 +55,7 @@ __device__ __forceinline__ void norm_pos(const VrHashGridDesc& g, const double* 
     o[a] = __ldg(rays + a * stride + r);
     d[a] = __ldg(rays + (3 + a) * stride + r);
   }
-  norm_pos_od(g, o, d, m, u);
+  norm_pos_od(g, bi, o, d, m, u);
 }
 
 struct Corners {

@@ -451,7 +451,7 @@ __device__ __forceinline__ void encode_row(const VrHashGridDesc& g, const float2
     dy = (float)d[1];
     dz = (float)d[2];
     float u[3];
-    norm_pos_od(g, o, d, m, u);
+    norm_pos_od(g, box_inv(g), o, d, m, u);
 #pragma unroll
     for (int l = 0; l < 16; ++l) {
       Corners c;
@@ -644,7 +644,7 @@ __device__ __forceinline__ void fetch_row(RowIn& x, const __half2* __restrict__ 
       double o[3];
 #pragma unroll
       for (int a = 0; a < 3; ++a) o[a] = __ldg(rays + a * stride + r);
-      norm_pos_od(g, o, x.d, sample_mid(t0[i], t1[i]), x.u);
+      norm_pos_od(g, box_inv(g), o, x.d, sample_mid(t0[i], t1[i]), x.u);
     } else if (FUSED) {  // positions written by the hash-grid forward
       x.u[0] = __ldcs(pos + i);
       x.u[1] = __ldcs(pos + n + i);
