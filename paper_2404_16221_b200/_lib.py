@@ -185,8 +185,9 @@ def load(path: str | os.PathLike | None = None) -> C.CDLL:
     global _LIB
     if _LIB is not None:
         return _LIB
-    p = Path(path) if path else (CHECKED_PATH if os.environ.get("VR_CHECKED") == "1"
-                                 else LIB_PATH)
+    # VR_LIB_PATH: another build of the same ABI (A/B comparisons of kernel variants)
+    p = Path(path) if path else Path(os.environ["VR_LIB_PATH"]) if os.environ.get(
+        "VR_LIB_PATH") else (CHECKED_PATH if os.environ.get("VR_CHECKED") == "1" else LIB_PATH)
     if not p.exists():
         raise ImportError(
             f"volray B200 library not built: {p} is missing (run __graft_entry__.build() "
