@@ -698,7 +698,9 @@ def run_workload(cfg_name, args, rank, world, local, dev, group, red_dev, headli
            # sparse backward: the fraction of each field backward's samples with a non-zero
            # upstream gradient (the rest sit behind opaque surfaces: exactly zero gradients)
            "active_rows": {k: round(timer.samples.get(k, 0) / v, 4)
-                           for k, v in timer.dense.items() if v}}
+                           for k, v in timer.dense.items() if v},
+           # K4's forward stages its inputs by TMA when tensor maps can be encoded
+           "tma": bool(_lib.load().vr_tma_available())}
     del pool, batches
     torch.cuda.synchronize()
     torch.cuda.empty_cache()

@@ -1121,6 +1121,10 @@ int launch_bwd(const void* w, const void* enc, const double* rays, int64_t strid
                float* grad_table, void* ws, size_t ws_bytes, const float* pos,
                const int32_t* rows, const int32_t* n_rows, void* stream, int max_ctas = 0) {
   using LY = mlp::BwdLayout<DENS>;
+  if (n > INT32_MAX) {  // the prefetch pipeline carries sample indices as int32
+    set_error("vr_mlp_bwd_tc: more than 2^31 - 1 samples in one call");
+    return VR_ERR_BAD_ARG;
+  }
   int rc = set_smem(mlp::k_mlp_bwd_tc<FUSED, DENS>, LY::SMEM, "mlp bwd: smem attribute");
   if (rc != VR_OK) return rc;
   VrHashGridDesc gd;
