@@ -949,10 +949,9 @@ __global__ void __launch_bounds__(SEG_WARPS * 32, 2)
       Pre cur = pre_id();
       int seg = sp.sf;
 #pragma unroll
-      for (int k = 0; k < K4_LANE; ++k)  // the exps first (independent), then the fold
-        keep_alpha((double)in.v[k].x, in.b[k] - in.a[k], keep[k], alpha[k]);
-#pragma unroll
       for (int k = 0; k < K4_LANE; ++k) {
+        keep[k] = 1.0;
+        alpha[k] = 0.0;
         sid[k] = seg;
         if (k < sp.cnt) {
           const int64_t s = sp.s0 + k;
@@ -961,6 +960,8 @@ __global__ void __launch_bounds__(SEG_WARPS * 32, 2)
             cur = pre_id();
           }
           sid[k] = seg;
+          // (in the fold, not ahead of it: the backward spills with the exps hoisted)
+          keep_alpha((double)in.v[k].x, in.b[k] - in.a[k], keep[k], alpha[k]);
           const double m = sample_mid(in.a[k], in.b[k]) - SG[seg].te;
           const double w = cur.T * alpha[k];
           cur.A += w;
