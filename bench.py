@@ -570,7 +570,8 @@ def run_workload(cfg_name, args, rank, world, local, dev, group, red_dev, headli
                "ms_per_step": t_total / args.steps,
                "share_of_step": t_total / args.steps / ms_instrumented}
         reqs = ev.get("l2_read_requests_per_sample", 0.0) + ev.get("l2_red_requests_per_sample", 0.0)
-        if reqs > 1.0:  # gather / scatter kernels: the L2 request roofline they run against
+        if reqs > 1.0 and ("hash" in k or k == "vr_field_bwd_tc"):
+            # the hash-grid gather / scatter kernels: the L2 request roofline they run against
             ceil = ceilings.get("l2_red_requests_per_s" if ev.get("l2_red_requests_per_sample", 0)
                                 > ev.get("l2_read_requests_per_sample", 0)
                                 else "l2_gather_requests_per_s")
