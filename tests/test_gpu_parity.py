@@ -293,6 +293,25 @@ def test_segment_bwd_with_forward_totals(name):
               _lib.ptr(b.offsets), R, b.region_cnt, _lib.ptr(T), _lib.stream_ptr())
     torch.cuda.synchronize()
     assert torch.equal(T, pk[:, :, 0])
+    # the forward with its inputs staged by TMA (n_samples given) == per-lane loads, bit for
+    # bit, packets and float64 totals
+    assert _lib.load().vr_tma_available() == 1
+    n_tma = p._tma_n(b.n_samples, b.t0, b.t1, sr)
+    assert n_tma == b.n_samples
+    res = []
+    for n_arg in (0, n_tma):
+        pk2 = torch.empty_like(pk)
+        tot2 = torch.empty_like(totals)
+        _lib.call("vr_segment_fwd", _lib.ptr(b.t0), _lib.ptr(b.t1), _lib.ptr(sr),
+                  _lib.ptr(b.offsets), _lib.ptr(b.seg_first), _lib.ptr(b.ray_te), R,
+                  b.region_cnt, _lib.ptr(pk2), _lib.ptr(tot2), _lib.ptr(p.err), n_arg,
+                  _lib.stream_ptr())
+        res.append((pk2, tot2))
+    torch.cuda.synchronize()
+    p.check()
+    assert torch.equal(res[0][0].view(torch.int32), res[1][0].view(torch.int32))
+    live = (b.counts.reshape(-1) > 0).repeat_interleave(7)  # totals of non-empty segments
+    assert torch.equal(res[0][1][live], res[1][1][live])
 
 
 @pytest.mark.parametrize("world", [2, 4])
