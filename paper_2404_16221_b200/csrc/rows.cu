@@ -66,33 +66,43 @@ __global__ void __launch_bounds__(AR_SCAN_THREADS)
   if (threadIdx.x == 0) *n_rows = carry;
 }
 
+// All 16 rounds' warp counts at once (16 ballots per warp into shared memory, one barrier),
+// then each thread places its elements: round k's elements precede round k + 1's, and
+// within a round the warps' in order (two barriers per chunk instead of 32).
 __global__ void __launch_bounds__(AR_THREADS)
     k_rows_write(const uint16_t* __restrict__ masks, const int32_t* __restrict__ offsets,
                  int64_t n, int32_t* __restrict__ rows) {
-  __shared__ int32_t warp_tot[AR_THREADS / 32];
+  constexpr int NW = AR_THREADS / 32;
+  __shared__ int32_t cnt[AR_PER][NW];  // round k, warp w: active elements
+  __shared__ int32_t base_k[AR_PER];   // round k's first output slot (relative)
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const uint32_t mask = masks[(int64_t)blockIdx.x * AR_THREADS + threadIdx.x];
   const int64_t base = (int64_t)blockIdx.x * AR_CHUNK + threadIdx.x;
-  int32_t out = offsets[blockIdx.x];
-#pragma unroll 1
-  for (int k = 0; k < AR_PER; ++k) {
-    const bool on = (mask >> k) & 1u;
-    const uint32_t bal = __ballot_sync(0xffffffffu, on);
-    if (lane == 0) warp_tot[warp] = __popc(bal);
-    __syncthreads();
-    int32_t before = 0, all = 0;
+  uint32_t bal[AR_PER];
 #pragma unroll
-    for (int w = 0; w < AR_THREADS / 32; ++w) {
-      const int32_t t = warp_tot[w];
-      before += w < warp ? t : 0;
-      all += t;
-    }
-    if (on) {
-      const int32_t pos = out + before + __popc(bal & ((1u << lane) - 1u));
-      rows[pos] = (int32_t)(base + (int64_t)k * AR_THREADS);
-    }
-    out += all;
-    __syncthreads();  // warp_tot is rewritten by the next k
+  for (int k = 0; k < AR_PER; ++k) {
+    bal[k] = __ballot_sync(0xffffffffu, (mask >> k) & 1u);
+    if (lane == 0) cnt[k][warp] = __popc(bal[k]);
+  }
+  __syncthreads();
+  if (threadIdx.x < AR_PER) {  // per round: the total, then an exclusive scan below
+    int32_t t = 0;
+#pragma unroll
+    for (int w = 0; w < NW; ++w) t += cnt[threadIdx.x][w];
+    base_k[threadIdx.x] = t;
+  }
+  __syncthreads();
+  const int32_t out0 = offsets[blockIdx.x];
+  int32_t run = 0;
+#pragma unroll
+  for (int k = 0; k < AR_PER; ++k) {
+    int32_t before = 0;
+#pragma unroll
+    for (int w = 0; w < NW; ++w) before += w < warp ? cnt[k][w] : 0;
+    if ((mask >> k) & 1u)
+      rows[out0 + run + before + __popc(bal[k] & ((1u << lane) - 1u))] =
+          (int32_t)(base + (int64_t)k * AR_THREADS);
+    run += base_k[k];
   }
 }
 
