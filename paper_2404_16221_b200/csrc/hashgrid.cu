@@ -265,6 +265,8 @@ __global__ void k_hash_rep_reduce(const VrHashGridDesc g, const RepPlan plan,
     const int64_t size_l = g.offset[l + 1] - g.offset[l];
     float2* w = ws + plan.off[l] + e;
     float2 acc = make_float2(0.f, 0.f);
+    // the replicas' loads unrolled (independent), the sum in replica order as before
+#pragma unroll 8
     for (int r = 0; r < plan.R[l]; ++r) {
       const float2 v = w[r * size_l];
       acc.x += v.x;
