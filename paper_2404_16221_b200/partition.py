@@ -81,97 +81,118 @@ class PartitionTree:
         return t
 
 
-def _aspect_score(size: np.ndarray) -> float:
-    g = float(np.cbrt(float(np.prod(size))))
-    return float(np.abs(np.log(size / g)).sum())
+def _halves(box: Aabb, axis: int, plane: float):
+    """The (low, high) children of ``box`` cut at ``plane`` on ``axis``."""
+    lo_mx, hi_mn = box.mx.copy(), box.mn.copy()
+    lo_mx[axis] = plane
+    hi_mn[axis] = plane
+    return Aabb(box.mn, lo_mx), Aabb(hi_mn, box.mx)
 
 
-def _median_plane(coords: np.ndarray) -> float:
-    c = np.sort(coords)
-    n = c.size
-    if n % 2 == 1:
-        return float(c[(n - 1) // 2])
-    return 0.5 * (float(c[n // 2 - 1]) + float(c[n // 2]))
+def _cubeness(sizes: np.ndarray) -> np.ndarray:
+    """Sum over a box's three extents of |log(extent / geometric-mean extent)| (0 for a
+    cube), for every box of ``sizes[..., 3]`` (partitioner.py:83-86)."""
+    with np.errstate(divide="ignore", invalid="ignore"):  # (non-candidate axes: 0 extents)
+        gm = np.cbrt(np.prod(sizes, axis=-1))
+        return np.abs(np.log(sizes / gm[..., None])).sum(axis=-1)
 
 
 def choose_split(points: np.ndarray, box: Aabb):
-    """Median plane per axis, most-cubic children win, ties x<y<z (partitioner.py:97-128)."""
+    """Split plane of one node (partitioner.py:97-128): on each axis the median of the
+    points' coordinates (mean of the two middle ones for an even count); an axis is a
+    candidate when the plane lies strictly inside the box and leaves points on both sides
+    (low side: coordinate <= plane); of the candidates, the one whose two children are the
+    most cube-like wins, the lower axis on a tie.  All three axes are evaluated at once."""
     pts = np.asarray(points, dtype=np.float64).reshape(-1, 3)
-    if pts.shape[0] < 2:
+    n = pts.shape[0]
+    if n < 2:
         raise InsufficientPointsError("need at least 2 points to split")
-    best = None
-    for axis in range(3):
-        coords = pts[:, axis]
-        plane = _median_plane(coords)
-        n_low = int(np.count_nonzero(coords <= plane))
-        if n_low == 0 or n_low == pts.shape[0]:
-            continue
-        if not (box.mn[axis] < plane < box.mx[axis]):
-            continue
-        lo_size = box.size.copy()
-        lo_size[axis] = plane - box.mn[axis]
-        hi_size = box.size.copy()
-        hi_size[axis] = box.mx[axis] - plane
-        score = _aspect_score(lo_size) + _aspect_score(hi_size)
-        if best is None or score < best[0]:
-            best = (score, axis, plane)
-    if best is None:
+    srt = np.sort(pts, axis=0)
+    planes = srt[(n - 1) // 2] if n % 2 else 0.5 * (srt[n // 2 - 1] + srt[n // 2])
+    n_low = np.count_nonzero(pts <= planes, axis=0)
+    ok = (n_low > 0) & (n_low < n) & (box.mn < planes) & (planes < box.mx)
+    if not ok.any():
         raise DegenerateSplitError("no axis separates the points inside the box")
-    return best[1], best[2]
+    # children extents per candidate axis: [axis][low/high][extent]
+    ext = np.broadcast_to(box.size, (3, 2, 3)).copy()
+    ax = np.arange(3)
+    ext[ax, 0, ax] = planes - box.mn
+    ext[ax, 1, ax] = box.mx - planes
+    cube = _cubeness(ext)
+    score = np.where(ok, cube[:, 0] + cube[:, 1], np.inf)
+    axis = int(np.argmin(score))
+    return axis, float(planes[axis])
+
+
+def _grow(root_box: Aabb, depth: int, cut, payload) -> PartitionTree:
+    """Complete binary tree built one level at a time.  ``cut(payload, box, level)`` returns
+    (axis, plane) of a node; ``payload`` (e.g. the node's points) is handed to the children
+    split by the same rule as the points' owner lookup: low child iff coordinate <= plane
+    for the build, i.e. the reference's median split (partitioner.py:131-163).  In a
+    complete tree the depth-first leaf order is the bottom level's left-to-right order,
+    which numbers the tiles.  A node whose cut fails stops its subtree; the error raised is
+    the one the reference's depth-first recursion meets first (smallest pre-order key)."""
+    level = [(root_box, payload)]
+    cuts = []  # per level: (axis, plane) of each node, left to right
+    failed = []  # (pre-order key, exception)
+    for d in range(depth):
+        row, nxt = [], []
+        for i, (box, pl) in enumerate(level):
+            if box is None:  # below a failed node
+                row.append(None)
+                nxt += [(None, None), (None, None)]
+                continue
+            try:
+                axis, plane = cut(pl, box, d)
+            except (InsufficientPointsError, DegenerateSplitError) as e:
+                failed.append(((i << (depth - d), d), e))
+                row.append(None)
+                nxt += [(None, None), (None, None)]
+                continue
+            row.append((axis, plane))
+            lo_box, hi_box = _halves(box, axis, plane)
+            if pl is None:
+                nxt += [(lo_box, None), (hi_box, None)]
+            else:
+                sel = pl[:, axis] <= plane
+                nxt += [(lo_box, pl[sel]), (hi_box, pl[~sel])]
+        cuts.append(row)
+        level = nxt
+    if failed:
+        raise min(failed, key=lambda f: f[0])[1]
+    nodes = [LeafNode(i, box) for i, (box, _) in enumerate(level)]
+    leaves = tuple(nodes)
+    for row in reversed(cuts):  # assemble bottom-up
+        nodes = [SplitNode(a, p, nodes[2 * i], nodes[2 * i + 1]) for i, (a, p) in enumerate(row)]
+    return PartitionTree(root_box, nodes[0], depth, leaves)
 
 
 def build_tree(points, root_box: Aabb, depth: int) -> PartitionTree:
-    """Recursive median splits down to 2^depth leaves (partitioner.py:131-163)."""
+    """Median-split tree with 2^depth leaves over ``points`` (partitioner.py:131-163)."""
     pts = np.asarray(points, dtype=np.float64).reshape(-1, 3)
     if depth < 0:
         raise ValueError("depth must be >= 0")
     if pts.shape[0] < 2 ** depth:
         raise InsufficientPointsError(f"{pts.shape[0]} points cannot fill {2 ** depth} tiles")
-    leaves = []
 
-    def rec(p, box, d):
-        if d == 0:
-            leaf = LeafNode(len(leaves), box)
-            leaves.append(leaf)
-            return leaf
+    def cut(p, box, d):
         if p.shape[0] < 2:
             raise InsufficientPointsError("a subtree ran out of points to split")
-        axis, plane = choose_split(p, box)
-        low_sel = p[:, axis] <= plane
-        lo_mx = box.mx.copy()
-        lo_mx[axis] = plane
-        hi_mn = box.mn.copy()
-        hi_mn[axis] = plane
-        low = rec(p[low_sel], Aabb(box.mn, lo_mx), d - 1)
-        high = rec(p[~low_sel], Aabb(hi_mn, box.mx), d - 1)
-        return SplitNode(axis, plane, low, high)
+        return choose_split(p, box)
 
-    root = rec(pts, root_box, depth)
-    return PartitionTree(root_box, root, depth, tuple(leaves))
+    return _grow(root_box, depth, cut, pts)
 
 
 def grid_tree(root_box: Aabb, splits) -> PartitionTree:
     """Tree of midpoint splits along a fixed axis sequence, e.g. "xxx" = 8 x-strips,
     "xyx" = a 4x2 grid.  Used for the synthetic street/city workloads."""
-    leaves = []
+    axes = [AXES.index(c) for c in splits]
 
-    def rec(box, level):
-        if level == len(splits):
-            leaf = LeafNode(len(leaves), box)
-            leaves.append(leaf)
-            return leaf
-        axis = AXES.index(splits[level])
-        plane = float(0.5 * (box.mn[axis] + box.mx[axis]))
-        lo_mx = box.mx.copy()
-        lo_mx[axis] = plane
-        hi_mn = box.mn.copy()
-        hi_mn[axis] = plane
-        low = rec(Aabb(box.mn, lo_mx), level + 1)
-        high = rec(Aabb(hi_mn, box.mx), level + 1)
-        return SplitNode(axis, plane, low, high)
+    def cut(_, box, d):
+        a = axes[d]
+        return a, float(0.5 * (box.mn[a] + box.mx[a]))
 
-    root = rec(root_box, 0)
-    return PartitionTree(root_box, root, len(splits), tuple(leaves))
+    return _grow(root_box, len(axes), cut, None)
 
 
 def locate(tree: PartitionTree, p) -> int:
@@ -276,14 +297,12 @@ def rays_to_points(rays, root: Aabb, dt: float, max_points: int, seed: int,
 
 
 def default_root_box(points: np.ndarray) -> Aabb:
-    """Point-cloud bounding box inflated by 1% per axis about its centre
-    (partitioner.py:232-239)."""
+    """Bounding box of the points grown by 0.5 % of its extent on each side (1e-3 on a flat
+    axis), partitioner.py:232-239."""
     pts = np.asarray(points, dtype=np.float64).reshape(-1, 3)
-    mn = pts.min(axis=0)
-    mx = pts.max(axis=0)
-    extent = mx - mn
-    pad = np.where(extent > 0.0, 0.005 * extent, 1e-3)
-    return Aabb(mn - pad, mx + pad)
+    lo, hi = pts.min(axis=0), pts.max(axis=0)
+    grow = np.where(hi - lo > 0.0, 0.005 * (hi - lo), 1e-3)
+    return Aabb(lo - grow, hi + grow)
 
 
 def balance_report(tree: PartitionTree, points, rays=None, dt: float = None,
@@ -312,41 +331,38 @@ def balance_report(tree: PartitionTree, points, rays=None, dt: float = None,
     return report
 
 
-def _node_to_json(node) -> dict:
-    if isinstance(node, LeafNode):
-        return {"tile_id": node.tile_id, "box": node.box.to_json()}
-    return {"axis": AXES[node.axis], "plane": float(node.plane),
-            "low": _node_to_json(node.low), "high": _node_to_json(node.high)}
-
-
-def _node_from_json(d: dict, box: Aabb, leaves: list):
-    if "tile_id" in d:
-        leaf = LeafNode(int(d["tile_id"]), Aabb.from_json(d["box"]))
-        if leaf.tile_id != len(leaves):
-            raise ValueError("leaf tile_ids must be depth-first sequential")
-        leaves.append(leaf)
-        return leaf
-    axis = AXES.index(d["axis"])
-    plane = float(d["plane"])
-    lo_mx = box.mx.copy()
-    lo_mx[axis] = plane
-    hi_mn = box.mn.copy()
-    hi_mn[axis] = plane
-    low = _node_from_json(d["low"], Aabb(box.mn, lo_mx), leaves)
-    high = _node_from_json(d["high"], Aabb(hi_mn, box.mx), leaves)
-    return SplitNode(axis, plane, low, high)
-
-
 def tree_to_json(tree: PartitionTree) -> dict:
-    """Same field order as partitioner.tree_to_json (partitioner.py:305-311)."""
-    return {"root_box": tree.root_box.to_json(), "depth": tree.depth,
-            "root": _node_to_json(tree.root)}
+    """The reference's tree JSON (partitioner.py:274-311): {root_box, depth, root}; a split
+    node is {axis: "x"|"y"|"z", plane, low, high}, a leaf {tile_id, box}."""
+
+    def enc(node):
+        if isinstance(node, SplitNode):
+            return {"axis": AXES[node.axis], "plane": float(node.plane),
+                    "low": enc(node.low), "high": enc(node.high)}
+        return {"tile_id": node.tile_id, "box": node.box.to_json()}
+
+    return {"root_box": tree.root_box.to_json(), "depth": tree.depth, "root": enc(tree.root)}
 
 
 def tree_from_json(d: dict) -> PartitionTree:
+    """Inverse of tree_to_json; leaves must be numbered depth-first (partitioner.py:282-324).
+    Split boxes are recomputed from the planes, leaf boxes read as stored."""
     root_box = Aabb.from_json(d["root_box"])
     leaves = []
-    root = _node_from_json(d["root"], root_box, leaves)
+
+    def dec(nd, box):
+        if "tile_id" not in nd:
+            axis = AXES.index(nd["axis"])
+            plane = float(nd["plane"])
+            lo_box, hi_box = _halves(box, axis, plane)
+            low = dec(nd["low"], lo_box)
+            return SplitNode(axis, plane, low, dec(nd["high"], hi_box))
+        if int(nd["tile_id"]) != len(leaves):
+            raise ValueError("leaf tile_ids must be depth-first sequential")
+        leaves.append(LeafNode(len(leaves), Aabb.from_json(nd["box"])))
+        return leaves[-1]
+
+    root = dec(d["root"], root_box)
     return PartitionTree(root_box, root, int(d["depth"]), tuple(leaves))
 
 
