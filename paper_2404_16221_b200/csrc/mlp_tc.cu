@@ -128,10 +128,13 @@ __device__ __forceinline__ void put8(uint8_t* tile, int r, int cb, const float* 
   *reinterpret_cast<uint4*>(tile + tile_off(TILE, r, cb * 8)) = q;
 }
 // ReLU on the packed fp16 pair: fp16(max(x, 0)) == max(fp16(x), 0) (rounding is monotonic
-// and keeps the sign; a negative x may give -0, equal to +0 everywhere downstream — the
-// backward's ReLU mask tests the magnitude bits), one HMNMX2 per pair instead of two FMNMX
+// and keeps the sign), done by the conversion itself (cvt.rn.relu.f16x2.f32: one F2FP per
+// pair, no separate max).  .x = a, .y = b as __floats2half2_rn; the first PTX source
+// operand fills the upper half.
 __device__ __forceinline__ __half2 relu_h2(float a, float b) {
-  return __hmax2(__floats2half2_rn(a, b), __float2half2_rn(0.f));
+  uint32_t u;
+  asm("cvt.rn.relu.f16x2.f32 %0, %1, %2;" : "=r"(u) : "f"(b), "f"(a));
+  return *reinterpret_cast<__half2*>(&u);
 }
 __device__ __forceinline__ void put_relu8(uint8_t* tile, int r, int cb, const float* v) {
   uint4 q;
