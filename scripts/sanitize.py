@@ -8,7 +8,9 @@ Variants: fused (sample-major tcgen05 MLP backward + fused hash scatter), split 
 backward + side-stream scatter), level (level-major hash kernels), density (density-only
 proposal fields + the interlevel loss), cuda (CUDA-core reference MLP), render (the render
 path), sample (the sample-broadcast protocol).  Each runs two training steps of a 2-region
-hash-grid pool on 96 rays and checks the loss is finite.
+hash-grid pool on 96 rays and checks the loss is finite.  c4 (not in the default list): two
+steps of the c4 bench pool (8 regions at full model size, level-major kernels, proposal
+fields, interlevel loss, sparse backward, TMA K4, record-index K5) on 65,536 of its rays.
 """
 from __future__ import annotations
 
@@ -61,6 +63,21 @@ def main():
     r = rays()
     tg = np.random.default_rng(1).uniform(0, 1, size=(r.shape[1], 3))
     for v in todo:
+        if v == "c4":
+            import bench
+            from paper_2404_16221_b200.workloads import CONFIGS, make_rays, make_targets
+            w = CONFIGS["c4"]
+            pool = bench.build_pool(w, 0, 1, "cuda:0", None)
+            rr = torch.from_numpy(make_rays(w, seed=0, n=65536)).to("cuda:0")
+            tt = torch.from_numpy(make_targets(65536, seed=100)).to("cuda:0")
+            for step in (1, 2):
+                loss = pool.train_step(rr, tt, w.dt, lr=1e-2, step=step,
+                                       lambda_interlevel=w.interlevel)
+            assert np.isfinite(loss.item())
+            print(f"{v}: ok loss {loss.item():.6f}", flush=True)
+            del pool
+            torch.cuda.empty_cache()
+            continue
         pool = pool_for(v)
         if v == "render":
             out, _ = pool.render_rays(r, 0.03)
